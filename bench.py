@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""Benchmark: one semismooth-Newton iteration of the hot path.
+
+A step = K1 constitutive update (E, Ep, Hard -> S, flags, packed D at plastic
+points) + K2/K6 tangent assembly (K = K_elast + sum_plastic B^T w (D - C) B
+into the cached CSR pattern) over the whole configuration, inputs resident in
+HBM.  Default workload: BASELINE.json configs[1] ("cfg2": 2D Q2-8 serendipity
+512x512, von Mises a=1e4, Y=450, 30% plastic, 2.36M integration points).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config cfgX] [--impl reference]
+
+Prints ONE JSON line on rank 0 (driver contract): value = integration
+points / s over all ranks; e2e = the same through the public API with host
+buffers (H2D E, D2H S + flags + K every step); roofline = the dominant kernel
+(tangent assembly) against MEASURED_PEAKS.json; cpu_baseline = the oracle
+port of the reference algorithm on a bounded sample, 1 host core.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tangent-stiffness assembly: integration points/s and achieved HBM GB/s vs peak"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes
+
+def algorithmic_bytes(cfg, n_int, n_plastic, nnz, n_nodes, n_e, n_p):
+    hist = 6 if cfg.model == "vm" else 0  # Hard read only for VM
+    epr = 6 if cfg.model != "elastic" else 0
+    constitutive = 8 * (6 + epr + hist + 6) * n_int + n_int + 288 * n_plastic
+    assembly = 8 * nnz + 8 * cfg.dim * n_nodes + 4 * n_p * n_e
+    tangent_kernel = 8 * nnz + 288 * n_plastic + n_int + 8 * cfg.dim * n_nodes + 4 * n_p * n_e
+    return constitutive, assembly, tangent_kernel
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port of the reference algorithm
+
+def _cpu_slab(args):
+    name, ny0, ny1 = args
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    from oracle import oracle as O
+    from paper_1805_04155_b200.synthetic import CONFIGS, displacement
+    cfg = CONFIGS[name]
+    n = cfg.n
+    # y-slab (2D) / z-slab (3D) of the full mesh: cells [ny0, ny1)
+    if cfg.dim == 2:
+        active = np.zeros((n, n), np.uint8)
+        active[ny0:ny1, :] = 1
+        coord, elem, _ = O.structured_mesh(cfg.family, 2, n, n, 0, 1.0 / n, 1.0 / n, 0.0, active)
+    else:
+        coord, elem, _ = O.structured_mesh(cfg.family, 3, n, n, ny1 - ny0, 1.0 / n, 1.0 / n, 1.0 / n)
+        coord = coord.copy()
+        coord[:, 2] += ny0 / n
+    K, G = O.elastic_moduli(cfg.young, cfg.poisson)
+    cache = O.Cache(cfg.family, cfg.dim, coord, elem, G, K)
+    u = displacement(coord, cfg.seed)
+    E1 = cache.strains(u)
+    if cfg.model == "elastic":
+        return cache.n_int, cache.elastic_assembly_seconds, 0
+    if cfg.model == "vm":
+        crit = O.constitutive_vm(E1, None, None, G, K, cfg.p1, 0.0)["crit"]
+        s = cfg.p2 / np.quantile(crit, 1.0 - cfg.target)
+        p1, p2, model = cfg.p1, cfg.p2, 1
+    else:
+        eta, c = O.dp_parameters(cfg.p1, cfg.p2)
+        s = 1.0
+        for _ in range(80):
+            f = O.constitutive_dp(s * E1, None, G, K, eta, c)["plastic"].mean()
+            if abs(f - cfg.target) < 0.02:
+                break
+            s *= 1.15 if f < cfg.target else 0.9
+        p1, p2, model = eta, c, 2
+    E = s * E1
+    z = np.zeros_like(E)
+    cache.time_iteration(model, E, z, z, p1, p2)  # warm-up
+    times = []
+    for _ in range(3):
+        t, npl = cache.time_iteration(model, E, z, z, p1, p2)
+        times.append(t)
+    return cache.n_int, statistics.median(times), npl
+
+
+def cpu_baseline(name, rows, procs=1):
+    """Time the reference algorithm (oracle mode A) on `rows` cell rows per
+    process; returns ip/s aggregated over processes."""
+    from paper_1805_04155_b200.synthetic import CONFIGS
+    cfg = CONFIGS[name]
+    tasks = []
+    for p in range(procs):
+        y0 = (p * rows) % cfg.n
+        tasks.append((name, y0, min(cfg.n, y0 + rows)))
+    t0 = time.perf_counter()
+    if procs == 1:
+        res = [_cpu_slab(tasks[0])]
+    else:
+        import multiprocessing as mp
+        with mp.get_context("spawn").Pool(procs) as pool:
+            res = pool.map(_cpu_slab, tasks)
+    wall = time.perf_counter() - t0
+    n_int = sum(r[0] for r in res)
+    t_max = max(r[1] for r in res)
+    return n_int / t_max, n_int, t_max, wall
+
+
+# ---------------------------------------------------------------------------
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU port of the reference path on the host cores."""
+    from paper_1805_04155_b200.synthetic import CONFIGS
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    rows = args.cpu_rows
+    vals = []
+    t_all = time.perf_counter()
+    for _ in range(max(args.steps, 1)):
+        v, n_int, t_max, wall = cpu_baseline(args.config, rows, procs=cores)
+        vals.append(v)
+        if time.perf_counter() - t_all > 240:
+            break
+    value = statistics.median(vals)
+    sample = (f"{cores} processes x {rows} cell rows of {args.config} "
+              f"({n_int} integration points per step), evaluate_constitutive + "
+              f"assemble_tangent_stiffness restated (oracle mode A), median of 3 per process")
+    line = {
+        "metric": METRIC, "value": value, "unit": "ip/s", "impl": "reference",
+        "n_gpus": world, "steps": len(vals), "warmup": args.warmup,
+        "ms_per_step": 1e3 * n_int / value, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config},
+        "cpu_baseline": {"value": value, "unit": "ip/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "ip/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--target", type=float, default=None, help="plastic fraction override")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-rows", type=int, default=None)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.cpu_rows is None:
+        args.cpu_rows = {"cfg1": 256, "cfg2": 48, "cfg3": 4, "cfg4": 8, "cfg5": 4}[args.config]
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1805_04155_b200 import build as B
+    B.build()
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.synthetic import CONFIGS, make_workload
+    cfg = CONFIGS[args.config]
+    z_range = None
+    if world > 1:
+        # weak scaling: every rank owns a full copy-sized workload (replica);
+        # see DESIGN.md §Multi-GPU for the slab partition of one mesh.
+        pass
+    wl = make_workload(cfg, target=args.target, device=dev, z_range=z_range)
+    cache, mat = wl.cache, wl.mat
+    n_int, nnz = cache.n_int, cache.nnz
+    stream = torch.cuda.Stream(dev)
+    eng = P.TangentEngine(cache, mat, stream=stream)
+    E = wl.E.contiguous()
+    hbm_peak, peak_src = load_peaks()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    elastic = cfg.model == "elastic"
+    if elastic:
+        # cfg1: the timed region is K5, the elastic assembly into the pattern
+        Kout = torch.empty((nnz,), dtype=torch.float64, device=dev)
+
+        def launch():
+            with torch.cuda.stream(stream):
+                P.api._check(P.api.L.lib().epfem_assemble_elastic(eng.ctx.handle, cache.handle,
+                                                                 P.api._ptr(Kout)))
+        launches_per_step = 1
+    else:
+        with torch.cuda.stream(stream):
+            eng.capture(E)
+
+        def launch():
+            eng.replay()
+        launches_per_step = 2
+
+    # warm-up
+    for _ in range(args.warmup):
+        launch()
+    torch.cuda.synchronize(dev)
+    barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            launch()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    t_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_per_step = t_ms / args.steps
+    value = world * n_int / (ms_per_step * 1e-3)
+
+    n_plastic = int((eng.flags & 1).sum().item()) if not elastic else 0
+    info = cache.info
+    cons_b, asm_b, tan_b = algorithmic_bytes(cfg, n_int, n_plastic, nnz, info.n_nodes,
+                                             info.n_elements, info.n_p)
+    # per-kernel device time on the launching stream (not graph-captured)
+    k_ms = {}
+    if not elastic:
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        lib = P.api.L.lib()
+        tot_c = tot_t = 0.0
+        reps = max(args.steps, 5)
+        for _ in range(reps):
+            evs[0].record(stream)
+            P.api._check(lib.epfem_constitutive(eng.ctx.handle, P.api.C.byref(eng._mv), P.api._ptr(E),
+                                                None, None, P.api.C.byref(eng._out)))
+            evs[1].record(stream)
+            P.api._check(lib.epfem_assemble_tangent(eng.ctx.handle, cache.handle, n_int,
+                                                    P.api._ptr(eng.D), P.api._ptr(eng.flags),
+                                                    P.api._ptr(eng.K)))
+            evs[2].record(stream)
+            torch.cuda.synchronize(dev)
+            tot_c += evs[0].elapsed_time(evs[1])
+            tot_t += evs[1].elapsed_time(evs[2])
+        k_ms = {"constitutive": tot_c / reps, "tangent": tot_t / reps}
+        dom_bytes, dom_ms, dom = tan_b, k_ms["tangent"], "tangent (K2+K6 row-block gather)"
+    else:
+        dom_bytes, dom_ms, dom = asm_b, ms_per_step, "elastic (K5 row-block gather)"
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    step_bytes = cons_b + asm_b if not elastic else asm_b
+    step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
+
+    # ------------------------------------------------------------------ e2e
+    e2e = None
+    if not args.no_e2e:
+        hE = torch.empty_like(E, device="cpu").pin_memory()
+        hE.copy_(E)
+        if elastic:
+            outs = [torch.empty((nnz,), dtype=torch.float64).pin_memory()]
+        else:
+            outs = [torch.empty((n_int, 6), dtype=torch.float64).pin_memory(),
+                    torch.empty((n_int,), dtype=torch.uint8).pin_memory(),
+                    torch.empty((nnz,), dtype=torch.float64).pin_memory()]
+        dE = torch.empty_like(E)
+        ctx = P.Context(local, stream=stream, synchronous=False)
+
+        def e2e_step():
+            with torch.cuda.stream(stream):
+                if elastic:
+                    P.api._check(P.api.L.lib().epfem_assemble_elastic(ctx.handle, cache.handle,
+                                                                     P.api._ptr(Kout)))
+                    outs[0].copy_(Kout, non_blocking=True)
+                    return
+                dE.copy_(hE, non_blocking=True)
+                S, flags, D, K = eng.step(dE)
+                outs[0].copy_(S, non_blocking=True)
+                outs[1].copy_(flags, non_blocking=True)
+                outs[2].copy_(K, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2e_steps = max(3, min(args.steps, 10))
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
+        h2d = 0 if elastic else E.numel() * 8
+        d2h = sum(o.numel() * o.element_size() for o in outs)
+        e2e = {"value": world * n_int / (e_ms * 1e-3), "unit": "ip/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms}
+
+    # ------------------------------------------------------------ cpu baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, ns, tm, wall = cpu_baseline(args.config, args.cpu_rows, procs=1)
+        cpu = {"value": v, "unit": "ip/s", "cores": 1, "kind": "port",
+               "sample": (f"{args.cpu_rows} cell rows of {args.config} ({ns} integration points), "
+                          f"oracle mode A = reference algorithm restated (Eigen-semantics "
+                          f"triplets->CSC->conservative products), median of 3, {tm:.3f} s/iter")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "ip/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "element": f"{cfg.family} {cfg.dim}D",
+                       "mesh": f"{cfg.n}^{cfg.dim}", "model": cfg.model,
+                       "n_int": n_int, "nnz": nnz, "n_dofs": info.n_dofs,
+                       "plastic_fraction": n_plastic / n_int if n_int else 0.0,
+                       "strain_scale": wl.scale,
+                       "l2": "inputs larger than L2 (working set "
+                             f"{(step_bytes + 8 * nnz) / 1e9:.2f} GB > 126 MB)",
+                       "parallelism": f"replica x{world}" if world > 1 else "single GPU"},
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+                         "algorithmic_bytes": dom_bytes, "kernel_ms": dom_ms,
+                         "peak_source": peak_src},
+            "roofline_step": {"algorithmic_bytes": step_bytes, "achieved": step_gbs,
+                              "frac": step_gbs / hbm_peak},
+            "kernels_ms": k_ms,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

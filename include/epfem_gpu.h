@@ -1,0 +1,198 @@
+/*
+ * epfem_gpu.h — C-ABI of the B200-native tangent-stiffness path.
+ *
+ * Drop-in boundary for the reference's hot path (/root/reference/proj):
+ *
+ *   reference entry point (C++ / Eigen)                      replaced by
+ *   -------------------------------------------------------  ------------------------------
+ *   evaluate_constitutive        include/epfem/constitutive.hpp:96-98
+ *   constitutive_elastic/vm/dp   include/epfem/constitutive.hpp:67,80-81,92-93
+ *                                src/constitutive.cpp:76-225    epfem_constitutive
+ *   build_assembly_cache         include/epfem/assembly.hpp:53
+ *                                src/assembly.cpp:224-256       epfem_cache_build
+ *   jacobians / weights          include/epfem/assembly.hpp:20-21
+ *                                src/assembly.cpp:96-137        epfem_cache_geometry
+ *   AssemblyCache::K_elast       include/epfem/assembly.hpp:45  epfem_cache_K_elast
+ *   assemble_elastic_stiffness   include/epfem/assembly.hpp:55  epfem_assemble_elastic
+ *   assemble_tangent_stiffness   include/epfem/assembly.hpp:59-60
+ *                                src/assembly.cpp:262-289       epfem_assemble_tangent (packed D)
+ *                                                               epfem_assemble_tangent_ds (36 x n_int DS)
+ *   sparsity of K (Eigen CSC)    src/linalg.cpp:28-35           epfem_cache_pattern
+ *   AssemblyCache::strains       include/epfem/assembly.hpp:50  epfem_strains
+ *   internal_forces              include/epfem/assembly.hpp:63  epfem_internal_forces
+ *   elastic_moduli/dp_parameters include/epfem/constitutive.hpp:11,16
+ *                                                               epfem_elastic_moduli, epfem_dp_parameters
+ *   epfem::Error (what())        include/epfem/types.hpp:20-22  status code + epfem_last_error()
+ *
+ * Conventions
+ *  - Every array argument is a DEVICE pointer unless stated otherwise, with
+ *    the reference's column-major Eigen byte layout: E/Ep/Hard/S are 6 x n_int
+ *    (48 B per integration point, Voigt order s11 s22 s33 s12 s23 s31, strains
+ *    with engineering shears), DS is 36 x n_int (a column-major 6x6 block per
+ *    point), coord is dim x n_nodes, elem is n_p x n_elements (int32, 0-based).
+ *  - K is returned in CSR with int64 row_ptr and int32 col_idx, columns sorted
+ *    ascending.  K is structurally symmetric, so these arrays are also the
+ *    reference's CSC (Eigen SparseMatrix<double>) arrays.  The pattern is the
+ *    structural one (explicit zeros kept), identical for K_elast and every
+ *    tangent, exactly as Eigen's conservative products produce it.
+ *  - Calls are stream-ordered on the context's stream and do not synchronize,
+ *    except epfem_cache_build and epfem_ctx_sync.  Device-side failures (DP
+ *    zero deviator) are latched in the context and reported by the next
+ *    epfem_ctx_sync.  With epfem_ctx_set_sync(ctx, 1) every call synchronizes
+ *    and reports, which is the reference's exception behaviour.
+ *  - Status: 0 on success, EPFEM_ERR_* otherwise; epfem_last_error() returns
+ *    the message (thread-local), using the reference's texts, e.g.
+ *    "assemble_tangent_stiffness: size mismatch",
+ *    "jacobians: nonpositive det J in element 0",
+ *    "constitutive_dp: zero deviator in smooth return".
+ *  - There is no CPU fallback: without a CUDA device every call fails with
+ *    EPFEM_ERR_CUDA.
+ */
+#ifndef EPFEM_GPU_H
+#define EPFEM_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EPFEM_GPU_ABI_VERSION 1
+
+enum epfem_status {
+  EPFEM_OK = 0,
+  EPFEM_ERR_INVALID = 1,        /* argument / size mismatch (reference: epfem::Error) */
+  EPFEM_ERR_DEGENERATE = 2,     /* nonpositive det J */
+  EPFEM_ERR_ZERO_DEVIATOR = 3,  /* DP smooth return with zero deviator */
+  EPFEM_ERR_CUDA = 4,           /* CUDA runtime / launch failure */
+  EPFEM_ERR_NOMEM = 5,
+  EPFEM_ERR_UNSUPPORTED = 6     /* e.g. node valence > 255 */
+};
+
+/* epfem::ElementFamily order (reference_elements.hpp:10) */
+enum epfem_family { EPFEM_P1 = 0, EPFEM_P2 = 1, EPFEM_Q1 = 2, EPFEM_Q2 = 3 };
+
+/* MaterialField::plastic variant (constitutive.hpp:120-129) */
+enum epfem_model {
+  EPFEM_MODEL_ELASTIC = 0,        /* std::monostate */
+  EPFEM_MODEL_VON_MISES = 1,      /* VonMisesParams {a, Y} */
+  EPFEM_MODEL_DRUCKER_PRAGER = 2  /* DruckerPragerParams {eta, c} */
+};
+
+/* per-point flag byte written by epfem_constitutive */
+enum epfem_flag { EPFEM_FLAG_PLASTIC = 1, EPFEM_FLAG_SMOOTH = 2, EPFEM_FLAG_APEX = 4 };
+
+/* Packed consistent tangent: 21 upper-triangle entries of the symmetric 6x6
+ * block, plane-strain entries first, padded to 24 doubles (192 B = 6 full
+ * 32-B sectors).  Entry k holds D(EPFEM_D_ROW[k], EPFEM_D_COL[k]):
+ *   k : 0  1  2  3  4  5 | 6  7  8  9 10 11 12 13 14 15 16 17 18 19 20
+ *   i : 0  0  0  1  1  3 | 0  0  0  1  1  1  2  2  2  2  3  3  4  4  5
+ *   j : 0  1  3  1  3  3 | 2  4  5  2  4  5  2  3  4  5  4  5  4  5  5
+ * The D blocks of the reference are bitwise symmetric, so this
+ * packing is lossless. */
+#define EPFEM_D_STRIDE 24
+
+/* Material field.  Arrays (device, length n_int) override the uniform value
+ * when non-NULL.  p1/p2 = (a, Y) for von Mises, (eta, c) for Drucker-Prager. */
+typedef struct epfem_material {
+  int model;
+  int64_t n_int;
+  const double* shear;
+  const double* bulk;
+  const double* p1;
+  const double* p2;
+  double shear_u, bulk_u, p1_u, p2_u;
+} epfem_material;
+
+/* Mesh (mesh.hpp:15-35): coord dim x n_nodes, elem n_p x n_elements. */
+typedef struct epfem_mesh {
+  int dim;
+  int family;
+  int64_t n_nodes;
+  int64_t n_elements;
+  const double* coord;
+  const int32_t* elem;
+} epfem_mesh;
+
+/* Outputs of epfem_constitutive; any NULL output is skipped. */
+typedef struct epfem_constitutive_out {
+  double* S;             /* 6 x n_int stress, every point */
+  uint8_t* flags;        /* n_int flag bytes (EPFEM_FLAG_*) */
+  double* D;             /* EPFEM_D_STRIDE x n_int packed tangent, plastic points only */
+  double* DS;            /* 36 x n_int reference layout, every point (elastic: C, apex: 0) */
+  double* Ep;            /* 6 x n_int updated plastic strain */
+  double* Hard;          /* 6 x n_int updated back stress (VM; zero for DP/elastic) */
+  uint8_t* plastic_mask; /* n_int bool */
+  uint8_t* smooth_mask;  /* n_int bool (DP) */
+  uint8_t* apex_mask;    /* n_int bool (DP) */
+  double* crit;          /* n_int |s_tr| - Y (VM) */
+} epfem_constitutive_out;
+
+typedef struct epfem_cache_info {
+  int dim, family, n_p, n_q, n_strain;
+  int max_row_nodes;     /* max neighbour nodes of any node (row block width / dim) */
+  int64_t n_nodes, n_elements, n_int, n_dofs, nnz;
+  double build_seconds;  /* wall time of epfem_cache_build (elastic_assembly_seconds) */
+  double pattern_seconds, elastic_seconds; /* GPU event time of pattern+slot map and K_elast */
+} epfem_cache_info;
+
+typedef struct epfem_ctx epfem_ctx;
+typedef struct epfem_cache epfem_cache;
+
+const char* epfem_last_error(void);
+int epfem_abi_version(void);
+
+int epfem_ctx_create(int device, void* cuda_stream, epfem_ctx** out);
+int epfem_ctx_set_stream(epfem_ctx* ctx, void* cuda_stream);
+int epfem_ctx_set_sync(epfem_ctx* ctx, int synchronous);
+int epfem_ctx_sync(epfem_ctx* ctx);
+int epfem_ctx_destroy(epfem_ctx* ctx);
+
+/* Host scalars (constitutive.cpp:11-30). mode: 1 = three_d, 0 = plane_strain. */
+int epfem_elastic_moduli(double young, double poisson, double* bulk, double* shear);
+int epfem_dp_parameters(double c0, double phi, int mode, double* eta, double* c);
+
+/* K1: constitutive update at every integration point (constitutive.cpp:76-225).
+ * Ep_prev / Hard_prev may be NULL (zero history). */
+int epfem_constitutive(epfem_ctx* ctx, const epfem_material* mat, const double* E,
+                       const double* Ep_prev, const double* Hard_prev,
+                       const epfem_constitutive_out* out);
+
+/* One-time cache: jacobians + weights, CSR pattern (K3), element->slot map
+ * (K4), K_elast (K5).  Synchronous; fails with EPFEM_ERR_DEGENERATE naming the
+ * first element with det J <= 0. */
+int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_material* mat,
+                      epfem_cache** out);
+int epfem_cache_destroy(epfem_cache* cache);
+int epfem_cache_get_info(const epfem_cache* cache, epfem_cache_info* info);
+int epfem_cache_pattern(const epfem_cache* cache, const int64_t** row_ptr,
+                        const int32_t** col_idx);
+int epfem_cache_K_elast(const epfem_cache* cache, const double** values);
+/* det (n_int), weight = |det| w_q (n_int), inv (dim*dim x n_int column-major) */
+int epfem_cache_geometry(const epfem_cache* cache, const double** det,
+                         const double** weight, const double** inv);
+
+/* K5 recomputed into K_values (nnz doubles) (assembly.cpp:258-260). */
+int epfem_assemble_elastic(epfem_ctx* ctx, const epfem_cache* cache, double* K_values);
+
+/* K6+K2: K = K_elast + sum over plastic points of B^T w (D - C) B, written
+ * into the cached pattern (assembly.cpp:262-289).  Rows with no plastic
+ * contribution are bitwise copies of K_elast. */
+int epfem_assemble_tangent(epfem_ctx* ctx, const epfem_cache* cache, int64_t n_int,
+                           const double* D, const uint8_t* flags, double* K_values);
+/* Same, reading the reference layout: DS 36 x n_int, plastic_cols bool. */
+int epfem_assemble_tangent_ds(epfem_ctx* ctx, const epfem_cache* cache, int64_t n_int,
+                              const double* DS, const uint8_t* plastic_cols,
+                              double* K_values);
+
+/* K8: E = B u, 2D embedded in Voigt rows {0,1,3} (assembly.cpp:211-222). */
+int epfem_strains(epfem_ctx* ctx, const epfem_cache* cache, const double* u, double* E);
+/* K9: F = B^T (weight * S) (assembly.cpp:291-301). */
+int epfem_internal_forces(epfem_ctx* ctx, const epfem_cache* cache, const double* S,
+                          double* F);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EPFEM_GPU_H */

@@ -1,0 +1,88 @@
+"""Build libepfem_gpu.so in-tree with nvcc for sm_100a (no JIT, no torch
+extension machinery: the product is a plain C-ABI shared library).
+
+    python -m paper_1805_04155_b200.build            # incremental
+    python -m paper_1805_04155_b200.build --force
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OBJ = os.path.join(PKG, "_obj")
+LIBDIR = os.path.join(PKG, "lib")
+LIB = os.path.join(LIBDIR, "libepfem_gpu.so")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                      "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr",
+                      "-I", os.path.join(ROOT, "include")]
+
+# per-source extra flags: the constitutive kernel reproduces the reference's
+# (FMA-free) operation order bit for bit.
+SOURCES = {
+    "constitutive.cu": ["--fmad=false"],
+    "assembly.cu": [],
+    "capi.cu": [],
+    "tables.cpp": [],
+}
+HEADERS = ["common.cuh", "kernels.cuh"]
+
+
+def nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _stale(out: str, deps: list[str]) -> bool:
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(LIBDIR, exist_ok=True)
+    hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "epfem_gpu.h")]
+    objs = []
+    for src, extra in SOURCES.items():
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(OBJ, src + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [path] + hdrs + [__file__]):
+            if src.endswith(".cpp"):
+                cmd = ["g++", "-O2", "-fPIC", "-std=c++17", "-ffp-contract=off",
+                       "-I", "/usr/local/cuda/include", "-I", os.path.join(ROOT, "include"),
+                       "-c", path, "-o", obj]
+            else:
+                cmd = [nvcc()] + NVCC_COMMON + extra + ["-c", path, "-o", obj]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            subprocess.check_call(cmd)
+    if force or _stale(LIB, objs):
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart_static"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.check_call(cmd)
+    return LIB
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", "--verbose", action="store_true")
+    args = ap.parse_args(argv)
+    print(build(force=args.force, verbose=args.verbose))
+
+
+if __name__ == "__main__":
+    sys.exit(main())

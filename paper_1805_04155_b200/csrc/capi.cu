@@ -1,0 +1,415 @@
+// C-ABI implementation (include/epfem_gpu.h): contexts, the device-resident
+// assembly cache, argument validation with the reference's error texts, and
+// dispatch to the sm_100a kernels.  No CPU compute path exists: every entry
+// point fails with EPFEM_ERR_CUDA when no CUDA device is present.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace epfem_gpu {
+
+thread_local std::string g_msg;
+
+void set_error(const std::string& msg) { g_msg = msg; }
+int fail(int code, const std::string& msg) {
+  g_msg = msg;
+  return code;
+}
+int cuda_fail(cudaError_t err, const char* what) {
+  g_msg = std::string("CUDA error: ") + cudaGetErrorString(err) + " (" + what + ")";
+  return EPFEM_ERR_CUDA;
+}
+
+}  // namespace epfem_gpu
+
+using namespace epfem_gpu;
+
+struct epfem_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  bool sync = false;
+  DevErr* err = nullptr;  // device
+};
+
+struct epfem_cache {
+  epfem_cache_info info{};
+  double* gradhat = nullptr;  // device tables
+  double* wq = nullptr;
+  int32_t* elem = nullptr;    // private copy of connectivity
+  double* det = nullptr;
+  double* inv = nullptr;
+  double* weight = nullptr;
+  double* shear = nullptr;    // moduli snapshot (AssemblyCache::shear/bulk)
+  double* bulk = nullptr;
+  double shear_u = 0, bulk_u = 0;
+  PatternOut pat;
+  double* K_elast = nullptr;
+};
+
+namespace {
+
+int check_ctx(epfem_ctx* ctx) {
+  if (!ctx) return fail(EPFEM_ERR_INVALID, "null context");
+  return 0;
+}
+
+// Read and clear the latched device error; translate to the reference text.
+int poll_device_error(epfem_ctx* ctx, const char* degenerate_prefix) {
+  DevErr h{};
+  EPFEM_CUDA_TRY(cudaMemcpyAsync(&h, ctx->err, sizeof(DevErr), cudaMemcpyDeviceToHost, ctx->stream));
+  EPFEM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  if (h.code == 0) return 0;
+  DevErr z{};
+  z.index = ~0ull;
+  EPFEM_CUDA_TRY(cudaMemcpy(ctx->err, &z, sizeof(DevErr), cudaMemcpyHostToDevice));
+  if (h.code == EPFEM_ERR_ZERO_DEVIATOR)
+    return fail(h.code, "constitutive_dp: zero deviator in smooth return");
+  if (h.code == EPFEM_ERR_DEGENERATE)
+    return fail(h.code, std::string(degenerate_prefix ? degenerate_prefix : "jacobians") +
+                            ": nonpositive det J in element " + std::to_string(h.index));
+  return fail(h.code, "device error");
+}
+
+int finish(epfem_ctx* ctx) {
+  EPFEM_CUDA_TRY(cudaGetLastError());
+  if (ctx->sync) return poll_device_error(ctx, nullptr);
+  return 0;
+}
+
+bool aligned16(const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+const char* epfem_last_error(void) { return g_msg.c_str(); }
+int epfem_abi_version(void) { return EPFEM_GPU_ABI_VERSION; }
+
+int epfem_ctx_create(int device, void* cuda_stream, epfem_ctx** out) {
+  if (!out) return fail(EPFEM_ERR_INVALID, "null output");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(EPFEM_ERR_CUDA, "epfem_gpu: no CUDA device available (there is no CPU fallback)");
+  if (device < 0 || device >= n) return fail(EPFEM_ERR_INVALID, "epfem_gpu: invalid device");
+  EPFEM_CUDA_TRY(cudaSetDevice(device));
+  epfem_ctx* c = new epfem_ctx;
+  c->device = device;
+  c->stream = (cudaStream_t)cuda_stream;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  e = cudaMalloc(&c->err, sizeof(DevErr));
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaMalloc(err)");
+  }
+  DevErr z{};
+  z.index = ~0ull;
+  cudaMemcpy(c->err, &z, sizeof(DevErr), cudaMemcpyHostToDevice);
+  *out = c;
+  return 0;
+}
+
+int epfem_ctx_set_stream(epfem_ctx* ctx, void* cuda_stream) {
+  if (int rc = check_ctx(ctx)) return rc;
+  ctx->stream = (cudaStream_t)cuda_stream;
+  return 0;
+}
+
+int epfem_ctx_set_sync(epfem_ctx* ctx, int synchronous) {
+  if (int rc = check_ctx(ctx)) return rc;
+  ctx->sync = synchronous != 0;
+  return 0;
+}
+
+int epfem_ctx_sync(epfem_ctx* ctx) {
+  if (int rc = check_ctx(ctx)) return rc;
+  EPFEM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return poll_device_error(ctx, nullptr);
+}
+
+int epfem_ctx_destroy(epfem_ctx* ctx) {
+  if (!ctx) return 0;
+  cudaFree(ctx->err);
+  delete ctx;
+  return 0;
+}
+
+int epfem_elastic_moduli(double young, double poisson, double* bulk, double* shear) {
+  // constitutive.cpp:11-18
+  if (young <= 0.0) return fail(EPFEM_ERR_INVALID, "elastic_moduli: Young modulus must be > 0");
+  if (poisson <= -1.0 || poisson >= 0.5)
+    return fail(EPFEM_ERR_INVALID, "elastic_moduli: Poisson ratio must lie in (-1, 1/2)");
+  *bulk = young / (3.0 * (1.0 - 2.0 * poisson));
+  *shear = young / (2.0 * (1.0 + poisson));
+  return 0;
+}
+
+int epfem_dp_parameters(double c0, double phi, int mode, double* eta, double* c) {
+  // constitutive.cpp:20-30
+  if (c0 <= 0.0 || phi <= 0.0 || phi >= M_PI / 2.0)
+    return fail(EPFEM_ERR_INVALID, "dp_parameters: require c0 > 0 and phi in (0, pi/2)");
+  if (mode == 1) {
+    const double denom = std::sqrt(3.0) * (3.0 + std::sin(phi));
+    *eta = 6.0 * std::sin(phi) / denom;
+    *c = c0 * 6.0 * std::cos(phi) / denom;
+  } else {
+    const double t = std::tan(phi);
+    const double denom = std::sqrt(9.0 + 12.0 * t * t);
+    *eta = 3.0 * t / denom;
+    *c = c0 * 3.0 / denom;
+  }
+  return 0;
+}
+
+int epfem_constitutive(epfem_ctx* ctx, const epfem_material* mat, const double* E,
+                       const double* Ep_prev, const double* Hard_prev,
+                       const epfem_constitutive_out* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!mat || !out) return fail(EPFEM_ERR_INVALID, "evaluate_constitutive: null argument");
+  if (mat->n_int < 0) return fail(EPFEM_ERR_INVALID, "evaluate_constitutive: size mismatch");
+  if (mat->n_int > 0 && !E) return fail(EPFEM_ERR_INVALID, "evaluate_constitutive: null strain");
+  const void* ptrs[] = {E, Ep_prev, Hard_prev, out->S, out->D, out->DS, out->Ep, out->Hard};
+  for (const void* p : ptrs)
+    if (!aligned16(p))
+      return fail(EPFEM_ERR_INVALID, "evaluate_constitutive: arrays must be 16-byte aligned");
+  ConstArgs a{};
+  a.n = mat->n_int;
+  a.E = E;
+  a.Ep = Ep_prev;
+  a.Hard = mat->model == EPFEM_MODEL_VON_MISES ? Hard_prev : nullptr;
+  a.G = mat->shear;
+  a.K = mat->bulk;
+  a.p1 = mat->p1;
+  a.p2 = mat->p2;
+  a.Gu = mat->shear_u;
+  a.Ku = mat->bulk_u;
+  a.p1u = mat->p1_u;
+  a.p2u = mat->p2_u;
+  a.S = out->S;
+  a.flags = out->flags;
+  a.D = out->D;
+  a.DS = out->DS;
+  a.Ep_out = out->Ep;
+  a.Hard_out = out->Hard;
+  a.pm = out->plastic_mask;
+  a.sm = out->smooth_mask;
+  a.am = out->apex_mask;
+  a.crit = out->crit;
+  a.err = ctx->err;
+  if (int rc = launch_constitutive(mat->model, a, ctx->stream, ctx->num_sms)) return rc;
+  return finish(ctx);
+}
+
+int epfem_cache_destroy(epfem_cache* c) {
+  if (!c) return 0;
+  void* ptrs[] = {c->gradhat, c->wq,          c->elem,        c->det,          c->inv,
+                  c->weight,  c->shear,       c->bulk,        c->pat.n2e_ptr,  c->pat.n2e,
+                  c->pat.nbr_ptr, c->pat.row_ptr, c->pat.col_idx, c->pat.slot, c->K_elast};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete c;
+  return 0;
+}
+
+static GatherArgs gather_args(const epfem_cache* c) {
+  GatherArgs g{};
+  g.n_nodes = c->info.n_nodes;
+  g.elem = c->elem;
+  g.n2e_ptr = c->pat.n2e_ptr;
+  g.n2e = c->pat.n2e;
+  g.slot = c->pat.slot;
+  g.nbr_ptr = c->pat.nbr_ptr;
+  g.inv = c->inv;
+  g.weight = c->weight;
+  g.gradhat = c->gradhat;
+  g.shear = c->shear;
+  g.bulk = c->bulk;
+  g.shear_u = c->shear_u;
+  g.bulk_u = c->bulk_u;
+  g.max_seg = c->info.dim * c->info.dim * c->info.max_row_nodes;
+  return g;
+}
+
+int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_material* mat,
+                      epfem_cache** out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!mesh || !mat || !out) return fail(EPFEM_ERR_INVALID, "build_assembly_cache: null argument");
+  *out = nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  HostTables tab;
+  if (!make_tables(mesh->family, mesh->dim, &tab))
+    return fail(EPFEM_ERR_INVALID, "invalid element type: family=" + std::to_string(mesh->family) +
+                                       ", dim=" + std::to_string(mesh->dim));
+  const int64_t n_int = mesh->n_elements * tab.nq;
+  if (mat->n_int != n_int)
+    return fail(EPFEM_ERR_INVALID, "build_assembly_cache: material field size mismatch");
+  if (mesh->n_nodes >= (int64_t)INT32_MAX / mesh->dim)
+    return fail(EPFEM_ERR_UNSUPPORTED, "build_assembly_cache: too many nodes for int32 columns");
+  cudaStream_t st = ctx->stream;
+  epfem_cache* c = new epfem_cache;
+  epfem_cache_info& I = c->info;
+  I.dim = mesh->dim;
+  I.family = mesh->family;
+  I.n_p = tab.np;
+  I.n_q = tab.nq;
+  I.n_strain = mesh->dim == 3 ? 6 : 3;
+  I.n_nodes = mesh->n_nodes;
+  I.n_elements = mesh->n_elements;
+  I.n_int = n_int;
+  I.n_dofs = mesh->n_nodes * mesh->dim;
+  auto bail = [&](int rc) {
+    epfem_cache_destroy(c);
+    return rc;
+  };
+#define CT(expr)                                          \
+  do {                                                    \
+    cudaError_t _e = (expr);                              \
+    if (_e != cudaSuccess) return bail(cuda_fail(_e, #expr)); \
+  } while (0)
+  const size_t tg = sizeof(double) * tab.nq * tab.np * tab.dim;
+  CT(cudaMalloc(&c->gradhat, tg));
+  CT(cudaMalloc(&c->wq, sizeof(double) * tab.nq));
+  CT(cudaMemcpyAsync(c->gradhat, tab.gradhat, tg, cudaMemcpyHostToDevice, st));
+  CT(cudaMemcpyAsync(c->wq, tab.weights, sizeof(double) * tab.nq, cudaMemcpyHostToDevice, st));
+  const size_t elem_bytes = sizeof(int32_t) * (size_t)tab.np * mesh->n_elements;
+  CT(cudaMalloc(&c->elem, std::max<size_t>(elem_bytes, 4)));
+  CT(cudaMemcpyAsync(c->elem, mesh->elem, elem_bytes, cudaMemcpyDeviceToDevice, st));
+  CT(cudaMalloc(&c->det, sizeof(double) * std::max<int64_t>(n_int, 1)));
+  CT(cudaMalloc(&c->weight, sizeof(double) * std::max<int64_t>(n_int, 1)));
+  CT(cudaMalloc(&c->inv, sizeof(double) * mesh->dim * mesh->dim * std::max<int64_t>(n_int, 1)));
+  // moduli snapshot
+  c->shear_u = mat->shear_u;
+  c->bulk_u = mat->bulk_u;
+  if (mat->shear) {
+    CT(cudaMalloc(&c->shear, sizeof(double) * n_int));
+    CT(cudaMemcpyAsync(c->shear, mat->shear, sizeof(double) * n_int, cudaMemcpyDeviceToDevice, st));
+  }
+  if (mat->bulk) {
+    CT(cudaMalloc(&c->bulk, sizeof(double) * n_int));
+    CT(cudaMemcpyAsync(c->bulk, mat->bulk, sizeof(double) * n_int, cudaMemcpyDeviceToDevice, st));
+  }
+  if (n_int > 0) {
+    if (int rc = launch_jacobians(I.family, I.dim, I.n_elements, c->elem, mesh->coord, c->gradhat,
+                                  c->wq, c->det, c->inv, c->weight, ctx->err, st, ctx->num_sms))
+      return bail(rc);
+    if (int rc = poll_device_error(ctx, "jacobians")) return bail(rc);
+  }
+  cudaEvent_t ev[3];
+  for (auto& e : ev) CT(cudaEventCreate(&e));
+  CT(cudaEventRecord(ev[0], st));
+  if (int rc = build_pattern(I.family, I.dim, I.n_nodes, I.n_elements, c->elem, st, ctx->num_sms, &c->pat))
+    return bail(rc);
+  CT(cudaEventRecord(ev[1], st));
+  I.nnz = c->pat.nnz;
+  I.max_row_nodes = c->pat.max_nbr;
+  CT(cudaMalloc(&c->K_elast, sizeof(double) * std::max<int64_t>(I.nnz, 1)));
+  GatherArgs g = gather_args(c);
+  g.out = c->K_elast;
+  if (int rc = launch_gather(I.family, I.dim, 0, g, st)) return bail(rc);
+  CT(cudaEventRecord(ev[2], st));
+  CT(cudaStreamSynchronize(st));
+  float ms_p = 0, ms_e = 0;
+  cudaEventElapsedTime(&ms_p, ev[0], ev[1]);
+  cudaEventElapsedTime(&ms_e, ev[1], ev[2]);
+  for (auto& e : ev) cudaEventDestroy(e);
+  I.pattern_seconds = ms_p * 1e-3;
+  I.elastic_seconds = ms_e * 1e-3;
+  I.build_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+#undef CT
+  *out = c;
+  return 0;
+}
+
+int epfem_cache_get_info(const epfem_cache* c, epfem_cache_info* info) {
+  if (!c || !info) return fail(EPFEM_ERR_INVALID, "null argument");
+  *info = c->info;
+  return 0;
+}
+
+int epfem_cache_pattern(const epfem_cache* c, const int64_t** row_ptr, const int32_t** col_idx) {
+  if (!c) return fail(EPFEM_ERR_INVALID, "null cache");
+  if (row_ptr) *row_ptr = c->pat.row_ptr;
+  if (col_idx) *col_idx = c->pat.col_idx;
+  return 0;
+}
+
+int epfem_cache_K_elast(const epfem_cache* c, const double** values) {
+  if (!c || !values) return fail(EPFEM_ERR_INVALID, "null argument");
+  *values = c->K_elast;
+  return 0;
+}
+
+int epfem_cache_geometry(const epfem_cache* c, const double** det, const double** weight,
+                         const double** inv) {
+  if (!c) return fail(EPFEM_ERR_INVALID, "null cache");
+  if (det) *det = c->det;
+  if (weight) *weight = c->weight;
+  if (inv) *inv = c->inv;
+  return 0;
+}
+
+int epfem_assemble_elastic(epfem_ctx* ctx, const epfem_cache* c, double* K_values) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!c || !K_values) return fail(EPFEM_ERR_INVALID, "assemble_elastic_stiffness: null argument");
+  GatherArgs g = gather_args(c);
+  g.out = K_values;
+  if (int rc = launch_gather(c->info.family, c->info.dim, 0, g, ctx->stream)) return rc;
+  return finish(ctx);
+}
+
+static int tangent_common(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int, const double* D,
+                          const uint8_t* flags, double* K_values, int mode) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
+  if (n_int != c->info.n_int) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: size mismatch");
+  if (!K_values || (n_int > 0 && (!D || !flags)))
+    return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null argument");
+  if (!aligned16(D)) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: D must be 16-byte aligned");
+  GatherArgs g = gather_args(c);
+  g.D = D;
+  g.flags = flags;
+  g.base = c->K_elast;
+  g.out = K_values;
+  if (int rc = launch_gather(c->info.family, c->info.dim, mode, g, ctx->stream)) return rc;
+  return finish(ctx);
+}
+
+int epfem_assemble_tangent(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int, const double* D,
+                           const uint8_t* flags, double* K_values) {
+  return tangent_common(ctx, c, n_int, D, flags, K_values, 1);
+}
+
+int epfem_assemble_tangent_ds(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int,
+                              const double* DS, const uint8_t* plastic_cols, double* K_values) {
+  return tangent_common(ctx, c, n_int, DS, plastic_cols, K_values, 2);
+}
+
+int epfem_strains(epfem_ctx* ctx, const epfem_cache* c, const double* u, double* E) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!c || !u || !E) return fail(EPFEM_ERR_INVALID, "strains: null argument");
+  if (!aligned16(E)) return fail(EPFEM_ERR_INVALID, "strains: E must be 16-byte aligned");
+  if (c->info.n_int == 0) return 0;
+  if (int rc = launch_strains(c->info.family, c->info.dim, c->info.n_elements, c->elem, c->inv,
+                              c->gradhat, u, E, ctx->stream, ctx->num_sms))
+    return rc;
+  return finish(ctx);
+}
+
+int epfem_internal_forces(epfem_ctx* ctx, const epfem_cache* c, const double* S, double* F) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!c || !S || !F) return fail(EPFEM_ERR_INVALID, "internal_forces: null argument");
+  if (c->info.n_nodes == 0) return 0;
+  if (int rc = launch_internal_forces(c->info.family, c->info.dim, c->info.n_nodes, c->pat.n2e_ptr,
+                                      c->pat.n2e, c->inv, c->weight, c->gradhat, S, F, ctx->stream,
+                                      ctx->num_sms))
+    return rc;
+  return finish(ctx);
+}
+
+}  // extern "C"

@@ -1,0 +1,81 @@
+// Kernel argument structs and launcher declarations shared by the .cu files.
+#pragma once
+
+#include "common.cuh"
+
+namespace epfem_gpu {
+
+// Kernel argument structs shared by the launchers and capi.cu.
+struct ConstArgs {
+  int64_t n;
+  const double* E;
+  const double* Ep;
+  const double* Hard;
+  const double* G;
+  const double* K;
+  const double* p1;
+  const double* p2;
+  double Gu, Ku, p1u, p2u;
+  double* S;
+  uint8_t* flags;
+  double* D;
+  double* DS;
+  double* Ep_out;
+  double* Hard_out;
+  uint8_t* pm;
+  uint8_t* sm;
+  uint8_t* am;
+  double* crit;
+  DevErr* err;
+};
+struct GatherArgs {
+  int64_t n_nodes;
+  const int32_t* elem;
+  const int64_t* n2e_ptr;
+  const int32_t* n2e;
+  const uint8_t* slot;
+  const int64_t* nbr_ptr;
+  const double* inv;
+  const double* weight;
+  const double* gradhat;
+  const double* shear;
+  const double* bulk;
+  double shear_u, bulk_u;
+  const double* D;
+  const uint8_t* flags;
+  const double* base;
+  double* out;
+  int max_seg;
+};
+struct PatternOut {
+  int64_t* n2e_ptr = nullptr;
+  int32_t* n2e = nullptr;
+  int64_t* nbr_ptr = nullptr;
+  int64_t* row_ptr = nullptr;
+  int32_t* col_idx = nullptr;
+  uint8_t* slot = nullptr;
+  int64_t nnz = 0;
+  int max_nbr = 0;
+};
+
+
+enum GatherMode { G_ELASTIC = 0, G_TANGENT_PACKED = 1, G_TANGENT_DS36 = 2 };
+
+int launch_constitutive(int model, const ConstArgs& a, cudaStream_t st, int num_sms);
+
+int launch_jacobians(int family, int dim, int64_t n_e, const int32_t* elem, const double* coord,
+                     const double* gradhat, const double* wq, double* det, double* inv,
+                     double* weight, DevErr* err, cudaStream_t st, int num_sms);
+int build_pattern(int family, int dim, int64_t n_nodes, int64_t n_e, const int32_t* elem,
+                  cudaStream_t st, int num_sms, PatternOut* o);
+int launch_gather(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);
+int launch_strains(int family, int dim, int64_t n_e, const int32_t* elem, const double* inv,
+                   const double* gradhat, const double* u, double* E, cudaStream_t st,
+                   int num_sms);
+int launch_internal_forces(int family, int dim, int64_t n_nodes, const int64_t* n2e_ptr,
+                           const int32_t* n2e, const double* inv, const double* weight,
+                           const double* gradhat, const double* S, double* F_out,
+                           cudaStream_t st, int num_sms);
+
+
+}  // namespace epfem_gpu

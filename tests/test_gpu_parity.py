@@ -1,0 +1,313 @@
+"""GPU parity: the C-ABI kernels against the pinned CPU oracle.
+
+Bar (BASELINE.json north_star):
+  * CSR pattern (row_ptr, col_idx) and plastic / smooth / apex flags bit-exact;
+  * K row-scaled |dK_ij| <= 1e-12 max_k |K_ref(i,k)|;
+  * S within 1e-12 of max(|sigma|_inf, yield); D within 1e-12 ||C||_max —
+    the constitutive kernel reproduces the oracle's operation order without
+    FMA, so S/D/Ep/Hard are in fact compared bit for bit;
+  * an all-elastic iteration returns K bitwise equal to K_elast.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import FAMILIES, GOLDEN, elastic_C, row_scaled_error, small_mesh, sym_block
+
+pytestmark = pytest.mark.gpu
+
+
+def _g(name):
+    return np.load(os.path.join(GOLDEN, name + ".npy"))
+
+
+def _t(a, dev, dtype=torch.float64):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dtype)
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _blocks(DS):
+    return DS.reshape(-1, 6, 6).transpose(0, 2, 1)
+
+
+# ---------------------------------------------------------------------------
+# K1 constitutive
+
+def test_vm_batch_bitwise_vs_oracle(cuda, oracle):
+    import paper_1805_04155_b200 as P
+    E, Ep, H = _g("vm_E"), _g("vm_Ep"), _g("vm_Hard")
+    G, K, a, Y = _g("vm_G"), _g("vm_K"), _g("vm_a"), _g("vm_Y")
+    ref = oracle.constitutive_vm(E, Ep, H, G, K, a, Y)
+    n = E.shape[0]
+    mat = P.MaterialField(n, _t(G, cuda), _t(K, cuda), P.VonMisesParams(_t(a, cuda), _t(Y, cuda)))
+    ev = P.constitutive_vm(_t(E, cuda), _t(Ep, cuda), _t(H, cuda), mat)
+    assert np.array_equal(_np(ev.plastic_mask).astype(np.uint8), ref["plastic"])
+    for k, got in (("S", ev.S), ("DS", ev.DS), ("Ep", ev.Ep), ("Hard", ev.Hard), ("crit", ev.crit)):
+        assert np.array_equal(_np(got), ref[k]), k
+    st = P.evaluate_constitutive(_t(E, cuda), P.IntegrationState(_t(E, cuda), _t(Ep, cuda), _t(H, cuda),
+                                 None, None, None, None, None), mat)
+    pl = ref["plastic"].astype(bool)
+    assert np.array_equal(_np(st.flags) & 1, ref["plastic"])
+    D = _np(P.unpack_D(st.D))[pl]
+    assert np.array_equal(D, ref["DS"][pl])
+
+
+def test_dp_batch_bitwise_vs_oracle(cuda, oracle):
+    import paper_1805_04155_b200 as P
+    E, Ep = _g("dp_E"), _g("dp_Ep")
+    G, K, eta, c = _g("dp_G"), _g("dp_K"), _g("dp_eta"), _g("dp_c")
+    ref = oracle.constitutive_dp(E, Ep, G, K, eta, c)
+    n = E.shape[0]
+    mat = P.MaterialField(n, _t(G, cuda), _t(K, cuda), P.DruckerPragerParams(_t(eta, cuda), _t(c, cuda)))
+    ev = P.constitutive_dp(_t(E, cuda), _t(Ep, cuda), mat)
+    assert np.array_equal(_np(ev.smooth_mask).astype(np.uint8), ref["smooth"])
+    assert np.array_equal(_np(ev.apex_mask).astype(np.uint8), ref["apex"])
+    for k, got in (("S", ev.S), ("DS", ev.DS), ("Ep", ev.Ep)):
+        assert np.array_equal(_np(got), ref[k]), k
+    prev = P.IntegrationState(_t(E, cuda), _t(Ep, cuda), torch.zeros((n, 6), dtype=torch.float64, device=cuda),
+                              None, None, None, None, None)
+    st = P.evaluate_constitutive(_t(E, cuda), prev, mat)
+    fl = _np(st.flags)
+    assert np.array_equal((fl >> 1) & 1, ref["smooth"]) and np.array_equal((fl >> 2) & 1, ref["apex"])
+    assert np.abs(_np(st.Hard)).max() == 0.0  # evaluate_constitutive keeps Hard = 0 for DP
+    pl = ref["plastic"].astype(bool)
+    assert np.array_equal(_np(P.unpack_D(st.D))[pl], ref["DS"][pl])
+
+
+def test_elastic_model_and_uniform_material(cuda, oracle):
+    import paper_1805_04155_b200 as P
+    E = np.random.default_rng(3).uniform(-1, 1, (777, 6))
+    K, G = 2.0, 1.5
+    ref = oracle.constitutive_elastic(E, G, K)
+    ev = P.constitutive_elastic(_t(E, cuda), P.uniform_elastic(777, K, G))
+    assert np.array_equal(_np(ev.S), ref["S"]) and np.array_equal(_np(ev.DS), ref["DS"])
+
+
+def test_constitutive_known_answers(cuda):
+    import paper_1805_04155_b200 as P
+    G, K, eta, c = 1.2, 2.1, 0.4, 0.6
+    E = torch.zeros((2, 6), dtype=torch.float64, device=cuda)
+    E[1, :3] = 10.0
+    ev = P.constitutive_dp(E, torch.zeros_like(E), P.uniform_drucker_prager(2, K, G, eta, c))
+    assert not bool(ev.apex_mask[0]) and bool(ev.apex_mask[1])
+    assert torch.allclose(ev.S[1, :3], torch.full((3,), c / eta, dtype=torch.float64, device=cuda), rtol=1e-13)
+    assert float(ev.DS[1].abs().max()) == 0.0
+    E = torch.zeros((1, 6), dtype=torch.float64, device=cuda)
+    E[0, 3] = 2.0
+    ev = P.constitutive_vm(E, torch.zeros_like(E), torch.zeros_like(E), P.uniform_von_mises(1, 1.7, 1.1, 0.0, 0.8))
+    assert bool(ev.plastic_mask[0]) and float(ev.Hard.abs().max()) == 0.0
+
+
+def test_constitutive_size_mismatch_raises(cuda):
+    import paper_1805_04155_b200 as P
+    E = torch.zeros((4, 6), dtype=torch.float64, device=cuda)
+    with pytest.raises(P.Error, match="constitutive_vm: size mismatch"):
+        P.constitutive_vm(E, E[:3], E, P.uniform_von_mises(4, 1, 1, 0, 1))
+
+
+# ---------------------------------------------------------------------------
+# assembly, all eight element types
+
+def _caches(cuda, oracle, family, dim, young=10.0, nu=0.3):
+    import paper_1805_04155_b200 as P
+    coord, elem = small_mesh(oracle, family, dim)
+    K, G = oracle.elastic_moduli(young, nu)
+    ocache = oracle.Cache(family, dim, coord, elem, G, K)
+    mesh = P.Mesh(P.ElementType(family, dim), _t(coord, cuda), _t(elem, cuda, torch.int32))
+    gcache = P.build_assembly_cache(mesh, P.uniform_elastic(ocache.n_int, K, G))
+    return ocache, gcache, K, G
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("family", FAMILIES)
+def test_pattern_and_elastic_stiffness(cuda, oracle, family, dim):
+    import paper_1805_04155_b200 as P
+    oc, gc, K, G = _caches(cuda, oracle, family, dim)
+    ref = oc.K_elast()
+    assert gc.nnz == ref.nnz
+    assert np.array_equal(_np(gc.row_ptr), ref.indptr)
+    assert np.array_equal(_np(gc.col_idx), ref.indices)
+    kel = _np(gc.K_elast.values)
+    assert row_scaled_error(kel, ref.data, ref.indptr) <= 1e-12
+    # recomputed elastic assembly is deterministic
+    again = _np(P.assemble_elastic_stiffness(gc).values)
+    assert np.array_equal(again.view(np.uint64), kel.view(np.uint64))
+    det, w, inv = oc.arrays()
+    gdet, ginv = gc.jac
+    assert np.abs(_np(gdet) - det).max() <= 1e-13 * np.abs(det).max()
+    assert np.abs(_np(gc.weight) - w).max() <= 1e-13 * np.abs(w).max()
+    assert np.abs(_np(ginv) - inv).max() <= 1e-12 * np.abs(inv).max()
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("family", FAMILIES)
+def test_tangent_matches_oracle(cuda, oracle, family, dim):
+    import paper_1805_04155_b200 as P
+    oc, gc, K, G = _caches(cuda, oracle, family, dim, 5.0, 0.2)
+    rng = np.random.default_rng(41)
+    C = elastic_C(K, G)
+    n = oc.n_int
+    kel = _np(gc.K_elast.values)
+    for frac in (0.0, 0.5, 1.0):
+        pl = (rng.uniform(size=n) < frac).astype(np.uint8)
+        D = np.stack([C + 0.3 * sym_block(rng) if p else C for p in pl])
+        DS = D.transpose(0, 2, 1).reshape(n, 36).copy()
+        ref = oc.tangent(DS, pl)
+        got = P.assemble_tangent_stiffness(gc, _t(DS, cuda), _t(pl, cuda, torch.uint8).bool())
+        gv = _np(got.values)
+        assert row_scaled_error(gv, ref.data, ref.indptr) <= 1e-12, frac
+        # packed hot-path layout
+        Dp = np.zeros((n, 24))
+        from paper_1805_04155_b200._lib import D_COL, D_ROW
+        Dp[:, :21] = D[:, D_ROW, D_COL]
+        gp = _np(P.assemble_tangent_packed(gc, _t(Dp, cuda), _t(pl, cuda, torch.uint8)).values)
+        assert np.array_equal(gp.view(np.uint64), gv.view(np.uint64))
+        if frac == 0.0:
+            assert np.array_equal(gv.view(np.uint64), kel.view(np.uint64))
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("family", FAMILIES)
+def test_strains_and_internal_forces(cuda, oracle, family, dim):
+    import paper_1805_04155_b200 as P
+    oc, gc, K, G = _caches(cuda, oracle, family, dim, 3.0, 0.3)
+    u = np.random.default_rng(43).uniform(-1, 1, oc.n_dofs)
+    E_ref = oc.strains(u)
+    E = _np(gc.strains(_t(u, cuda)))
+    assert np.abs(E - E_ref).max() <= 1e-12 * np.abs(E_ref).max()
+    S = oracle.constitutive_elastic(E_ref, G, K)["S"]
+    F_ref = oc.internal_forces(S)
+    F = _np(P.internal_forces(gc, _t(S, cuda)))
+    assert np.abs(F - F_ref).max() <= 1e-12 * np.abs(F_ref).max()
+
+
+def test_degenerate_element_reported(cuda):
+    import paper_1805_04155_b200 as P
+    coord = torch.tensor([[0, 0, 0], [1, 0, 0], [0, 1, 0], [1, 1, 0.0]], dtype=torch.float64, device=cuda)
+    elem = torch.tensor([[0, 1, 2, 3]], dtype=torch.int32, device=cuda)
+    with pytest.raises(P.Error, match="jacobians: nonpositive det J in element 0"):
+        P.build_assembly_cache(P.Mesh(P.ElementType("P1", 3), coord, elem), P.uniform_elastic(1, 1.0, 1.0))
+
+
+def test_tangent_size_mismatch(cuda, oracle):
+    import paper_1805_04155_b200 as P
+    oc, gc, K, G = _caches(cuda, oracle, "Q1", 2)
+    DS = torch.zeros((gc.n_int - 1, 36), dtype=torch.float64, device=cuda)
+    with pytest.raises(P.Error, match="assemble_tangent_stiffness: size mismatch"):
+        P.assemble_tangent_stiffness(gc, DS, torch.zeros(gc.n_int - 1, dtype=torch.bool, device=cuda))
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configurations: full hot path on reduced meshes vs the oracle's
+# reference-algorithm pipeline (evaluate_constitutive + assemble_tangent_stiffness)
+
+REDUCED = {"cfg1": 16, "cfg2": 24, "cfg3": 5, "cfg4": 8, "cfg5": 5}
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+def test_config_pipeline_vs_oracle(cuda, oracle, name):
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.synthetic import CONFIGS, displacement
+    cfg = CONFIGS[name]
+    n = REDUCED[name]
+    mesh = cfg.mesh(n)
+    mat = cfg.material(mesh.n_int)
+    K, G = P.elastic_moduli(cfg.young, cfg.poisson)
+    oc = oracle.Cache(cfg.family, cfg.dim, mesh.coord, mesh.elem, G, K)
+    gc = P.build_assembly_cache(P.Mesh.from_structured(mesh, cuda), mat)
+    assert np.array_equal(_np(gc.row_ptr), oc.K_elast().indptr)
+    assert np.array_equal(_np(gc.col_idx), oc.K_elast().indices)
+    u = displacement(mesh.coord, cfg.seed)
+    E1 = oc.strains(u)
+    if cfg.model == "elastic":
+        assert row_scaled_error(_np(gc.K_elast.values), oc.K_elast().data, oc.K_elast().indptr) <= 1e-12
+        return
+    # scale so that a fraction of points yields (oracle decides, same E bytes to both)
+    if cfg.model == "vm":
+        crit = oracle.constitutive_vm(E1, None, None, G, K, cfg.p1, 0.0)["crit"]  # |s_tr| at Y=0
+        s = cfg.p2 / np.quantile(crit, 1.0 - cfg.target)
+    else:
+        eta, c = P.dp_parameters(cfg.p1, cfg.p2)
+        s = 1.0
+        for _ in range(60):
+            f = oracle.constitutive_dp(s * E1, None, G, K, eta, c)["plastic"].mean()
+            s *= 1.3 if f < cfg.target else 0.8
+            if abs(f - cfg.target) < 0.05:
+                break
+    E = s * E1
+    if cfg.model == "vm":
+        ref = oracle.constitutive_vm(E, None, None, G, K, cfg.p1, cfg.p2)
+    else:
+        eta, c = P.dp_parameters(cfg.p1, cfg.p2)
+        ref = oracle.constitutive_dp(E, None, G, K, eta, c)
+    pl = ref["plastic"]
+    assert 0 < pl.sum() < pl.size
+    Kref = oc.tangent(ref["DS"], pl)
+    eng = P.TangentEngine(gc, mat)
+    Et = _t(E, cuda)
+    S, flags, D, Kv = eng.step(Et)
+    eng.sync()
+    assert np.array_equal(_np(flags) & 1, pl)
+    if cfg.model == "dp":
+        assert np.array_equal((_np(flags) >> 1) & 1, ref["smooth"])
+        assert np.array_equal((_np(flags) >> 2) & 1, ref["apex"])
+    assert np.array_equal(_np(S), ref["S"])
+    m = pl.astype(bool)
+    assert np.array_equal(_np(P.unpack_D(D))[m], ref["DS"][m])
+    assert row_scaled_error(_np(Kv), Kref.data, Kref.indptr) <= 1e-12
+    # CUDA-graph replay gives the same bits
+    eng.capture(Et)
+    eng.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(_np(eng.K).view(np.uint64), _np(Kv).view(np.uint64))
+
+
+# ---------------------------------------------------------------------------
+# full-size configurations: size-independent properties
+
+FULL_NNZ = {"cfg1": 1_841_156, "cfg2": 49_315_844, "cfg3": 547_739_145,
+            "cfg4": 1_001_561_769, "cfg5": 2_118_711_609}
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+def test_full_size_pattern_and_properties(cuda, name):
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.synthetic import CONFIGS, make_workload
+    cfg = CONFIGS[name]
+    target = {"cfg4": 0.25, "cfg5": 0.5}.get(name)
+    wl = make_workload(cfg, target=target, device=cuda)
+    gc = wl.cache
+    assert gc.nnz == FULL_NNZ[name]
+    rp = gc.row_ptr
+    assert int(rp[0]) == 0 and int(rp[-1]) == gc.nnz and bool((rp[1:] >= rp[:-1]).all())
+    # columns sorted ascending within each row
+    ci = gc.col_idx.long()
+    starts = torch.zeros(gc.nnz, dtype=torch.bool, device=cuda)
+    starts[rp[:-1].clamp(max=gc.nnz - 1)] = True
+    assert bool(((ci[1:] > ci[:-1]) | starts[1:]).all())
+    # rigid translation in the nullspace of K_elast; K_elast symmetric
+    Kel = gc.K_elast
+    scale = float(Kel.values.abs().max())
+    ones = torch.ones(gc.info.n_dofs, dtype=torch.float64, device=cuda)
+    assert float(Kel.matvec(ones).abs().max()) <= 1e-9 * scale
+    x = torch.randn(gc.info.n_dofs, dtype=torch.float64, device=cuda)
+    y = torch.randn(gc.info.n_dofs, dtype=torch.float64, device=cuda)
+    lhs, rhs = float(y @ Kel.matvec(x)), float(x @ Kel.matvec(y))
+    assert abs(lhs - rhs) <= 1e-9 * max(abs(lhs), 1.0)
+    if cfg.model == "elastic":
+        return
+    eng = P.TangentEngine(gc, wl.mat)
+    S, flags, D, Kv = eng.step(wl.E)
+    eng.sync()
+    frac = float((flags & 1).double().mean())
+    assert abs(frac - wl.fraction) < 1e-12
+    # tangent symmetric too, and rows without plastic neighbours equal K_elast bitwise
+    Kt = P.CsrMatrix(gc.row_ptr, gc.col_idx, Kv)
+    lhs, rhs = float(y @ Kt.matvec(x)), float(x @ Kt.matvec(y))
+    assert abs(lhs - rhs) <= 1e-9 * max(abs(lhs), 1.0)
