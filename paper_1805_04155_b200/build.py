@@ -29,6 +29,7 @@ NVCC_COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
 SOURCES = {
     "constitutive.cu": ["--fmad=false"],
     "assembly.cu": [],
+    "tangent.cu": [],
     "capi.cu": [],
     "tables.cpp": [],
 }

@@ -48,6 +48,8 @@ struct epfem_cache {
   double shear_u = 0, bulk_u = 0;
   PatternOut pat;
   double* K_elast = nullptr;
+  double* scratch = nullptr;  // tangent workspace (symmetric dK_e per element)
+  unsigned* emask = nullptr;  // per-element plastic-point bitmask
 };
 
 namespace {
@@ -209,7 +211,8 @@ int epfem_cache_destroy(epfem_cache* c) {
   if (!c) return 0;
   void* ptrs[] = {c->gradhat, c->wq,          c->elem,        c->det,          c->inv,
                   c->weight,  c->shear,       c->bulk,        c->pat.n2e_ptr,  c->pat.n2e,
-                  c->pat.nbr_ptr, c->pat.row_ptr, c->pat.col_idx, c->pat.slot, c->K_elast};
+                  c->pat.nbr_ptr, c->pat.row_ptr, c->pat.col_idx, c->pat.slot, c->K_elast,
+                  c->scratch, c->emask};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -232,6 +235,9 @@ static GatherArgs gather_args(const epfem_cache* c) {
   g.shear_u = c->shear_u;
   g.bulk_u = c->bulk_u;
   g.max_seg = c->info.dim * c->info.dim * c->info.max_row_nodes;
+  g.n_elements = c->info.n_elements;
+  g.scratch = c->scratch;
+  g.emask = c->emask;
   return g;
 }
 
@@ -308,6 +314,9 @@ int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_materi
   I.nnz = c->pat.nnz;
   I.max_row_nodes = c->pat.max_nbr;
   CT(cudaMalloc(&c->K_elast, sizeof(double) * std::max<int64_t>(I.nnz, 1)));
+  CT(cudaMalloc(&c->scratch, sizeof(double) * std::max<size_t>(
+                                 tangent_workspace_doubles(I.family, I.dim, I.n_elements), 1)));
+  CT(cudaMalloc(&c->emask, sizeof(unsigned) * std::max<int64_t>(I.n_elements, 1)));
   GatherArgs g = gather_args(c);
   g.out = c->K_elast;
   if (int rc = launch_gather(I.family, I.dim, 0, g, st)) return bail(rc);
@@ -376,7 +385,7 @@ static int tangent_common(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int, c
   g.flags = flags;
   g.base = c->K_elast;
   g.out = K_values;
-  if (int rc = launch_gather(c->info.family, c->info.dim, mode, g, ctx->stream)) return rc;
+  if (int rc = launch_tangent(c->info.family, c->info.dim, mode, g, ctx->stream)) return rc;
   return finish(ctx);
 }
 

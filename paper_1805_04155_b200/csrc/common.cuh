@@ -65,6 +65,14 @@ __host__ __device__ constexpr int pk_index(int i, int j) {
   return T[i][j];
 }
 
+#ifdef __CUDACC__
+// Same table for runtime (non-unrolled) indices: constant bank, no local memory.
+static __constant__ signed char c_pk_table[36] = {0, 1, 6,  2,  7,  8,  1, 3,  9,  4,  10, 11,
+                                                  6, 9, 12, 13, 14, 15, 2, 4,  13, 5,  16, 17,
+                                                  7, 10, 14, 16, 18, 19, 8, 11, 15, 17, 19, 20};
+__device__ __forceinline__ int pk_index_rt(int i, int j) { return c_pk_table[i * 6 + j]; }
+#endif
+
 // Latched device-side error word owned by a context.
 struct DevErr {
   int code;            // first epfem_status raised on device (0 = none)

@@ -46,6 +46,9 @@ struct GatherArgs {
   const double* base;
   double* out;
   int max_seg;
+  int64_t n_elements;
+  double* scratch;   // tangent workspace: symmetric dK_e per element
+  unsigned* emask;   // per-element plastic-point bitmask
 };
 struct PatternOut {
   int64_t* n2e_ptr = nullptr;
@@ -69,6 +72,8 @@ int launch_jacobians(int family, int dim, int64_t n_e, const int32_t* elem, cons
 int build_pattern(int family, int dim, int64_t n_nodes, int64_t n_e, const int32_t* elem,
                   cudaStream_t st, int num_sms, PatternOut* o);
 int launch_gather(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);
+int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);
+size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements);
 int launch_strains(int family, int dim, int64_t n_e, const int32_t* elem, const double* inv,
                    const double* gradhat, const double* u, double* E, cudaStream_t st,
                    int num_sms);
