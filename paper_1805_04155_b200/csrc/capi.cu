@@ -50,6 +50,7 @@ struct epfem_cache {
   double* K_elast = nullptr;
   double* scratch = nullptr;  // tangent workspace (symmetric dK_e per element)
   unsigned* emask = nullptr;  // per-element plastic-point bitmask
+  int npc = 64, max_span = 0; // row-stream plan
 };
 
 namespace {
@@ -238,6 +239,15 @@ static GatherArgs gather_args(const epfem_cache* c) {
   g.n_elements = c->info.n_elements;
   g.scratch = c->scratch;
   g.emask = c->emask;
+  g.npc = c->npc;
+  g.max_span = c->max_span;
+  // packed elastic operator C = K VOL + 2G DEV (voigt.hpp:72-74) for a uniform material
+  for (int i = 0; i < 6; ++i)
+    for (int j = i; j < 6; ++j) {
+      const double vol = (i < 3 && j < 3) ? 1.0 : 0.0;
+      const double dev = ((i == j) ? (i < 3 ? 1.0 : 0.5) : 0.0) - vol / 3.0;
+      g.Cu[pk_index(i, j)] = c->bulk_u * vol + 2.0 * c->shear_u * dev;
+    }
   return g;
 }
 
@@ -317,6 +327,9 @@ int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_materi
   CT(cudaMalloc(&c->scratch, sizeof(double) * std::max<size_t>(
                                  tangent_workspace_doubles(I.family, I.dim, I.n_elements), 1)));
   CT(cudaMalloc(&c->emask, sizeof(unsigned) * std::max<int64_t>(I.n_elements, 1)));
+  if (I.n_nodes > 0)
+    if (int rc = plan_row_stream(I.n_nodes, I.dim, c->pat.nbr_ptr, st, &c->npc, &c->max_span))
+      return bail(rc);
   GatherArgs g = gather_args(c);
   g.out = c->K_elast;
   if (int rc = launch_gather(I.family, I.dim, 0, g, st)) return bail(rc);

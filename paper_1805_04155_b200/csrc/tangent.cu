@@ -1,22 +1,26 @@
 // K2 + K6: the per-iteration tangent  K = K_elast + sum_{plastic q} B_q^T w_q (D_q - C_q) B_q
 // (assembly.cpp:262-289), as two deterministic passes without atomics.
 //
-// Pass 1, k_elem_delta (element-centric, one thread per symmetric node-pair
-// block (a <= b) of an element): for every element with at least one plastic
-// integration point, the per-point work is done ONCE per (element, point):
-// dphi_p = J^-1 ghat_p for all nodes, Dw = w (D - C) (reduced to the plane-
-// strain rows in 2D), T_a = B_a^T Dw for all nodes, then each thread adds
-// T_a B_b to its block in registers.  The symmetric element matrix dK_e
-// (NB = NP(NP+1)/2 blocks of dim x dim) goes to a per-element workspace
-// record, and the element's plastic-point bitmask to emask[e].  Elements with
-// no plastic point write only their (zero) mask.
+// Pass 1, k_elem_delta (element-centric; one thread per symmetric node-pair
+// block (a <= b) of an element, several elements per CTA).  For every element
+// with at least one plastic integration point the per-point work is done ONCE
+// per (element, point) and shared through shared memory:
+//     dphi_p = J^-1 ghat_p            (all nodes)
+//     Dw     = w (D - C)              (plane-strain rows {0,1,3} in 2D)
+//     T_p    = B_p^T Dw               (all nodes)
+//     block(a,b) += T_a B_b           (each thread, in registers)
+// The symmetric element matrix dK_e (NB = NP(NP+1)/2 blocks of dim x dim)
+// goes to a per-element workspace record and the element's plastic-point
+// bitmask to emask[e].  Shared buffers are double-buffered on the point
+// index, so a point costs two CTA barriers.
 //
-// Pass 2, k_row_gather (row-centric, one warp per node a = the contiguous
-// value segment of its dim rows): the warp reads emask of the node's items;
-// with none plastic it copies K_elast[seg] -> K[seg] bitwise; otherwise it
-// adds every plastic item's block row a of dK_e (transposed blocks for b < a)
-// into a shared-memory image of the segment at the cached slots, then streams
-// K[seg] = K_elast[seg] + image.
+// Pass 2, k_row_stream (row-centric; one CTA per range of NPC consecutive
+// nodes = one contiguous value range of K, because a node's dim rows are
+// contiguous and nodes are numbered in row order).  The CTA streams
+// K_elast[range] into a shared-memory image, each warp adds the plastic
+// items' block rows of dK_e for its nodes at the cached slots (one warp per
+// node: no two writers per row), and the image is streamed out to K[range].
+// Rows without plastic contributions are copied bitwise.
 #include "kernels.cuh"
 
 namespace epfem_gpu {
@@ -28,156 +32,150 @@ __host__ __device__ constexpr int blk_index(int a, int b) {  // a <= b
   return a * (2 * NP - a + 1) / 2 + (b - a);
 }
 
-__device__ __forceinline__ double t_iota(int i) { return i < 3 ? 1.0 : 0.0; }
-__device__ __forceinline__ double t_dev(int i, int j) {
-  return ((i == j) ? (i < 3 ? 1.0 : 0.5) : 0.0) - t_iota(i) * t_iota(j) / 3.0;
-}
-__device__ __forceinline__ double t_cel(double K, double G, int i, int j) {
-  return K * (t_iota(i) * t_iota(j)) + 2.0 * G * t_dev(i, j);
-}
+// Voigt operators as constant tables for runtime indices (voigt.hpp:49-74).
+static __constant__ double c_vol[36] = {1, 1, 1, 0, 0, 0, 1, 1, 1, 0, 0, 0, 1, 1, 1, 0, 0, 0,
+                                        0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+static __constant__ double c_dev[36] = {
+    1.0 - 1.0 / 3.0, -1.0 / 3.0, -1.0 / 3.0, 0, 0, 0, -1.0 / 3.0, 1.0 - 1.0 / 3.0, -1.0 / 3.0, 0,
+    0, 0, -1.0 / 3.0, -1.0 / 3.0, 1.0 - 1.0 / 3.0, 0, 0, 0, 0, 0, 0, 0.5, 0, 0, 0, 0, 0, 0, 0.5,
+    0, 0, 0, 0, 0, 0, 0.5};
 
 constexpr int kDeltaThreads = 256;
 
 template <int DIM, int NP, int NQ, int MODE>
 __global__ void __launch_bounds__(kDeltaThreads) k_elem_delta(GatherArgs a) {
   constexpr int NS = DIM == 3 ? 6 : 3;
-  constexpr int NSP = NS * (NS + 1) / 2;
   constexpr int NB = NP * (NP + 1) / 2;
   constexpr int EPB = NB >= kDeltaThreads ? 1 : kDeltaThreads / NB;  // elements per CTA
-  constexpr int R[6] = {0, 1, DIM == 3 ? 2 : 3, 3, 4, 5};          // assembly rows
-  __shared__ double s_dphi[EPB][NP][DIM];
-  __shared__ double s_dw[EPB][NSP];
-  __shared__ double s_T[EPB][NP][DIM][NS];
+  static_assert(NB >= NP + NS, "phase-1 thread mapping");
+  __shared__ double s_dphi[2][EPB][NP][DIM];
+  __shared__ double s_dw[2][EPB][NS][NS];
+  __shared__ double s_T[2][EPB][NP][DIM][NS];
   __shared__ double s_ghat[NQ * NP * DIM];
   __shared__ unsigned s_mask[EPB];
-  __shared__ int s_any;
+  __shared__ unsigned s_union;
 
   const int tid = threadIdx.x;
-  const int le = tid / NB;           // local element
-  const int t = tid - le * NB;       // block index inside the element
+  const int le = tid / NB;        // local element
+  const int t = tid - le * NB;    // block index inside the element
   const int64_t e = (int64_t)blockIdx.x * EPB + le;
   const bool live = le < EPB && e < a.n_elements;
 
-  for (int k = tid; k < NQ * NP * DIM; k += blockDim.x) s_ghat[k] = __ldg(a.gradhat + k);
   if (tid < EPB) s_mask[tid] = 0u;
-  if (tid == 0) s_any = 0;
+  if (tid == 0) s_union = 0u;
   __syncthreads();
-  // plastic-point bitmask of each element
   for (int k = tid; k < EPB * NQ; k += blockDim.x) {
     const int l = k / NQ, q = k - l * NQ;
     const int64_t el = (int64_t)blockIdx.x * EPB + l;
     if (el < a.n_elements && (__ldg(a.flags + el * NQ + q) & 1)) {
       atomicOr(&s_mask[l], 1u << q);
-      s_any = 1;
+      atomicOr(&s_union, 1u << q);
     }
   }
+  for (int k = tid; k < NQ * NP * DIM; k += blockDim.x) s_ghat[k] = __ldg(a.gradhat + k);
   __syncthreads();
   if (tid < EPB) {
     const int64_t el = (int64_t)blockIdx.x * EPB + tid;
     if (el < a.n_elements) a.emask[el] = s_mask[tid];
   }
-  if (!s_any) return;  // CTA-uniform
+  unsigned todo = s_union;  // CTA-uniform
+  if (!todo) return;
 
-  // this thread's block (pa, pb), pa <= pb
-  int pa = 0, pb = 0;
-  {
-    int r = t;
-    while (pa < NP && r >= NP - pa) {
-      r -= NP - pa;
-      ++pa;
-    }
-    pb = pa + r;
+  int pa = 0, r = t;  // this thread's block (pa, pb), pa <= pb
+  while (pa < NP - 1 && r >= NP - pa) {
+    r -= NP - pa;
+    ++pa;
   }
+  const int pb = pa + r;
   const unsigned mask = live ? s_mask[le] : 0u;
+  const bool uniform_c = a.shear == nullptr && a.bulk == nullptr;
   double blk[DIM][DIM];
 #pragma unroll
   for (int i = 0; i < DIM; ++i)
 #pragma unroll
     for (int j = 0; j < DIM; ++j) blk[i][j] = 0.0;
 
-  const double Gu = a.shear_u, Ku = a.bulk_u;
-  for (int q = 0; q < NQ; ++q) {
+  int buf = 0;
+  while (todo) {
+    const int q = __ffs(todo) - 1;
+    todo &= todo - 1u;
     const bool on = (mask >> q) & 1u;
     const int64_t m = e * NQ + q;
-    // phase 1: geometry and effective material block
+    // phase 1: geometry (threads 0..NP-1) and one row of Dw per thread (NP..NP+NS-1)
     if (on) {
       if (t < NP) {
         const double* Ji = a.inv + m * DIM * DIM;
         double J[DIM * DIM];
 #pragma unroll
         for (int k = 0; k < DIM * DIM; ++k) J[k] = __ldg(Ji + k);
+        const double* g = s_ghat + (q * NP + t) * DIM;
 #pragma unroll
         for (int i = 0; i < DIM; ++i) {
           double s = 0.0;
 #pragma unroll
-          for (int j = 0; j < DIM; ++j) s += J[j * DIM + i] * s_ghat[(q * NP + t) * DIM + j];
-          s_dphi[le][t][i] = s;
+          for (int j = 0; j < DIM; ++j) s += J[j * DIM + i] * g[j];
+          s_dphi[buf][le][t][i] = s;
         }
-      }
-      for (int k = t; k < NSP; k += NB) {
-        // k -> (r, c), r <= c, row-major upper triangle of the NS x NS block
-        int r = 0, rem = k;
-        while (rem >= NS - r) {
-          rem -= NS - r;
-          ++r;
+      } else if (t < NP + NS) {
+        const int rr = t - NP;
+        const int ri = (DIM == 2 && rr == 2) ? 3 : rr;  // assembly row -> Voigt row
+        const double w = __ldg(a.weight + m);
+        double G2 = 0.0, Km = 0.0;
+        if (!uniform_c) {
+          G2 = 2.0 * (a.shear ? __ldg(a.shear + m) : a.shear_u);
+          Km = a.bulk ? __ldg(a.bulk + m) : a.bulk_u;
         }
-        const int c = r + rem;
-        const int ri = R[r], ci = R[c];
-        const double Gm = a.shear ? __ldg(a.shear + m) : Gu;
-        const double Km = a.bulk ? __ldg(a.bulk + m) : Ku;
-        double d;
-        if (MODE == G_TANGENT_PACKED) d = __ldg(a.D + m * EPFEM_D_STRIDE + pk_index_rt(ri, ci));
-        else d = __ldg(a.D + m * 36 + ci * 6 + ri);
-        s_dw[le][k] = __ldg(a.weight + m) * (d - t_cel(Km, Gm, ri, ci));
-      }
-    }
-    __syncthreads();
-    // phase 2: T_p = B_p^T Dw for every node p
-    if (on) {
-      for (int k = t; k < NP * DIM; k += NB) {
-        const int p = k / DIM, i = k - p * DIM;
-        const double* g = s_dphi[le][p];
-        auto Dw = [&](int r, int c) {
-          const int lo = r < c ? r : c, hi = r < c ? c : r;
-          return s_dw[le][lo * NS - lo * (lo - 1) / 2 + (hi - lo)];
-        };
 #pragma unroll
         for (int c = 0; c < NS; ++c) {
-          double v;
-          if constexpr (DIM == 3) {
-            // B rows e11,e22,e33,2e12,2e23,2e31 (assembly.cpp:162-171)
-            if (i == 0) v = g[0] * Dw(0, c) + g[1] * Dw(3, c) + g[2] * Dw(5, c);
-            else if (i == 1) v = g[1] * Dw(1, c) + g[0] * Dw(3, c) + g[2] * Dw(4, c);
-            else v = g[2] * Dw(2, c) + g[1] * Dw(4, c) + g[0] * Dw(5, c);
-          } else {
-            // rows e11, e22, 2e12 (assembly.cpp:173-176)
-            if (i == 0) v = g[0] * Dw(0, c) + g[1] * Dw(2, c);
-            else v = g[1] * Dw(1, c) + g[0] * Dw(2, c);
-          }
-          s_T[le][p][i][c] = v;
+          const int ci = (DIM == 2 && c == 2) ? 3 : c;
+          const double d = MODE == G_TANGENT_PACKED
+                               ? __ldg(a.D + m * EPFEM_D_STRIDE + pk_index_rt(ri, ci))
+                               : __ldg(a.D + m * 36 + ci * 6 + ri);
+          const double cel = uniform_c ? a.Cu[pk_index_rt(ri, ci)]
+                                       : Km * c_vol[ri * 6 + ci] + G2 * c_dev[ri * 6 + ci];
+          s_dw[buf][le][rr][c] = w * (d - cel);
         }
       }
     }
     __syncthreads();
-    // phase 3: block (pa, pb) += T_pa B_pb
+    // phase 2: T_p = B_p^T Dw, thread <-> (p, column c)
+    if (on) {
+      for (int k = t; k < NP * NS; k += NB) {
+        const int p = k / NS, c = k - p * NS;
+        const double* g = s_dphi[buf][le][p];
+        double(*Dw)[NS] = s_dw[buf][le];
+        if constexpr (DIM == 3) {
+          // B rows e11,e22,e33,2e12,2e23,2e31 (assembly.cpp:162-171)
+          s_T[buf][le][p][0][c] = g[0] * Dw[0][c] + g[1] * Dw[3][c] + g[2] * Dw[5][c];
+          s_T[buf][le][p][1][c] = g[1] * Dw[1][c] + g[0] * Dw[3][c] + g[2] * Dw[4][c];
+          s_T[buf][le][p][2][c] = g[2] * Dw[2][c] + g[1] * Dw[4][c] + g[0] * Dw[5][c];
+        } else {
+          // rows e11, e22, 2e12 (assembly.cpp:173-176)
+          s_T[buf][le][p][0][c] = g[0] * Dw[0][c] + g[1] * Dw[2][c];
+          s_T[buf][le][p][1][c] = g[1] * Dw[1][c] + g[0] * Dw[2][c];
+        }
+      }
+    }
+    __syncthreads();
+    // phase 3: block (pa, pb) += T_pa B_pb.  The next point writes the other
+    // buffer, so no barrier is needed before it.
     if (on && live) {
-      const double* h = s_dphi[le][pb];
+      const double* h = s_dphi[buf][le][pb];
+      const double h0 = h[0], h1 = h[1], h2 = DIM == 3 ? h[DIM - 1] : 0.0;
 #pragma unroll
       for (int i = 0; i < DIM; ++i) {
-        const double* T = s_T[le][pa][i];
+        const double* T = s_T[buf][le][pa][i];
         if constexpr (DIM == 3) {
-          blk[i][0] += T[0] * h[0] + T[3] * h[1] + T[5] * h[2];
-          blk[i][1] += T[1] * h[1] + T[3] * h[0] + T[4] * h[2];
-          blk[i][2] += T[2] * h[2] + T[4] * h[1] + T[5] * h[0];
+          blk[i][0] += T[0] * h0 + T[3] * h1 + T[5] * h2;
+          blk[i][1] += T[1] * h1 + T[3] * h0 + T[4] * h2;
+          blk[i][DIM - 1] += T[2] * h2 + T[4] * h1 + T[5] * h0;
         } else {
-          blk[i][0] += T[0] * h[0] + T[2] * h[1];
-          blk[i][1] += T[1] * h[1] + T[2] * h[0];
+          blk[i][0] += T[0] * h0 + T[2] * h1;
+          blk[i][1] += T[1] * h1 + T[2] * h0;
         }
       }
     }
-    // the next iteration's phase 1 rewrites s_dphi/s_dw only after this
-    // barrier, so phase 3 readers are done
-    __syncthreads();
+    buf ^= 1;
   }
   if (live && mask) {
     double* out = a.scratch + ((size_t)e * NB + t) * DIM * DIM;
@@ -188,67 +186,97 @@ __global__ void __launch_bounds__(kDeltaThreads) k_elem_delta(GatherArgs a) {
   }
 }
 
-constexpr int kRowWarps = 8;
+constexpr int kStreamThreads = 256;
+
+// Stream n doubles src -> dst (either may be smem), 16-byte vectors when the
+// two addresses share alignment.
+__device__ __forceinline__ void stream_copy(double* __restrict__ dst, const double* __restrict__ src,
+                                            int n, int tid, int nthreads) {
+  const bool same = (((uintptr_t)dst ^ (uintptr_t)src) & 15u) == 0;
+  if (same) {
+    const int head = (((uintptr_t)src & 15u) != 0) ? 1 : 0;
+    if (tid == 0 && head && n > 0) dst[0] = src[0];
+    const int nv = (n - head) / 2;
+    const double2* s2 = reinterpret_cast<const double2*>(src + head);
+    double2* d2 = reinterpret_cast<double2*>(dst + head);
+    for (int k = tid; k < nv; k += nthreads) d2[k] = s2[k];
+    const int tail = head + 2 * nv;
+    if (tid == 0 && tail < n) dst[tail] = src[tail];
+  } else {
+    for (int k = tid; k < n; k += nthreads) dst[k] = src[k];
+  }
+}
 
 template <int DIM, int NP, int NQ>
-__global__ void __launch_bounds__(32 * kRowWarps) k_row_gather(GatherArgs a) {
-  extern __shared__ double smem[];
+__global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int npc) {
+  extern __shared__ __align__(16) double img_raw[];
   constexpr int NB = NP * (NP + 1) / 2;
   constexpr int D2 = DIM * DIM;
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  double* acc = smem + (size_t)wib * a.max_seg;
-  const int64_t node = (int64_t)blockIdx.x * kRowWarps + wib;
-  if (node >= a.n_nodes) return;
-
-  const int64_t i0 = __ldg(a.n2e_ptr + node);
-  const int nit = (int)(__ldg(a.n2e_ptr + node + 1) - i0);
-  const int64_t nb0 = __ldg(a.nbr_ptr + node);
-  const int nn = (int)(__ldg(a.nbr_ptr + node + 1) - nb0);
-  const int seg_len = D2 * nn;
-  const int64_t sb = nb0 * D2;
-  const double* __restrict__ base = a.base + sb;
-  double* __restrict__ out = a.out + sb;
-
-  // which of the node's items (element, local index) carry plastic points
-  unsigned plastic_items = 0u;
-  bool any_plastic = false;
-  for (int c = 0; c < nit; c += 32) {
-    bool pl = false;
-    if (c + lane < nit) {
-      const int32_t item = __ldg(a.n2e + i0 + c + lane);
-      pl = __ldg(a.emask + item / NP) != 0u;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t n0 = (int64_t)blockIdx.x * npc;
+  const int64_t n1 = min(n0 + (int64_t)npc, a.n_nodes);
+  const int64_t v0 = __ldg(a.nbr_ptr + n0) * D2;
+  const int64_t v1 = __ldg(a.nbr_ptr + n1) * D2;
+  const int len = (int)(v1 - v0);
+  // keep the image at the same 16-byte phase as the global range
+  double* img = img_raw + (v0 & 1);
+  stream_copy(img, a.base + v0, len, tid, blockDim.x);
+  __syncthreads();
+  for (int64_t node = n0 + warp; node < n1; node += kStreamThreads / 32) {
+    const int64_t i0 = __ldg(a.n2e_ptr + node);
+    const int nit = (int)(__ldg(a.n2e_ptr + node + 1) - i0);
+    const int64_t nb0 = __ldg(a.nbr_ptr + node);
+    const int nn = (int)(__ldg(a.nbr_ptr + node + 1) - nb0);
+    const int row_len = DIM * nn;
+    double* seg = img + (nb0 * D2 - v0);
+    for (int c = 0; c < nit; c += 32) {
+      int32_t item = 0;
+      bool pl = false;
+      if (c + lane < nit) {
+        item = __ldg(a.n2e + i0 + c + lane);
+        pl = __ldg(a.emask + item / NP) != 0u;
+      }
+      unsigned bal = __ballot_sync(0xffffffffu, pl);
+      while (bal) {
+        const int src = __ffs(bal) - 1;
+        bal &= bal - 1u;
+        const int32_t it = __shfl_sync(0xffffffffu, item, src);
+        const int64_t el = it / NP;
+        const int pa = it - (int)el * NP;
+        const double* rec = a.scratch + (size_t)el * NB * D2;
+        // lane <-> (pb, i); j loop
+        for (int k = lane; k < NP * DIM; k += 32) {
+          const int pb = k / DIM, i = k - pb * DIM;
+          const int slot = __ldg(a.slot + (int64_t)it * NP + pb);
+          double* dst = seg + i * row_len + slot * DIM;
+          if (pa <= pb) {
+            const double* s = rec + blk_index<NP>(pa, pb) * D2 + i * DIM;
+#pragma unroll
+            for (int j = 0; j < DIM; ++j) dst[j] += __ldg(s + j);
+          } else {
+            const double* s = rec + blk_index<NP>(pb, pa) * D2 + i;
+#pragma unroll
+            for (int j = 0; j < DIM; ++j) dst[j] += __ldg(s + j * DIM);
+          }
+        }
+        __syncwarp();
+      }
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, pl);
-    if (c == 0) plastic_items = bal;
-    any_plastic |= bal != 0u;
   }
-  if (!any_plastic) {
-    for (int k = lane; k < seg_len; k += 32) out[k] = __ldg(base + k);
-    return;
+  __syncthreads();
+  stream_copy(a.out + v0, img, len, tid, blockDim.x);
+}
+
+__global__ void k_range_span(int64_t n_nodes, int npc, int d2, const int64_t* __restrict__ nbr_ptr,
+                             int* out) {
+  int m = 0;
+  const int64_t n_ranges = (n_nodes + npc - 1) / npc;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_ranges;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n0 = r * npc, n1 = min(n0 + (int64_t)npc, n_nodes);
+    m = max(m, (int)((nbr_ptr[n1] - nbr_ptr[n0]) * d2));
   }
-  const bool full_scan = nit > 32;  // rare high-valence node: re-read the masks
-  for (int k = lane; k < seg_len; k += 32) acc[k] = 0.0;
-  __syncwarp();
-  const int row_len = DIM * nn;
-  for (int it = 0; it < nit; ++it) {
-    if (!full_scan && !((plastic_items >> it) & 1u)) continue;
-    const int32_t item = __ldg(a.n2e + i0 + it);
-    const int64_t e = item / NP;
-    if (full_scan && __ldg(a.emask + e) == 0u) continue;
-    const int pa = item - (int)e * NP;
-    const double* rec = a.scratch + (size_t)e * NB * D2;
-    for (int k = lane; k < NP * D2; k += 32) {
-      const int pb = k / D2, ij = k - pb * D2;
-      const int i = ij / DIM, j = ij - i * DIM;
-      const int slot = __ldg(a.slot + (int64_t)item * NP + pb);
-      double v;
-      if (pa <= pb) v = __ldg(rec + blk_index<NP>(pa, pb) * D2 + i * DIM + j);
-      else v = __ldg(rec + blk_index<NP>(pb, pa) * D2 + j * DIM + i);
-      acc[i * row_len + slot * DIM + j] += v;
-    }
-    __syncwarp();
-  }
-  for (int k = lane; k < seg_len; k += 32) out[k] = __ldg(base + k) + acc[k];
+  atomicMax(out, m);
 }
 
 }  // namespace
@@ -260,6 +288,28 @@ size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements) {
     nb = (size_t)NP * (NP + 1) / 2 * decltype(D)::value * decltype(D)::value;
   });
   return nb * (size_t)n_elements;
+}
+
+// Nodes per CTA for the row stream: the largest power of two <= 64 whose
+// widest value range fits the shared-memory budget (two CTAs per SM).
+int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, cudaStream_t st,
+                    int* npc_out, int* span_out) {
+  const int budget = 100 * 1024 / 8 - 2;  // doubles
+  int* d = nullptr;
+  EPFEM_CUDA_TRY(cudaMalloc(&d, sizeof(int)));
+  int npc = 64, span = 0;
+  for (;;) {
+    EPFEM_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(int), st));
+    k_range_span<<<256, 256, 0, st>>>(n_nodes, npc, dim * dim, nbr_ptr, d);
+    EPFEM_CUDA_TRY(cudaMemcpyAsync(&span, d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+    if (span <= budget || npc == 1) break;
+    npc /= 2;
+  }
+  cudaFree(d);
+  *npc_out = npc;
+  *span_out = span;
+  return 0;
 }
 
 int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st) {
@@ -278,14 +328,14 @@ int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStrea
       else
         k_elem_delta<DIM, NP, NQ, G_TANGENT_DS36><<<(unsigned)blocks, threads, 0, st>>>(a);
     }
-    const int64_t rblocks = (a.n_nodes + kRowWarps - 1) / kRowWarps;
-    const size_t smem = sizeof(double) * (size_t)a.max_seg * kRowWarps;
-    auto kern = k_row_gather<DIM, NP, NQ>;
+    const int64_t rblocks = (a.n_nodes + a.npc - 1) / a.npc;
+    const size_t smem = sizeof(double) * ((size_t)a.max_span + 2);
+    auto kern = k_row_stream<DIM, NP, NQ>;
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) { rc = cuda_fail(e, "cudaFuncSetAttribute"); return; }
     }
-    kern<<<(unsigned)rblocks, 32 * kRowWarps, smem, st>>>(a);
+    kern<<<(unsigned)rblocks, kStreamThreads, smem, st>>>(a, a.npc);
   });
   if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
   if (rc) return rc;

@@ -84,8 +84,13 @@ def dense_elastic_oracle(oracle, family, dim, coord, elem, bulk, shear):
     return K
 
 
-def row_scaled_error(got_vals, want_vals, row_ptr):
-    """max_ij |dK_ij| / max_k |K_ref(i,k)| (SURVEY.md §8(a) parity definition)."""
+def row_scaled_error(got_vals, want_vals, row_ptr, base_vals=None):
+    """max_ij |dK_ij| / max_k |K_ref(i,k)| (SURVEY.md §8(a) parity definition).
+
+    ``base_vals`` (K_elast) widens the row scale to max_k(|K_ref|, |K_elast|):
+    Drucker-Prager apex points have D = 0, so K_elast + dK cancels to round-off
+    in rows surrounded by apex points and |K_ref| alone is no scale for the
+    rounding of either implementation there."""
     got = np.asarray(got_vals)
     want = np.asarray(want_vals)
     rp = np.asarray(row_ptr)
@@ -93,6 +98,8 @@ def row_scaled_error(got_vals, want_vals, row_ptr):
     rows = np.repeat(np.arange(rp.shape[0] - 1), np.diff(rp))
     rowmax = np.zeros(rp.shape[0] - 1)
     np.maximum.at(rowmax, rows, np.abs(want))
+    if base_vals is not None:
+        np.maximum.at(rowmax, rows, np.abs(np.asarray(base_vals)))
     scale = np.where(rowmax > 0, rowmax, 1.0)
     return float((diff / scale[rows]).max()) if diff.size else 0.0
 
