@@ -50,7 +50,7 @@ struct epfem_cache {
   double* K_elast = nullptr;
   double* scratch = nullptr;  // tangent workspace (symmetric dK_e per element)
   unsigned* emask = nullptr;  // per-element plastic-point bitmask
-  int npc = 64, max_span = 0; // row-stream plan
+  int npc = 64, max_span = 0, max_items = 0;  // row-stream plan
 };
 
 namespace {
@@ -241,6 +241,7 @@ static GatherArgs gather_args(const epfem_cache* c) {
   g.emask = c->emask;
   g.npc = c->npc;
   g.max_span = c->max_span;
+  g.max_items = c->max_items;
   // packed elastic operator C = K VOL + 2G DEV (voigt.hpp:72-74) for a uniform material
   for (int i = 0; i < 6; ++i)
     for (int j = i; j < 6; ++j) {
@@ -328,7 +329,8 @@ int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_materi
                                  tangent_workspace_doubles(I.family, I.dim, I.n_elements), 1)));
   CT(cudaMalloc(&c->emask, sizeof(unsigned) * std::max<int64_t>(I.n_elements, 1)));
   if (I.n_nodes > 0)
-    if (int rc = plan_row_stream(I.n_nodes, I.dim, c->pat.nbr_ptr, st, &c->npc, &c->max_span))
+    if (int rc = plan_row_stream(I.n_nodes, I.dim, c->pat.nbr_ptr, c->pat.n2e_ptr, st, &c->npc,
+                                 &c->max_span, &c->max_items))
       return bail(rc);
   GatherArgs g = gather_args(c);
   g.out = c->K_elast;

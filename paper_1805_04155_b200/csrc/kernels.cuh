@@ -51,6 +51,7 @@ struct GatherArgs {
   unsigned* emask;   // per-element plastic-point bitmask
   int npc;           // nodes per CTA of the row stream
   int max_span;      // widest value range of any row-stream CTA (doubles)
+  int max_items;     // most (element, node) items of any row-stream CTA
   double Cu[21];     // packed elastic operator when the material is uniform
 };
 struct PatternOut {
@@ -77,8 +78,8 @@ int build_pattern(int family, int dim, int64_t n_nodes, int64_t n_e, const int32
 int launch_gather(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);
 int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);
 size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements);
-int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, cudaStream_t st,
-                    int* npc_out, int* span_out);
+int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
+                    cudaStream_t st, int* npc_out, int* span_out, int* items_out);
 int launch_strains(int family, int dim, int64_t n_e, const int32_t* elem, const double* inv,
                    const double* gradhat, const double* u, double* E, cudaStream_t st,
                    int num_sms);

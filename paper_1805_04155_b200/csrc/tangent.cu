@@ -186,6 +186,151 @@ __global__ void __launch_bounds__(kDeltaThreads) k_elem_delta(GatherArgs a) {
   }
 }
 
+// Pass 1 for small elements (NP <= 8): one lane per (element, node a).  A
+// group of GW = pow2ceil(NP) lanes holds one element; each lane forms its own
+// dphi_a, receives the others by shuffles, builds Dw and T_a = B_a^T Dw in
+// registers and accumulates the whole block row a.  It writes the blocks
+// (a, b >= a) of the symmetric record.  No barriers, only the element's own
+// plastic points are visited (warp-uniform loop over the union of the groups'
+// masks).
+template <int NP>
+struct LaneGroup {
+  static constexpr int GW = NP <= 2 ? 2 : NP <= 4 ? 4 : 8;
+};
+
+template <int DIM, int NP, int NQ, int MODE>
+__global__ void __launch_bounds__(256) k_elem_delta_lane(GatherArgs a) {
+  constexpr int NS = DIM == 3 ? 6 : 3;
+  constexpr int GW = LaneGroup<NP>::GW;
+  constexpr int EPW = 32 / GW;
+  constexpr int D2 = DIM * DIM;
+  constexpr int NB = NP * (NP + 1) / 2;
+  constexpr int RV[3] = {0, 1, 3};  // 2D assembly rows -> Voigt rows
+  __shared__ double s_ghat[NQ * NP * DIM];
+  for (int k = threadIdx.x; k < NQ * NP * DIM; k += blockDim.x) s_ghat[k] = __ldg(a.gradhat + k);
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int g = lane / GW, p = lane - g * GW;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t e = warp * EPW + g;
+  const bool elem_ok = e < a.n_elements;
+  const bool node_ok = elem_ok && p < NP;
+  const unsigned full = 0xffffffffu;
+  const unsigned gmask = (GW == 32 ? full : ((1u << GW) - 1u));
+
+  // plastic-point bitmask of this lane's element
+  unsigned mask = 0u;
+#pragma unroll
+  for (int q0 = 0; q0 < NQ; q0 += GW) {
+    const bool f = elem_ok && q0 + p < NQ && (__ldg(a.flags + e * NQ + q0 + p) & 1);
+    const unsigned b = __ballot_sync(full, f);
+    mask |= ((b >> (g * GW)) & gmask) << q0;
+  }
+  if (elem_ok && p == 0) a.emask[e] = mask;
+  unsigned todo = __reduce_or_sync(full, mask);
+  if (!todo) return;
+
+  const bool uniform_c = a.shear == nullptr && a.bulk == nullptr;
+  double blk[NP][DIM][DIM];
+#pragma unroll
+  for (int b = 0; b < NP; ++b)
+#pragma unroll
+    for (int i = 0; i < DIM; ++i)
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) blk[b][i][j] = 0.0;
+
+  while (todo) {
+    const int q = __ffs(todo) - 1;
+    todo &= todo - 1u;
+    const bool on = node_ok && ((mask >> q) & 1u);
+    const int64_t m = e * NQ + q;
+    double gself[DIM];
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) gself[i] = 0.0;
+    double w = 0.0;
+    if (on) {
+      const double* Ji = a.inv + m * D2;
+      const double* gh = s_ghat + (q * NP + p) * DIM;
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) s += __ldg(Ji + j * DIM + i) * gh[j];
+        gself[i] = s;
+      }
+      w = __ldg(a.weight + m);
+    }
+    // Dw = w (D - C) on the assembly rows, then T_a = B_a^T Dw
+    double T[DIM][NS];
+    if (on) {
+      double Dw[NS][NS];
+      double G2 = 0.0, Km = 0.0;
+      if (!uniform_c) {
+        G2 = 2.0 * (a.shear ? __ldg(a.shear + m) : a.shear_u);
+        Km = a.bulk ? __ldg(a.bulk + m) : a.bulk_u;
+      }
+#pragma unroll
+      for (int r = 0; r < NS; ++r)
+#pragma unroll
+        for (int c = r; c < NS; ++c) {
+          const int ri = DIM == 3 ? r : RV[r], ci = DIM == 3 ? c : RV[c];
+          const double d = MODE == G_TANGENT_PACKED
+                               ? __ldg(a.D + m * EPFEM_D_STRIDE + pk_index(ri, ci))
+                               : __ldg(a.D + m * 36 + ci * 6 + ri);
+          const double vol = (ri < 3 && ci < 3) ? 1.0 : 0.0;
+          const double dev = ((ri == ci) ? (ri < 3 ? 1.0 : 0.5) : 0.0) - vol / 3.0;
+          const double cel = uniform_c ? a.Cu[pk_index(ri, ci)] : Km * vol + G2 * dev;
+          Dw[r][c] = Dw[c][r] = w * (d - cel);
+        }
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        if constexpr (DIM == 3) {
+          T[0][c] = gself[0] * Dw[0][c] + gself[1] * Dw[3][c] + gself[2] * Dw[5][c];
+          T[1][c] = gself[1] * Dw[1][c] + gself[0] * Dw[3][c] + gself[2] * Dw[4][c];
+          T[DIM - 1][c] = gself[2] * Dw[2][c] + gself[1] * Dw[4][c] + gself[0] * Dw[5][c];
+        } else {
+          T[0][c] = gself[0] * Dw[0][c] + gself[1] * Dw[2][c];
+          T[1][c] = gself[1] * Dw[1][c] + gself[0] * Dw[2][c];
+        }
+      }
+    }
+    // block row: blk[b] += T_a B_b with dphi_b shuffled from lane b
+#pragma unroll
+    for (int b = 0; b < NP; ++b) {
+      double h[DIM];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) h[i] = __shfl_sync(full, gself[i], g * GW + b);
+      if (on) {
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) {
+          if constexpr (DIM == 3) {
+            blk[b][i][0] += T[i][0] * h[0] + T[i][3] * h[1] + T[i][5] * h[2];
+            blk[b][i][1] += T[i][1] * h[1] + T[i][3] * h[0] + T[i][4] * h[2];
+            blk[b][i][DIM - 1] += T[i][2] * h[2] + T[i][4] * h[1] + T[i][5] * h[0];
+          } else {
+            blk[b][i][0] += T[i][0] * h[0] + T[i][2] * h[1];
+            blk[b][i][1] += T[i][1] * h[1] + T[i][2] * h[0];
+          }
+        }
+      }
+    }
+  }
+  if (node_ok && mask) {
+    double* rec = a.scratch + (size_t)e * NB * D2;
+#pragma unroll
+    for (int b = 0; b < NP; ++b) {
+      if (b >= p) {
+        double* o = rec + blk_index<NP>(p, b) * D2;
+#pragma unroll
+        for (int i = 0; i < DIM; ++i)
+#pragma unroll
+          for (int j = 0; j < DIM; ++j) o[i * DIM + j] = blk[b][i][j];
+      }
+    }
+  }
+}
+
 constexpr int kStreamThreads = 256;
 
 // Stream n doubles src -> dst (either may be smem), 16-byte vectors when the
@@ -215,52 +360,54 @@ __global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n0 = (int64_t)blockIdx.x * npc;
   const int64_t n1 = min(n0 + (int64_t)npc, a.n_nodes);
+  const int nloc = (int)(n1 - n0);
   const int64_t v0 = __ldg(a.nbr_ptr + n0) * D2;
   const int64_t v1 = __ldg(a.nbr_ptr + n1) * D2;
+  const int64_t i_begin = __ldg(a.n2e_ptr + n0);
+  const int nitems = (int)(__ldg(a.n2e_ptr + n1) - i_begin);
   const int len = (int)(v1 - v0);
-  // keep the image at the same 16-byte phase as the global range
-  double* img = img_raw + (v0 & 1);
+  // layout: [image | item (int) | iptr (int) | vptr (int)]
+  double* img = img_raw + (v0 & 1);  // same 16-byte phase as the global range
+  int* s_item = reinterpret_cast<int*>(img_raw + a.max_span + 2);
+  int* s_iptr = s_item + a.max_items;
+  int* s_vptr = s_iptr + npc + 1;
+  // stage the range's items (plastic ones kept, others -1) and node offsets
+  for (int k = tid; k < nitems; k += blockDim.x) {
+    const int32_t it = __ldg(a.n2e + i_begin + k);
+    s_item[k] = __ldg(a.emask + it / NP) ? it : -1;
+  }
+  for (int k = tid; k <= nloc; k += blockDim.x) {
+    s_iptr[k] = (int)(__ldg(a.n2e_ptr + n0 + k) - i_begin);
+    s_vptr[k] = (int)(__ldg(a.nbr_ptr + n0 + k) * D2 - v0);
+  }
   stream_copy(img, a.base + v0, len, tid, blockDim.x);
   __syncthreads();
-  for (int64_t node = n0 + warp; node < n1; node += kStreamThreads / 32) {
-    const int64_t i0 = __ldg(a.n2e_ptr + node);
-    const int nit = (int)(__ldg(a.n2e_ptr + node + 1) - i0);
-    const int64_t nb0 = __ldg(a.nbr_ptr + node);
-    const int nn = (int)(__ldg(a.nbr_ptr + node + 1) - nb0);
-    const int row_len = DIM * nn;
-    double* seg = img + (nb0 * D2 - v0);
-    for (int c = 0; c < nit; c += 32) {
-      int32_t item = 0;
-      bool pl = false;
-      if (c + lane < nit) {
-        item = __ldg(a.n2e + i0 + c + lane);
-        pl = __ldg(a.emask + item / NP) != 0u;
-      }
-      unsigned bal = __ballot_sync(0xffffffffu, pl);
-      while (bal) {
-        const int src = __ffs(bal) - 1;
-        bal &= bal - 1u;
-        const int32_t it = __shfl_sync(0xffffffffu, item, src);
-        const int64_t el = it / NP;
-        const int pa = it - (int)el * NP;
-        const double* rec = a.scratch + (size_t)el * NB * D2;
-        // lane <-> (pb, i); j loop
-        for (int k = lane; k < NP * DIM; k += 32) {
-          const int pb = k / DIM, i = k - pb * DIM;
-          const int slot = __ldg(a.slot + (int64_t)it * NP + pb);
-          double* dst = seg + i * row_len + slot * DIM;
-          if (pa <= pb) {
-            const double* s = rec + blk_index<NP>(pa, pb) * D2 + i * DIM;
+  for (int ln = warp; ln < nloc; ln += kStreamThreads / 32) {
+    const int ib = s_iptr[ln], ie = s_iptr[ln + 1];
+    const int row_len = (s_vptr[ln + 1] - s_vptr[ln]) / DIM;
+    double* seg = img + s_vptr[ln];
+    for (int k0 = ib; k0 < ie; ++k0) {
+      const int it = s_item[k0];  // warp-uniform
+      if (it < 0) continue;
+      const int64_t el = it / NP;
+      const int pa = it - (int)el * NP;
+      const double* rec = a.scratch + (size_t)el * NB * D2;
+      // lane <-> (pb, i); j loop
+      for (int k = lane; k < NP * DIM; k += 32) {
+        const int pb = k / DIM, i = k - pb * DIM;
+        const int slot = __ldg(a.slot + (int64_t)it * NP + pb);
+        double* dst = seg + i * row_len + slot * DIM;
+        if (pa <= pb) {
+          const double* s = rec + blk_index<NP>(pa, pb) * D2 + i * DIM;
 #pragma unroll
-            for (int j = 0; j < DIM; ++j) dst[j] += __ldg(s + j);
-          } else {
-            const double* s = rec + blk_index<NP>(pb, pa) * D2 + i;
+          for (int j = 0; j < DIM; ++j) dst[j] += __ldg(s + j);
+        } else {
+          const double* s = rec + blk_index<NP>(pb, pa) * D2 + i;
 #pragma unroll
-            for (int j = 0; j < DIM; ++j) dst[j] += __ldg(s + j * DIM);
-          }
+          for (int j = 0; j < DIM; ++j) dst[j] += __ldg(s + j * DIM);
         }
-        __syncwarp();
       }
+      __syncwarp();
     }
   }
   __syncthreads();
@@ -268,15 +415,17 @@ __global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int
 }
 
 __global__ void k_range_span(int64_t n_nodes, int npc, int d2, const int64_t* __restrict__ nbr_ptr,
-                             int* out) {
-  int m = 0;
+                             const int64_t* __restrict__ n2e_ptr, int* out) {
+  int m = 0, mi = 0;
   const int64_t n_ranges = (n_nodes + npc - 1) / npc;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_ranges;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t n0 = r * npc, n1 = min(n0 + (int64_t)npc, n_nodes);
     m = max(m, (int)((nbr_ptr[n1] - nbr_ptr[n0]) * d2));
+    mi = max(mi, (int)(n2e_ptr[n1] - n2e_ptr[n0]));
   }
   atomicMax(out, m);
+  atomicMax(out + 1, mi);
 }
 
 }  // namespace
@@ -292,23 +441,25 @@ size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements) {
 
 // Nodes per CTA for the row stream: the largest power of two <= 64 whose
 // widest value range fits the shared-memory budget (two CTAs per SM).
-int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, cudaStream_t st,
-                    int* npc_out, int* span_out) {
-  const int budget = 100 * 1024 / 8 - 2;  // doubles
+int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
+                    cudaStream_t st, int* npc_out, int* span_out, int* items_out) {
+  const int budget = 100 * 1024;  // bytes of dynamic smem: two CTAs per SM
   int* d = nullptr;
-  EPFEM_CUDA_TRY(cudaMalloc(&d, sizeof(int)));
-  int npc = 64, span = 0;
+  EPFEM_CUDA_TRY(cudaMalloc(&d, 2 * sizeof(int)));
+  int npc = 64, h[2] = {0, 0};
   for (;;) {
-    EPFEM_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(int), st));
-    k_range_span<<<256, 256, 0, st>>>(n_nodes, npc, dim * dim, nbr_ptr, d);
-    EPFEM_CUDA_TRY(cudaMemcpyAsync(&span, d, sizeof(int), cudaMemcpyDeviceToHost, st));
+    EPFEM_CUDA_TRY(cudaMemsetAsync(d, 0, 2 * sizeof(int), st));
+    k_range_span<<<256, 256, 0, st>>>(n_nodes, npc, dim * dim, nbr_ptr, n2e_ptr, d);
+    EPFEM_CUDA_TRY(cudaMemcpyAsync(h, d, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
     EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
-    if (span <= budget || npc == 1) break;
+    const size_t bytes = 8 * ((size_t)h[0] + 2) + 4 * ((size_t)h[1] + 2 * (npc + 1));
+    if (bytes <= (size_t)budget || npc == 1) break;
     npc /= 2;
   }
   cudaFree(d);
   *npc_out = npc;
-  *span_out = span;
+  *span_out = h[0];
+  *items_out = h[1];
   return 0;
 }
 
@@ -321,15 +472,35 @@ int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStrea
     constexpr int NB = NP * (NP + 1) / 2;
     constexpr int EPB = NB >= kDeltaThreads ? 1 : kDeltaThreads / NB;
     constexpr int threads = ((EPB * NB + 31) / 32) * 32;
+    static const bool force_cta = [] {
+      const char* v = getenv("EPFEM_DELTA");
+      return v && v[0] == 'c';
+    }();
     if (a.n_elements > 0) {
-      const int64_t blocks = (a.n_elements + EPB - 1) / EPB;
-      if (mode == G_TANGENT_PACKED)
-        k_elem_delta<DIM, NP, NQ, G_TANGENT_PACKED><<<(unsigned)blocks, threads, 0, st>>>(a);
-      else
-        k_elem_delta<DIM, NP, NQ, G_TANGENT_DS36><<<(unsigned)blocks, threads, 0, st>>>(a);
+      bool done = false;
+      if constexpr (NP <= 8) {
+        if (!force_cta) {
+          constexpr int EPW = 32 / LaneGroup<NP>::GW;
+          const int64_t warps = (a.n_elements + EPW - 1) / EPW;
+          const int64_t blocks = (warps + 7) / 8;
+          if (mode == G_TANGENT_PACKED)
+            k_elem_delta_lane<DIM, NP, NQ, G_TANGENT_PACKED><<<(unsigned)blocks, 256, 0, st>>>(a);
+          else
+            k_elem_delta_lane<DIM, NP, NQ, G_TANGENT_DS36><<<(unsigned)blocks, 256, 0, st>>>(a);
+          done = true;
+        }
+      }
+      if (!done) {
+        const int64_t blocks = (a.n_elements + EPB - 1) / EPB;
+        if (mode == G_TANGENT_PACKED)
+          k_elem_delta<DIM, NP, NQ, G_TANGENT_PACKED><<<(unsigned)blocks, threads, 0, st>>>(a);
+        else
+          k_elem_delta<DIM, NP, NQ, G_TANGENT_DS36><<<(unsigned)blocks, threads, 0, st>>>(a);
+      }
     }
     const int64_t rblocks = (a.n_nodes + a.npc - 1) / a.npc;
-    const size_t smem = sizeof(double) * ((size_t)a.max_span + 2);
+    const size_t smem = sizeof(double) * ((size_t)a.max_span + 2) +
+                        sizeof(int) * ((size_t)a.max_items + 2 * ((size_t)a.npc + 1));
     auto kern = k_row_stream<DIM, NP, NQ>;
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
