@@ -331,6 +331,182 @@ __global__ void __launch_bounds__(256) k_elem_delta_lane(GatherArgs a) {
   }
 }
 
+// Pass 1, staged form (default).  Phase 1: one thread per (element, point)
+// of the CTA's elements issues that point's loads (J^-1, w, packed D) with no
+// dependence on any other point, and stages dphi_p for all nodes and the
+// packed Dw = w (D - C) in shared memory.  Phase 2: one thread per (element,
+// node a, block chunk) loops over the element's plastic points reading only
+// shared memory: T_a = B_a^T Dw, block(a, b) += T_a B_b for the b of its
+// chunk, in registers.  Two CTA barriers in total.
+template <int DIM, int NP>
+struct StagedCfg {
+  static constexpr int BCH = DIM == 2 ? 1 : (NP <= 4 ? 1 : (NP <= 10 ? 2 : 4));
+  static constexpr int CS = (NP + BCH - 1) / BCH;  // blocks per chunk
+};
+
+template <int DIM, int NP, int NQ, int MODE>
+__global__ void __launch_bounds__(256) k_elem_delta_staged(GatherArgs a) {
+  constexpr int NS = DIM == 3 ? 6 : 3;
+  constexpr int NSP = NS * (NS + 1) / 2;
+  constexpr int D2 = DIM * DIM;
+  constexpr int NB = NP * (NP + 1) / 2;
+  constexpr int REC = NP * DIM + NSP;
+  constexpr int BCH = StagedCfg<DIM, NP>::BCH, CS = StagedCfg<DIM, NP>::CS;
+  constexpr int BUDGET = 5120;  // doubles of staged data per CTA (40 KB)
+  constexpr int E1 = 256 / (NP * BCH), E2 = BUDGET / (NQ * REC);
+  constexpr int EPB = (E1 < E2 ? E1 : E2) > 0 ? (E1 < E2 ? E1 : E2) : 1;
+  constexpr int RV[6] = {0, 1, DIM == 3 ? 2 : 3, 3, 4, 5};  // assembly row -> Voigt row
+  __shared__ double s_st[EPB][NQ][REC];
+  __shared__ unsigned s_mask[EPB];
+
+  const int tid = threadIdx.x;
+  const int64_t e0 = (int64_t)blockIdx.x * EPB;
+  if (tid < EPB) s_mask[tid] = 0u;
+  __syncthreads();
+  const bool uniform_c = a.shear == nullptr && a.bulk == nullptr;
+  // phase 1
+  for (int k = tid; k < EPB * NQ; k += blockDim.x) {
+    const int le = k / NQ, q = k - le * NQ;
+    const int64_t e = e0 + le;
+    if (e >= a.n_elements) continue;
+    const int64_t m = e * NQ + q;
+    if (!(__ldg(a.flags + m) & 1)) continue;
+    atomicOr(&s_mask[le], 1u << q);
+    double J[D2];
+#pragma unroll
+    for (int t = 0; t < D2; ++t) J[t] = __ldg(a.inv + m * D2 + t);
+    const double w = __ldg(a.weight + m);
+    double dv[NSP];
+    {
+      int k2 = 0;
+#pragma unroll
+      for (int r = 0; r < NS; ++r)
+#pragma unroll
+        for (int c = r; c < NS; ++c, ++k2) {
+          const int ri = RV[r], ci = RV[c];
+          dv[k2] = MODE == G_TANGENT_PACKED ? __ldg(a.D + m * EPFEM_D_STRIDE + pk_index(ri, ci))
+                                            : __ldg(a.D + m * 36 + ci * 6 + ri);
+        }
+    }
+    double* st = s_st[le][q];
+#pragma unroll 4
+    for (int p = 0; p < NP; ++p) {
+      const double* gh = a.gradhat + (q * NP + p) * DIM;
+      double g[DIM];
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) g[j] = __ldg(gh + j);
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) s += J[j * DIM + i] * g[j];
+        st[p * DIM + i] = s;
+      }
+    }
+    double G2 = 0.0, Km = 0.0;
+    if (!uniform_c) {
+      G2 = 2.0 * (a.shear ? __ldg(a.shear + m) : a.shear_u);
+      Km = a.bulk ? __ldg(a.bulk + m) : a.bulk_u;
+    }
+    int k2 = 0;
+#pragma unroll
+    for (int r = 0; r < NS; ++r)
+#pragma unroll
+      for (int c = r; c < NS; ++c, ++k2) {
+        const int ri = RV[r], ci = RV[c];
+        const double vol = (ri < 3 && ci < 3) ? 1.0 : 0.0;
+        const double dev = ((ri == ci) ? (ri < 3 ? 1.0 : 0.5) : 0.0) - vol / 3.0;
+        const double cel = uniform_c ? a.Cu[pk_index(ri, ci)] : Km * vol + G2 * dev;
+        st[NP * DIM + k2] = w * (dv[k2] - cel);
+      }
+  }
+  __syncthreads();
+  if (tid < EPB && e0 + tid < a.n_elements) a.emask[e0 + tid] = s_mask[tid];
+  // phase 2
+  if (tid >= EPB * NP * BCH) return;
+  const int le = tid / (NP * BCH);
+  const int rr = tid - le * (NP * BCH);
+  const int pa = rr / BCH, ch = rr - pa * BCH;
+  const int b0 = ch * CS;
+  const int64_t e = e0 + le;
+  if (e >= a.n_elements) return;
+  unsigned mask = s_mask[le];
+  if (!mask) return;
+  double blk[CS][DIM][DIM];
+#pragma unroll
+  for (int b = 0; b < CS; ++b)
+#pragma unroll
+    for (int i = 0; i < DIM; ++i)
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) blk[b][i][j] = 0.0;
+  while (mask) {
+    const int q = __ffs(mask) - 1;
+    mask &= mask - 1u;
+    const double* st = s_st[le][q];
+    const double* dw = st + NP * DIM;
+    auto Dw = [&](int r, int c) {  // compile-time indices after unrolling
+      const int lo = r < c ? r : c, hi = r < c ? c : r;
+      return dw[lo * NS - lo * (lo - 1) / 2 + (hi - lo)];
+    };
+    double ga[DIM];
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) ga[i] = st[pa * DIM + i];
+    double T[DIM][NS];
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+      if constexpr (DIM == 3) {
+        // B rows e11,e22,e33,2e12,2e23,2e31 (assembly.cpp:162-171)
+        T[0][c] = ga[0] * Dw(0, c) + ga[1] * Dw(3, c) + ga[2] * Dw(5, c);
+        T[1][c] = ga[1] * Dw(1, c) + ga[0] * Dw(3, c) + ga[2] * Dw(4, c);
+        T[DIM - 1][c] = ga[2] * Dw(2, c) + ga[1] * Dw(4, c) + ga[0] * Dw(5, c);
+      } else {
+        // rows e11, e22, 2e12 (assembly.cpp:173-176)
+        T[0][c] = ga[0] * Dw(0, c) + ga[1] * Dw(2, c);
+        T[1][c] = ga[1] * Dw(1, c) + ga[0] * Dw(2, c);
+      }
+    }
+#pragma unroll
+    for (int bb = 0; bb < CS; ++bb) {
+      const int b = b0 + bb;
+      if (b >= NP) break;
+      const double* h = st + b * DIM;
+      const double h0 = h[0], h1 = h[1], h2 = DIM == 3 ? h[DIM - 1] : 0.0;
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        if constexpr (DIM == 3) {
+          blk[bb][i][0] += T[i][0] * h0 + T[i][3] * h1 + T[i][5] * h2;
+          blk[bb][i][1] += T[i][1] * h1 + T[i][3] * h0 + T[i][4] * h2;
+          blk[bb][i][DIM - 1] += T[i][2] * h2 + T[i][4] * h1 + T[i][5] * h0;
+        } else {
+          blk[bb][i][0] += T[i][0] * h0 + T[i][2] * h1;
+          blk[bb][i][1] += T[i][1] * h1 + T[i][2] * h0;
+        }
+      }
+    }
+  }
+  double* rec = a.scratch + (size_t)e * NB * D2;
+#pragma unroll
+  for (int bb = 0; bb < CS; ++bb) {
+    const int b = b0 + bb;
+    if (b >= NP) break;
+    if (b >= pa) {
+      double* o = rec + blk_index<NP>(pa, b) * D2;
+#pragma unroll
+      for (int i = 0; i < DIM; ++i)
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) o[i * DIM + j] = blk[bb][i][j];
+    }
+  }
+}
+
+template <int DIM, int NP, int NQ>
+constexpr int staged_epb() {
+  constexpr int NS = DIM == 3 ? 6 : 3;
+  constexpr int REC = NP * DIM + NS * (NS + 1) / 2;
+  constexpr int E1 = 256 / (NP * StagedCfg<DIM, NP>::BCH), E2 = 5120 / (NQ * REC);
+  return (E1 < E2 ? E1 : E2) > 0 ? (E1 < E2 ? E1 : E2) : 1;
+}
+
 constexpr int kStreamThreads = 256;
 
 // Stream n doubles src -> dst (either may be smem), 16-byte vectors when the
@@ -472,14 +648,24 @@ int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStrea
     constexpr int NB = NP * (NP + 1) / 2;
     constexpr int EPB = NB >= kDeltaThreads ? 1 : kDeltaThreads / NB;
     constexpr int threads = ((EPB * NB + 31) / 32) * 32;
-    static const bool force_cta = [] {
+    // pass-1 variant: staged (default), 'lane' or 'cta' via EPFEM_DELTA (A/B runs)
+    static const char variant = [] {
       const char* v = getenv("EPFEM_DELTA");
-      return v && v[0] == 'c';
+      return v ? v[0] : 's';
     }();
     if (a.n_elements > 0) {
       bool done = false;
+      if (variant == 's') {
+        constexpr int SEPB = staged_epb<DIM, NP, NQ>();
+        const int64_t blocks = (a.n_elements + SEPB - 1) / SEPB;
+        if (mode == G_TANGENT_PACKED)
+          k_elem_delta_staged<DIM, NP, NQ, G_TANGENT_PACKED><<<(unsigned)blocks, 256, 0, st>>>(a);
+        else
+          k_elem_delta_staged<DIM, NP, NQ, G_TANGENT_DS36><<<(unsigned)blocks, 256, 0, st>>>(a);
+        done = true;
+      }
       if constexpr (NP <= 8) {
-        if (!force_cta) {
+        if (!done && variant == 'l') {
           constexpr int EPW = 32 / LaneGroup<NP>::GW;
           const int64_t warps = (a.n_elements + EPW - 1) / EPW;
           const int64_t blocks = (warps + 7) / 8;
