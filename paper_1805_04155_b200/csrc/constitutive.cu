@@ -49,15 +49,17 @@ __device__ __forceinline__ void store6(double* p, int64_t q, const double* v) {
 template <class F>
 __device__ __forceinline__ void write_tangent(const ConstArgs& a, int64_t q, bool plastic, F f) {
   if (a.D && plastic) {
-    double v[EPFEM_D_STRIDE];
-#pragma unroll
-    for (int i = 0; i < 6; ++i)
-#pragma unroll
-      for (int j = i; j < 6; ++j) v[pk_index(i, j)] = f(i, j);
-    v[21] = v[22] = v[23] = 0.0;
+    // entry k holds D(PR[k], PC[k]) (epfem_gpu.h); stored pairwise as soon as
+    // computed so the block never lives in registers as a whole
+    constexpr int PR[24] = {0, 0, 0, 1, 1, 3, 0, 0, 0, 1, 1, 1, 2, 2, 2, 2, 3, 3, 4, 4, 5, 0, 0, 0};
+    constexpr int PC[24] = {0, 1, 3, 1, 3, 3, 2, 4, 5, 2, 4, 5, 2, 3, 4, 5, 4, 5, 4, 5, 5, 0, 0, 0};
     double2* d2 = reinterpret_cast<double2*>(a.D + (int64_t)EPFEM_D_STRIDE * q);
 #pragma unroll
-    for (int k = 0; k < EPFEM_D_STRIDE / 2; ++k) d2[k] = make_double2(v[2 * k], v[2 * k + 1]);
+    for (int k = 0; k < EPFEM_D_STRIDE / 2; ++k) {
+      const double x = 2 * k < 21 ? f(PR[2 * k], PC[2 * k]) : 0.0;
+      const double y = 2 * k + 1 < 21 ? f(PR[2 * k + 1], PC[2 * k + 1]) : 0.0;
+      d2[k] = make_double2(x, y);
+    }
   }
   if (a.DS) {
     double2* d2 = reinterpret_cast<double2*>(a.DS + 36 * q);
@@ -70,8 +72,16 @@ __device__ __forceinline__ void write_tangent(const ConstArgs& a, int64_t q, boo
   }
 }
 
-template <int MODEL>
+// LEAN: the hot-path instance (S, flags, packed D only); the reference-layout
+// outputs are compiled out so the kernel keeps its registers low.
+template <int MODEL, bool LEAN>
 __global__ void __launch_bounds__(256) k_constitutive(ConstArgs a) {
+  if (LEAN) {
+    a.DS = nullptr;
+    a.Ep_out = a.Hard_out = nullptr;
+    a.pm = a.sm = a.am = nullptr;
+    a.crit = nullptr;
+  }
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < a.n; q += stride) {
     const double G = a.G ? __ldg(a.G + q) : a.Gu;
@@ -257,10 +267,20 @@ int launch_constitutive(int model, const ConstArgs& a, cudaStream_t st, int num_
   int64_t blocks = (a.n + threads - 1) / threads;
   const int64_t cap = (int64_t)num_sms * 16;  // grid-stride beyond 16 CTAs/SM
   if (blocks > cap) blocks = cap;
+  const bool lean = !a.DS && !a.Ep_out && !a.Hard_out && !a.pm && !a.sm && !a.am && !a.crit;
   switch (model) {
-    case EPFEM_MODEL_ELASTIC: k_constitutive<EPFEM_MODEL_ELASTIC><<<(int)blocks, threads, 0, st>>>(a); break;
-    case EPFEM_MODEL_VON_MISES: k_constitutive<EPFEM_MODEL_VON_MISES><<<(int)blocks, threads, 0, st>>>(a); break;
-    case EPFEM_MODEL_DRUCKER_PRAGER: k_constitutive<EPFEM_MODEL_DRUCKER_PRAGER><<<(int)blocks, threads, 0, st>>>(a); break;
+    case EPFEM_MODEL_ELASTIC:
+      if (lean) k_constitutive<EPFEM_MODEL_ELASTIC, true><<<(int)blocks, threads, 0, st>>>(a);
+      else k_constitutive<EPFEM_MODEL_ELASTIC, false><<<(int)blocks, threads, 0, st>>>(a);
+      break;
+    case EPFEM_MODEL_VON_MISES:
+      if (lean) k_constitutive<EPFEM_MODEL_VON_MISES, true><<<(int)blocks, threads, 0, st>>>(a);
+      else k_constitutive<EPFEM_MODEL_VON_MISES, false><<<(int)blocks, threads, 0, st>>>(a);
+      break;
+    case EPFEM_MODEL_DRUCKER_PRAGER:
+      if (lean) k_constitutive<EPFEM_MODEL_DRUCKER_PRAGER, true><<<(int)blocks, threads, 0, st>>>(a);
+      else k_constitutive<EPFEM_MODEL_DRUCKER_PRAGER, false><<<(int)blocks, threads, 0, st>>>(a);
+      break;
     default: return fail(EPFEM_ERR_INVALID, "evaluate_constitutive: unknown material model");
   }
   EPFEM_CUDA_TRY(cudaGetLastError());

@@ -568,20 +568,16 @@ __global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int
       const int64_t el = it / NP;
       const int pa = it - (int)el * NP;
       const double* rec = a.scratch + (size_t)el * NB * D2;
-      // lane <-> (pb, i); j loop
-      for (int k = lane; k < NP * DIM; k += 32) {
-        const int pb = k / DIM, i = k - pb * DIM;
+      // lane <-> entry (pb, i, j) of block row pa; block (pb, pa) read
+      // transposed when pb < pa (branch-free addressing)
+      for (int k = lane; k < NP * D2; k += 32) {
+        const int pb = k / D2, ij = k - pb * D2;
+        const int i = ij / DIM, j = ij - i * DIM;
+        const bool up = pa <= pb;
+        const int lo = up ? pa : pb, hi = up ? pb : pa;
+        const int src = blk_index<NP>(lo, hi) * D2 + (up ? ij : j * DIM + i);
         const int slot = __ldg(a.slot + (int64_t)it * NP + pb);
-        double* dst = seg + i * row_len + slot * DIM;
-        if (pa <= pb) {
-          const double* s = rec + blk_index<NP>(pa, pb) * D2 + i * DIM;
-#pragma unroll
-          for (int j = 0; j < DIM; ++j) dst[j] += __ldg(s + j);
-        } else {
-          const double* s = rec + blk_index<NP>(pb, pa) * D2 + i;
-#pragma unroll
-          for (int j = 0; j < DIM; ++j) dst[j] += __ldg(s + j * DIM);
-        }
+        seg[i * row_len + slot * DIM + j] += __ldg(rec + src);
       }
       __syncwarp();
     }
