@@ -324,7 +324,9 @@ int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_materi
   CT(cudaEventRecord(ev[1], st));
   I.nnz = c->pat.nnz;
   I.max_row_nodes = c->pat.max_nbr;
-  CT(cudaMalloc(&c->K_elast, sizeof(double) * std::max<int64_t>(I.nnz, 1)));
+  // two doubles of padding: the row stream reads 16-byte-aligned ranges
+  CT(cudaMalloc(&c->K_elast, sizeof(double) * (I.nnz + 2)));
+  CT(cudaMemsetAsync(c->K_elast + I.nnz, 0, 2 * sizeof(double), st));
   CT(cudaMalloc(&c->scratch, sizeof(double) * std::max<size_t>(
                                  tangent_workspace_doubles(I.family, I.dim, I.n_elements), 1)));
   CT(cudaMalloc(&c->emask, sizeof(unsigned) * std::max<int64_t>(I.n_elements, 1)));
@@ -394,7 +396,8 @@ static int tangent_common(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int, c
   if (n_int != c->info.n_int) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: size mismatch");
   if (!K_values || (n_int > 0 && (!D || !flags)))
     return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null argument");
-  if (!aligned16(D)) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: D must be 16-byte aligned");
+  if (!aligned16(D) || !aligned16(K_values))
+    return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: D and K must be 16-byte aligned");
   GatherArgs g = gather_args(c);
   g.D = D;
   g.flags = flags;

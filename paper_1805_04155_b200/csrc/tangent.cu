@@ -509,28 +509,56 @@ constexpr int staged_epb() {
 
 constexpr int kStreamThreads = 256;
 
-// Stream n doubles src -> dst (either may be smem), 16-byte vectors when the
-// two addresses share alignment.
-__device__ __forceinline__ void stream_copy(double* __restrict__ dst, const double* __restrict__ src,
-                                            int n, int tid, int nthreads) {
-  const bool same = (((uintptr_t)dst ^ (uintptr_t)src) & 15u) == 0;
-  if (same) {
-    const int head = (((uintptr_t)src & 15u) != 0) ? 1 : 0;
-    if (tid == 0 && head && n > 0) dst[0] = src[0];
-    const int nv = (n - head) / 2;
-    const double2* s2 = reinterpret_cast<const double2*>(src + head);
-    double2* d2 = reinterpret_cast<double2*>(dst + head);
-    for (int k = tid; k < nv; k += nthreads) d2[k] = s2[k];
-    const int tail = head + 2 * nv;
-    if (tid == 0 && tail < n) dst[tail] = src[tail];
-  } else {
-    for (int k = tid; k < n; k += nthreads) dst[k] = src[k];
-  }
+// --- TMA bulk-copy / mbarrier helpers (sm_90+ PTX, used on sm_100a) --------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// global -> shared, completion counted on the mbarrier (bytes % 16 == 0)
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// shared -> global bulk store, then wait for completion
+__device__ __forceinline__ void tma_store_1d_sync(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// The K_elast range [v0, v1) is read with ONE TMA bulk copy of the enclosing
+// 16-byte-aligned range into the shared image (the K_elast allocation is
+// padded by two doubles), overlapped with the item staging; the image goes
+// back to K with one TMA bulk store of the aligned interior plus at most two
+// edge doubles.
 template <int DIM, int NP, int NQ>
 __global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int npc) {
-  extern __shared__ __align__(16) double img_raw[];
+  extern __shared__ __align__(128) double img_raw[];
+  __shared__ uint64_t s_bar;
   constexpr int NB = NP * (NP + 1) / 2;
   constexpr int D2 = DIM * DIM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -539,14 +567,24 @@ __global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int
   const int nloc = (int)(n1 - n0);
   const int64_t v0 = __ldg(a.nbr_ptr + n0) * D2;
   const int64_t v1 = __ldg(a.nbr_ptr + n1) * D2;
+  const int64_t a0 = v0 & ~int64_t(1), a1 = (v1 + 1) & ~int64_t(1);
   const int64_t i_begin = __ldg(a.n2e_ptr + n0);
   const int nitems = (int)(__ldg(a.n2e_ptr + n1) - i_begin);
-  const int len = (int)(v1 - v0);
-  // layout: [image | item (int) | iptr (int) | vptr (int)]
-  double* img = img_raw + (v0 & 1);  // same 16-byte phase as the global range
+  // layout: [image (aligned to a0) | item (int) | iptr (int) | vptr (int)]
+  double* img = img_raw + (v0 - a0);  // img[k] <-> global v0 + k
   int* s_item = reinterpret_cast<int*>(img_raw + a.max_span + 2);
   int* s_iptr = s_item + a.max_items;
   int* s_vptr = s_iptr + npc + 1;
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0 && a1 > a0) {
+    const unsigned bytes = (unsigned)((a1 - a0) * 8);
+    mbar_expect_tx(&s_bar, bytes);
+    tma_load_1d(img_raw, a.base + a0, bytes, &s_bar);
+  }
   // stage the range's items (plastic ones kept, others -1) and node offsets
   for (int k = tid; k < nitems; k += blockDim.x) {
     const int32_t it = __ldg(a.n2e + i_begin + k);
@@ -556,8 +594,8 @@ __global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int
     s_iptr[k] = (int)(__ldg(a.n2e_ptr + n0 + k) - i_begin);
     s_vptr[k] = (int)(__ldg(a.nbr_ptr + n0 + k) * D2 - v0);
   }
-  stream_copy(img, a.base + v0, len, tid, blockDim.x);
   __syncthreads();
+  if (a1 > a0) mbar_wait(&s_bar, 0);
   for (int ln = warp; ln < nloc; ln += kStreamThreads / 32) {
     const int ib = s_iptr[ln], ie = s_iptr[ln + 1];
     const int row_len = (s_vptr[ln + 1] - s_vptr[ln]) / DIM;
@@ -582,8 +620,14 @@ __global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int
       __syncwarp();
     }
   }
+  fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
   __syncthreads();
-  stream_copy(a.out + v0, img, len, tid, blockDim.x);
+  if (tid == 0 && v1 > v0) {
+    const int64_t s0 = (v0 + 1) & ~int64_t(1), s1 = v1 & ~int64_t(1);
+    if (v0 & 1) a.out[v0] = img[0];
+    if ((v1 & 1) && v1 - 1 >= s0) a.out[v1 - 1] = img[v1 - 1 - v0];
+    if (s1 > s0) tma_store_1d_sync(a.out + s0, img + (s0 - v0), (unsigned)((s1 - s0) * 8));
+  }
 }
 
 __global__ void k_range_span(int64_t n_nodes, int npc, int d2, const int64_t* __restrict__ nbr_ptr,
