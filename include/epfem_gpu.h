@@ -185,6 +185,16 @@ int epfem_assemble_tangent_ds(epfem_ctx* ctx, const epfem_cache* cache, int64_t 
                               const double* DS, const uint8_t* plastic_cols,
                               double* K_values);
 
+/* One Newton iteration's hot path, fused: evaluate_constitutive followed by
+ * assemble_tangent_stiffness (solver.cpp:24,28-29).  Writes out->S,
+ * out->flags and out->D (all three required; the other outputs must be NULL)
+ * and K_values, with the same bits as epfem_constitutive followed by
+ * epfem_assemble_tangent.  The cache's material snapshot must be `mat`'s
+ * moduli. */
+int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* cache, const epfem_material* mat,
+                      const double* E, const double* Ep_prev, const double* Hard_prev,
+                      const epfem_constitutive_out* out, double* K_values);
+
 /* K8: E = B u, 2D embedded in Voigt rows {0,1,3} (assembly.cpp:211-222). */
 int epfem_strains(epfem_ctx* ctx, const epfem_cache* cache, const double* u, double* E);
 /* K9: F = B^T (weight * S) (assembly.cpp:291-301). */

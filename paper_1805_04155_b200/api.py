@@ -603,7 +603,9 @@ class TangentEngine:
     launches in a CUDA graph so a step is one graph launch.
     """
 
-    def __init__(self, cache: AssemblyCache, mat: MaterialField, stream: Optional[torch.cuda.Stream] = None):
+    def __init__(self, cache: AssemblyCache, mat: MaterialField, stream: Optional[torch.cuda.Stream] = None,
+                 fused: bool = True):
+        self.fused = fused
         self.cache = cache
         self.mat = mat
         self.device = cache.device
@@ -623,6 +625,11 @@ class TangentEngine:
     def step(self, E: torch.Tensor, Ep: Optional[torch.Tensor] = None,
              Hard: Optional[torch.Tensor] = None):
         lib = L.lib()
+        if self.fused:
+            _check(lib.epfem_newton_step(self.ctx.handle, self.cache.handle, C.byref(self._mv),
+                                         _ptr(E), _ptr(Ep), _ptr(Hard), C.byref(self._out),
+                                         _ptr(self.K)))
+            return self.S, self.flags, self.D, self.K
         _check(lib.epfem_constitutive(self.ctx.handle, C.byref(self._mv), _ptr(E), _ptr(Ep),
                                       _ptr(Hard), C.byref(self._out)))
         _check(lib.epfem_assemble_tangent(self.ctx.handle, self.cache.handle, self.cache.n_int,

@@ -169,9 +169,9 @@ int epfem_dp_parameters(double c0, double phi, int mode, double* eta, double* c)
   return 0;
 }
 
-int epfem_constitutive(epfem_ctx* ctx, const epfem_material* mat, const double* E,
-                       const double* Ep_prev, const double* Hard_prev,
-                       const epfem_constitutive_out* out) {
+static int const_args(epfem_ctx* ctx, const epfem_material* mat, const double* E,
+                      const double* Ep_prev, const double* Hard_prev,
+                      const epfem_constitutive_out* out, ConstArgs* pa) {
   if (int rc = check_ctx(ctx)) return rc;
   if (!mat || !out) return fail(EPFEM_ERR_INVALID, "evaluate_constitutive: null argument");
   if (mat->n_int < 0) return fail(EPFEM_ERR_INVALID, "evaluate_constitutive: size mismatch");
@@ -180,7 +180,8 @@ int epfem_constitutive(epfem_ctx* ctx, const epfem_material* mat, const double* 
   for (const void* p : ptrs)
     if (!aligned16(p))
       return fail(EPFEM_ERR_INVALID, "evaluate_constitutive: arrays must be 16-byte aligned");
-  ConstArgs a{};
+  ConstArgs& a = *pa;
+  a = ConstArgs{};
   a.n = mat->n_int;
   a.E = E;
   a.Ep = Ep_prev;
@@ -204,6 +205,14 @@ int epfem_constitutive(epfem_ctx* ctx, const epfem_material* mat, const double* 
   a.am = out->apex_mask;
   a.crit = out->crit;
   a.err = ctx->err;
+  return 0;
+}
+
+int epfem_constitutive(epfem_ctx* ctx, const epfem_material* mat, const double* E,
+                       const double* Ep_prev, const double* Hard_prev,
+                       const epfem_constitutive_out* out) {
+  ConstArgs a;
+  if (int rc = const_args(ctx, mat, E, Ep_prev, Hard_prev, out, &a)) return rc;
   if (int rc = launch_constitutive(mat->model, a, ctx->stream, ctx->num_sms)) return rc;
   return finish(ctx);
 }
@@ -415,6 +424,32 @@ int epfem_assemble_tangent(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int, 
 int epfem_assemble_tangent_ds(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int,
                               const double* DS, const uint8_t* plastic_cols, double* K_values) {
   return tangent_common(ctx, c, n_int, DS, plastic_cols, K_values, 2);
+}
+
+int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
+                      const double* E, const double* Ep_prev, const double* Hard_prev,
+                      const epfem_constitutive_out* out, double* K_values) {
+  ConstArgs a;
+  if (int rc = const_args(ctx, mat, E, Ep_prev, Hard_prev, out, &a)) return rc;
+  if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
+  if (mat->n_int != c->info.n_int)
+    return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: size mismatch");
+  if (c->info.n_int > 0 && (!out->S || !out->flags || !out->D))
+    return fail(EPFEM_ERR_INVALID, "newton_step: S, flags and D outputs are required");
+  if (out->DS || out->Ep || out->Hard || out->plastic_mask || out->smooth_mask || out->apex_mask ||
+      out->crit)
+    return fail(EPFEM_ERR_INVALID, "newton_step: only S, flags and D are produced");
+  if (!K_values || !aligned16(K_values))
+    return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: K must be 16-byte aligned");
+  GatherArgs g = gather_args(c);
+  g.D = out->D;
+  g.flags = out->flags;
+  g.base = c->K_elast;
+  g.out = K_values;
+  if (int rc = launch_newton_fused(mat->model, c->info.family, c->info.dim, a, g, ctx->stream))
+    return rc;
+  if (int rc = launch_row_stream(c->info.family, c->info.dim, g, ctx->stream)) return rc;
+  return finish(ctx);
 }
 
 int epfem_strains(epfem_ctx* ctx, const epfem_cache* c, const double* u, double* E) {

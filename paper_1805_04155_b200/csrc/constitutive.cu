@@ -1,4 +1,5 @@
-// K1: fused per-integration-point constitutive update (sm_100a).
+// K1: per-integration-point constitutive update (sm_100a), standalone and
+// fused with the element tangent delta (epfem_newton_step).
 //
 // One thread per integration point.  Reads E, Ep_prev [, Hard_prev] (48 B
 // each, AoS like the reference's 6 x n_int column-major Mat) and writes
@@ -13,9 +14,15 @@
 // the reference's operation order (constitutive.cpp:90-196, voigt.hpp:11-51),
 // so S, D and — what parity requires bit-exactly — the plastic/elastic
 // decision (crit <= 0 is elastic, constitutive.cpp:117,169,172) reproduce the
-// oracle's bits.  The kernel is HBM-bound (~150 B in / 50-250 B out per point
-// vs ~200 flops), so the lost FMA contraction costs nothing measurable.
-#include "kernels.cuh"
+// oracle's bits.  The kernel is HBM-bound, so the lost FMA contraction costs
+// nothing measurable; the fused delta math uses explicit __fma_rn (delta.cuh).
+//
+// k_newton_fused: a CTA owns EPB whole elements (their points are
+// contiguous, m = e * NQ + q).  Phase 1 = the point update above; at plastic
+// points the thread also stages dphi and w (D - C) for the element delta
+// straight from registers (D is never re-read).  Phase 2 builds dK_e
+// (delta.cuh).  The row stream (tangent.cu) then assembles K.
+#include "delta.cuh"
 
 namespace epfem_gpu {
 
@@ -72,6 +79,201 @@ __device__ __forceinline__ void write_tangent(const ConstArgs& a, int64_t q, boo
   }
 }
 
+struct NoSink {
+  template <class F>
+  __device__ __forceinline__ void operator()(F&&) const {}
+};
+
+// The return map at point q (constitutive.cpp:76-196).  `sink(f)` is called
+// at plastic points with the tangent functor f(i, j) = D(i, j).  Returns the
+// plastic flag.
+template <int MODEL, class Sink>
+__device__ __forceinline__ bool eval_point(const ConstArgs& a, int64_t q, Sink& sink) {
+  const double G = a.G ? __ldg(a.G + q) : a.Gu;
+  const double K = a.K ? __ldg(a.K + q) : a.Ku;
+  double e[6], ep[6];
+  load6(a.E, q, e);
+  if (a.Ep) load6(a.Ep, q, ep);
+  else
+#pragma unroll
+    for (int i = 0; i < 6; ++i) ep[i] = 0.0;
+  double etr[6], de[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) etr[i] = e[i] - ep[i];
+  // dev_e = DEV * e_tr, summed in column order
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    double s = devop(i, 0) * etr[0];
+#pragma unroll
+    for (int k = 1; k < 6; ++k) s = s + devop(i, k) * etr[k];
+    de[i] = s;
+  }
+  const double tr = (etr[0] + etr[1]) + etr[2];
+
+  if (MODEL == EPFEM_MODEL_ELASTIC) {
+    // S = C E (constitutive.cpp:76-88), evaluated on E itself
+    double s6[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      double s = cel(K, G, i, 0) * e[0];
+#pragma unroll
+      for (int k = 1; k < 6; ++k) s = s + cel(K, G, i, k) * e[k];
+      s6[i] = s;
+    }
+    if (a.S) store6(a.S, q, s6);
+    if (a.flags) a.flags[q] = 0;
+    if (a.pm) a.pm[q] = 0;
+    if (a.sm) a.sm[q] = 0;
+    if (a.am) a.am[q] = 0;
+    const double z6[6] = {0, 0, 0, 0, 0, 0};
+    if (a.Ep_out) store6(a.Ep_out, q, z6);
+    if (a.Hard_out) store6(a.Hard_out, q, z6);
+    write_tangent(a, q, false, [&](int i, int j) { return cel(K, G, i, j); });
+    return false;
+  } else if (MODEL == EPFEM_MODEL_VON_MISES) {
+    // radial return with linear kinematic hardening (constitutive.cpp:105-134)
+    const double am = a.p1 ? __ldg(a.p1 + q) : a.p1u;
+    const double Y = a.p2 ? __ldg(a.p2 + q) : a.p2u;
+    double h[6];
+    if (a.Hard) load6(a.Hard, q, h);
+    else
+#pragma unroll
+      for (int i = 0; i < 6; ++i) h[i] = 0.0;
+    const double ktr = K * tr;
+    double sig[6], s[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) sig[i] = ktr * iota(i) + 2.0 * G * de[i];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) s[i] = 2.0 * G * de[i] - h[i];
+    const double n1 = s[0] * s[0] + s[1] * s[1] + s[2] * s[2];
+    const double n2 = s[3] * s[3] + s[4] * s[4] + s[5] * s[5];
+    const double ns = sqrt(n1 + 2.0 * n2);
+    const double crit = ns - Y;
+    if (a.crit) a.crit[q] = crit;
+    const bool plastic = !(crit <= 0.0);
+    if (a.flags) a.flags[q] = plastic ? EPFEM_FLAG_PLASTIC : 0;
+    if (a.pm) a.pm[q] = plastic;
+    if (a.sm) a.sm[q] = 0;
+    if (a.am) a.am[q] = 0;
+    if (!plastic) {
+      if (a.S) store6(a.S, q, sig);
+      if (a.Ep_out) store6(a.Ep_out, q, ep);
+      if (a.Hard_out) store6(a.Hard_out, q, h);
+      write_tangent(a, q, false, [&](int i, int j) { return cel(K, G, i, j); });
+      return false;
+    }
+    double nh[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) nh[i] = s[i] / ns;
+    const double denom = 2.0 * G + am;
+    const double lam = crit / denom;
+    double out[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) out[i] = sig[i] - 2.0 * G * lam * nh[i];
+    if (a.S) store6(a.S, q, out);
+    const double c4 = 4.0 * G * G / denom;
+    const double cy = c4 * Y / ns;
+    auto f = [&](int i, int j) {
+      return cel(K, G, i, j) - c4 * devop(i, j) + cy * (devop(i, j) - nh[i] * nh[j]);
+    };
+    write_tangent(a, q, true, f);
+    sink(f);
+    if (a.Hard_out) {
+#pragma unroll
+      for (int i = 0; i < 6; ++i) out[i] = h[i] + (am * lam) * nh[i];
+      store6(a.Hard_out, q, out);
+    }
+    if (a.Ep_out) {
+#pragma unroll
+      for (int i = 0; i < 6; ++i) out[i] = ep[i] + lam * (i < 3 ? nh[i] : nh[i] * 2.0);
+      store6(a.Ep_out, q, out);
+    }
+    return true;
+  } else {
+    // Drucker-Prager perfect plasticity (constitutive.cpp:152-194)
+    const double eta = a.p1 ? __ldg(a.p1 + q) : a.p1u;
+    const double c = a.p2 ? __ldg(a.p2 + q) : a.p2u;
+    const double sqrt2 = sqrt(2.0);
+    double dot = etr[0] * de[0];
+#pragma unroll
+    for (int i = 1; i < 6; ++i) dot = dot + etr[i] * de[i];
+    const double ne = sqrt(fmax(0.0, dot));
+    const double rho = 2.0 * G * ne;
+    const double p = K * tr;
+    const double da = K * eta * eta;
+    const double dsm = G + da;
+    const double crit1 = rho / sqrt2 + eta * p - c;
+    const double crit2 = eta * p - da * rho / (G * sqrt2) - c;
+    double sig[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) sig[i] = p * iota(i) + 2.0 * G * de[i];
+    const double z6[6] = {0, 0, 0, 0, 0, 0};
+    if (a.Hard_out) store6(a.Hard_out, q, z6);  // evaluate_constitutive keeps Hard = 0 for DP
+    if (crit1 <= 0.0) {
+      if (a.flags) a.flags[q] = 0;
+      if (a.pm) a.pm[q] = 0;
+      if (a.sm) a.sm[q] = 0;
+      if (a.am) a.am[q] = 0;
+      if (a.S) store6(a.S, q, sig);
+      if (a.Ep_out) store6(a.Ep_out, q, ep);
+      write_tangent(a, q, false, [&](int i, int j) { return cel(K, G, i, j); });
+      return false;
+    }
+    if (crit2 <= 0.0) {
+      if (a.flags) a.flags[q] = EPFEM_FLAG_PLASTIC | EPFEM_FLAG_SMOOTH;
+      if (a.pm) a.pm[q] = 1;
+      if (a.sm) a.sm[q] = 1;
+      if (a.am) a.am[q] = 0;
+      if (ne <= 0.0) {
+        raise_dev(a.err, EPFEM_ERR_ZERO_DEVIATOR, (unsigned long long)q);
+        return false;
+      }
+      const double lam = crit1 / dsm;
+      double nh[6], mh[6], out[6];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) nh[i] = de[i] / ne;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) mh[i] = sqrt2 * G * nh[i] + K * eta * iota(i);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) out[i] = sig[i] - lam * mh[i];
+      if (a.S) store6(a.S, q, out);
+      const double c1 = 2.0 * sqrt2 * G * G * lam / rho;
+      auto f = [&](int i, int j) {
+        return cel(K, G, i, j) - c1 * (devop(i, j) - nh[i] * nh[j]) - mh[i] * mh[j] / dsm;
+      };
+      write_tangent(a, q, true, f);
+      sink(f);
+      if (a.Ep_out) {
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const double nst = i < 3 ? nh[i] : nh[i] * 2.0;
+          out[i] = ep[i] + lam * ((sqrt2 / 2.0) * nst + (eta / 3.0) * iota(i));
+        }
+        store6(a.Ep_out, q, out);
+      }
+      return true;
+    }
+    if (a.flags) a.flags[q] = EPFEM_FLAG_PLASTIC | EPFEM_FLAG_APEX;
+    if (a.pm) a.pm[q] = 1;
+    if (a.sm) a.sm[q] = 0;
+    if (a.am) a.am[q] = 1;
+    double out[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) out[i] = (c / eta) * iota(i);
+    if (a.S) store6(a.S, q, out);
+    auto f = [&](int, int) { return 0.0; };
+    write_tangent(a, q, true, f);
+    sink(f);
+    if (a.Ep_out) {
+      const double sh = c / (3.0 * K * eta);
+#pragma unroll
+      for (int i = 0; i < 6; ++i) out[i] = e[i] - sh * iota(i);
+      store6(a.Ep_out, q, out);
+    }
+    return true;
+  }
+}
+
 // LEAN: the hot-path instance (S, flags, packed D only); the reference-layout
 // outputs are compiled out so the kernel keeps its registers low.
 template <int MODEL, bool LEAN>
@@ -82,181 +284,45 @@ __global__ void __launch_bounds__(256) k_constitutive(ConstArgs a) {
     a.pm = a.sm = a.am = nullptr;
     a.crit = nullptr;
   }
+  NoSink none;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < a.n; q += stride) {
-    const double G = a.G ? __ldg(a.G + q) : a.Gu;
-    const double K = a.K ? __ldg(a.K + q) : a.Ku;
-    double e[6], ep[6];
-    load6(a.E, q, e);
-    if (a.Ep) load6(a.Ep, q, ep);
-    else
-#pragma unroll
-      for (int i = 0; i < 6; ++i) ep[i] = 0.0;
-    double etr[6], de[6];
-#pragma unroll
-    for (int i = 0; i < 6; ++i) etr[i] = e[i] - ep[i];
-    // dev_e = DEV * e_tr, summed in column order
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {
-      double s = devop(i, 0) * etr[0];
-#pragma unroll
-      for (int k = 1; k < 6; ++k) s = s + devop(i, k) * etr[k];
-      de[i] = s;
-    }
-    const double tr = (etr[0] + etr[1]) + etr[2];
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < a.n; q += stride)
+    eval_point<MODEL>(a, q, none);
+}
 
-    if (MODEL == EPFEM_MODEL_ELASTIC) {
-      // S = C E (constitutive.cpp:76-88), evaluated on E itself
-      double s6[6];
-#pragma unroll
-      for (int i = 0; i < 6; ++i) {
-        double s = cel(K, G, i, 0) * e[0];
-#pragma unroll
-        for (int k = 1; k < 6; ++k) s = s + cel(K, G, i, k) * e[k];
-        s6[i] = s;
-      }
-      if (a.S) store6(a.S, q, s6);
-      if (a.flags) a.flags[q] = 0;
-      if (a.pm) a.pm[q] = 0;
-      if (a.sm) a.sm[q] = 0;
-      if (a.am) a.am[q] = 0;
-      const double z6[6] = {0, 0, 0, 0, 0, 0};
-      if (a.Ep_out) store6(a.Ep_out, q, z6);
-      if (a.Hard_out) store6(a.Hard_out, q, z6);
-      write_tangent(a, q, false, [&](int i, int j) { return cel(K, G, i, j); });
-    } else if (MODEL == EPFEM_MODEL_VON_MISES) {
-      // radial return with linear kinematic hardening (constitutive.cpp:105-134)
-      const double am = a.p1 ? __ldg(a.p1 + q) : a.p1u;
-      const double Y = a.p2 ? __ldg(a.p2 + q) : a.p2u;
-      double h[6];
-      if (a.Hard) load6(a.Hard, q, h);
-      else
-#pragma unroll
-        for (int i = 0; i < 6; ++i) h[i] = 0.0;
-      const double ktr = K * tr;
-      double sig[6], s[6];
-#pragma unroll
-      for (int i = 0; i < 6; ++i) sig[i] = ktr * iota(i) + 2.0 * G * de[i];
-#pragma unroll
-      for (int i = 0; i < 6; ++i) s[i] = 2.0 * G * de[i] - h[i];
-      const double n1 = s[0] * s[0] + s[1] * s[1] + s[2] * s[2];
-      const double n2 = s[3] * s[3] + s[4] * s[4] + s[5] * s[5];
-      const double ns = sqrt(n1 + 2.0 * n2);
-      const double crit = ns - Y;
-      if (a.crit) a.crit[q] = crit;
-      const bool plastic = !(crit <= 0.0);
-      if (a.flags) a.flags[q] = plastic ? EPFEM_FLAG_PLASTIC : 0;
-      if (a.pm) a.pm[q] = plastic;
-      if (a.sm) a.sm[q] = 0;
-      if (a.am) a.am[q] = 0;
-      if (!plastic) {
-        if (a.S) store6(a.S, q, sig);
-        if (a.Ep_out) store6(a.Ep_out, q, ep);
-        if (a.Hard_out) store6(a.Hard_out, q, h);
-        write_tangent(a, q, false, [&](int i, int j) { return cel(K, G, i, j); });
-      } else {
-        double nh[6];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) nh[i] = s[i] / ns;
-        const double denom = 2.0 * G + am;
-        const double lam = crit / denom;
-        double out[6];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) out[i] = sig[i] - 2.0 * G * lam * nh[i];
-        if (a.S) store6(a.S, q, out);
-        const double c4 = 4.0 * G * G / denom;
-        const double cy = c4 * Y / ns;
-        write_tangent(a, q, true, [&](int i, int j) {
-          return cel(K, G, i, j) - c4 * devop(i, j) + cy * (devop(i, j) - nh[i] * nh[j]);
-        });
-        if (a.Hard_out) {
-#pragma unroll
-          for (int i = 0; i < 6; ++i) out[i] = h[i] + (am * lam) * nh[i];
-          store6(a.Hard_out, q, out);
-        }
-        if (a.Ep_out) {
-#pragma unroll
-          for (int i = 0; i < 6; ++i) out[i] = ep[i] + lam * (i < 3 ? nh[i] : nh[i] * 2.0);
-          store6(a.Ep_out, q, out);
-        }
-      }
-    } else {
-      // Drucker-Prager perfect plasticity (constitutive.cpp:152-194)
-      const double eta = a.p1 ? __ldg(a.p1 + q) : a.p1u;
-      const double c = a.p2 ? __ldg(a.p2 + q) : a.p2u;
-      const double sqrt2 = sqrt(2.0);
-      double dot = etr[0] * de[0];
-#pragma unroll
-      for (int i = 1; i < 6; ++i) dot = dot + etr[i] * de[i];
-      const double ne = sqrt(fmax(0.0, dot));
-      const double rho = 2.0 * G * ne;
-      const double p = K * tr;
-      const double da = K * eta * eta;
-      const double dsm = G + da;
-      const double crit1 = rho / sqrt2 + eta * p - c;
-      const double crit2 = eta * p - da * rho / (G * sqrt2) - c;
-      double sig[6];
-#pragma unroll
-      for (int i = 0; i < 6; ++i) sig[i] = p * iota(i) + 2.0 * G * de[i];
-      const double z6[6] = {0, 0, 0, 0, 0, 0};
-      if (a.Hard_out) store6(a.Hard_out, q, z6);  // evaluate_constitutive keeps Hard = 0 for DP
-      if (crit1 <= 0.0) {
-        if (a.flags) a.flags[q] = 0;
-        if (a.pm) a.pm[q] = 0;
-        if (a.sm) a.sm[q] = 0;
-        if (a.am) a.am[q] = 0;
-        if (a.S) store6(a.S, q, sig);
-        if (a.Ep_out) store6(a.Ep_out, q, ep);
-        write_tangent(a, q, false, [&](int i, int j) { return cel(K, G, i, j); });
-      } else if (crit2 <= 0.0) {
-        if (a.flags) a.flags[q] = EPFEM_FLAG_PLASTIC | EPFEM_FLAG_SMOOTH;
-        if (a.pm) a.pm[q] = 1;
-        if (a.sm) a.sm[q] = 1;
-        if (a.am) a.am[q] = 0;
-        if (ne <= 0.0) {
-          raise_dev(a.err, EPFEM_ERR_ZERO_DEVIATOR, (unsigned long long)q);
-          continue;
-        }
-        const double lam = crit1 / dsm;
-        double nh[6], mh[6], out[6];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) nh[i] = de[i] / ne;
-#pragma unroll
-        for (int i = 0; i < 6; ++i) mh[i] = sqrt2 * G * nh[i] + K * eta * iota(i);
-#pragma unroll
-        for (int i = 0; i < 6; ++i) out[i] = sig[i] - lam * mh[i];
-        if (a.S) store6(a.S, q, out);
-        const double c1 = 2.0 * sqrt2 * G * G * lam / rho;
-        write_tangent(a, q, true, [&](int i, int j) {
-          return cel(K, G, i, j) - c1 * (devop(i, j) - nh[i] * nh[j]) - mh[i] * mh[j] / dsm;
-        });
-        if (a.Ep_out) {
-#pragma unroll
-          for (int i = 0; i < 6; ++i) {
-            const double nst = i < 3 ? nh[i] : nh[i] * 2.0;
-            out[i] = ep[i] + lam * ((sqrt2 / 2.0) * nst + (eta / 3.0) * iota(i));
-          }
-          store6(a.Ep_out, q, out);
-        }
-      } else {
-        if (a.flags) a.flags[q] = EPFEM_FLAG_PLASTIC | EPFEM_FLAG_APEX;
-        if (a.pm) a.pm[q] = 1;
-        if (a.sm) a.sm[q] = 0;
-        if (a.am) a.am[q] = 1;
-        double out[6];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) out[i] = (c / eta) * iota(i);
-        if (a.S) store6(a.S, q, out);
-        write_tangent(a, q, true, [&](int, int) { return 0.0; });
-        if (a.Ep_out) {
-          const double sh = c / (3.0 * K * eta);
-#pragma unroll
-          for (int i = 0; i < 6; ++i) out[i] = e[i] - sh * iota(i);
-          store6(a.Ep_out, q, out);
-        }
-      }
-    }
+constexpr int kFusedBudget = 5120;  // doubles of staged records per CTA (40 KB)
+
+template <int MODEL, int DIM, int NP, int NQ>
+__global__ void __launch_bounds__(256) k_newton_fused(ConstArgs c, GatherArgs g) {
+  using Cfg = DeltaCfg<DIM, NP>;
+  constexpr int EPB = delta_epb<DIM, NP, NQ, kFusedBudget>();
+  __shared__ double s_st[EPB][NQ][Cfg::REC];
+  __shared__ unsigned s_mask[EPB];
+  c.DS = nullptr;  // hot path: S, flags, packed D only
+  c.Ep_out = c.Hard_out = nullptr;
+  c.pm = c.sm = c.am = nullptr;
+  c.crit = nullptr;
+
+  const int tid = threadIdx.x;
+  const int64_t e0 = (int64_t)blockIdx.x * EPB;
+  if (tid < EPB) s_mask[tid] = 0u;
+  __syncthreads();
+  for (int k = tid; k < EPB * NQ; k += blockDim.x) {
+    const int le = k / NQ, q = k - le * NQ;
+    const int64_t e = e0 + le;
+    if (e >= g.n_elements) continue;
+    const int64_t m = e * NQ + q;
+    double* st = s_st[le][q];
+    auto stage = [&](auto&& f) {
+      atomicOr(&s_mask[le], 1u << q);
+      stage_geometry<DIM, NP>(st, g.inv + m * Cfg::D2, g.gradhat, q);
+      stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f);
+    };
+    eval_point<MODEL>(c, m, stage);
   }
+  __syncthreads();
+  if (tid < EPB && e0 + tid < g.n_elements) g.emask[e0 + tid] = s_mask[tid];
+  delta_phase2<DIM, NP, NQ, EPB>(s_st, s_mask, tid, e0, g.n_elements, g.scratch);
 }
 
 }  // namespace
@@ -283,6 +349,31 @@ int launch_constitutive(int model, const ConstArgs& a, cudaStream_t st, int num_
       break;
     default: return fail(EPFEM_ERR_INVALID, "evaluate_constitutive: unknown material model");
   }
+  EPFEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
+                        cudaStream_t st) {
+  if (g.n_elements == 0) return 0;
+  bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
+    constexpr int DIM = decltype(D)::value;
+    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
+    constexpr int EPB = delta_epb<DIM, NP, NQ, kFusedBudget>();
+    const unsigned blocks = (unsigned)((g.n_elements + EPB - 1) / EPB);
+    switch (model) {
+      case EPFEM_MODEL_VON_MISES:
+        k_newton_fused<EPFEM_MODEL_VON_MISES, DIM, NP, NQ><<<blocks, 256, 0, st>>>(c, g);
+        break;
+      case EPFEM_MODEL_DRUCKER_PRAGER:
+        k_newton_fused<EPFEM_MODEL_DRUCKER_PRAGER, DIM, NP, NQ><<<blocks, 256, 0, st>>>(c, g);
+        break;
+      default:
+        k_newton_fused<EPFEM_MODEL_ELASTIC, DIM, NP, NQ><<<blocks, 256, 0, st>>>(c, g);
+        break;
+    }
+  });
+  if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
   EPFEM_CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -1,0 +1,184 @@
+// Element tangent-delta building blocks shared by the standalone pass
+// (tangent.cu) and the fused constitutive + delta kernel (constitutive.cu).
+// All multiply-adds are explicit __fma_rn so both translation units (one is
+// compiled with --fmad=false) produce identical bits.
+//
+//   staged record per (element, point), REC doubles in shared memory:
+//     [ dphi_p (NP x DIM) | Dw = w (D - C), packed upper triangle (NSP) ]
+//   workspace record per element (global), NB = NP(NP+1)/2 blocks of dim x dim:
+//     block (a, b), a <= b, at blk_index(a, b) * dim^2, row-major
+#pragma once
+
+#include "kernels.cuh"
+
+namespace epfem_gpu {
+
+template <int NP>
+__host__ __device__ constexpr int blk_index(int a, int b) {  // a <= b
+  return a * (2 * NP - a + 1) / 2 + (b - a);
+}
+
+template <int DIM, int NP>
+struct DeltaCfg {
+  static constexpr int NS = DIM == 3 ? 6 : 3;
+  static constexpr int NSP = NS * (NS + 1) / 2;
+  static constexpr int D2 = DIM * DIM;
+  static constexpr int NB = NP * (NP + 1) / 2;
+  static constexpr int REC = NP * DIM + NSP;
+  // block-row chunks per node in phase 2 (register budget)
+  static constexpr int BCH = DIM == 2 ? 1 : (NP <= 4 ? 1 : (NP <= 10 ? 2 : 4));
+  static constexpr int CS = (NP + BCH - 1) / BCH;
+};
+
+// elements per CTA: phase-2 threads (NP * BCH per element) fit 256 threads and
+// the staged records fit BUDGET doubles of shared memory
+template <int DIM, int NP, int NQ, int BUDGET>
+__host__ __device__ constexpr int delta_epb() {
+  constexpr int E1 = 256 / (NP * DeltaCfg<DIM, NP>::BCH);
+  constexpr int E2 = BUDGET / (NQ * DeltaCfg<DIM, NP>::REC);
+  constexpr int E = E1 < E2 ? E1 : E2;
+  return E > 0 ? E : 1;
+}
+
+// assembly row r -> Voigt row (2D plane strain uses {0,1,3}, assembly.cpp:92)
+template <int DIM>
+__device__ __forceinline__ constexpr int arow(int r) {
+  return (DIM == 2 && r == 2) ? 3 : r;
+}
+
+// dphi_p = J^-1 ghat_p for every node of the element at point q.
+template <int DIM, int NP>
+__device__ __forceinline__ void stage_geometry(double* st, const double* __restrict__ inv_m,
+                                               const double* __restrict__ gradhat, int q) {
+  double J[DIM * DIM];
+#pragma unroll
+  for (int t = 0; t < DIM * DIM; ++t) J[t] = __ldg(inv_m + t);
+#pragma unroll 4
+  for (int p = 0; p < NP; ++p) {
+    const double* gh = gradhat + (q * NP + p) * DIM;
+    double g[DIM];
+#pragma unroll
+    for (int j = 0; j < DIM; ++j) g[j] = __ldg(gh + j);
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) {
+      double s = __dmul_rn(J[i], g[0]);
+#pragma unroll
+      for (int j = 1; j < DIM; ++j) s = __fma_rn(J[j * DIM + i], g[j], s);
+      st[p * DIM + i] = s;
+    }
+  }
+}
+
+// Dw(r, c) = w (D(R r, R c) - C(R r, R c)) packed upper triangle.  Dfun gives
+// the tangent entry D(i, j) in Voigt indices.
+template <int DIM, class Dfun>
+__device__ __forceinline__ void stage_dw(double* dwst, double w, const GatherArgs& a, int64_t m,
+                                         Dfun&& Dv) {
+  constexpr int NS = DIM == 3 ? 6 : 3;
+  const bool uniform_c = a.shear == nullptr && a.bulk == nullptr;
+  double G2 = 0.0, Km = 0.0;
+  if (!uniform_c) {
+    G2 = 2.0 * (a.shear ? __ldg(a.shear + m) : a.shear_u);
+    Km = a.bulk ? __ldg(a.bulk + m) : a.bulk_u;
+  }
+  int k = 0;
+#pragma unroll
+  for (int r = 0; r < NS; ++r)
+#pragma unroll
+    for (int c = r; c < NS; ++c, ++k) {
+      const int ri = arow<DIM>(r), ci = arow<DIM>(c);
+      const double vol = (ri < 3 && ci < 3) ? 1.0 : 0.0;
+      const double dev = ((ri == ci) ? (ri < 3 ? 1.0 : 0.5) : 0.0) - vol / 3.0;
+      const double cel = uniform_c ? a.Cu[pk_index(ri, ci)] : __fma_rn(G2, dev, __dmul_rn(Km, vol));
+      dwst[k] = __dmul_rn(w, __dsub_rn(Dv(ri, ci), cel));
+    }
+}
+
+// Phase 2: thread (element le, node pa, chunk ch) accumulates the blocks
+// (pa, b) for the b of its chunk over the element's plastic points from the
+// staged records, then writes the blocks with b >= pa to the workspace.
+template <int DIM, int NP, int NQ, int EPB>
+__device__ __forceinline__ void delta_phase2(const double (*s_st)[NQ][DeltaCfg<DIM, NP>::REC],
+                                             const unsigned* s_mask, int tid, int64_t e0,
+                                             int64_t n_elements, double* __restrict__ scratch) {
+  using Cfg = DeltaCfg<DIM, NP>;
+  constexpr int NS = Cfg::NS, D2 = Cfg::D2, NB = Cfg::NB, BCH = Cfg::BCH, CS = Cfg::CS;
+  if (tid >= EPB * NP * BCH) return;
+  const int le = tid / (NP * BCH);
+  const int rr = tid - le * (NP * BCH);
+  const int pa = rr / BCH, ch = rr - pa * BCH;
+  const int b0 = ch * CS;
+  const int64_t e = e0 + le;
+  if (e >= n_elements) return;
+  unsigned mask = s_mask[le];
+  if (!mask) return;
+  double blk[CS][DIM][DIM];
+#pragma unroll
+  for (int b = 0; b < CS; ++b)
+#pragma unroll
+    for (int i = 0; i < DIM; ++i)
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) blk[b][i][j] = 0.0;
+  while (mask) {
+    const int q = __ffs(mask) - 1;
+    mask &= mask - 1u;
+    const double* st = s_st[le][q];
+    const double* dw = st + NP * DIM;
+    auto Dw = [&](int r, int c) {  // compile-time indices after unrolling
+      const int lo = r < c ? r : c, hi = r < c ? c : r;
+      return dw[lo * NS - lo * (lo - 1) / 2 + (hi - lo)];
+    };
+    double ga[DIM];
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) ga[i] = st[pa * DIM + i];
+    double T[DIM][NS];  // T_a = B_a^T Dw
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+      if constexpr (DIM == 3) {
+        // B rows e11,e22,e33,2e12,2e23,2e31 (assembly.cpp:162-171)
+        T[0][c] = __fma_rn(ga[2], Dw(5, c), __fma_rn(ga[1], Dw(3, c), __dmul_rn(ga[0], Dw(0, c))));
+        T[1][c] = __fma_rn(ga[2], Dw(4, c), __fma_rn(ga[0], Dw(3, c), __dmul_rn(ga[1], Dw(1, c))));
+        T[DIM - 1][c] =
+            __fma_rn(ga[0], Dw(5, c), __fma_rn(ga[1], Dw(4, c), __dmul_rn(ga[2], Dw(2, c))));
+      } else {
+        // rows e11, e22, 2e12 (assembly.cpp:173-176)
+        T[0][c] = __fma_rn(ga[1], Dw(2, c), __dmul_rn(ga[0], Dw(0, c)));
+        T[1][c] = __fma_rn(ga[0], Dw(2, c), __dmul_rn(ga[1], Dw(1, c)));
+      }
+    }
+#pragma unroll
+    for (int bb = 0; bb < CS; ++bb) {
+      const int b = b0 + bb;
+      if (b >= NP) break;
+      const double* h = st + b * DIM;
+      const double h0 = h[0], h1 = h[1], h2 = DIM == 3 ? h[DIM - 1] : 0.0;
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        if constexpr (DIM == 3) {
+          blk[bb][i][0] = __fma_rn(T[i][5], h2, __fma_rn(T[i][3], h1, __fma_rn(T[i][0], h0, blk[bb][i][0])));
+          blk[bb][i][1] = __fma_rn(T[i][4], h2, __fma_rn(T[i][3], h0, __fma_rn(T[i][1], h1, blk[bb][i][1])));
+          blk[bb][i][DIM - 1] =
+              __fma_rn(T[i][5], h0, __fma_rn(T[i][4], h1, __fma_rn(T[i][2], h2, blk[bb][i][DIM - 1])));
+        } else {
+          blk[bb][i][0] = __fma_rn(T[i][2], h1, __fma_rn(T[i][0], h0, blk[bb][i][0]));
+          blk[bb][i][1] = __fma_rn(T[i][2], h0, __fma_rn(T[i][1], h1, blk[bb][i][1]));
+        }
+      }
+    }
+  }
+  double* rec = scratch + (size_t)e * NB * D2;
+#pragma unroll
+  for (int bb = 0; bb < CS; ++bb) {
+    const int b = b0 + bb;
+    if (b >= NP) break;
+    if (b >= pa) {
+      double* o = rec + blk_index<NP>(pa, b) * D2;
+#pragma unroll
+      for (int i = 0; i < DIM; ++i)
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) o[i * DIM + j] = blk[bb][i][j];
+    }
+  }
+}
+
+}  // namespace epfem_gpu

@@ -77,6 +77,9 @@ int build_pattern(int family, int dim, int64_t n_nodes, int64_t n_e, const int32
                   cudaStream_t st, int num_sms, PatternOut* o);
 int launch_gather(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);
 int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);
+int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st);
+int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
+                        cudaStream_t st);
 size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements);
 int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
                     cudaStream_t st, int* npc_out, int* span_out, int* items_out);

@@ -266,6 +266,12 @@ def test_config_pipeline_vs_oracle(cuda, oracle, name):
     eng.replay()
     torch.cuda.synchronize()
     assert np.array_equal(_np(eng.K).view(np.uint64), _np(Kv).view(np.uint64))
+    # the fused Newton step and the separate constitutive + tangent calls agree bitwise
+    sep = P.TangentEngine(gc, mat, fused=False)
+    S2, f2, D2, K2 = sep.step(Et)
+    sep.sync()
+    assert np.array_equal(_np(f2), _np(eng.flags)) and np.array_equal(_np(S2), _np(eng.S))
+    assert np.array_equal(_np(K2).view(np.uint64), _np(eng.K).view(np.uint64))
 
 
 # ---------------------------------------------------------------------------
