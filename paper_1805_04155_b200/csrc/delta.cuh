@@ -32,9 +32,9 @@ struct DeltaCfg {
 
 // elements per CTA: phase-2 threads (NP * BCH per element) fit 256 threads and
 // the staged records fit BUDGET doubles of shared memory
-template <int DIM, int NP, int NQ, int BUDGET>
+template <int DIM, int NP, int NQ, int BUDGET, int THREADS = 256>
 __host__ __device__ constexpr int delta_epb() {
-  constexpr int E1 = 256 / (NP * DeltaCfg<DIM, NP>::BCH);
+  constexpr int E1 = THREADS / (NP * DeltaCfg<DIM, NP>::BCH);
   constexpr int E2 = BUDGET / (NQ * DeltaCfg<DIM, NP>::REC);
   constexpr int E = E1 < E2 ? E1 : E2;
   return E > 0 ? E : 1;
