@@ -45,12 +45,14 @@ def load_peaks():
 # algorithmic bytes
 
 def algorithmic_bytes(cfg, n_int, n_plastic, nnz, n_nodes, n_e, n_p):
+    """constitutive 8 (E + Ep [+ Hard for VM] + S) + 1 flag
+    byte per point + 288 B of D per plastic point; assembly one write of
+    every K value + coordinates + connectivity."""
     hist = 6 if cfg.model == "vm" else 0  # Hard read only for VM
     epr = 6 if cfg.model != "elastic" else 0
     constitutive = 8 * (6 + epr + hist + 6) * n_int + n_int + 288 * n_plastic
     assembly = 8 * nnz + 8 * cfg.dim * n_nodes + 4 * n_p * n_e
-    tangent_kernel = 8 * nnz + 288 * n_plastic + n_int + 8 * cfg.dim * n_nodes + 4 * n_p * n_e
-    return constitutive, assembly, tangent_kernel
+    return constitutive, assembly
 
 
 # ---------------------------------------------------------------------------
@@ -216,6 +218,80 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_slabs(args, rank, world, dev, cfg):
+    """N GPUs: one z-slab (y-slab in 2D) of the configuration's mesh per rank,
+    interface-layer exchange over NCCL each step (paper_1805_04155_b200/dist.py).
+    Strong scaling: the total work is the whole mesh."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.dist import DistributedTangent, make_plan
+    from paper_1805_04155_b200.synthetic import displacement, plastic_fraction
+    plan = make_plan(cfg.family, cfg.dim, cfg.n, world, rank)
+    eng = DistributedTangent(plan, cfg.material, dev)
+    u = torch.from_numpy(displacement(plan.mesh.coord, cfg.seed)).to(dev)
+    E1 = eng.cache.strains(u)
+    p0, p1 = plan.own_points
+    E1 = E1[p0:p1].contiguous()
+    # global amplitude: bisection on the all-reduced plastic count
+    target = cfg.target if args.target is None else args.target
+    n_own = torch.tensor([p1 - p0], dtype=torch.float64, device=dev)
+    dist.all_reduce(n_own)
+
+    def gfrac(s):
+        f = torch.tensor([plastic_fraction(s * E1, eng.mat_own) * (p1 - p0)], dtype=torch.float64,
+                         device=dev)
+        dist.all_reduce(f)
+        return float(f) / float(n_own)
+
+    lo, hi = 0.0, 1.0
+    while gfrac(hi) < target and hi < 1e12:
+        lo, hi = hi, hi * 4.0
+    for _ in range(40):
+        mid = 0.5 * (lo + hi)
+        lo, hi = (mid, hi) if gfrac(mid) < target else (lo, mid)
+    E = (hi * E1).contiguous()
+    Ep0 = torch.zeros_like(E)
+    Hard0 = torch.zeros_like(E) if cfg.model == "vm" else None
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        eng.step(E, Ep0, Hard0)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            eng.step(E, Ep0, Hard0)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    dist.barrier()
+    t = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t) / args.steps
+    n_total = float(n_own)
+    npl = torch.tensor([float((eng.flags[p0:p1] & 1).sum())], dtype=torch.float64, device=dev)
+    dist.all_reduce(npl)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": n_total / (ms_per_step * 1e-3), "unit": "ip/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "element": f"{cfg.family} {cfg.dim}D",
+                       "mesh": f"{cfg.n}^{cfg.dim}", "model": cfg.model, "n_int": int(n_total),
+                       "plastic_fraction": float(npl) / n_total,
+                       "parallelism": f"slab x{world} (one halo cell layer, NCCL interface exchange)",
+                       "l2": "inputs larger than L2"},
+            "gpu_launches": 3 * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -251,17 +327,19 @@ def main():
     import paper_1805_04155_b200 as P
     from paper_1805_04155_b200.synthetic import CONFIGS, make_workload
     cfg = CONFIGS[args.config]
-    z_range = None
-    if world > 1:
-        # weak scaling: every rank owns a full copy-sized workload (replica);
-        # see DESIGN.md §Multi-GPU for the slab partition of one mesh.
-        pass
-    wl = make_workload(cfg, target=args.target, device=dev, z_range=z_range)
+    if world > 1 and cfg.model != "elastic":
+        return run_slabs(args, rank, world, dev, cfg)
+    wl = make_workload(cfg, target=args.target, device=dev)
     cache, mat = wl.cache, wl.mat
     n_int, nnz = cache.n_int, cache.nnz
     stream = torch.cuda.Stream(dev)
     eng = P.TangentEngine(cache, mat, stream=stream)
     E = wl.E.contiguous()
+    # plastic history of the previous time step: zero (BASELINE configs), but
+    # passed as real arrays and read every step like the reference does
+    # (evaluate_constitutive reads prev.Ep / prev.Hard, solver.cpp:24)
+    Ep0 = torch.zeros_like(E) if cfg.model != "elastic" else None
+    Hard0 = torch.zeros_like(E) if cfg.model == "vm" else None
     hbm_peak, peak_src = load_peaks()
 
     def barrier():
@@ -287,11 +365,11 @@ def main():
         launches_per_step = 1
     else:
         with torch.cuda.stream(stream):
-            eng.capture(E)
+            eng.capture(E, Ep0, Hard0)
 
         def launch():
             eng.replay()
-        launches_per_step = 2
+        launches_per_step = 2  # k_newton_fused + k_row_stream (one CUDA graph)
 
     # warm-up
     for _ in range(args.warmup):
@@ -313,31 +391,38 @@ def main():
 
     n_plastic = int((eng.flags & 1).sum().item()) if not elastic else 0
     info = cache.info
-    cons_b, asm_b, tan_b = algorithmic_bytes(cfg, n_int, n_plastic, nnz, info.n_nodes,
-                                             info.n_elements, info.n_p)
-    # per-kernel device time on the launching stream (not graph-captured)
-    k_ms = {}
+    cons_b, asm_b = algorithmic_bytes(cfg, n_int, n_plastic, nnz, info.n_nodes,
+                                      info.n_elements, info.n_p)
+    # per-kernel device time, each half of the step launched alone on the
+    # stream (the same kernels the graph replays), CUDA events around it
+    k_ms, k_gbs = {}, {}
     if not elastic:
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         lib = P.api.L.lib()
+        C_ = P.api.C
         tot_c = tot_t = 0.0
         reps = max(args.steps, 5)
         for _ in range(reps):
             evs[0].record(stream)
-            P.api._check(lib.epfem_constitutive(eng.ctx.handle, P.api.C.byref(eng._mv), P.api._ptr(E),
-                                                None, None, P.api.C.byref(eng._out)))
+            P.api._check(lib.epfem_constitutive_delta(eng.ctx.handle, cache.handle, C_.byref(eng._mv),
+                                                      P.api._ptr(E), P.api._ptr(Ep0),
+                                                      P.api._ptr(Hard0), C_.byref(eng._out)))
             evs[1].record(stream)
-            P.api._check(lib.epfem_assemble_tangent(eng.ctx.handle, cache.handle, n_int,
-                                                    P.api._ptr(eng.D), P.api._ptr(eng.flags),
-                                                    P.api._ptr(eng.K)))
+            P.api._check(lib.epfem_assemble_rows(eng.ctx.handle, cache.handle, P.api._ptr(eng.K)))
             evs[2].record(stream)
             torch.cuda.synchronize(dev)
             tot_c += evs[0].elapsed_time(evs[1])
             tot_t += evs[1].elapsed_time(evs[2])
-        k_ms = {"constitutive": tot_c / reps, "tangent": tot_t / reps}
-        dom_bytes, dom_ms, dom = tan_b, k_ms["tangent"], "tangent (K2+K6 row-block gather)"
+        k_ms = {"k_newton_fused (constitutive + element delta)": tot_c / reps,
+                "k_row_stream (K = K_elast + sum dK_e)": tot_t / reps}
+        k_gbs = {"k_newton_fused (constitutive + element delta)": cons_b / (tot_c / reps * 1e-3) / 1e9,
+                 "k_row_stream (K = K_elast + sum dK_e)": asm_b / (tot_t / reps * 1e-3) / 1e9}
+        if tot_t >= tot_c:
+            dom_bytes, dom_ms, dom = asm_b, tot_t / reps, "k_row_stream (K = K_elast + sum dK_e)"
+        else:
+            dom_bytes, dom_ms, dom = cons_b, tot_c / reps, "k_newton_fused (constitutive + element delta)"
     else:
-        dom_bytes, dom_ms, dom = asm_b, ms_per_step, "elastic (K5 row-block gather)"
+        dom_bytes, dom_ms, dom = asm_b, ms_per_step, "k_gather<elastic> (K5)"
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     step_bytes = cons_b + asm_b if not elastic else asm_b
     step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
@@ -345,15 +430,21 @@ def main():
     # ------------------------------------------------------------------ e2e
     e2e = None
     if not args.no_e2e:
-        hE = torch.empty_like(E, device="cpu").pin_memory()
-        hE.copy_(E)
+        # the reference-facing call with HOST buffers: E, Ep, Hard in (pinned,
+        # H2D every step), S, flag bytes and K values out (D2H every step);
+        # the packed D stays on the device (its consumer, the tangent
+        # assembly, runs inside the same call)
+        host_in = [E] + [x for x in (Ep0, Hard0) if x is not None]
+        h_in = [torch.empty_like(x, device="cpu").pin_memory() for x in host_in]
+        for h, x in zip(h_in, host_in):
+            h.copy_(x)
+        d_in = [torch.empty_like(x) for x in host_in]
         if elastic:
             outs = [torch.empty((nnz,), dtype=torch.float64).pin_memory()]
         else:
             outs = [torch.empty((n_int, 6), dtype=torch.float64).pin_memory(),
                     torch.empty((n_int,), dtype=torch.uint8).pin_memory(),
                     torch.empty((nnz,), dtype=torch.float64).pin_memory()]
-        dE = torch.empty_like(E)
         ctx = P.Context(local, stream=stream, synchronous=False)
 
         def e2e_step():
@@ -363,8 +454,11 @@ def main():
                                                                      P.api._ptr(Kout)))
                     outs[0].copy_(Kout, non_blocking=True)
                     return
-                dE.copy_(hE, non_blocking=True)
-                S, flags, D, K = eng.step(dE)
+                for d, h in zip(d_in, h_in):
+                    d.copy_(h, non_blocking=True)
+                ep = d_in[1] if Ep0 is not None else None
+                hd = d_in[2] if Hard0 is not None else None
+                S, flags, D, K = eng.step(d_in[0], ep, hd)
                 outs[0].copy_(S, non_blocking=True)
                 outs[1].copy_(flags, non_blocking=True)
                 outs[2].copy_(K, non_blocking=True)
@@ -381,7 +475,7 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize(dev)
         e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
-        h2d = 0 if elastic else E.numel() * 8
+        h2d = 0 if elastic else sum(x.numel() * 8 for x in h_in)
         d2h = sum(o.numel() * o.element_size() for o in outs)
         e2e = {"value": world * n_int / (e_ms * 1e-3), "unit": "ip/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e_ms}
@@ -417,6 +511,7 @@ def main():
             "roofline_step": {"algorithmic_bytes": step_bytes, "achieved": step_gbs,
                               "frac": step_gbs / hbm_peak},
             "kernels_ms": k_ms,
+            "kernels_algorithmic_gbs": k_gbs,
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -194,6 +194,14 @@ int epfem_assemble_tangent_ds(epfem_ctx* ctx, const epfem_cache* cache, int64_t 
 int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* cache, const epfem_material* mat,
                       const double* E, const double* Ep_prev, const double* Hard_prev,
                       const epfem_constitutive_out* out, double* K_values);
+/* The two halves of epfem_newton_step, for callers that overlap them with
+ * other work: (1) constitutive update + element tangent deltas into the
+ * cache's workspace, (2) K = K_elast + assembled deltas.  (2) must follow the
+ * (1) that produced the workspace, on the same stream. */
+int epfem_constitutive_delta(epfem_ctx* ctx, const epfem_cache* cache, const epfem_material* mat,
+                             const double* E, const double* Ep_prev, const double* Hard_prev,
+                             const epfem_constitutive_out* out);
+int epfem_assemble_rows(epfem_ctx* ctx, const epfem_cache* cache, double* K_values);
 
 /* K8: E = B u, 2D embedded in Voigt rows {0,1,3} (assembly.cpp:211-222). */
 int epfem_strains(epfem_ctx* ctx, const epfem_cache* cache, const double* u, double* E);

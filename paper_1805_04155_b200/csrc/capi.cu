@@ -426,9 +426,9 @@ int epfem_assemble_tangent_ds(epfem_ctx* ctx, const epfem_cache* c, int64_t n_in
   return tangent_common(ctx, c, n_int, DS, plastic_cols, K_values, 2);
 }
 
-int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
+static int delta_part(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
                       const double* E, const double* Ep_prev, const double* Hard_prev,
-                      const epfem_constitutive_out* out, double* K_values) {
+                      const epfem_constitutive_out* out) {
   ConstArgs a;
   if (int rc = const_args(ctx, mat, E, Ep_prev, Hard_prev, out, &a)) return rc;
   if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
@@ -439,16 +439,42 @@ int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* c, const epfem_material
   if (out->DS || out->Ep || out->Hard || out->plastic_mask || out->smooth_mask || out->apex_mask ||
       out->crit)
     return fail(EPFEM_ERR_INVALID, "newton_step: only S, flags and D are produced");
-  if (!K_values || !aligned16(K_values))
-    return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: K must be 16-byte aligned");
   GatherArgs g = gather_args(c);
   g.D = out->D;
   g.flags = out->flags;
+  return launch_newton_fused(mat->model, c->info.family, c->info.dim, a, g, ctx->stream);
+}
+
+static int rows_part(epfem_ctx* ctx, const epfem_cache* c, double* K_values) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
+  if (!K_values || !aligned16(K_values))
+    return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: K must be 16-byte aligned");
+  GatherArgs g = gather_args(c);
   g.base = c->K_elast;
   g.out = K_values;
-  if (int rc = launch_newton_fused(mat->model, c->info.family, c->info.dim, a, g, ctx->stream))
-    return rc;
-  if (int rc = launch_row_stream(c->info.family, c->info.dim, g, ctx->stream)) return rc;
+  return launch_row_stream(c->info.family, c->info.dim, g, ctx->stream);
+}
+
+int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
+                      const double* E, const double* Ep_prev, const double* Hard_prev,
+                      const epfem_constitutive_out* out, double* K_values) {
+  if (!K_values || !aligned16(K_values))
+    return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: K must be 16-byte aligned");
+  if (int rc = delta_part(ctx, c, mat, E, Ep_prev, Hard_prev, out)) return rc;
+  if (int rc = rows_part(ctx, c, K_values)) return rc;
+  return finish(ctx);
+}
+
+int epfem_constitutive_delta(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
+                             const double* E, const double* Ep_prev, const double* Hard_prev,
+                             const epfem_constitutive_out* out) {
+  if (int rc = delta_part(ctx, c, mat, E, Ep_prev, Hard_prev, out)) return rc;
+  return finish(ctx);
+}
+
+int epfem_assemble_rows(epfem_ctx* ctx, const epfem_cache* c, double* K_values) {
+  if (int rc = rows_part(ctx, c, K_values)) return rc;
   return finish(ctx);
 }
 

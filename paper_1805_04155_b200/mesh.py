@@ -128,13 +128,16 @@ class StructuredMesh:
 def structured_mesh(family: str, dim: int, nx: int, ny: int, nz: int = 0,
                     hx: float | None = None, hy: float | None = None,
                     hz: float | None = None, active: np.ndarray | None = None,
-                    z_range: tuple[int, int] | None = None) -> StructuredMesh:
+                    z_range: tuple[int, int] | None = None,
+                    slab: tuple[int, int] | None = None) -> StructuredMesh:
     """build_structured (mesh.cpp:136-210) on an nx x ny (x nz) cell grid.
 
     ``active`` is an (ny, nx) in-plane cell mask (all active by default).
-    ``z_range=(k0, k1)`` restricts the cell layers to k0 <= k < k1 (a z-slab
-    of the full grid, numbered as its own mesh); fine z indices stay global
-    so coordinates equal those of the full mesh.
+    ``slab=(k0, k1)`` (alias ``z_range`` in 3D) restricts the cells along the
+    LAST axis (z in 3D, y in 2D) to k0 <= k < k1: a slab of the full grid,
+    numbered as its own mesh.  Because the numbering is last-axis-major, the
+    slab's nodes are a contiguous range of the full mesh's nodes, in the same
+    order; fine indices and coordinates stay global.
     """
     t = ElementType(family, dim)
     hx = 1.0 / nx if hx is None else hx
@@ -142,13 +145,20 @@ def structured_mesh(family: str, dim: int, nx: int, ny: int, nz: int = 0,
     if dim == 3:
         hz = 1.0 / nz if hz is None else hz
     pats = np.array(cell_patterns(t), dtype=np.int64)  # (n_pat, n_p, 3)
+    slab = slab if slab is not None else z_range
     k0, k1 = (0, nz) if dim == 3 else (0, 1)
-    if z_range is not None:
-        k0, k1 = z_range
-    fx, fy = 2 * nx + 1, 2 * ny + 1
+    jlo, jhi = 0, ny
+    if slab is not None:
+        if dim == 3:
+            k0, k1 = slab
+        else:
+            jlo, jhi = slab
+    fx = 2 * nx + 1
+    fy = 2 * (jhi - jlo) + 1
     fz = 2 * (k1 - k0) + 1 if dim == 3 else 1
     act = np.ones((ny, nx), dtype=bool) if active is None else np.asarray(active, bool).reshape(ny, nx)
-    jj, ii = np.nonzero(act)                      # row-major: j slow, i fast
+    act = act[jlo:jhi]
+    jj, ii = np.nonzero(act)                      # row-major: j slow, i fast (local j)
     kk = np.arange(k1 - k0, dtype=np.int64)
     # cells in (k, j, i) order
     ck = np.repeat(kk, jj.size)
@@ -166,7 +176,7 @@ def structured_mesh(family: str, dim: int, nx: int, ny: int, nz: int = 0,
     elem = node_of[fid].reshape(-1, pats.shape[1]).astype(np.int32)
     ids = np.flatnonzero(used)
     fa = ids % fx
-    fb = (ids // fx) % fy
+    fb = (ids // fx) % fy + 2 * jlo
     fc = ids // (fx * fy) + (2 * k0 if dim == 3 else 0)
     coord = np.empty((n_nodes, dim))
     coord[:, 0] = 0.5 * hx * fa

@@ -274,6 +274,31 @@ def test_config_pipeline_vs_oracle(cuda, oracle, name):
     assert np.array_equal(_np(K2).view(np.uint64), _np(eng.K).view(np.uint64))
 
 
+@pytest.mark.parametrize("name", ["cfg2", "cfg4"])
+def test_slab_data_path_on_one_rank(cuda, name):
+    """dist.DistributedTangent (K1 on own points, exchange, tangent on the
+    extended slab) run as a single rank equals the fused single-GPU step."""
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.dist import DistributedTangent, make_plan
+    from paper_1805_04155_b200.synthetic import CONFIGS, displacement
+    cfg = CONFIGS[name]
+    n = REDUCED[name]
+    plan = make_plan(cfg.family, cfg.dim, n, 1, 0)
+    dt = DistributedTangent(plan, cfg.material, cuda)
+    from paper_1805_04155_b200.synthetic import calibrate
+    E1 = dt.cache.strains(torch.from_numpy(displacement(plan.mesh.coord, cfg.seed)).to(cuda))
+    s, frac = calibrate(E1, dt.mat_ext, 0.3)
+    assert 0.2 < frac < 0.4
+    E = (s * E1).contiguous()
+    S, flags, K = dt.step(E)
+    dt.ctx.sync()
+    eng = P.TangentEngine(dt.cache, dt.mat_ext)
+    S2, f2, D2, K2 = eng.step(E)
+    eng.sync()
+    assert np.array_equal(_np(flags), _np(f2)) and np.array_equal(_np(S), _np(S2))
+    assert np.array_equal(_np(K).view(np.uint64), _np(K2).view(np.uint64))
+
+
 # ---------------------------------------------------------------------------
 # full-size configurations: size-independent properties
 
