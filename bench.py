@@ -59,58 +59,64 @@ def algorithmic_bytes(cfg, n_int, n_plastic, nnz, n_nodes, n_e, n_p):
 # clocks sampling during the timed region
 
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons polled through NVML in a thread for the
+    duration of the timed region (the same counters `nvidia-smi
+    --query-gpu=clocks.sm,clocks_event_reasons.*` reads; NVML polls fast
+    enough for sub-100-ms regions).  Falls back to no samples without NVML."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index=0):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except OSError:
-            self.proc = None
+            import pynvml as N
+            N.nvmlInit()
+            self._N = N
+            self._h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(self._h, N.NVML_CLOCK_SM))
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception:
+            self._N = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _poll(self):
+        N = self._N
+        self.samples.append(float(N.nvmlDeviceGetClockInfo(self._h, N.NVML_CLOCK_SM)))
+        mask = N.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        for nm, bit in self.REASONS.items():
+            if mask & bit:
+                self.reasons.add(nm)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._poll()
+            except Exception:
+                return
+            time.sleep(0.0005)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
+        self._stop.set()
+        if self._N is not None:
+            self._t.join(timeout=2)
             try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+                self._poll()  # at least one sample at the end of the region
+            except Exception:
+                pass
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "source": "NVML polled during the timed region"}
 
 
 # ---------------------------------------------------------------------------
@@ -438,47 +444,77 @@ def main():
         h_in = [torch.empty_like(x, device="cpu").pin_memory() for x in host_in]
         for h, x in zip(h_in, host_in):
             h.copy_(x)
-        d_in = [torch.empty_like(x) for x in host_in]
+        # Steps are pipelined over two buffer sets and three streams: the
+        # upload of step i+1 (h2d stream) and the download of step i (d2h
+        # stream) overlap on the full-duplex PCIe link while the compute
+        # stream runs the hot path; every step still moves all its own bytes.
+        nbuf = 1 if elastic else 2
+        d_in = [[torch.empty_like(x) for x in host_in] for _ in range(nbuf)]
         if elastic:
-            outs = [torch.empty((nnz,), dtype=torch.float64).pin_memory()]
+            outs = [[torch.empty((nnz,), dtype=torch.float64).pin_memory()]]
+            engines = [None]
         else:
-            outs = [torch.empty((n_int, 6), dtype=torch.float64).pin_memory(),
-                    torch.empty((n_int,), dtype=torch.uint8).pin_memory(),
-                    torch.empty((nnz,), dtype=torch.float64).pin_memory()]
+            outs = [[torch.empty((n_int, 6), dtype=torch.float64).pin_memory(),
+                     torch.empty((n_int,), dtype=torch.uint8).pin_memory(),
+                     torch.empty((nnz,), dtype=torch.float64).pin_memory()] for _ in range(nbuf)]
+            engines = [eng] + [P.TangentEngine(cache, mat, stream=stream) for _ in range(nbuf - 1)]
         ctx = P.Context(local, stream=stream, synchronous=False)
+        h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        ev_in = [torch.cuda.Event() for _ in range(nbuf)]
+        ev_comp = [torch.cuda.Event() for _ in range(nbuf)]
+        ev_out = [torch.cuda.Event() for _ in range(nbuf)]
+        used = [False] * nbuf
 
-        def e2e_step():
-            with torch.cuda.stream(stream):
-                if elastic:
+        def e2e_step(i):
+            b = i % nbuf
+            if elastic:
+                with torch.cuda.stream(stream):
                     P.api._check(P.api.L.lib().epfem_assemble_elastic(ctx.handle, cache.handle,
                                                                      P.api._ptr(Kout)))
-                    outs[0].copy_(Kout, non_blocking=True)
-                    return
-                for d, h in zip(d_in, h_in):
+                    outs[0][0].copy_(Kout, non_blocking=True)
+                return
+            if used[b]:
+                h2d_s.wait_event(ev_comp[b])     # inputs of buffer b consumed
+                stream.wait_event(ev_out[b])     # outputs of buffer b downloaded
+            with torch.cuda.stream(h2d_s):
+                for d, h in zip(d_in[b], h_in):
                     d.copy_(h, non_blocking=True)
-                ep = d_in[1] if Ep0 is not None else None
-                hd = d_in[2] if Hard0 is not None else None
-                S, flags, D, K = eng.step(d_in[0], ep, hd)
-                outs[0].copy_(S, non_blocking=True)
-                outs[1].copy_(flags, non_blocking=True)
-                outs[2].copy_(K, non_blocking=True)
+                ev_in[b].record(h2d_s)
+            stream.wait_event(ev_in[b])
+            ep = d_in[b][1] if Ep0 is not None else None
+            hd = d_in[b][2] if Hard0 is not None else None
+            S, flags, D, K = engines[b].step(d_in[b][0], ep, hd)
+            ev_comp[b].record(stream)
+            d2h_s.wait_event(ev_comp[b])
+            with torch.cuda.stream(d2h_s):
+                outs[b][0].copy_(S, non_blocking=True)
+                outs[b][1].copy_(flags, non_blocking=True)
+                outs[b][2].copy_(K, non_blocking=True)
+                ev_out[b].record(d2h_s)
+            used[b] = True
 
-        for _ in range(2):
-            e2e_step()
+        for i in range(2):
+            e2e_step(i)
         torch.cuda.synchronize(dev)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e2e_steps = max(3, min(args.steps, 10))
+        e2e_steps = max(4, min(args.steps, 12))
         e0.record(stream)
-        for _ in range(e2e_steps):
-            e2e_step()
+        h2d_s.wait_event(e0)
+        d2h_s.wait_event(e0)
+        for i in range(e2e_steps):
+            e2e_step(i)
+        stream.wait_stream(d2h_s)
+        stream.wait_stream(h2d_s)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
         h2d = 0 if elastic else sum(x.numel() * 8 for x in h_in)
-        d2h = sum(o.numel() * o.element_size() for o in outs)
+        d2h = sum(o.numel() * o.element_size() for o in outs[0])
         e2e = {"value": world * n_int / (e_ms * 1e-3), "unit": "ip/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms}
+               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms,
+               "how": "epfem_newton_step with host E/Ep/Hard in and S/flags/K out every step; "
+                      "H2D, compute, D2H on three streams, double-buffered across steps"}
 
     # ------------------------------------------------------------ cpu baseline
     cpu = None
