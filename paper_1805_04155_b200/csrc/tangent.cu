@@ -225,10 +225,15 @@ size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements) {
 // widest value range and item list fit the shared-memory budget.
 int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
                     cudaStream_t st, int* npc_out, int* span_out, int* items_out) {
-  const int budget = 100 * 1024;  // bytes of dynamic smem: two CTAs per SM
+  // bytes of dynamic smem per CTA and the starting node count; EPFEM_ROW_KB /
+  // EPFEM_ROW_NPC override them for tuning runs
+  int budget = (dim == 2 ? 100 : 40) * 1024;
+  int npc = 64;
+  if (const char* v = getenv("EPFEM_ROW_KB")) budget = atoi(v) * 1024;
+  if (const char* v = getenv("EPFEM_ROW_NPC")) npc = atoi(v);
   int* d = nullptr;
   EPFEM_CUDA_TRY(cudaMalloc(&d, 2 * sizeof(int)));
-  int npc = 64, h[2] = {0, 0};
+  int h[2] = {0, 0};
   for (;;) {
     EPFEM_CUDA_TRY(cudaMemsetAsync(d, 0, 2 * sizeof(int), st));
     k_range_span<<<256, 256, 0, st>>>(n_nodes, npc, dim * dim, nbr_ptr, n2e_ptr, d);
