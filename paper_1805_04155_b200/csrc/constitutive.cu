@@ -290,13 +290,10 @@ __global__ void __launch_bounds__(256) k_constitutive(ConstArgs a) {
     eval_point<MODEL>(a, q, none);
 }
 
-constexpr int kFusedThreads = 128;
-constexpr int kFusedBudget = 2560;  // doubles of staged records per CTA (20 KB)
-
 template <int MODEL, int DIM, int NP, int NQ>
-__global__ void __launch_bounds__(kFusedThreads) k_newton_fused(ConstArgs c, GatherArgs g) {
-  using Cfg = DeltaCfg<DIM, NP>;
-  constexpr int EPB = delta_epb<DIM, NP, NQ, kFusedBudget, kFusedThreads>();
+__global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS) k_newton_fused(ConstArgs c, GatherArgs g) {
+  using Cfg = DeltaCfg<DIM, NP, NQ>;
+  constexpr int EPB = Cfg::EPB;
   __shared__ double s_st[EPB][NQ][Cfg::REC];
   __shared__ unsigned s_mask[EPB];
   c.DS = nullptr;  // hot path: S, flags, packed D only
@@ -323,7 +320,7 @@ __global__ void __launch_bounds__(kFusedThreads) k_newton_fused(ConstArgs c, Gat
   }
   __syncthreads();
   if (tid < EPB && e0 + tid < g.n_elements) g.emask[e0 + tid] = s_mask[tid];
-  delta_phase2<DIM, NP, NQ, EPB>(s_st, s_mask, tid, e0, g.n_elements, g.scratch);
+  delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, g.n_elements, g.scratch);
 }
 
 }  // namespace
@@ -360,17 +357,17 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
   bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
     constexpr int DIM = decltype(D)::value;
     constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
-    constexpr int EPB = delta_epb<DIM, NP, NQ, kFusedBudget, kFusedThreads>();
-    const unsigned blocks = (unsigned)((g.n_elements + EPB - 1) / EPB);
+    using Cfg = DeltaCfg<DIM, NP, NQ>;
+    const unsigned blocks = (unsigned)((g.n_elements + Cfg::EPB - 1) / Cfg::EPB);
     switch (model) {
       case EPFEM_MODEL_VON_MISES:
-        k_newton_fused<EPFEM_MODEL_VON_MISES, DIM, NP, NQ><<<blocks, kFusedThreads, 0, st>>>(c, g);
+        k_newton_fused<EPFEM_MODEL_VON_MISES, DIM, NP, NQ><<<blocks, Cfg::THREADS, 0, st>>>(c, g);
         break;
       case EPFEM_MODEL_DRUCKER_PRAGER:
-        k_newton_fused<EPFEM_MODEL_DRUCKER_PRAGER, DIM, NP, NQ><<<blocks, kFusedThreads, 0, st>>>(c, g);
+        k_newton_fused<EPFEM_MODEL_DRUCKER_PRAGER, DIM, NP, NQ><<<blocks, Cfg::THREADS, 0, st>>>(c, g);
         break;
       default:
-        k_newton_fused<EPFEM_MODEL_ELASTIC, DIM, NP, NQ><<<blocks, kFusedThreads, 0, st>>>(c, g);
+        k_newton_fused<EPFEM_MODEL_ELASTIC, DIM, NP, NQ><<<blocks, Cfg::THREADS, 0, st>>>(c, g);
         break;
     }
   });

@@ -7,6 +7,12 @@
 //     [ dphi_p (NP x DIM) | Dw = w (D - C), packed upper triangle (NSP) ]
 //   workspace record per element (global), NB = NP(NP+1)/2 blocks of dim x dim:
 //     block (a, b), a <= b, at blk_index(a, b) * dim^2, row-major
+//
+// Phase 2 computes only the symmetric blocks (a, b >= a).  Block row a is cut
+// into chunks of CS blocks; one thread owns one (a, chunk): it forms
+// T_a = B_a^T Dw once per plastic point and adds T_a B_b for the b of its
+// chunk.  FMA per plastic point: NT*|T| + NB*|block| (vs NP*|T| + NP^2*|block|
+// for full block rows), and no thread holds more than CS blocks.
 #pragma once
 
 #include "kernels.cuh"
@@ -18,27 +24,27 @@ __host__ __device__ constexpr int blk_index(int a, int b) {  // a <= b
   return a * (2 * NP - a + 1) / 2 + (b - a);
 }
 
-template <int DIM, int NP>
+template <int DIM, int NP, int NQ>
 struct DeltaCfg {
   static constexpr int NS = DIM == 3 ? 6 : 3;
   static constexpr int NSP = NS * (NS + 1) / 2;
   static constexpr int D2 = DIM * DIM;
   static constexpr int NB = NP * (NP + 1) / 2;
   static constexpr int REC = NP * DIM + NSP;
-  // block-row chunks per node in phase 2 (register budget)
-  static constexpr int BCH = DIM == 2 ? 1 : (NP <= 4 ? 1 : (NP <= 10 ? 2 : 4));
-  static constexpr int CS = (NP + BCH - 1) / BCH;
+  static constexpr int CS = (DIM == 3 && NP >= 20) ? 5 : 4;  // blocks per phase-2 thread
+  static constexpr int nt() {
+    int s = 0;
+    for (int a = 0; a < NP; ++a) s += (NP - a + CS - 1) / CS;
+    return s;
+  }
+  static constexpr int NT = nt();                        // phase-2 threads per element
+  static constexpr int TPE = NQ > NT ? NQ : NT;           // threads per element
+  static constexpr int MAXT = 128;
+  static constexpr int BUDGET = 5120;                     // doubles of staged records per CTA
+  static constexpr int E1 = MAXT / TPE, E2 = BUDGET / (NQ * REC);
+  static constexpr int EPB = (E1 < E2 ? E1 : E2) > 0 ? (E1 < E2 ? E1 : E2) : 1;
+  static constexpr int THREADS = ((EPB * TPE + 31) / 32) * 32;
 };
-
-// elements per CTA: phase-2 threads (NP * BCH per element) fit 256 threads and
-// the staged records fit BUDGET doubles of shared memory
-template <int DIM, int NP, int NQ, int BUDGET, int THREADS = 256>
-__host__ __device__ constexpr int delta_epb() {
-  constexpr int E1 = THREADS / (NP * DeltaCfg<DIM, NP>::BCH);
-  constexpr int E2 = BUDGET / (NQ * DeltaCfg<DIM, NP>::REC);
-  constexpr int E = E1 < E2 ? E1 : E2;
-  return E > 0 ? E : 1;
-}
 
 // assembly row r -> Voigt row (2D plane strain uses {0,1,3}, assembly.cpp:92)
 template <int DIM>
@@ -94,20 +100,24 @@ __device__ __forceinline__ void stage_dw(double* dwst, double w, const GatherArg
     }
 }
 
-// Phase 2: thread (element le, node pa, chunk ch) accumulates the blocks
-// (pa, b) for the b of its chunk over the element's plastic points from the
-// staged records, then writes the blocks with b >= pa to the workspace.
-template <int DIM, int NP, int NQ, int EPB>
-__device__ __forceinline__ void delta_phase2(const double (*s_st)[NQ][DeltaCfg<DIM, NP>::REC],
-                                             const unsigned* s_mask, int tid, int64_t e0,
-                                             int64_t n_elements, double* __restrict__ scratch) {
-  using Cfg = DeltaCfg<DIM, NP>;
-  constexpr int NS = Cfg::NS, D2 = Cfg::D2, NB = Cfg::NB, BCH = Cfg::BCH, CS = Cfg::CS;
-  if (tid >= EPB * NP * BCH) return;
-  const int le = tid / (NP * BCH);
-  const int rr = tid - le * (NP * BCH);
-  const int pa = rr / BCH, ch = rr - pa * BCH;
-  const int b0 = ch * CS;
+// Phase 2: thread (element le, row a, chunk starting at block c0 >= a)
+// accumulates the blocks (a, b), c0 <= b < c0 + CS, over the element's
+// plastic points from the staged records, then writes them to the workspace.
+template <int DIM, int NP, int NQ>
+__device__ __forceinline__ void delta_phase2(
+    const double (*s_st)[NQ][DeltaCfg<DIM, NP, NQ>::REC], const unsigned* s_mask, int tid,
+    int64_t e0, int64_t n_elements, double* __restrict__ scratch) {
+  using Cfg = DeltaCfg<DIM, NP, NQ>;
+  constexpr int NS = Cfg::NS, D2 = Cfg::D2, NB = Cfg::NB, CS = Cfg::CS, NT = Cfg::NT;
+  if (tid >= Cfg::EPB * NT) return;
+  const int le = tid / NT;
+  int k = tid - le * NT, a = 0;
+  while ((NP - a + CS - 1) / CS <= k) {
+    k -= (NP - a + CS - 1) / CS;
+    ++a;
+  }
+  const int c0 = a + k * CS;
+  const int nb = NP - c0 < CS ? NP - c0 : CS;
   const int64_t e = e0 + le;
   if (e >= n_elements) return;
   unsigned mask = s_mask[le];
@@ -130,7 +140,7 @@ __device__ __forceinline__ void delta_phase2(const double (*s_st)[NQ][DeltaCfg<D
     };
     double ga[DIM];
 #pragma unroll
-    for (int i = 0; i < DIM; ++i) ga[i] = st[pa * DIM + i];
+    for (int i = 0; i < DIM; ++i) ga[i] = st[a * DIM + i];
     double T[DIM][NS];  // T_a = B_a^T Dw
 #pragma unroll
     for (int c = 0; c < NS; ++c) {
@@ -148,20 +158,20 @@ __device__ __forceinline__ void delta_phase2(const double (*s_st)[NQ][DeltaCfg<D
     }
 #pragma unroll
     for (int bb = 0; bb < CS; ++bb) {
-      const int b = b0 + bb;
-      if (b >= NP) break;
-      const double* h = st + b * DIM;
-      const double h0 = h[0], h1 = h[1], h2 = DIM == 3 ? h[DIM - 1] : 0.0;
+      if (bb < nb) {
+        const double* h = st + (c0 + bb) * DIM;
+        const double h0 = h[0], h1 = h[1], h2 = DIM == 3 ? h[DIM - 1] : 0.0;
 #pragma unroll
-      for (int i = 0; i < DIM; ++i) {
-        if constexpr (DIM == 3) {
-          blk[bb][i][0] = __fma_rn(T[i][5], h2, __fma_rn(T[i][3], h1, __fma_rn(T[i][0], h0, blk[bb][i][0])));
-          blk[bb][i][1] = __fma_rn(T[i][4], h2, __fma_rn(T[i][3], h0, __fma_rn(T[i][1], h1, blk[bb][i][1])));
-          blk[bb][i][DIM - 1] =
-              __fma_rn(T[i][5], h0, __fma_rn(T[i][4], h1, __fma_rn(T[i][2], h2, blk[bb][i][DIM - 1])));
-        } else {
-          blk[bb][i][0] = __fma_rn(T[i][2], h1, __fma_rn(T[i][0], h0, blk[bb][i][0]));
-          blk[bb][i][1] = __fma_rn(T[i][2], h0, __fma_rn(T[i][1], h1, blk[bb][i][1]));
+        for (int i = 0; i < DIM; ++i) {
+          if constexpr (DIM == 3) {
+            blk[bb][i][0] = __fma_rn(T[i][5], h2, __fma_rn(T[i][3], h1, __fma_rn(T[i][0], h0, blk[bb][i][0])));
+            blk[bb][i][1] = __fma_rn(T[i][4], h2, __fma_rn(T[i][3], h0, __fma_rn(T[i][1], h1, blk[bb][i][1])));
+            blk[bb][i][DIM - 1] =
+                __fma_rn(T[i][5], h0, __fma_rn(T[i][4], h1, __fma_rn(T[i][2], h2, blk[bb][i][DIM - 1])));
+          } else {
+            blk[bb][i][0] = __fma_rn(T[i][2], h1, __fma_rn(T[i][0], h0, blk[bb][i][0]));
+            blk[bb][i][1] = __fma_rn(T[i][2], h0, __fma_rn(T[i][1], h1, blk[bb][i][1]));
+          }
         }
       }
     }
@@ -169,10 +179,8 @@ __device__ __forceinline__ void delta_phase2(const double (*s_st)[NQ][DeltaCfg<D
   double* rec = scratch + (size_t)e * NB * D2;
 #pragma unroll
   for (int bb = 0; bb < CS; ++bb) {
-    const int b = b0 + bb;
-    if (b >= NP) break;
-    if (b >= pa) {
-      double* o = rec + blk_index<NP>(pa, b) * D2;
+    if (bb < nb) {
+      double* o = rec + blk_index<NP>(a, c0 + bb) * D2;
 #pragma unroll
       for (int i = 0; i < DIM; ++i)
 #pragma unroll

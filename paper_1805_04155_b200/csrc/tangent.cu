@@ -26,12 +26,10 @@ namespace epfem_gpu {
 
 namespace {
 
-constexpr int kDeltaBudget = 5120;  // doubles of staged records per CTA (40 KB)
-
 template <int DIM, int NP, int NQ, int MODE>
-__global__ void __launch_bounds__(256) k_elem_delta_staged(GatherArgs a) {
-  using Cfg = DeltaCfg<DIM, NP>;
-  constexpr int EPB = delta_epb<DIM, NP, NQ, kDeltaBudget>();
+__global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS) k_elem_delta_staged(GatherArgs a) {
+  using Cfg = DeltaCfg<DIM, NP, NQ>;
+  constexpr int EPB = Cfg::EPB;
   constexpr int NS = Cfg::NS, REC = Cfg::REC;
   __shared__ double s_st[EPB][NQ][REC];
   __shared__ unsigned s_mask[EPB];
@@ -70,7 +68,7 @@ __global__ void __launch_bounds__(256) k_elem_delta_staged(GatherArgs a) {
   }
   __syncthreads();
   if (tid < EPB && e0 + tid < a.n_elements) a.emask[e0 + tid] = s_mask[tid];
-  delta_phase2<DIM, NP, NQ, EPB>(s_st, s_mask, tid, e0, a.n_elements, a.scratch);
+  delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, a.n_elements, a.scratch);
 }
 
 constexpr int kStreamThreads = 256;
@@ -277,13 +275,13 @@ int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStrea
   bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
     constexpr int DIM = decltype(D)::value;
     constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
-    constexpr int EPB = delta_epb<DIM, NP, NQ, kDeltaBudget>();
+    using Cfg = DeltaCfg<DIM, NP, NQ>;
     if (a.n_elements > 0) {
-      const int64_t blocks = (a.n_elements + EPB - 1) / EPB;
+      const int64_t blocks = (a.n_elements + Cfg::EPB - 1) / Cfg::EPB;
       if (mode == G_TANGENT_PACKED)
-        k_elem_delta_staged<DIM, NP, NQ, G_TANGENT_PACKED><<<(unsigned)blocks, 256, 0, st>>>(a);
+        k_elem_delta_staged<DIM, NP, NQ, G_TANGENT_PACKED><<<(unsigned)blocks, Cfg::THREADS, 0, st>>>(a);
       else
-        k_elem_delta_staged<DIM, NP, NQ, G_TANGENT_DS36><<<(unsigned)blocks, 256, 0, st>>>(a);
+        k_elem_delta_staged<DIM, NP, NQ, G_TANGENT_DS36><<<(unsigned)blocks, Cfg::THREADS, 0, st>>>(a);
     }
   });
   if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
