@@ -33,7 +33,7 @@ SOURCES = {
     "capi.cu": [],
     "tables.cpp": [],
 }
-HEADERS = ["common.cuh", "kernels.cuh", "delta.cuh"]
+HEADERS = ["common.cuh", "kernels.cuh", "delta.cuh", "tma.cuh"]
 
 
 def nvcc() -> str:

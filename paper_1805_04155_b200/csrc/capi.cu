@@ -306,8 +306,12 @@ int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_materi
   CT(cudaMalloc(&c->elem, std::max<size_t>(elem_bytes, 4)));
   CT(cudaMemcpyAsync(c->elem, mesh->elem, elem_bytes, cudaMemcpyDeviceToDevice, st));
   CT(cudaMalloc(&c->det, sizeof(double) * std::max<int64_t>(n_int, 1)));
-  CT(cudaMalloc(&c->weight, sizeof(double) * std::max<int64_t>(n_int, 1)));
-  CT(cudaMalloc(&c->inv, sizeof(double) * mesh->dim * mesh->dim * std::max<int64_t>(n_int, 1)));
+  // padding: the pipelined kernel reads 16-byte-aligned windows of these
+  CT(cudaMalloc(&c->weight, sizeof(double) * (n_int + 4)));
+  CT(cudaMalloc(&c->inv, sizeof(double) * mesh->dim * mesh->dim * (n_int + 4)));
+  CT(cudaMemsetAsync(c->weight + n_int, 0, 4 * sizeof(double), st));
+  CT(cudaMemsetAsync(c->inv + (size_t)mesh->dim * mesh->dim * n_int, 0,
+                     4 * sizeof(double) * mesh->dim * mesh->dim, st));
   // moduli snapshot
   c->shear_u = mat->shear_u;
   c->bulk_u = mat->bulk_u;

@@ -84,16 +84,39 @@ struct NoSink {
   __device__ __forceinline__ void operator()(F&&) const {}
 };
 
+// Where a point's E / Ep / Hard come from: global memory (grid-stride
+// kernels) or a shared-memory tile filled by TMA (pipelined fused kernel).
+struct GlobalIn {
+  const ConstArgs& a;
+  __device__ __forceinline__ void e(int64_t q, double* v) const { load6(a.E, q, v); }
+  __device__ __forceinline__ void ep(int64_t q, double* v) const { load6(a.Ep, q, v); }
+  __device__ __forceinline__ void hard(int64_t q, double* v) const { load6(a.Hard, q, v); }
+};
+struct SmemIn {
+  const double* E;
+  const double* Ep;
+  const double* H;
+  int li;  // point index inside the tile
+  __device__ __forceinline__ static void ld(const double* p, int li, double* v) {
+    const double2* p2 = reinterpret_cast<const double2*>(p + 6 * li);
+    const double2 a = p2[0], b = p2[1], c = p2[2];
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y;
+  }
+  __device__ __forceinline__ void e(int64_t, double* v) const { ld(E, li, v); }
+  __device__ __forceinline__ void ep(int64_t, double* v) const { ld(Ep, li, v); }
+  __device__ __forceinline__ void hard(int64_t, double* v) const { ld(H, li, v); }
+};
+
 // The return map at point q (constitutive.cpp:76-196).  `sink(f)` is called
 // at plastic points with the tangent functor f(i, j) = D(i, j).  Returns the
 // plastic flag.
-template <int MODEL, class Sink>
-__device__ __forceinline__ bool eval_point(const ConstArgs& a, int64_t q, Sink& sink) {
+template <int MODEL, class In, class Sink>
+__device__ __forceinline__ bool eval_point(const ConstArgs& a, int64_t q, const In& in, Sink& sink) {
   const double G = a.G ? __ldg(a.G + q) : a.Gu;
   const double K = a.K ? __ldg(a.K + q) : a.Ku;
   double e[6], ep[6];
-  load6(a.E, q, e);
-  if (a.Ep) load6(a.Ep, q, ep);
+  in.e(q, e);
+  if (a.Ep) in.ep(q, ep);
   else
 #pragma unroll
     for (int i = 0; i < 6; ++i) ep[i] = 0.0;
@@ -135,7 +158,7 @@ __device__ __forceinline__ bool eval_point(const ConstArgs& a, int64_t q, Sink& 
     const double am = a.p1 ? __ldg(a.p1 + q) : a.p1u;
     const double Y = a.p2 ? __ldg(a.p2 + q) : a.p2u;
     double h[6];
-    if (a.Hard) load6(a.Hard, q, h);
+    if (a.Hard) in.hard(q, h);
     else
 #pragma unroll
       for (int i = 0; i < 6; ++i) h[i] = 0.0;
@@ -287,7 +310,7 @@ __global__ void __launch_bounds__(256) k_constitutive(ConstArgs a) {
   NoSink none;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < a.n; q += stride)
-    eval_point<MODEL>(a, q, none);
+    eval_point<MODEL>(a, q, GlobalIn{a}, none);
 }
 
 template <int MODEL, int DIM, int NP, int NQ>
@@ -316,11 +339,110 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS) k_newton_fused
       stage_geometry<DIM, NP>(st, g.inv + m * Cfg::D2, g.gradhat, q);
       stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f);
     };
-    eval_point<MODEL>(c, m, stage);
+    eval_point<MODEL>(c, m, GlobalIn{c}, stage);
   }
   __syncthreads();
   if (tid < EPB && e0 + tid < g.n_elements) g.emask[e0 + tid] = s_mask[tid];
   delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, g.n_elements, g.scratch);
+}
+
+// Per-buffer shared-memory tile of the pipelined kernel (doubles): the
+// group's E, Ep, Hard (6 per point), J^-1 (dim^2 per point, one extra point
+// for the 16-byte alignment shift) and w (two extra).
+template <int DIM, int NP, int NQ>
+struct PipeTile {
+  static constexpr int PPG = DeltaCfg<DIM, NP, NQ>::EPB * NQ;  // points per group
+  static constexpr int D2 = DIM * DIM;
+  static constexpr int r2(int n) { return (n + 1) & ~1; }
+  static constexpr int OE = 0, OEP = OE + 6 * PPG, OH = OEP + 6 * PPG, OI = OH + 6 * PPG;
+  static constexpr int OW = OI + r2((PPG + 1) * D2);
+  static constexpr int SIZE = OW + r2(PPG + 2);
+  static constexpr size_t BYTES = 2 * SIZE * sizeof(double);
+};
+
+// k_newton_pipe: the fused kernel made persistent and software-pipelined.
+// Each CTA walks groups of EPB elements (grid-stride); one elected thread
+// issues TMA bulk copies of the NEXT group's E / Ep / Hard / J^-1 / w into
+// the other half of a double-buffered tile (mbarrier completion) while the
+// CTA computes the current group from shared memory, so the point update
+// never waits on a global load.  Outputs and arithmetic are identical to
+// k_newton_fused.
+template <int MODEL, int DIM, int NP, int NQ>
+__global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS)
+    k_newton_pipe(ConstArgs c, GatherArgs g, int64_t n_groups) {
+  using Cfg = DeltaCfg<DIM, NP, NQ>;
+  using Tile = PipeTile<DIM, NP, NQ>;
+  constexpr int EPB = Cfg::EPB, PPG = Tile::PPG, D2 = Tile::D2;
+  extern __shared__ __align__(128) double tiles[];
+  __shared__ double s_st[EPB][NQ][Cfg::REC];
+  __shared__ unsigned s_mask[EPB];
+  __shared__ uint64_t s_bar[2];
+  c.DS = nullptr;  // hot path: S, flags, packed D only
+  c.Ep_out = c.Hard_out = nullptr;
+  c.pm = c.sm = c.am = nullptr;
+  c.crit = nullptr;
+  const int tid = threadIdx.x;
+  const int64_t n_int = g.n_elements * NQ;
+
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  auto issue = [&](int64_t grp, int b) {  // one thread
+    double* t = tiles + b * Tile::SIZE;
+    const int64_t p0 = grp * PPG;
+    const int np = (int)min((int64_t)PPG, n_int - p0);
+    const int sh = (int)(p0 & 1);  // J^-1 / w source shifted down to a 16-byte boundary
+    const unsigned be = (unsigned)np * 48u;
+    const unsigned bi = (unsigned)(((np + sh) * D2 * 8 + 15) & ~15);
+    const unsigned bw = (unsigned)(((np + sh) * 8 + 15) & ~15);
+    unsigned total = be + bi + bw;
+    if (c.Ep) total += be;
+    if (c.Hard) total += be;
+    mbar_expect_tx(&s_bar[b], total);
+    tma_load_1d(t + Tile::OE, c.E + 6 * p0, be, &s_bar[b]);
+    if (c.Ep) tma_load_1d(t + Tile::OEP, c.Ep + 6 * p0, be, &s_bar[b]);
+    if (c.Hard) tma_load_1d(t + Tile::OH, c.Hard + 6 * p0, be, &s_bar[b]);
+    tma_load_1d(t + Tile::OI, g.inv + (p0 - sh) * D2, bi, &s_bar[b]);
+    tma_load_1d(t + Tile::OW, g.weight + (p0 - sh), bw, &s_bar[b]);
+  };
+  int64_t grp = blockIdx.x;
+  if (tid == 0 && grp < n_groups) issue(grp, 0);
+  for (int it = 0; grp < n_groups; grp += gridDim.x, ++it) {
+    const int b = it & 1;
+    const int64_t nxt = grp + gridDim.x;
+    // buffer b^1 was released by the barrier that closed the previous iteration;
+    // order those generic-proxy reads before the async-proxy (TMA) writes
+    if (tid == 0 && nxt < n_groups) {
+      fence_proxy_async_smem();
+      issue(nxt, b ^ 1);
+    }
+    if (tid < EPB) s_mask[tid] = 0u;
+    mbar_wait(&s_bar[b], (unsigned)(it >> 1) & 1u);
+    __syncthreads();
+    const double* t = tiles + b * Tile::SIZE;
+    const int64_t e0 = grp * EPB;
+    const int sh = (int)((grp * PPG) & 1);
+    for (int k = tid; k < PPG; k += blockDim.x) {
+      const int le = k / NQ, q = k - le * NQ;
+      const int64_t e = e0 + le;
+      if (e >= g.n_elements) continue;
+      const int64_t m = e * NQ + q;
+      double* st = s_st[le][q];
+      auto stage = [&](auto&& f) {
+        atomicOr(&s_mask[le], 1u << q);
+        stage_geometry<DIM, NP>(st, t + Tile::OI + (k + sh) * D2, g.gradhat, q);
+        stage_dw<DIM>(st + NP * DIM, t[Tile::OW + k + sh], g, m, f);
+      };
+      eval_point<MODEL>(c, m, SmemIn{t + Tile::OE, t + Tile::OEP, t + Tile::OH, k}, stage);
+    }
+    __syncthreads();
+    if (tid < EPB && e0 + tid < g.n_elements) g.emask[e0 + tid] = s_mask[tid];
+    delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, g.n_elements, g.scratch);
+    __syncthreads();
+  }
 }
 
 }  // namespace
@@ -351,13 +473,51 @@ int launch_constitutive(int model, const ConstArgs& a, cudaStream_t st, int num_
   return 0;
 }
 
+template <int MODEL, int DIM, int NP, int NQ>
+static int launch_pipe(const ConstArgs& c, const GatherArgs& g, cudaStream_t st) {
+  using Cfg = DeltaCfg<DIM, NP, NQ>;
+  using Tile = PipeTile<DIM, NP, NQ>;
+  auto kern = k_newton_pipe<MODEL, DIM, NP, NQ>;
+  static int per_sm = -1, num_sms = 0;
+  if (per_sm < 0) {
+    EPFEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)Tile::BYTES));
+    EPFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::THREADS,
+                                                                 Tile::BYTES));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int64_t n_groups = (g.n_elements + Cfg::EPB - 1) / Cfg::EPB;
+  const int64_t grid = std::min<int64_t>(n_groups, (int64_t)per_sm * num_sms);
+  kern<<<(unsigned)grid, Cfg::THREADS, Tile::BYTES, st>>>(c, g, n_groups);
+  EPFEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
                         cudaStream_t st) {
   if (g.n_elements == 0) return 0;
+  static const bool pipe = [] {
+    const char* v = getenv("EPFEM_FUSED");  // "plain" selects the non-pipelined kernel (A/B runs)
+    return !(v && v[0] == 'p' && v[1] == 'l');
+  }();
+  int rc = 0;
   bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
     constexpr int DIM = decltype(D)::value;
     constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
     using Cfg = DeltaCfg<DIM, NP, NQ>;
+    if (pipe) {
+      switch (model) {
+        case EPFEM_MODEL_VON_MISES: rc = launch_pipe<EPFEM_MODEL_VON_MISES, DIM, NP, NQ>(c, g, st); break;
+        case EPFEM_MODEL_DRUCKER_PRAGER:
+          rc = launch_pipe<EPFEM_MODEL_DRUCKER_PRAGER, DIM, NP, NQ>(c, g, st);
+          break;
+        default: rc = launch_pipe<EPFEM_MODEL_ELASTIC, DIM, NP, NQ>(c, g, st); break;
+      }
+      return;
+    }
     const unsigned blocks = (unsigned)((g.n_elements + Cfg::EPB - 1) / Cfg::EPB);
     switch (model) {
       case EPFEM_MODEL_VON_MISES:
@@ -372,6 +532,7 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
     }
   });
   if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
+  if (rc) return rc;
   EPFEM_CUDA_TRY(cudaGetLastError());
   return 0;
 }

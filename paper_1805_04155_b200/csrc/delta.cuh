@@ -16,6 +16,7 @@
 #pragma once
 
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace epfem_gpu {
 
@@ -54,11 +55,11 @@ __device__ __forceinline__ constexpr int arow(int r) {
 
 // dphi_p = J^-1 ghat_p for every node of the element at point q.
 template <int DIM, int NP>
-__device__ __forceinline__ void stage_geometry(double* st, const double* __restrict__ inv_m,
+__device__ __forceinline__ void stage_geometry(double* st, const double* inv_m,
                                                const double* __restrict__ gradhat, int q) {
-  double J[DIM * DIM];
+  double J[DIM * DIM];  // inv_m may point to global or shared memory
 #pragma unroll
-  for (int t = 0; t < DIM * DIM; ++t) J[t] = __ldg(inv_m + t);
+  for (int t = 0; t < DIM * DIM; ++t) J[t] = inv_m[t];
 #pragma unroll 4
   for (int p = 0; p < NP; ++p) {
     const double* gh = gradhat + (q * NP + p) * DIM;
