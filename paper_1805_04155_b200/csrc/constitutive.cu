@@ -314,7 +314,8 @@ __global__ void __launch_bounds__(256) k_constitutive(ConstArgs a) {
 }
 
 template <int MODEL, int DIM, int NP, int NQ>
-__global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS) k_newton_fused(ConstArgs c, GatherArgs g) {
+__global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? 8 : 1)
+    k_newton_fused(ConstArgs c, GatherArgs g) {
   using Cfg = DeltaCfg<DIM, NP, NQ>;
   constexpr int EPB = Cfg::EPB;
   __shared__ double s_st[EPB][NQ][Cfg::REC];
@@ -499,9 +500,12 @@ static int launch_pipe(const ConstArgs& c, const GatherArgs& g, cudaStream_t st)
 int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
                         cudaStream_t st) {
   if (g.n_elements == 0) return 0;
+  // The TMA-pipelined variant measured slower than the plain one on B200
+  // (cfg2: 0.255 vs 0.224 ms; the kernel is bound by FP64 dependency chains,
+  // not load latency), so it is opt-in: EPFEM_FUSED=pipe.
   static const bool pipe = [] {
-    const char* v = getenv("EPFEM_FUSED");  // "plain" selects the non-pipelined kernel (A/B runs)
-    return !(v && v[0] == 'p' && v[1] == 'l');
+    const char* v = getenv("EPFEM_FUSED");
+    return v && v[0] == 'p' && v[1] == 'i';
   }();
   int rc = 0;
   bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
