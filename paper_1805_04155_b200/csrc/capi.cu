@@ -27,12 +27,17 @@ int cuda_fail(cudaError_t err, const char* what) {
 
 using namespace epfem_gpu;
 
+constexpr int kMaxChunks = 32;
+
 struct epfem_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   bool sync = false;
   DevErr* err = nullptr;  // device
+  // side stream + events of the overlapped (chunked) Newton step
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk[kMaxChunks] = {};
 };
 
 struct epfem_cache {
@@ -51,6 +56,10 @@ struct epfem_cache {
   double* scratch = nullptr;  // tangent workspace (symmetric dK_e per element)
   unsigned* emask = nullptr;  // per-element plastic-point bitmask
   int npc = 64, max_span = 0, max_items = 0;  // row-stream plan
+  // overlapped Newton step: row chunk k (nodes [nchunk[k], nchunk[k+1]))
+  // needs exactly the element chunks 0..k (elements [echunk[j], echunk[j+1]))
+  int n_chunks = 1;
+  int64_t nchunk[kMaxChunks + 1] = {}, echunk[kMaxChunks + 1] = {};
 };
 
 namespace {
@@ -113,6 +122,17 @@ int epfem_ctx_create(int device, void* cuda_stream, epfem_ctx** out) {
   DevErr z{};
   z.index = ~0ull;
   cudaMemcpy(c->err, &z, sizeof(DevErr), cudaMemcpyHostToDevice);
+  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+    epfem_ctx_destroy(c);
+    return cuda_fail(cudaGetLastError(), "side stream / events");
+  }
+  for (auto& ev : c->ev_chunk)
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+      epfem_ctx_destroy(c);
+      return cuda_fail(cudaGetLastError(), "chunk events");
+    }
   *out = c;
   return 0;
 }
@@ -137,7 +157,12 @@ int epfem_ctx_sync(epfem_ctx* ctx) {
 
 int epfem_ctx_destroy(epfem_ctx* ctx) {
   if (!ctx) return 0;
-  cudaFree(ctx->err);
+  if (ctx->err) cudaFree(ctx->err);
+  for (auto ev : ctx->ev_chunk)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   delete ctx;
   return 0;
 }
@@ -251,6 +276,10 @@ static GatherArgs gather_args(const epfem_cache* c) {
   g.npc = c->npc;
   g.max_span = c->max_span;
   g.max_items = c->max_items;
+  g.e_begin = 0;
+  g.e_end = c->info.n_elements;
+  g.n_begin = 0;
+  g.n_end = c->info.n_nodes;
   // packed elastic operator C = K VOL + 2G DEV (voigt.hpp:72-74) for a uniform material
   for (int i = 0; i < 6; ++i)
     for (int j = i; j < 6; ++j) {
@@ -347,6 +376,23 @@ int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_materi
     if (int rc = plan_row_stream(I.n_nodes, I.dim, c->pat.nbr_ptr, c->pat.n2e_ptr, st, &c->npc,
                                  &c->max_span, &c->max_items))
       return bail(rc);
+  {
+    // overlap plan: ~8 chunks of >= 64K nodes (EPFEM_CHUNKS overrides)
+    int want = (int)std::min<int64_t>(8, std::max<int64_t>(1, I.n_nodes / 65536));
+    if (const char* v = getenv("EPFEM_CHUNKS")) want = std::max(1, std::min(kMaxChunks, atoi(v)));
+    if (want > 1 && I.n_nodes > 0) {
+      const int n = plan_chunks(I.n_nodes, I.n_elements, I.n_p, c->pat.n2e_ptr, c->pat.n2e, c->npc,
+                                want, c->nchunk, c->echunk, st);
+      if (n < 0) return bail(EPFEM_ERR_CUDA);
+      c->n_chunks = n;
+    } else {
+      c->n_chunks = 1;
+      c->nchunk[0] = 0;
+      c->nchunk[1] = I.n_nodes;
+      c->echunk[0] = 0;
+      c->echunk[1] = I.n_elements;
+    }
+  }
   GatherArgs g = gather_args(c);
   g.out = c->K_elast;
   if (int rc = launch_gather(I.family, I.dim, 0, g, st)) return bail(rc);
@@ -430,11 +476,10 @@ int epfem_assemble_tangent_ds(epfem_ctx* ctx, const epfem_cache* c, int64_t n_in
   return tangent_common(ctx, c, n_int, DS, plastic_cols, K_values, 2);
 }
 
-static int delta_part(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
+static int delta_args(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
                       const double* E, const double* Ep_prev, const double* Hard_prev,
-                      const epfem_constitutive_out* out) {
-  ConstArgs a;
-  if (int rc = const_args(ctx, mat, E, Ep_prev, Hard_prev, out, &a)) return rc;
+                      const epfem_constitutive_out* out, ConstArgs* a, GatherArgs* g) {
+  if (int rc = const_args(ctx, mat, E, Ep_prev, Hard_prev, out, a)) return rc;
   if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
   if (mat->n_int != c->info.n_int)
     return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: size mismatch");
@@ -443,10 +488,45 @@ static int delta_part(epfem_ctx* ctx, const epfem_cache* c, const epfem_material
   if (out->DS || out->Ep || out->Hard || out->plastic_mask || out->smooth_mask || out->apex_mask ||
       out->crit)
     return fail(EPFEM_ERR_INVALID, "newton_step: only S, flags and D are produced");
-  GatherArgs g = gather_args(c);
-  g.D = out->D;
-  g.flags = out->flags;
+  *g = gather_args(c);
+  g->D = out->D;
+  g->flags = out->flags;
+  return 0;
+}
+
+static int delta_part(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
+                      const double* E, const double* Ep_prev, const double* Hard_prev,
+                      const epfem_constitutive_out* out) {
+  ConstArgs a;
+  GatherArgs g;
+  if (int rc = delta_args(ctx, c, mat, E, Ep_prev, Hard_prev, out, &a, &g)) return rc;
   return launch_newton_fused(mat->model, c->info.family, c->info.dim, a, g, ctx->stream);
+}
+
+// Overlapped step: element chunk k (fused kernel) on the context stream,
+// row chunk k (row stream) on the side stream after chunk k's event, so the
+// memory-bound assembly of chunk k runs under the compute-bound update of
+// chunk k+1.  Fork/join events keep the call ordered on the context stream
+// (and capturable into one CUDA graph).
+static int overlapped_step(epfem_ctx* ctx, const epfem_cache* c, int model, const ConstArgs& a,
+                           GatherArgs g, double* K_values) {
+  g.base = c->K_elast;
+  g.out = K_values;
+  EPFEM_CUDA_TRY(cudaEventRecord(ctx->ev_fork, ctx->stream));
+  EPFEM_CUDA_TRY(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+  for (int k = 0; k < c->n_chunks; ++k) {
+    g.e_begin = c->echunk[k];
+    g.e_end = c->echunk[k + 1];
+    if (int rc = launch_newton_fused(model, c->info.family, c->info.dim, a, g, ctx->stream)) return rc;
+    EPFEM_CUDA_TRY(cudaEventRecord(ctx->ev_chunk[k], ctx->stream));
+    EPFEM_CUDA_TRY(cudaStreamWaitEvent(ctx->side, ctx->ev_chunk[k], 0));
+    g.n_begin = c->nchunk[k];
+    g.n_end = c->nchunk[k + 1];
+    if (int rc = launch_row_stream(c->info.family, c->info.dim, g, ctx->side)) return rc;
+  }
+  EPFEM_CUDA_TRY(cudaEventRecord(ctx->ev_join, ctx->side));
+  EPFEM_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+  return 0;
 }
 
 static int rows_part(epfem_ctx* ctx, const epfem_cache* c, double* K_values) {
@@ -465,6 +545,13 @@ int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* c, const epfem_material
                       const epfem_constitutive_out* out, double* K_values) {
   if (!K_values || !aligned16(K_values))
     return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: K must be 16-byte aligned");
+  if (c && c->n_chunks > 1) {
+    ConstArgs a;
+    GatherArgs g;
+    if (int rc = delta_args(ctx, c, mat, E, Ep_prev, Hard_prev, out, &a, &g)) return rc;
+    if (int rc = overlapped_step(ctx, c, mat->model, a, g, K_values)) return rc;
+    return finish(ctx);
+  }
   if (int rc = delta_part(ctx, c, mat, E, Ep_prev, Hard_prev, out)) return rc;
   if (int rc = rows_part(ctx, c, K_values)) return rc;
   return finish(ctx);

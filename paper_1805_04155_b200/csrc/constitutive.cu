@@ -326,13 +326,13 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? 8 :
   c.crit = nullptr;
 
   const int tid = threadIdx.x;
-  const int64_t e0 = (int64_t)blockIdx.x * EPB;
+  const int64_t e0 = g.e_begin + (int64_t)blockIdx.x * EPB;
   if (tid < EPB) s_mask[tid] = 0u;
   __syncthreads();
   for (int k = tid; k < EPB * NQ; k += blockDim.x) {
     const int le = k / NQ, q = k - le * NQ;
     const int64_t e = e0 + le;
-    if (e >= g.n_elements) continue;
+    if (e >= g.e_end) continue;
     const int64_t m = e * NQ + q;
     double* st = s_st[le][q];
     auto stage = [&](auto&& f) {
@@ -343,8 +343,8 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? 8 :
     eval_point<MODEL>(c, m, GlobalIn{c}, stage);
   }
   __syncthreads();
-  if (tid < EPB && e0 + tid < g.n_elements) g.emask[e0 + tid] = s_mask[tid];
-  delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, g.n_elements, g.scratch);
+  if (tid < EPB && e0 + tid < g.e_end) g.emask[e0 + tid] = s_mask[tid];
+  delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, g.e_end, g.scratch);
 }
 
 // Per-buffer shared-memory tile of the pipelined kernel (doubles): the
@@ -383,7 +383,8 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS)
   c.pm = c.sm = c.am = nullptr;
   c.crit = nullptr;
   const int tid = threadIdx.x;
-  const int64_t n_int = g.n_elements * NQ;
+  const int64_t n_int = g.e_end * NQ;
+  const int64_t pbase = g.e_begin * NQ;
 
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
@@ -393,7 +394,7 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS)
   __syncthreads();
   auto issue = [&](int64_t grp, int b) {  // one thread
     double* t = tiles + b * Tile::SIZE;
-    const int64_t p0 = grp * PPG;
+    const int64_t p0 = pbase + grp * PPG;
     const int np = (int)min((int64_t)PPG, n_int - p0);
     const int sh = (int)(p0 & 1);  // J^-1 / w source shifted down to a 16-byte boundary
     const unsigned be = (unsigned)np * 48u;
@@ -424,12 +425,12 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS)
     mbar_wait(&s_bar[b], (unsigned)(it >> 1) & 1u);
     __syncthreads();
     const double* t = tiles + b * Tile::SIZE;
-    const int64_t e0 = grp * EPB;
-    const int sh = (int)((grp * PPG) & 1);
+    const int64_t e0 = g.e_begin + grp * EPB;
+    const int sh = (int)((pbase + grp * PPG) & 1);
     for (int k = tid; k < PPG; k += blockDim.x) {
       const int le = k / NQ, q = k - le * NQ;
       const int64_t e = e0 + le;
-      if (e >= g.n_elements) continue;
+      if (e >= g.e_end) continue;
       const int64_t m = e * NQ + q;
       double* st = s_st[le][q];
       auto stage = [&](auto&& f) {
@@ -440,8 +441,8 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS)
       eval_point<MODEL>(c, m, SmemIn{t + Tile::OE, t + Tile::OEP, t + Tile::OH, k}, stage);
     }
     __syncthreads();
-    if (tid < EPB && e0 + tid < g.n_elements) g.emask[e0 + tid] = s_mask[tid];
-    delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, g.n_elements, g.scratch);
+    if (tid < EPB && e0 + tid < g.e_end) g.emask[e0 + tid] = s_mask[tid];
+    delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, g.e_end, g.scratch);
     __syncthreads();
   }
 }
@@ -490,7 +491,7 @@ static int launch_pipe(const ConstArgs& c, const GatherArgs& g, cudaStream_t st)
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (per_sm < 1) per_sm = 1;
   }
-  const int64_t n_groups = (g.n_elements + Cfg::EPB - 1) / Cfg::EPB;
+  const int64_t n_groups = (g.e_end - g.e_begin + Cfg::EPB - 1) / Cfg::EPB;
   const int64_t grid = std::min<int64_t>(n_groups, (int64_t)per_sm * num_sms);
   kern<<<(unsigned)grid, Cfg::THREADS, Tile::BYTES, st>>>(c, g, n_groups);
   EPFEM_CUDA_TRY(cudaGetLastError());
@@ -499,7 +500,7 @@ static int launch_pipe(const ConstArgs& c, const GatherArgs& g, cudaStream_t st)
 
 int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
                         cudaStream_t st) {
-  if (g.n_elements == 0) return 0;
+  if (g.e_end <= g.e_begin) return 0;
   // The TMA-pipelined variant measured slower than the plain one on B200
   // (cfg2: 0.255 vs 0.224 ms; the kernel is bound by FP64 dependency chains,
   // not load latency), so it is opt-in: EPFEM_FUSED=pipe.
@@ -522,7 +523,7 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
       }
       return;
     }
-    const unsigned blocks = (unsigned)((g.n_elements + Cfg::EPB - 1) / Cfg::EPB);
+    const unsigned blocks = (unsigned)((g.e_end - g.e_begin + Cfg::EPB - 1) / Cfg::EPB);
     switch (model) {
       case EPFEM_MODEL_VON_MISES:
         k_newton_fused<EPFEM_MODEL_VON_MISES, DIM, NP, NQ><<<blocks, Cfg::THREADS, 0, st>>>(c, g);

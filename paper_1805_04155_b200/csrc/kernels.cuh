@@ -53,6 +53,9 @@ struct GatherArgs {
   int max_span;      // widest value range of any row-stream CTA (doubles)
   int max_items;     // most (element, node) items of any row-stream CTA
   double Cu[21];     // packed elastic operator when the material is uniform
+  // sub-range processed by one launch (chunked, overlapped schedule)
+  int64_t e_begin, e_end;  // elements of the delta / fused kernels
+  int64_t n_begin, n_end;  // nodes of the row stream
 };
 struct PatternOut {
   int64_t* n2e_ptr = nullptr;
@@ -83,6 +86,9 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
 size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements);
 int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
                     cudaStream_t st, int* npc_out, int* span_out, int* items_out);
+int plan_chunks(int64_t n_nodes, int64_t n_elements, int np, const int64_t* n2e_ptr,
+                const int32_t* n2e, int npc, int n_chunks, int64_t* nchunk, int64_t* echunk,
+                cudaStream_t st);
 int launch_strains(int family, int dim, int64_t n_e, const int32_t* elem, const double* inv,
                    const double* gradhat, const double* u, double* E, cudaStream_t st,
                    int num_sms);

@@ -35,13 +35,13 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS) k_elem_delta_s
   __shared__ unsigned s_mask[EPB];
 
   const int tid = threadIdx.x;
-  const int64_t e0 = (int64_t)blockIdx.x * EPB;
+  const int64_t e0 = a.e_begin + (int64_t)blockIdx.x * EPB;
   if (tid < EPB) s_mask[tid] = 0u;
   __syncthreads();
   for (int k = tid; k < EPB * NQ; k += blockDim.x) {
     const int le = k / NQ, q = k - le * NQ;
     const int64_t e = e0 + le;
-    if (e >= a.n_elements) continue;
+    if (e >= a.e_end) continue;
     const int64_t m = e * NQ + q;
     if (!(__ldg(a.flags + m) & 1)) continue;
     atomicOr(&s_mask[le], 1u << q);
@@ -67,8 +67,8 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS) k_elem_delta_s
     });
   }
   __syncthreads();
-  if (tid < EPB && e0 + tid < a.n_elements) a.emask[e0 + tid] = s_mask[tid];
-  delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, a.n_elements, a.scratch);
+  if (tid < EPB && e0 + tid < a.e_end) a.emask[e0 + tid] = s_mask[tid];
+  delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, a.e_end, a.scratch);
 }
 
 constexpr int kStreamThreads = 256;
@@ -85,8 +85,8 @@ __global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int
   constexpr int NB = NP * (NP + 1) / 2;
   constexpr int D2 = DIM * DIM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t n0 = (int64_t)blockIdx.x * npc;
-  const int64_t n1 = min(n0 + (int64_t)npc, a.n_nodes);
+  const int64_t n0 = a.n_begin + (int64_t)blockIdx.x * npc;
+  const int64_t n1 = min(n0 + (int64_t)npc, a.n_end);
   const int nloc = (int)(n1 - n0);
   const int64_t v0 = __ldg(a.nbr_ptr + n0) * D2;
   const int64_t v1 = __ldg(a.nbr_ptr + n1) * D2;
@@ -167,7 +167,53 @@ __global__ void k_range_span(int64_t n_nodes, int npc, int d2, const int64_t* __
   atomicMax(out + 1, mi);
 }
 
+// largest element touching each node chunk (items are sorted, so a node's
+// last item holds its largest element)
+__global__ void k_chunk_emax(int64_t n_nodes, int np, int64_t nodes_per_chunk,
+                             const int64_t* __restrict__ n2e_ptr, const int32_t* __restrict__ n2e,
+                             unsigned long long* emax) {
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < n_nodes;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t hi = n2e_ptr[a + 1];
+    if (hi > n2e_ptr[a]) atomicMax(emax + a / nodes_per_chunk, (unsigned long long)(n2e[hi - 1] / np));
+  }
+}
+
 }  // namespace
+
+// Split the nodes into n_chunks ranges aligned to the row-stream CTA size and
+// the elements so that element chunk k holds exactly the elements the rows of
+// node chunk k need beyond chunks < k (monotone by construction).
+int plan_chunks(int64_t n_nodes, int64_t n_elements, int np, const int64_t* n2e_ptr,
+                const int32_t* n2e, int npc, int n_chunks, int64_t* nchunk, int64_t* echunk,
+                cudaStream_t st) {
+  int64_t per = ((n_nodes + n_chunks - 1) / n_chunks + npc - 1) / npc * npc;
+  if (per < npc) per = npc;
+  n_chunks = (int)((n_nodes + per - 1) / per);
+  unsigned long long* d = nullptr;
+  unsigned long long h[64];
+  // returns -1 (message set) on failure: the chunk count is the success value
+  if (cudaMalloc(&d, sizeof(unsigned long long) * n_chunks) != cudaSuccess ||
+      cudaMemsetAsync(d, 0, sizeof(unsigned long long) * n_chunks, st) != cudaSuccess)
+    return cuda_fail(cudaGetLastError(), "plan_chunks"), -1;
+  k_chunk_emax<<<256, 256, 0, st>>>(n_nodes, np, per, n2e_ptr, n2e, d);
+  if (cudaMemcpyAsync(h, d, sizeof(unsigned long long) * n_chunks, cudaMemcpyDeviceToHost, st) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess) {
+    cudaFree(d);
+    return cuda_fail(cudaGetLastError(), "plan_chunks"), -1;
+  }
+  cudaFree(d);
+  nchunk[0] = 0;
+  echunk[0] = 0;
+  int64_t run = 0;
+  for (int k = 0; k < n_chunks; ++k) {
+    nchunk[k + 1] = std::min<int64_t>(n_nodes, (int64_t)(k + 1) * per);
+    run = std::max<int64_t>(run, (int64_t)h[k] + 1);
+    echunk[k + 1] = k + 1 == n_chunks ? n_elements : std::min<int64_t>(run, n_elements);
+  }
+  return n_chunks;
+}
 
 size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements) {
   size_t nb = 0;
@@ -213,7 +259,8 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
   bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
     constexpr int DIM = decltype(D)::value;
     constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
-    const int64_t rblocks = (a.n_nodes + a.npc - 1) / a.npc;
+    const int64_t rblocks = (a.n_end - a.n_begin + a.npc - 1) / a.npc;
+    if (rblocks <= 0) return;
     const size_t smem = sizeof(double) * ((size_t)a.max_span + 2) +
                         sizeof(int) * ((size_t)a.max_items + 2 * ((size_t)a.npc + 1));
     auto kern = k_row_stream<DIM, NP, NQ>;
@@ -236,7 +283,7 @@ int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStrea
     constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
     using Cfg = DeltaCfg<DIM, NP, NQ>;
     if (a.n_elements > 0) {
-      const int64_t blocks = (a.n_elements + Cfg::EPB - 1) / Cfg::EPB;
+      const int64_t blocks = (a.e_end - a.e_begin + Cfg::EPB - 1) / Cfg::EPB;
       if (mode == G_TANGENT_PACKED)
         k_elem_delta_staged<DIM, NP, NQ, G_TANGENT_PACKED><<<(unsigned)blocks, Cfg::THREADS, 0, st>>>(a);
       else
