@@ -377,8 +377,11 @@ int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_materi
                                  &c->max_span, &c->max_items))
       return bail(rc);
   {
-    // overlap plan: ~8 chunks of >= 64K nodes (EPFEM_CHUNKS overrides)
-    int want = (int)std::min<int64_t>(8, std::max<int64_t>(1, I.n_nodes / 65536));
+    // overlap plan, opt-in via EPFEM_CHUNKS: measured on B200 the chunked
+    // two-stream schedule is slower than one fused + one row launch (cfg2:
+    // 0.412 ms at 4 chunks vs 0.377 ms) because each fused launch fills the
+    // GPU and the row-stream CTAs only start as it drains
+    int want = 1;
     if (const char* v = getenv("EPFEM_CHUNKS")) want = std::max(1, std::min(kMaxChunks, atoi(v)));
     if (want > 1 && I.n_nodes > 0) {
       const int n = plan_chunks(I.n_nodes, I.n_elements, I.n_p, c->pat.n2e_ptr, c->pat.n2e, c->npc,
