@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS)
       double* st = s_st[le][q];
       auto stage = [&](auto&& f) {
         atomicOr(&s_mask[le], 1u << q);
-        stage_geometry<DIM, NP>(st, t + Tile::OI + (k + sh) * D2, g.gradhat, q);
+        stage_geometry<DIM, NP, true>(st, t + Tile::OI + (k + sh) * D2, g.gradhat, q);
         stage_dw<DIM>(st + NP * DIM, t[Tile::OW + k + sh], g, m, f);
       };
       eval_point<MODEL>(c, m, SmemIn{t + Tile::OE, t + Tile::OEP, t + Tile::OH, k}, stage);

@@ -40,7 +40,10 @@ struct DeltaCfg {
   }
   static constexpr int NT = nt();                        // phase-2 threads per element
   static constexpr int TPE = NQ > NT ? NQ : NT;           // threads per element
-  static constexpr int MAXT = 128;
+#ifndef EPFEM_DELTA_MAXT
+#define EPFEM_DELTA_MAXT 128
+#endif
+  static constexpr int MAXT = EPFEM_DELTA_MAXT;
   static constexpr int BUDGET = 5120;                     // doubles of staged records per CTA
   static constexpr int E1 = MAXT / TPE, E2 = BUDGET / (NQ * REC);
   static constexpr int EPB = (E1 < E2 ? E1 : E2) > 0 ? (E1 < E2 ? E1 : E2) : 1;
@@ -54,12 +57,12 @@ __device__ __forceinline__ constexpr int arow(int r) {
 }
 
 // dphi_p = J^-1 ghat_p for every node of the element at point q.
-template <int DIM, int NP>
+template <int DIM, int NP, bool INV_IN_SMEM = false>
 __device__ __forceinline__ void stage_geometry(double* st, const double* inv_m,
                                                const double* __restrict__ gradhat, int q) {
-  double J[DIM * DIM];  // inv_m may point to global or shared memory
+  double J[DIM * DIM];
 #pragma unroll
-  for (int t = 0; t < DIM * DIM; ++t) J[t] = inv_m[t];
+  for (int t = 0; t < DIM * DIM; ++t) J[t] = INV_IN_SMEM ? inv_m[t] : __ldg(inv_m + t);
 #pragma unroll 4
   for (int p = 0; p < NP; ++p) {
     const double* gh = gradhat + (q * NP + p) * DIM;
