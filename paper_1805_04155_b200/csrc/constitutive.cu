@@ -86,11 +86,13 @@ struct NoSink {
 
 // Where a point's E / Ep / Hard come from: global memory (grid-stride
 // kernels) or a shared-memory tile filled by TMA (pipelined fused kernel).
-struct GlobalIn {
-  const ConstArgs& a;
-  __device__ __forceinline__ void e(int64_t q, double* v) const { load6(a.E, q, v); }
-  __device__ __forceinline__ void ep(int64_t q, double* v) const { load6(a.Ep, q, v); }
-  __device__ __forceinline__ void hard(int64_t q, double* v) const { load6(a.Hard, q, v); }
+struct GlobalIn {  // pointers by value: never take the address of the kernel arguments
+  const double* E;
+  const double* Ep;
+  const double* H;
+  __device__ __forceinline__ void e(int64_t q, double* v) const { load6(E, q, v); }
+  __device__ __forceinline__ void ep(int64_t q, double* v) const { load6(Ep, q, v); }
+  __device__ __forceinline__ void hard(int64_t q, double* v) const { load6(H, q, v); }
 };
 struct SmemIn {
   const double* E;
@@ -310,7 +312,7 @@ __global__ void __launch_bounds__(256) k_constitutive(ConstArgs a) {
   NoSink none;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < a.n; q += stride)
-    eval_point<MODEL>(a, q, GlobalIn{a}, none);
+    eval_point<MODEL>(a, q, GlobalIn{a.E, a.Ep, a.Hard}, none);
 }
 
 template <int MODEL, int DIM, int NP, int NQ>
@@ -340,7 +342,7 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? 8 :
       stage_geometry<DIM, NP>(st, g.inv + m * Cfg::D2, g.gradhat, q);
       stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f);
     };
-    eval_point<MODEL>(c, m, GlobalIn{c}, stage);
+    eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
   }
   __syncthreads();
   if (tid < EPB && e0 + tid < g.e_end) g.emask[e0 + tid] = s_mask[tid];
