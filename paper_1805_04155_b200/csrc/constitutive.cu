@@ -315,8 +315,11 @@ __global__ void __launch_bounds__(256) k_constitutive(ConstArgs a) {
     eval_point<MODEL>(a, q, GlobalIn{a.E, a.Ep, a.Hard}, none);
 }
 
+// minBlocks: 8 CTAs/SM in 2D (caps at 64 registers, measured faster); 0 in 3D
+// leaves ptxas its own heuristic (126 registers; an explicit 1 gives 144 and
+// is ~15% slower on cfg4).
 template <int MODEL, int DIM, int NP, int NQ>
-__global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? 8 : 1)
+__global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? 8 : 0)
     k_newton_fused(ConstArgs c, GatherArgs g) {
   using Cfg = DeltaCfg<DIM, NP, NQ>;
   constexpr int EPB = Cfg::EPB;
