@@ -64,11 +64,12 @@ def lib() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB):
+    path = os.environ.get("EPFEM_GPU_LIB", LIB)  # tuning experiments: an in-tree variant build
+    if not os.path.exists(path):
         raise ImportError(
-            f"libepfem_gpu.so not found at {LIB}; build it with "
+            f"libepfem_gpu.so not found at {path}; build it with "
             "`python -m paper_1805_04155_b200.build` (there is no CPU fallback)")
-    L = C.CDLL(LIB)
+    L = C.CDLL(path)
     L.epfem_last_error.restype = C.c_char_p
     L.epfem_abi_version.restype = C.c_int
     L.epfem_ctx_create.argtypes = [C.c_int, _P, C.POINTER(_P)]

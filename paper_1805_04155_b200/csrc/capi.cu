@@ -122,7 +122,11 @@ int epfem_ctx_create(int device, void* cuda_stream, epfem_ctx** out) {
   DevErr z{};
   z.index = ~0ull;
   cudaMemcpy(c->err, &z, sizeof(DevErr), cudaMemcpyHostToDevice);
-  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+  // the side stream carries the row stream of the overlapped step: highest
+  // priority, so its CTAs take SM slots ahead of the next fused chunk
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     epfem_ctx_destroy(c);
@@ -515,6 +519,10 @@ static int overlapped_step(epfem_ctx* ctx, const epfem_cache* c, int model, cons
                            GatherArgs g, double* K_values) {
   g.base = c->K_elast;
   g.out = K_values;
+  // EPFEM_CHUNK_SERIAL: both launches of a chunk on the context stream (the
+  // chunk's workspace is still L2-resident when its rows are assembled)
+  static const bool serial = getenv("EPFEM_CHUNK_SERIAL") != nullptr;
+  cudaStream_t rs = serial ? ctx->stream : ctx->side;
   EPFEM_CUDA_TRY(cudaEventRecord(ctx->ev_fork, ctx->stream));
   EPFEM_CUDA_TRY(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
   for (int k = 0; k < c->n_chunks; ++k) {
@@ -525,7 +533,7 @@ static int overlapped_step(epfem_ctx* ctx, const epfem_cache* c, int model, cons
     EPFEM_CUDA_TRY(cudaStreamWaitEvent(ctx->side, ctx->ev_chunk[k], 0));
     g.n_begin = c->nchunk[k];
     g.n_end = c->nchunk[k + 1];
-    if (int rc = launch_row_stream(c->info.family, c->info.dim, g, ctx->side)) return rc;
+    if (int rc = launch_row_stream(c->info.family, c->info.dim, g, rs)) return rc;
   }
   EPFEM_CUDA_TRY(cudaEventRecord(ctx->ev_join, ctx->side));
   EPFEM_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));

@@ -315,11 +315,11 @@ __global__ void __launch_bounds__(256) k_constitutive(ConstArgs a) {
     eval_point<MODEL>(a, q, GlobalIn{a.E, a.Ep, a.Hard}, none);
 }
 
-// minBlocks: 8 CTAs/SM in 2D (caps at 64 registers, measured faster); 0 in 3D
+// minBlocks: 1024 threads/SM in 2D (caps at 64 registers, measured faster); 0 in 3D
 // leaves ptxas its own heuristic (126 registers; an explicit 1 gives 144 and
 // is ~15% slower on cfg4).
 template <int MODEL, int DIM, int NP, int NQ>
-__global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? 8 : 0)
+__global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? 1024 / DeltaCfg<DIM, NP, NQ>::THREADS : 0)
     k_newton_fused(ConstArgs c, GatherArgs g) {
   using Cfg = DeltaCfg<DIM, NP, NQ>;
   constexpr int EPB = Cfg::EPB;
@@ -350,6 +350,113 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? 8 :
   __syncthreads();
   if (tid < EPB && e0 + tid < g.e_end) g.emask[e0 + tid] = s_mask[tid];
   delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, g.e_end, g.scratch);
+}
+
+// k_newton_warp (2D): the fused kernel with warp-owned elements (WarpCfg,
+// delta.cuh).  Lane l < EPW * NQ updates point q = l % NQ of element l / NQ;
+// the warp's plastic masks are one ballot; phase-2 lane l < EPW * NT builds
+// chunk l % NT of element l / NT.  No CTA barrier anywhere.  (Measured on
+// B200, cfg2: a persistent grid-stride version is ~10% slower, and adding a
+// cp.async prefetch of the next group's inputs slower still.)
+#ifndef EPFEM_WARP_MINB
+#define EPFEM_WARP_MINB 5
+#endif
+#ifndef EPFEM_EXP
+#define EPFEM_EXP 0  // timing experiments only: 1 = no phase 2, 2 = phase 2 without FP64 work
+#endif
+#ifndef EPFEM_EARLY_GEOM
+#define EPFEM_EARLY_GEOM 1
+#endif
+template <int MODEL, int NP, int NQ>
+__global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
+    k_newton_warp(ConstArgs c, GatherArgs g) {
+  constexpr int DIM = 2;
+  using W = WarpCfg<DIM, NP, NQ>;
+  static_assert(W::EPW * NQ <= 32 && W::EPW * W::NT <= 32, "warp mapping");
+  constexpr int EPW = W::EPW, REC = W::REC;
+  constexpr unsigned QMASK = NQ >= 32 ? 0xffffffffu : (1u << NQ) - 1u;
+  constexpr int RECB = W::NB * W::D2;  // doubles per element workspace record
+  __shared__ double s_st[W::WPB][EPW * NQ * REC];
+  __shared__ __align__(16) double s_out[W::WPB][EPW * RECB];
+  c.DS = nullptr;  // hot path: S, flags, packed D only
+  c.Ep_out = c.Hard_out = nullptr;
+  c.pm = c.sm = c.am = nullptr;
+  c.crit = nullptr;
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t e0 = g.e_begin + ((int64_t)blockIdx.x * W::WPB + w) * EPW;
+  if (e0 >= g.e_end) return;  // warp-uniform
+  double* st_w = s_st[w];
+  bool plastic = false;
+  if (lane < EPW * NQ) {
+    const int le = lane / NQ, q = lane - le * NQ;
+    const int64_t e = e0 + le;
+    if (e < g.e_end) {
+      const int64_t m = e * NQ + q;
+      double* st = st_w + lane * REC;
+#if EPFEM_EARLY_GEOM
+      // J^-1 and w are loaded with E / Ep / Hard, before the return map, so
+      // plastic points do not pay a second dependent memory round trip
+      double jinv[W::D2];
+      {
+        const double2* p2 = reinterpret_cast<const double2*>(g.inv + m * W::D2);
+#pragma unroll
+        for (int k = 0; k < W::D2 / 2; ++k) {
+          const double2 v = __ldg(p2 + k);
+          jinv[2 * k] = v.x;
+          jinv[2 * k + 1] = v.y;
+        }
+      }
+      const double wq = __ldg(g.weight + m);
+      auto stage = [&](auto&& f) {
+        stage_geometry<DIM, NP, true>(st, jinv, g.gradhat, q);
+        stage_dw<DIM>(st + NP * DIM, wq, g, m, f);
+      };
+#else
+      auto stage = [&](auto&& f) {
+        stage_geometry<DIM, NP>(st, g.inv + m * W::D2, g.gradhat, q);
+        stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f);
+      };
+#endif
+      plastic = eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
+    }
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, plastic);
+  __syncwarp();
+  if (lane < EPW && e0 + lane < g.e_end) g.emask[e0 + lane] = (bal >> (lane * NQ)) & QMASK;
+  if (EPFEM_EXP != 1 && lane < EPW * W::NT) {
+    const int le = lane / W::NT;
+    const int64_t e = e0 + le;
+    const unsigned mask = (bal >> (le * NQ)) & QMASK;
+    if (e < g.e_end && mask) {
+      int a, c0;
+      chunk_of<NP, W::CS>(lane - le * W::NT, a, c0);
+      double* rec = s_out[w] + le * RECB;  // staged, then one bulk store per element
+      if (EPFEM_EXP == 2) {  // same stores, staged values instead of the products
+        const double* st = st_w + le * NQ * REC;
+        for (int bb = 0; bb < W::CS && c0 + bb < NP; ++bb)
+          for (int k = 0; k < W::D2; ++k) rec[blk_index<NP>(a, c0 + bb) * W::D2 + k] = st[bb * 4 + k];
+      } else {
+        delta_chunk_uniform<DIM, NP, W::CS, REC>(st_w + le * NQ * REC, mask, a, c0, rec);
+      }
+    }
+  }
+  // the workspace records leave through the TMA unit: whole 1-KB-class
+  // records instead of 8-byte scattered stores from every lane
+  if (EPFEM_EXP != 1) {
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      int n = 0;
+      for (int le = 0; le < EPW; ++le)
+        if (e0 + le < g.e_end && ((bal >> (le * NQ)) & QMASK)) {
+          tma_store_1d(g.scratch + (size_t)(e0 + le) * RECB, s_out[w] + le * RECB,
+                       (unsigned)(RECB * sizeof(double)));
+          ++n;
+        }
+      if (n) tma_store_wait_read();
+    }
+  }
 }
 
 // Per-buffer shared-memory tile of the pipelined kernel (doubles): the
@@ -509,9 +616,14 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
   // The TMA-pipelined variant measured slower than the plain one on B200
   // (cfg2: 0.255 vs 0.224 ms; the kernel is bound by FP64 dependency chains,
   // not load latency), so it is opt-in: EPFEM_FUSED=pipe.
+  // EPFEM_FUSED=cta forces the CTA kernel in 2D (default there: k_newton_warp).
   static const bool pipe = [] {
     const char* v = getenv("EPFEM_FUSED");
     return v && v[0] == 'p' && v[1] == 'i';
+  }();
+  static const bool cta = [] {
+    const char* v = getenv("EPFEM_FUSED");
+    return v && v[0] == 'c' && v[1] == 't';
   }();
   int rc = 0;
   bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
@@ -527,6 +639,25 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
         default: rc = launch_pipe<EPFEM_MODEL_ELASTIC, DIM, NP, NQ>(c, g, st); break;
       }
       return;
+    }
+    if constexpr (DIM == 2) {
+      if (!cta) {
+        using W = WarpCfg<DIM, NP, NQ>;
+        const int64_t per = (int64_t)W::EPW * W::WPB;
+        const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
+        switch (model) {
+          case EPFEM_MODEL_VON_MISES:
+            k_newton_warp<EPFEM_MODEL_VON_MISES, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, g);
+            break;
+          case EPFEM_MODEL_DRUCKER_PRAGER:
+            k_newton_warp<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, g);
+            break;
+          default:
+            k_newton_warp<EPFEM_MODEL_ELASTIC, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, g);
+            break;
+        }
+        return;
+      }
     }
     const unsigned blocks = (unsigned)((g.e_end - g.e_begin + Cfg::EPB - 1) / Cfg::EPB);
     switch (model) {

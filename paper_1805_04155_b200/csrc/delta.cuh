@@ -193,4 +193,143 @@ __device__ __forceinline__ void delta_phase2(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-synchronous variant (2D): a warp owns EPW whole elements, so phase 1
+// and phase 2 meet at a __syncwarp instead of a CTA barrier, and the plastic
+// masks come from one __ballot_sync.  CS is the smallest chunk that fits the
+// most elements in a warp; every phase-2 lane runs exactly CS blocks (blocks
+// past the row end are computed on a clamped column and dropped), so the
+// block loop has no divergent branch.  Same FMA sequence per block as
+// delta_phase2, hence identical bits.
+template <int DIM, int NP, int NQ>
+struct WarpCfg {
+  static constexpr int NS = DIM == 3 ? 6 : 3;
+  static constexpr int NSP = NS * (NS + 1) / 2;
+  static constexpr int D2 = DIM * DIM;
+  static constexpr int NB = NP * (NP + 1) / 2;
+  static constexpr int REC = NP * DIM + NSP;
+  static constexpr int nt(int cs) {
+    int s = 0;
+    for (int a = 0; a < NP; ++a) s += (NP - a + cs - 1) / cs;
+    return s;
+  }
+  static constexpr int epw(int cs) {
+    const int t = NQ > nt(cs) ? NQ : nt(cs);
+    return 32 / t;
+  }
+  static constexpr int best_cs() {
+    int best = NP, be = 0;
+    for (int cs = 1; cs <= NP; ++cs)
+      if (epw(cs) > be) {
+        be = epw(cs);
+        best = cs;
+      }
+    return best;
+  }
+  static constexpr int CS = best_cs();
+  static constexpr int NT = nt(CS);
+  static constexpr int EPW = epw(CS);  // elements per warp
+#ifndef EPFEM_WARP_WPB
+#define EPFEM_WARP_WPB 4
+#endif
+  static constexpr int WPB = EPFEM_WARP_WPB;  // warps per CTA
+  static constexpr int THREADS = 32 * WPB;
+};
+
+// Blocks (a, c0 .. c0 + CS - 1) of one element from its staged records
+// st_e[q * REC], accumulated over the plastic points in `mask`, written to
+// the element's workspace record.
+#ifndef EPFEM_SUBCHUNK
+#define EPFEM_SUBCHUNK 0
+#endif
+template <int DIM, int NP, int CS, int REC>
+__device__ __forceinline__ void delta_chunk_uniform1(const double* st_e, unsigned mask, int a, int c0,
+                                                     double* __restrict__ rec);
+// CS blocks in passes of SUB (fewer live accumulators; T_a is recomputed per pass)
+template <int DIM, int NP, int CS, int REC>
+__device__ __forceinline__ void delta_chunk_uniform(const double* st_e, unsigned mask, int a, int c0,
+                                                    double* __restrict__ rec) {
+  constexpr int SUB = EPFEM_SUBCHUNK > 0 && EPFEM_SUBCHUNK < CS ? EPFEM_SUBCHUNK : CS;
+#pragma unroll 1
+  for (int s0 = 0; s0 < CS; s0 += SUB)
+    if (c0 + s0 < NP) delta_chunk_uniform1<DIM, NP, SUB, REC>(st_e, mask, a, c0 + s0, rec);
+}
+template <int DIM, int NP, int CS, int REC>
+__device__ __forceinline__ void delta_chunk_uniform1(const double* st_e, unsigned mask, int a, int c0,
+                                                     double* __restrict__ rec) {
+  constexpr int NS = DIM == 3 ? 6 : 3, D2 = DIM * DIM;
+  double blk[CS][DIM][DIM];
+#pragma unroll
+  for (int b = 0; b < CS; ++b)
+#pragma unroll
+    for (int i = 0; i < DIM; ++i)
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) blk[b][i][j] = 0.0;
+  while (mask) {
+    const int q = __ffs(mask) - 1;
+    mask &= mask - 1u;
+    const double* st = st_e + q * REC;
+    const double* dw = st + NP * DIM;
+    auto Dw = [&](int r, int c) {
+      const int lo = r < c ? r : c, hi = r < c ? c : r;
+      return dw[lo * NS - lo * (lo - 1) / 2 + (hi - lo)];
+    };
+    double ga[DIM];
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) ga[i] = st[a * DIM + i];
+    double T[DIM][NS];
+#pragma unroll
+    for (int c = 0; c < NS; ++c) {
+      if constexpr (DIM == 3) {
+        T[0][c] = __fma_rn(ga[2], Dw(5, c), __fma_rn(ga[1], Dw(3, c), __dmul_rn(ga[0], Dw(0, c))));
+        T[1][c] = __fma_rn(ga[2], Dw(4, c), __fma_rn(ga[0], Dw(3, c), __dmul_rn(ga[1], Dw(1, c))));
+        T[DIM - 1][c] =
+            __fma_rn(ga[0], Dw(5, c), __fma_rn(ga[1], Dw(4, c), __dmul_rn(ga[2], Dw(2, c))));
+      } else {
+        T[0][c] = __fma_rn(ga[1], Dw(2, c), __dmul_rn(ga[0], Dw(0, c)));
+        T[1][c] = __fma_rn(ga[0], Dw(2, c), __dmul_rn(ga[1], Dw(1, c)));
+      }
+    }
+#pragma unroll
+    for (int bb = 0; bb < CS; ++bb) {
+      const int b = c0 + bb < NP ? c0 + bb : NP - 1;  // clamped: result dropped below
+      const double* h = st + b * DIM;
+      const double h0 = h[0], h1 = h[1], h2 = DIM == 3 ? h[DIM - 1] : 0.0;
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        if constexpr (DIM == 3) {
+          blk[bb][i][0] = __fma_rn(T[i][5], h2, __fma_rn(T[i][3], h1, __fma_rn(T[i][0], h0, blk[bb][i][0])));
+          blk[bb][i][1] = __fma_rn(T[i][4], h2, __fma_rn(T[i][3], h0, __fma_rn(T[i][1], h1, blk[bb][i][1])));
+          blk[bb][i][DIM - 1] =
+              __fma_rn(T[i][5], h0, __fma_rn(T[i][4], h1, __fma_rn(T[i][2], h2, blk[bb][i][DIM - 1])));
+        } else {
+          blk[bb][i][0] = __fma_rn(T[i][2], h1, __fma_rn(T[i][0], h0, blk[bb][i][0]));
+          blk[bb][i][1] = __fma_rn(T[i][2], h0, __fma_rn(T[i][1], h1, blk[bb][i][1]));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int bb = 0; bb < CS; ++bb) {
+    if (c0 + bb < NP) {
+      double* o = rec + blk_index<NP>(a, c0 + bb) * D2;
+#pragma unroll
+      for (int i = 0; i < DIM; ++i)
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) o[i * DIM + j] = blk[bb][i][j];
+    }
+  }
+}
+
+// (row a, first column c0) of phase-2 slot k of an element, chunks of CS
+template <int NP, int CS>
+__device__ __forceinline__ void chunk_of(int k, int& a, int& c0) {
+  a = 0;
+  while ((NP - a + CS - 1) / CS <= k) {
+    k -= (NP - a + CS - 1) / CS;
+    ++a;
+  }
+  c0 = a + k * CS;
+}
+
 }  // namespace epfem_gpu

@@ -119,27 +119,51 @@ __global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int
   }
   __syncthreads();
   if (a1 > a0) mbar_wait(&s_bar, 0);
+  // Items are taken UB at a time: every lane first issues the loads of all
+  // UB items (slot byte + workspace value), then applies the adds in item
+  // order, so a node costs one memory round trip per UB items instead of
+  // one per item (the add order, hence the bits, is unchanged).
+  constexpr int KP = (NP * D2 + 31) / 32;
+  constexpr int UB = KP == 1 ? 4 : 1;  // 3D: wider rows already give ILP; registers matter more
   for (int ln = warp; ln < nloc; ln += kStreamThreads / 32) {
     const int ib = s_iptr[ln], ie = s_iptr[ln + 1];
     const int row_len = (s_vptr[ln + 1] - s_vptr[ln]) / DIM;
     double* seg = img + s_vptr[ln];
-    for (int k0 = ib; k0 < ie; ++k0) {
-      const int it = s_item[k0];  // warp-uniform
-      if (it < 0) continue;
-      const int64_t el = it / NP;
-      const int pa = it - (int)el * NP;
-      const double* rec = a.scratch + (size_t)el * NB * D2;
-      // lane <-> entry (pb, i, j) of block row pa; block (pb, pa) read
-      // transposed when pb < pa (branch-free addressing)
-      for (int k = lane; k < NP * D2; k += 32) {
-        const int pb = k / D2, ij = k - pb * D2;
-        const int i = ij / DIM, j = ij - i * DIM;
-        const bool up = pa <= pb;
-        const int lo = up ? pa : pb, hi = up ? pb : pa;
-        const int src = blk_index<NP>(lo, hi) * D2 + (up ? ij : j * DIM + i);
-        const int slot = __ldg(a.slot + (int64_t)it * NP + pb);
-        seg[i * row_len + slot * DIM + j] += __ldg(rec + src);
+    for (int kb = ib; kb < ie; kb += UB) {
+      double v[UB][KP];
+      int sl[UB][KP];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int it = kb + u < ie ? s_item[kb + u] : -1;  // warp-uniform
+        const int64_t el = it / NP;
+        const int pa = it - (int)el * NP;
+        const double* rec = a.scratch + (size_t)el * NB * D2;
+#pragma unroll
+        for (int kk = 0; kk < KP; ++kk) {
+          const int k = lane + 32 * kk;
+          sl[u][kk] = -1;
+          if (it >= 0 && k < NP * D2) {
+            // lane <-> entry (pb, i, j) of block row pa; block (pb, pa) read
+            // transposed when pb < pa (branch-free addressing)
+            const int pb = k / D2, ij = k - pb * D2;
+            const int i = ij / DIM, j = ij - i * DIM;
+            const bool up = pa <= pb;
+            const int lo = up ? pa : pb, hi = up ? pb : pa;
+            const int src = blk_index<NP>(lo, hi) * D2 + (up ? ij : j * DIM + i);
+            sl[u][kk] = __ldg(a.slot + (int64_t)it * NP + pb);
+            v[u][kk] = __ldg(rec + src);
+          }
+        }
       }
+#pragma unroll
+      for (int u = 0; u < UB; ++u)
+#pragma unroll
+        for (int kk = 0; kk < KP; ++kk)
+          if (sl[u][kk] >= 0) {
+            const int k = lane + 32 * kk;
+            const int ij = k % D2, i = ij / DIM, j = ij - i * DIM;
+            seg[i * row_len + sl[u][kk] * DIM + j] += v[u][kk];
+          }
       __syncwarp();
     }
   }
