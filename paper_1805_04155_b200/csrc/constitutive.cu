@@ -459,6 +459,48 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
   }
 }
 
+// k_newton_mma: k_newton_warp's phase 1 (EPW = 32 / NQ elements per warp)
+// followed by the tensor-core phase 2 (delta_mma_warp, delta.cuh).
+#ifndef EPFEM_MMA_MINB
+#define EPFEM_MMA_MINB 6
+#endif
+template <int MODEL, int DIM, int NP, int NQ>
+__global__ void __launch_bounds__(MmaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? EPFEM_MMA_MINB : 0)
+    k_newton_mma(ConstArgs c, GatherArgs g) {
+  using M = MmaCfg<DIM, NP, NQ>;
+  constexpr int EPW = M::EPW, REC = M::REC;
+  constexpr unsigned QMASK = NQ >= 32 ? 0xffffffffu : (1u << NQ) - 1u;
+  __shared__ double s_st[M::WPB][EPW * NQ * REC];
+  __shared__ __align__(16) double s_out[M::WPB][M::OUTB * M::RECB];
+  c.DS = nullptr;  // hot path: S, flags, packed D only
+  c.Ep_out = c.Hard_out = nullptr;
+  c.pm = c.sm = c.am = nullptr;
+  c.crit = nullptr;
+
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t e0 = g.e_begin + ((int64_t)blockIdx.x * M::WPB + w) * EPW;
+  if (e0 >= g.e_end) return;  // warp-uniform
+  double* st_w = s_st[w];
+  bool plastic = false;
+  if (lane < EPW * NQ) {
+    const int le = lane / NQ, q = lane - le * NQ;
+    const int64_t e = e0 + le;
+    if (e < g.e_end) {
+      const int64_t m = e * NQ + q;
+      double* st = st_w + lane * REC;
+      auto stage = [&](auto&& f) {
+        stage_geometry<DIM, NP>(st, g.inv + m * M::D2, g.gradhat, q);
+        stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f);
+      };
+      plastic = eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
+    }
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, plastic);
+  __syncwarp();
+  if (lane < EPW && e0 + lane < g.e_end) g.emask[e0 + lane] = (bal >> (lane * NQ)) & QMASK;
+  delta_mma_warp<DIM, NP, NQ>(st_w, s_out[w], bal, e0, g.e_end, g.scratch, lane);
+}
+
 // Per-buffer shared-memory tile of the pipelined kernel (doubles): the
 // group's E, Ep, Hard (6 per point), J^-1 (dim^2 per point, one extra point
 // for the 16-byte alignment shift) and w (two extra).
@@ -625,6 +667,14 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
     const char* v = getenv("EPFEM_FUSED");
     return v && v[0] == 'c' && v[1] == 't';
   }();
+  // phase 2 on the tensor pipe (k_newton_mma): opt-in, EPFEM_FUSED=mma.
+  // Correct (same parity tests) but measured slower on B200 for cfg2
+  // (0.253 vs 0.211 ms): the per-lane fragment gathers cost more issue
+  // slots than the DMMA saves.
+  static const int mma = [] {
+    const char* v = getenv("EPFEM_FUSED");
+    return (v && v[0] == 'm') ? 2 : 0;
+  }();
   int rc = 0;
   bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
     constexpr int DIM = decltype(D)::value;
@@ -637,6 +687,23 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
           rc = launch_pipe<EPFEM_MODEL_DRUCKER_PRAGER, DIM, NP, NQ>(c, g, st);
           break;
         default: rc = launch_pipe<EPFEM_MODEL_ELASTIC, DIM, NP, NQ>(c, g, st); break;
+      }
+      return;
+    }
+    if (mma == 2) {
+      using M = MmaCfg<DIM, NP, NQ>;
+      const int64_t per = (int64_t)M::EPW * M::WPB;
+      const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
+      switch (model) {
+        case EPFEM_MODEL_VON_MISES:
+          k_newton_mma<EPFEM_MODEL_VON_MISES, DIM, NP, NQ><<<blocks, M::THREADS, 0, st>>>(c, g);
+          break;
+        case EPFEM_MODEL_DRUCKER_PRAGER:
+          k_newton_mma<EPFEM_MODEL_DRUCKER_PRAGER, DIM, NP, NQ><<<blocks, M::THREADS, 0, st>>>(c, g);
+          break;
+        default:
+          k_newton_mma<EPFEM_MODEL_ELASTIC, DIM, NP, NQ><<<blocks, M::THREADS, 0, st>>>(c, g);
+          break;
       }
       return;
     }

@@ -332,4 +332,249 @@ __device__ __forceinline__ void chunk_of(int k, int& a, int& c0) {
   c0 = a + k * CS;
 }
 
+
+// ---------------------------------------------------------------------------
+// Tensor-core phase 2: dK_e = sum_q B_q^T (Dw_q B_q) on the FP64 tensor pipe
+// (mma.sync m8n8k4 f64, SASS DMMA.8x8x4; B200 runs it at the vector-FP64
+// rate but each instruction is 256 FMA, so the warp issues ~10x fewer
+// instructions and holds 2 accumulators per 8x8 tile instead of whole
+// blocks).  The element's dofs (node-major, dim per node) are cut into 8-dof
+// tiles; only upper tiles (I <= J) are formed.  Per plastic point and k-step
+// lane (g = lane / 4, t = lane % 4) supplies A[g][t] = B[4ks + t][8I + g] and
+// Y[t][g] = (Dw B)[4ks + t][8J + g]; rows past NS and dofs past NDOF are 0.
+// The warp owns one element at a time (warp-uniform loop over its plastic
+// points), so there is no per-lane chunking.  Records are the same symmetric
+// block layout as delta_phase2; a diagonal block split across two tiles
+// (3D nodes whose dofs straddle an 8-dof boundary) gets its lower entries
+// mirrored from the upper tile.
+template <int DIM, int NP, int NQ>
+struct MmaCfg {
+  static constexpr int NS = DIM == 3 ? 6 : 3;
+  static constexpr int NSP = NS * (NS + 1) / 2;
+  static constexpr int D2 = DIM * DIM;
+  static constexpr int NB = NP * (NP + 1) / 2;
+  static constexpr int REC = NP * DIM + NSP;  // staged doubles per point (as delta_phase2)
+  static constexpr int RECB = NB * D2;        // workspace doubles per element
+  static constexpr int NDOF = DIM * NP;
+  static constexpr int NT8 = (NDOF + 7) / 8;
+  static constexpr int NSYM = NT8 * (NT8 + 1) / 2;
+  static constexpr int KS = (NS + 3) / 4;
+  static constexpr int TPP = NSYM <= 12 ? NSYM : 12;  // tiles per pass (accumulator budget)
+  static constexpr int NPASS = (NSYM + TPP - 1) / TPP;
+  static constexpr int EPW = 32 / NQ;                 // elements per warp (phase 1 lanes)
+  static constexpr int OUTB = EPW * RECB * 8 <= 4096 ? EPW : 2;  // output record buffers per warp
+  // warps per CTA: keeps the static shared memory (staged records + output
+  // buffers) under 48 KB
+  static constexpr int WPB = DIM == 2 ? 4 : (NQ >= 27 ? 1 : 2);
+  static constexpr int THREADS = 32 * WPB;
+  static constexpr int tile_i(int s) {
+    int i = 0;
+    while (s >= NT8 - i) {
+      s -= NT8 - i;
+      ++i;
+    }
+    return i;
+  }
+  static constexpr int tile_j(int s) {
+    int i = 0;
+    while (s >= NT8 - i) {
+      s -= NT8 - i;
+      ++i;
+    }
+    return i + s;
+  }
+};
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// B[k][(node, comp)] of the strain-displacement operator from the node's
+// physical gradient g (assembly.cpp:162-176 row order)
+template <int DIM>
+__device__ __forceinline__ double b_entry(int k, int comp, const double* g) {
+  // 2 bits per (k, comp): index into g, 3 = structural zero
+  // 3D rows k: (g0,-,-) (-,g1,-) (-,-,g2) (g1,g0,-) (-,g2,g1) (g2,-,g0); 2D: (g0,-) (-,g1) (g1,g0)
+  constexpr unsigned long long T3 = 0x39bc6fdfcull;
+  constexpr unsigned long long T2 = 0x17cull;
+  const int idx = DIM == 3 ? (int)((T3 >> (2 * (k * 3 + comp))) & 3u) : (int)((T2 >> (2 * (k * 2 + comp))) & 3u);
+  return idx == 0 ? g[0] : idx == 1 ? g[1] : (DIM == 3 && idx == 2) ? g[DIM - 1] : 0.0;
+}
+
+// (Dw B)[k][(node, j)] = sum_m Dw[k][d_m(j)] g[e_m(j)], fixed order
+template <int DIM>
+__device__ __forceinline__ double y_entry(int k, int j, const double* g, const double* dw) {
+  constexpr int NS = DIM == 3 ? 6 : 3;
+  auto pk = [](int r, int c) {
+    const int lo = r < c ? r : c, hi = r < c ? c : r;
+    return lo * NS - lo * (lo - 1) / 2 + (hi - lo);
+  };
+  if constexpr (DIM == 3) {
+    // j=0: (0,g0) (3,g1) (5,g2); j=1: (1,g1) (3,g0) (4,g2); j=2: (2,g2) (4,g1) (5,g0)
+    const int d1 = j == 2 ? 4 : 3, d2 = j == 0 ? 5 : (j == 1 ? 4 : 5);
+    const double gj = j == 0 ? g[0] : j == 1 ? g[1] : g[2];
+    const double ge1 = j == 0 ? g[1] : j == 1 ? g[0] : g[1];
+    const double ge2 = j == 0 ? g[2] : j == 1 ? g[2] : g[0];
+    double s = __dmul_rn(dw[pk(k, j)], gj);
+    s = __fma_rn(dw[pk(k, d1)], ge1, s);
+    return __fma_rn(dw[pk(k, d2)], ge2, s);
+  } else {
+    // j=0: (0,g0) (2,g1); j=1: (1,g1) (2,g0)
+    const double gj = j == 0 ? g[0] : g[1];
+    const double go = j == 0 ? g[1] : g[0];
+    return __fma_rn(dw[pk(k, 2)], go, __dmul_rn(dw[pk(k, j)], gj));
+  }
+}
+
+// Phase 2 of IL elements on the tensor pipe, interleaved so that IL * TPP
+// independent accumulator chains hide the DMMA latency: staged records
+// st_w + le * NQ * REC (plastic points in masks[le]) -> symmetric block
+// records recs[le] (shared memory).
+template <int DIM, int NP, int NQ, int IL>
+__device__ __forceinline__ void delta_mma_elements(const double* st_w, const unsigned* masks,
+                                                   double* const* recs, int lane) {
+  using M = MmaCfg<DIM, NP, NQ>;
+  constexpr int NT8 = M::NT8, NDOF = M::NDOF, NS = M::NS, REC = M::REC, D2 = M::D2;
+  const int g = lane >> 2, t = lane & 3;
+  unsigned any = 0;
+#pragma unroll
+  for (int l = 0; l < IL; ++l) any |= masks[l];
+#pragma unroll 1
+  for (int pass = 0; pass < M::NPASS; ++pass) {
+    double acc[IL][M::TPP][2];
+#pragma unroll
+    for (int l = 0; l < IL; ++l)
+#pragma unroll
+      for (int s = 0; s < M::TPP; ++s) acc[l][s][0] = acc[l][s][1] = 0.0;
+    unsigned mk = any;
+    while (mk) {
+      const int q = __ffs(mk) - 1;
+      mk &= mk - 1u;
+#pragma unroll
+      for (int l = 0; l < IL; ++l) {
+        if (!((masks[l] >> q) & 1u)) continue;  // warp-uniform
+        const double* st = st_w + (l * NQ + q) * REC;
+        const double* dw = st + NP * DIM;
+        double gv[NT8][DIM];
+#pragma unroll
+        for (int T = 0; T < NT8; ++T) {
+          const int dof = 8 * T + g;
+          const int node = dof < NDOF ? dof / DIM : 0;
+#pragma unroll
+          for (int c = 0; c < DIM; ++c) gv[T][c] = st[node * DIM + c];
+        }
+#pragma unroll
+        for (int ks = 0; ks < M::KS; ++ks) {
+          const int k = 4 * ks + t;
+          double av[NT8], yv[NT8];
+#pragma unroll
+          for (int T = 0; T < NT8; ++T) {
+            const int dof = 8 * T + g;
+            const bool ok = dof < NDOF && k < NS;
+            const int comp = dof % DIM;
+            av[T] = ok ? b_entry<DIM>(k, comp, gv[T]) : 0.0;
+            yv[T] = ok ? y_entry<DIM>(k, comp, gv[T], dw) : 0.0;
+          }
+#pragma unroll
+          for (int s = 0; s < M::TPP; ++s) {
+            const int sg = pass * M::TPP + s;
+            if (sg < M::NSYM) dmma884(acc[l][s][0], acc[l][s][1], av[M::tile_i(sg)], yv[M::tile_j(sg)]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < IL; ++l) {
+      if (!masks[l]) continue;
+      double* rec = recs[l];
+#pragma unroll
+      for (int s = 0; s < M::TPP; ++s) {
+        const int sg = pass * M::TPP + s;
+        if (sg >= M::NSYM) continue;
+        const int I = M::tile_i(sg), J = M::tile_j(sg);
+        const int row = 8 * I + g;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = 8 * J + 2 * t + e;
+          if (row >= NDOF || col >= NDOF) continue;
+          const int an = row / DIM, i = row % DIM, bn = col / DIM, jj = col % DIM;
+          if (an < bn) {
+            rec[blk_index<NP>(an, bn) * D2 + i * DIM + jj] = acc[l][s][e];
+          } else if (an == bn) {
+            rec[blk_index<NP>(an, an) * D2 + i * DIM + jj] = acc[l][s][e];
+            if (I < J) rec[blk_index<NP>(an, an) * D2 + jj * DIM + i] = acc[l][s][e];
+          }
+        }
+      }
+    }
+  }
+}
+
+// Phase 2 + workspace store for the EPW elements of a warp (after the staged
+// records and the ballot `bal` of plastic points are in place).  2D: all EPW
+// elements interleaved (EPW * RECB fits the output buffers); 3D: one at a
+// time through OUTB = 2 rotating buffers.
+template <int DIM, int NP, int NQ>
+__device__ __forceinline__ void delta_mma_warp(const double* st_w, double* out_w, unsigned bal, int64_t e0,
+                                               int64_t e_end, double* __restrict__ scratch, int lane) {
+  using M = MmaCfg<DIM, NP, NQ>;
+  constexpr unsigned QMASK = NQ >= 32 ? 0xffffffffu : (1u << NQ) - 1u;
+  if constexpr (M::RECB % 2 != 0) {
+    // records not 16-byte multiples (P2 tet: 495 doubles): no bulk copies,
+    // one element at a time through the first buffer, coalesced lane stores
+#pragma unroll 1
+    for (int le = 0; le < M::EPW; ++le) {
+      const unsigned mask = e0 + le < e_end ? (bal >> (le * NQ)) & QMASK : 0u;
+      if (!mask) continue;  // warp-uniform
+      double* rec = out_w;
+      delta_mma_elements<DIM, NP, NQ, 1>(st_w + le * NQ * M::REC, &mask, &rec, lane);
+      __syncwarp();
+      double* dst = scratch + (size_t)(e0 + le) * M::RECB;
+      for (int k = lane; k < M::RECB; k += 32) dst[k] = rec[k];
+      __syncwarp();
+    }
+  } else if constexpr (M::OUTB == M::EPW) {
+    unsigned masks[M::EPW];
+    double* recs[M::EPW];
+#pragma unroll
+    for (int le = 0; le < M::EPW; ++le) {
+      masks[le] = e0 + le < e_end ? (bal >> (le * NQ)) & QMASK : 0u;
+      recs[le] = out_w + le * M::RECB;
+    }
+    if (!bal) return;
+    delta_mma_elements<DIM, NP, NQ, M::EPW>(st_w, masks, recs, lane);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      for (int le = 0; le < M::EPW; ++le)
+        if (masks[le])
+          tma_store_1d(scratch + (size_t)(e0 + le) * M::RECB, recs[le], (unsigned)(M::RECB * sizeof(double)));
+      tma_store_wait_read();
+    }
+  } else {
+    int issued = 0;
+#pragma unroll 1
+    for (int le = 0; le < M::EPW; ++le) {
+      const unsigned mask = e0 + le < e_end ? (bal >> (le * NQ)) & QMASK : 0u;
+      if (!mask) continue;  // warp-uniform
+      double* rec = out_w + (issued % M::OUTB) * M::RECB;
+      if (issued >= M::OUTB) {  // the buffer's previous bulk store must have read it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(M::OUTB - 1) : "memory");
+        __syncwarp();
+      }
+      delta_mma_elements<DIM, NP, NQ, 1>(st_w + le * NQ * M::REC, &mask, &rec, lane);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_1d(scratch + (size_t)(e0 + le) * M::RECB, rec, (unsigned)(M::RECB * sizeof(double)));
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      ++issued;
+    }
+    if (issued && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
 }  // namespace epfem_gpu

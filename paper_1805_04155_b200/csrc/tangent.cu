@@ -71,6 +71,126 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS) k_elem_delta_s
   delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, a.e_end, a.scratch);
 }
 
+// k_delta_warp (2D): pass 1 from a finished constitutive update (flags +
+// packed D or reference DS), warp-owned elements like k_newton_warp: lane
+// (element, q) stages dphi and w (D - C) of its point when plastic, the
+// ballot gives the element masks, phase-2 lanes build uniform chunks and the
+// element records leave through TMA bulk stores.  Same FMA sequence as the
+// fused kernel, hence identical bits.
+template <int NP, int NQ, int MODE>
+__global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS) k_delta_warp(GatherArgs a) {
+  constexpr int DIM = 2;
+  using W = WarpCfg<DIM, NP, NQ>;
+  constexpr int EPW = W::EPW, REC = W::REC, NS = W::NS;
+  constexpr unsigned QMASK = NQ >= 32 ? 0xffffffffu : (1u << NQ) - 1u;
+  constexpr int RECB = W::NB * W::D2;
+  __shared__ double s_st[W::WPB][EPW * NQ * REC];
+  __shared__ __align__(16) double s_out[W::WPB][EPW * RECB];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t e0 = a.e_begin + ((int64_t)blockIdx.x * W::WPB + w) * EPW;
+  if (e0 >= a.e_end) return;  // warp-uniform
+  double* st_w = s_st[w];
+  bool plastic = false;
+  if (lane < EPW * NQ) {
+    const int le = lane / NQ, q = lane - le * NQ;
+    const int64_t e = e0 + le;
+    if (e < a.e_end) {
+      const int64_t m = e * NQ + q;
+      plastic = (__ldg(a.flags + m) & 1) != 0;
+      if (plastic) {
+        double* st = st_w + lane * REC;
+        double dv[NS][NS];
+#pragma unroll
+        for (int r = 0; r < NS; ++r)
+#pragma unroll
+          for (int c = r; c < NS; ++c) {
+            const int ri = arow<DIM>(r), ci = arow<DIM>(c);
+            dv[r][c] = MODE == G_TANGENT_PACKED ? __ldg(a.D + m * EPFEM_D_STRIDE + pk_index(ri, ci))
+                                                : __ldg(a.D + m * 36 + ci * 6 + ri);
+          }
+        stage_geometry<DIM, NP>(st, a.inv + m * W::D2, a.gradhat, q);
+        stage_dw<DIM>(st + NP * DIM, __ldg(a.weight + m), a, m, [&](int ri, int ci) {
+          const int r = ri == 3 ? 2 : ri, c = ci == 3 ? 2 : ci;
+          return dv[r][c];
+        });
+      }
+    }
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, plastic);
+  __syncwarp();
+  if (lane < EPW && e0 + lane < a.e_end) a.emask[e0 + lane] = (bal >> (lane * NQ)) & QMASK;
+  if (lane < EPW * W::NT) {
+    const int le = lane / W::NT;
+    const unsigned mask = (bal >> (le * NQ)) & QMASK;
+    if (e0 + le < a.e_end && mask) {
+      int pa, c0;
+      chunk_of<NP, W::CS>(lane - le * W::NT, pa, c0);
+      delta_chunk_uniform<DIM, NP, W::CS, REC>(st_w + le * NQ * REC, mask, pa, c0, s_out[w] + le * RECB);
+    }
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    int n = 0;
+    for (int le = 0; le < EPW; ++le)
+      if (e0 + le < a.e_end && ((bal >> (le * NQ)) & QMASK)) {
+        tma_store_1d(a.scratch + (size_t)(e0 + le) * RECB, s_out[w] + le * RECB,
+                     (unsigned)(RECB * sizeof(double)));
+        ++n;
+      }
+    if (n) tma_store_wait_read();
+  }
+}
+
+// k_delta_mma: the tensor-core phase 2 (delta_mma_warp) behind the same
+// pass-1 staging as k_delta_warp, EPW = 32 / NQ elements per warp.
+template <int DIM, int NP, int NQ, int MODE>
+__global__ void __launch_bounds__(MmaCfg<DIM, NP, NQ>::THREADS) k_delta_mma(GatherArgs a) {
+  using M = MmaCfg<DIM, NP, NQ>;
+  constexpr int EPW = M::EPW, REC = M::REC, NS = M::NS;
+  constexpr unsigned QMASK = NQ >= 32 ? 0xffffffffu : (1u << NQ) - 1u;
+  __shared__ double s_st[M::WPB][EPW * NQ * REC];
+  __shared__ __align__(16) double s_out[M::WPB][M::OUTB * M::RECB];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t e0 = a.e_begin + ((int64_t)blockIdx.x * M::WPB + w) * EPW;
+  if (e0 >= a.e_end) return;  // warp-uniform
+  double* st_w = s_st[w];
+  bool plastic = false;
+  if (lane < EPW * NQ) {
+    const int le = lane / NQ, q = lane - le * NQ;
+    const int64_t e = e0 + le;
+    if (e < a.e_end) {
+      const int64_t m = e * NQ + q;
+      plastic = (__ldg(a.flags + m) & 1) != 0;
+      if (plastic) {
+        double* st = st_w + lane * REC;
+        double dv[NS][NS];
+#pragma unroll
+        for (int r = 0; r < NS; ++r)
+#pragma unroll
+          for (int c = r; c < NS; ++c) {
+            const int ri = arow<DIM>(r), ci = arow<DIM>(c);
+            dv[r][c] = MODE == G_TANGENT_PACKED ? __ldg(a.D + m * EPFEM_D_STRIDE + pk_index(ri, ci))
+                                                : __ldg(a.D + m * 36 + ci * 6 + ri);
+          }
+        stage_geometry<DIM, NP>(st, a.inv + m * M::D2, a.gradhat, q);
+        stage_dw<DIM>(st + NP * DIM, __ldg(a.weight + m), a, m, [&](int ri, int ci) {
+          int r = ri, c = ci;
+          if constexpr (DIM == 2) {
+            r = ri == 3 ? 2 : ri;
+            c = ci == 3 ? 2 : ci;
+          }
+          return dv[r][c];
+        });
+      }
+    }
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, plastic);
+  __syncwarp();
+  if (lane < EPW && e0 + lane < a.e_end) a.emask[e0 + lane] = (bal >> (lane * NQ)) & QMASK;
+  delta_mma_warp<DIM, NP, NQ>(st_w, s_out[w], bal, e0, a.e_end, a.scratch, lane);
+}
+
 constexpr int kStreamThreads = 256;
 
 // The K_elast range [v0, v1) is read with ONE TMA bulk copy of the enclosing
@@ -306,6 +426,36 @@ int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStrea
     constexpr int DIM = decltype(D)::value;
     constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
     using Cfg = DeltaCfg<DIM, NP, NQ>;
+    // same kernel family as the fused step (constitutive.cu): the tensor-core
+    // phase 2 only with EPFEM_FUSED=mma
+    static const int mma = [] {
+      const char* v = getenv("EPFEM_FUSED");
+      return (v && v[0] == 'm') ? 2 : 0;
+    }();
+    if (mma == 2) {
+      if (a.n_elements > 0) {
+        using M = MmaCfg<DIM, NP, NQ>;
+        const int64_t per = (int64_t)M::EPW * M::WPB;
+        const unsigned blocks = (unsigned)((a.e_end - a.e_begin + per - 1) / per);
+        if (mode == G_TANGENT_PACKED)
+          k_delta_mma<DIM, NP, NQ, G_TANGENT_PACKED><<<blocks, M::THREADS, 0, st>>>(a);
+        else
+          k_delta_mma<DIM, NP, NQ, G_TANGENT_DS36><<<blocks, M::THREADS, 0, st>>>(a);
+      }
+      return;
+    }
+    if constexpr (DIM == 2) {
+      if (a.n_elements > 0) {
+        using W = WarpCfg<DIM, NP, NQ>;
+        const int64_t per = (int64_t)W::EPW * W::WPB;
+        const unsigned blocks = (unsigned)((a.e_end - a.e_begin + per - 1) / per);
+        if (mode == G_TANGENT_PACKED)
+          k_delta_warp<NP, NQ, G_TANGENT_PACKED><<<blocks, W::THREADS, 0, st>>>(a);
+        else
+          k_delta_warp<NP, NQ, G_TANGENT_DS36><<<blocks, W::THREADS, 0, st>>>(a);
+      }
+      return;
+    }
     if (a.n_elements > 0) {
       const int64_t blocks = (a.e_end - a.e_begin + Cfg::EPB - 1) / Cfg::EPB;
       if (mode == G_TANGENT_PACKED)

@@ -372,3 +372,18 @@ def test_full_size_pattern_and_properties(cuda, name):
     Kt = P.CsrMatrix(gc.row_ptr, gc.col_idx, Kv)
     lhs, rhs = float(y @ Kt.matvec(x)), float(x @ Kt.matvec(y))
     assert abs(lhs - rhs) <= 1e-9 * max(abs(lhs), 1.0)
+
+
+# ---------------------------------------------------------------------------
+# opt-in kernel variants (EPFEM_FUSED, read once per process): each in a
+# fresh interpreter, same bar as the default path
+@pytest.mark.parametrize("variant,name", [("mma", "cfg2"), ("mma", "cfg3"), ("mma", "cfg4"),
+                                          ("cta", "cfg2"), ("pipe", "cfg2"), ("pipe", "cfg4")])
+def test_kernel_variants(cuda, oracle, variant, name):
+    import subprocess
+    import sys
+    env = dict(os.environ, EPFEM_FUSED=variant)
+    n = {"cfg2": 24, "cfg3": 4, "cfg4": 6}[name]
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "variant_check.py"), name,
+                        str(n)], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
