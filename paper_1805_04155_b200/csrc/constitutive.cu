@@ -321,6 +321,7 @@ __global__ void __launch_bounds__(256) k_constitutive(ConstArgs a) {
 template <int MODEL, int DIM, int NP, int NQ>
 __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? 1024 / DeltaCfg<DIM, NP, NQ>::THREADS : 0)
     k_newton_fused(ConstArgs c, GatherArgs g) {
+  pdl_trigger();
   using Cfg = DeltaCfg<DIM, NP, NQ>;
   constexpr int EPB = Cfg::EPB;
   __shared__ double s_st[EPB][NQ][Cfg::REC];
@@ -370,6 +371,7 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? 102
 template <int MODEL, int NP, int NQ>
 __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
     k_newton_warp(ConstArgs c, GatherArgs g) {
+  pdl_trigger();
   constexpr int DIM = 2;
   using W = WarpCfg<DIM, NP, NQ>;
   static_assert(W::EPW * NQ <= 32 && W::EPW * W::NT <= 32, "warp mapping");
@@ -467,6 +469,7 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
 template <int MODEL, int DIM, int NP, int NQ>
 __global__ void __launch_bounds__(MmaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? EPFEM_MMA_MINB : 0)
     k_newton_mma(ConstArgs c, GatherArgs g) {
+  pdl_trigger();
   using M = MmaCfg<DIM, NP, NQ>;
   constexpr int EPW = M::EPW, REC = M::REC;
   constexpr unsigned QMASK = NQ >= 32 ? 0xffffffffu : (1u << NQ) - 1u;
@@ -525,6 +528,7 @@ struct PipeTile {
 template <int MODEL, int DIM, int NP, int NQ>
 __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS)
     k_newton_pipe(ConstArgs c, GatherArgs g, int64_t n_groups) {
+  pdl_trigger();
   using Cfg = DeltaCfg<DIM, NP, NQ>;
   using Tile = PipeTile<DIM, NP, NQ>;
   constexpr int EPB = Cfg::EPB, PPG = Tile::PPG, D2 = Tile::D2;

@@ -28,6 +28,7 @@ namespace {
 
 template <int DIM, int NP, int NQ, int MODE>
 __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS) k_elem_delta_staged(GatherArgs a) {
+  pdl_trigger();
   using Cfg = DeltaCfg<DIM, NP, NQ>;
   constexpr int EPB = Cfg::EPB;
   constexpr int NS = Cfg::NS, REC = Cfg::REC;
@@ -79,6 +80,7 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS) k_elem_delta_s
 // fused kernel, hence identical bits.
 template <int NP, int NQ, int MODE>
 __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS) k_delta_warp(GatherArgs a) {
+  pdl_trigger();
   constexpr int DIM = 2;
   using W = WarpCfg<DIM, NP, NQ>;
   constexpr int EPW = W::EPW, REC = W::REC, NS = W::NS;
@@ -146,6 +148,7 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS) k_delta_warp(Gath
 // pass-1 staging as k_delta_warp, EPW = 32 / NQ elements per warp.
 template <int DIM, int NP, int NQ, int MODE>
 __global__ void __launch_bounds__(MmaCfg<DIM, NP, NQ>::THREADS) k_delta_mma(GatherArgs a) {
+  pdl_trigger();
   using M = MmaCfg<DIM, NP, NQ>;
   constexpr int EPW = M::EPW, REC = M::REC, NS = M::NS;
   constexpr unsigned QMASK = NQ >= 32 ? 0xffffffffu : (1u << NQ) - 1u;
@@ -228,14 +231,17 @@ __global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int
     mbar_expect_tx(&s_bar, bytes);
     tma_load_1d(img_raw, a.base + a0, bytes, &s_bar);
   }
-  // stage the range's items (plastic ones kept, others -1) and node offsets
-  for (int k = tid; k < nitems; k += blockDim.x) {
-    const int32_t it = __ldg(a.n2e + i_begin + k);
-    s_item[k] = __ldg(a.emask + it / NP) ? it : -1;
-  }
+  // node offsets (cache data, independent of the producer kernel)
   for (int k = tid; k <= nloc; k += blockDim.x) {
     s_iptr[k] = (int)(__ldg(a.n2e_ptr + n0 + k) - i_begin);
     s_vptr[k] = (int)(__ldg(a.nbr_ptr + n0 + k) * D2 - v0);
+  }
+  // everything below reads the producer's emask / workspace
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // stage the range's items (plastic ones kept, others -1)
+  for (int k = tid; k < nitems; k += blockDim.x) {
+    const int32_t it = __ldg(a.n2e + i_begin + k);
+    s_item[k] = __ldcg(a.emask + it / NP) ? it : -1;
   }
   __syncthreads();
   if (a1 > a0) mbar_wait(&s_bar, 0);
@@ -412,7 +418,23 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) { rc = cuda_fail(e, "cudaFuncSetAttribute"); return; }
     }
-    kern<<<(unsigned)rblocks, kStreamThreads, smem, st>>>(a, a.npc);
+    // Programmatic dependent launch: the CTAs may start while the producer
+    // of the workspace (fused / delta kernel) drains; they load K_elast and
+    // the item lists, then block in griddepcontrol.wait until the producer
+    // grid has completed and flushed (a no-op after a normal launch).
+    static const bool pdl = getenv("EPFEM_NO_PDL") == nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)rblocks);
+    cfg.blockDim = dim3(kStreamThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, a.npc);
+    if (e != cudaSuccess) rc = cuda_fail(e, "row stream launch");
   });
   if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
   if (rc) return rc;

@@ -58,6 +58,9 @@ __device__ __forceinline__ void tma_store_wait_read() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+// programmatic dependent launch: let the next kernel on the stream (launched
+// with programmatic stream serialization) start its independent prologue
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 // per-thread asynchronous global -> shared copies (LDGSTS), one commit group
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
