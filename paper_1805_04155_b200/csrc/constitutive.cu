@@ -461,6 +461,183 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
   }
 }
 
+// k_newton_ws (2D): the warp kernel split by role inside a persistent CTA.
+// P producer warps run phase 1 (one group of EPW elements at a time, like
+// k_newton_warp) into a private double-buffered slot of staged records and
+// hand it over through an mbarrier; CW consumer warps run phase 2 from the
+// slots and bulk-store the element records.  The producers never wait on
+// phase-2 arithmetic, so their loads keep streaming while the consumers'
+// FP64 work proceeds on the other warps.
+#ifndef EPFEM_WS_P
+#define EPFEM_WS_P 6
+#endif
+#ifndef EPFEM_WS_C
+#define EPFEM_WS_C 2
+#endif
+#ifndef EPFEM_WS_MINB
+#define EPFEM_WS_MINB 3
+#endif
+#ifndef EPFEM_WS_SUB
+#define EPFEM_WS_SUB 3
+#endif
+template <int NP, int NQ>
+struct WsCfg {
+  using W = WarpCfg<2, NP, NQ>;
+  static constexpr int P = EPFEM_WS_P, CW = EPFEM_WS_C, THREADS = 32 * (P + CW);
+  static constexpr int SLOT = W::EPW * NQ * W::REC;  // doubles per staged slot
+  static constexpr int RECB = W::NB * W::D2;
+  static constexpr size_t SMEM = sizeof(double) * ((size_t)P * 2 * SLOT + (size_t)CW * W::EPW * RECB);
+};
+template <int MODEL, int NP, int NQ>
+__global__ void __launch_bounds__(WsCfg<NP, NQ>::THREADS, EPFEM_WS_MINB)
+    k_newton_ws(ConstArgs c, GatherArgs g) {
+  pdl_trigger();
+  constexpr int DIM = 2;
+  using W = WarpCfg<DIM, NP, NQ>;
+  using S = WsCfg<NP, NQ>;
+  constexpr int P = S::P, CW = S::CW, EPW = W::EPW, REC = W::REC, SLOT = S::SLOT, RECB = S::RECB;
+  constexpr unsigned QMASK = NQ >= 32 ? 0xffffffffu : (1u << NQ) - 1u;
+  extern __shared__ __align__(128) double ws_smem[];
+  double* slots = ws_smem;                 // [P][2][SLOT]
+  double* outb = ws_smem + P * 2 * SLOT;   // [CW][EPW * RECB]
+  __shared__ uint64_t full[P][2], empty[P][2];
+  __shared__ unsigned s_bal[P][2];
+  __shared__ long long s_e0[P][2];
+  c.DS = nullptr;  // hot path: S, flags, packed D only
+  c.Ep_out = c.Hard_out = nullptr;
+  c.pm = c.sm = c.am = nullptr;
+  c.crit = nullptr;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int p = 0; p < P; ++p)
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&full[p][b], 1);
+        mbar_init(&empty[p][b], 1);
+      }
+    mbar_init_fence();
+  }
+  __syncthreads();
+  const int64_t n_groups = (g.e_end - g.e_begin + EPW - 1) / EPW;
+  if (w < P) {
+    // ---- producer: phase 1
+    const int64_t stride = (int64_t)gridDim.x * P;
+    int it = 0;
+    for (int64_t grp = (int64_t)blockIdx.x * P + w;; grp += stride, ++it) {
+      const int b = it & 1;
+      if (it >= 2) mbar_wait(&empty[w][b], ((it >> 1) & 1) ^ 1);
+      if (grp >= n_groups) {
+        if (lane == 0) {
+          s_e0[w][b] = -1;
+          mbar_arrive(&full[w][b]);
+        }
+        break;
+      }
+      double* st_w = slots + (w * 2 + b) * SLOT;
+      const int64_t e0 = g.e_begin + grp * EPW;
+      bool plastic = false;
+      if (lane < EPW * NQ) {
+        const int le = lane / NQ, q = lane - le * NQ;
+        const int64_t e = e0 + le;
+        if (e < g.e_end) {
+          const int64_t m = e * NQ + q;
+          double* st = st_w + lane * REC;
+          auto stage = [&](auto&& f) {
+            stage_geometry<DIM, NP>(st, g.inv + m * W::D2, g.gradhat, q);
+            stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f);
+          };
+          plastic = eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
+        }
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, plastic);
+      if (lane < EPW && e0 + lane < g.e_end) g.emask[e0 + lane] = (bal >> (lane * NQ)) & QMASK;
+      if (lane == 0) {
+        s_bal[w][b] = bal;
+        s_e0[w][b] = e0;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[w][b]);
+    }
+  } else {
+    // ---- consumer: phase 2 for producers cw, cw + CW, ...
+    const int cw = w - P;
+    double* out_w = outb + cw * EPW * RECB;
+    constexpr int NMY = (P + CW - 1) / CW;
+    int its[NMY];
+    unsigned done = 0;
+    const int nmy = (P - cw + CW - 1) / CW;
+#pragma unroll
+    for (int k = 0; k < NMY; ++k) its[k] = 0;
+    bool pending = false;  // bulk stores in flight from out_w
+    while (done != (1u << nmy) - 1u) {
+#pragma unroll
+      for (int k = 0; k < NMY; ++k) {
+        if (k >= nmy || ((done >> k) & 1u)) continue;
+        const int p = cw + k * CW, b = its[k] & 1;
+        mbar_wait(&full[p][b], (its[k] >> 1) & 1);
+        const long long e0 = s_e0[p][b];
+        if (e0 < 0) {
+          done |= 1u << k;
+          continue;
+        }
+        const unsigned bal = s_bal[p][b];
+        if (pending) {  // out_w must have been read by the previous bulk stores
+          if (lane == 0) tma_store_wait_read_only();
+          __syncwarp();
+          pending = false;
+        }
+        const double* st_w = slots + (p * 2 + b) * SLOT;
+        if (lane < EPW * W::NT) {
+          const int le = lane / W::NT;
+          const unsigned mask = (bal >> (le * NQ)) & QMASK;
+          if (e0 + le < g.e_end && mask) {
+            int a, c0;
+            chunk_of<NP, W::CS>(lane - le * W::NT, a, c0);
+            delta_chunk_uniform<DIM, NP, W::CS, REC, EPFEM_WS_SUB>(st_w + le * NQ * REC, mask, a, c0,
+                                                                     out_w + le * RECB);
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&empty[p][b]);  // staged records consumed
+          for (int le = 0; le < EPW; ++le)
+            if (e0 + le < g.e_end && ((bal >> (le * NQ)) & QMASK)) {
+              tma_store_1d(g.scratch + (size_t)(e0 + le) * RECB, out_w + le * RECB,
+                           (unsigned)(RECB * sizeof(double)));
+              pending = true;
+            }
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        pending = __shfl_sync(0xffffffffu, pending, 0);
+        ++its[k];
+      }
+    }
+    if (lane == 0) tma_store_wait_read_only();
+  }
+}
+
+template <int MODEL, int NP, int NQ>
+static int launch_ws(const ConstArgs& c, const GatherArgs& g, cudaStream_t st) {
+  using S = WsCfg<NP, NQ>;
+  auto kern = k_newton_ws<MODEL, NP, NQ>;
+  static int per_sm = -1, num_sms = 0;
+  if (per_sm < 0) {
+    EPFEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
+    EPFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, S::THREADS, S::SMEM));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (per_sm < 1) per_sm = 1;
+  }
+  using W = WarpCfg<2, NP, NQ>;
+  const int64_t n_groups = (g.e_end - g.e_begin + W::EPW - 1) / W::EPW;
+  const int64_t need = (n_groups + S::P - 1) / S::P;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)per_sm * num_sms));
+  kern<<<(unsigned)grid, S::THREADS, S::SMEM, st>>>(c, g);
+  EPFEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 // k_newton_mma: k_newton_warp's phase 1 (EPW = 32 / NQ elements per warp)
 // followed by the tensor-core phase 2 (delta_mma_warp, delta.cuh).
 #ifndef EPFEM_MMA_MINB
@@ -679,6 +856,11 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
     const char* v = getenv("EPFEM_FUSED");
     return (v && v[0] == 'm') ? 2 : 0;
   }();
+  // warp-specialized producer / consumer kernel (2D): EPFEM_FUSED=ws
+  static const bool ws = [] {
+    const char* v = getenv("EPFEM_FUSED");
+    return v && v[0] == 'w' && v[1] == 's';
+  }();
   int rc = 0;
   bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
     constexpr int DIM = decltype(D)::value;
@@ -712,6 +894,14 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
       return;
     }
     if constexpr (DIM == 2) {
+      if (ws) {
+        switch (model) {
+          case EPFEM_MODEL_VON_MISES: rc = launch_ws<EPFEM_MODEL_VON_MISES, NP, NQ>(c, g, st); break;
+          case EPFEM_MODEL_DRUCKER_PRAGER: rc = launch_ws<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ>(c, g, st); break;
+          default: rc = launch_ws<EPFEM_MODEL_ELASTIC, NP, NQ>(c, g, st); break;
+        }
+        return;
+      }
       if (!cta) {
         using W = WarpCfg<DIM, NP, NQ>;
         const int64_t per = (int64_t)W::EPW * W::WPB;

@@ -246,10 +246,10 @@ template <int DIM, int NP, int CS, int REC>
 __device__ __forceinline__ void delta_chunk_uniform1(const double* st_e, unsigned mask, int a, int c0,
                                                      double* __restrict__ rec);
 // CS blocks in passes of SUB (fewer live accumulators; T_a is recomputed per pass)
-template <int DIM, int NP, int CS, int REC>
+template <int DIM, int NP, int CS, int REC, int SUB_ = EPFEM_SUBCHUNK>
 __device__ __forceinline__ void delta_chunk_uniform(const double* st_e, unsigned mask, int a, int c0,
                                                     double* __restrict__ rec) {
-  constexpr int SUB = EPFEM_SUBCHUNK > 0 && EPFEM_SUBCHUNK < CS ? EPFEM_SUBCHUNK : CS;
+  constexpr int SUB = SUB_ > 0 && SUB_ < CS ? SUB_ : CS;
 #pragma unroll 1
   for (int s0 = 0; s0 < CS; s0 += SUB)
     if (c0 + s0 < NP) delta_chunk_uniform1<DIM, NP, SUB, REC>(st_e, mask, a, c0 + s0, rec);

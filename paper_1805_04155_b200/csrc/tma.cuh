@@ -20,6 +20,11 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
                "r"(bytes)
                : "memory");
 }
+// plain arrive (release at CTA scope: prior shared-memory writes are visible
+// to the thread that observes the phase completion)
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // wait for the completion of the mbarrier phase with the given parity
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
@@ -61,6 +66,10 @@ __device__ __forceinline__ void tma_store_wait_read() {
 // programmatic dependent launch: let the next kernel on the stream (launched
 // with programmatic stream serialization) start its independent prologue
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// wait until the thread's committed bulk stores have read their sources
+__device__ __forceinline__ void tma_store_wait_read_only() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 // per-thread asynchronous global -> shared copies (LDGSTS), one commit group
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
