@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(256) k_constitutive(ConstArgs a) {
 // leaves ptxas its own heuristic (126 registers; an explicit 1 gives 144 and
 // is ~15% slower on cfg4).
 template <int MODEL, int DIM, int NP, int NQ>
-__global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? 1024 / DeltaCfg<DIM, NP, NQ>::THREADS : 0)
+__global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DeltaCfg<DIM, NP, NQ>::MINB)
     k_newton_fused(ConstArgs c, GatherArgs g) {
   pdl_trigger();
   using Cfg = DeltaCfg<DIM, NP, NQ>;
@@ -350,7 +350,18 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? 102
   }
   __syncthreads();
   if (tid < EPB && e0 + tid < g.e_end) g.emask[e0 + tid] = s_mask[tid];
-  delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, g.e_end, g.scratch);
+  // phase 2: uniform chunks (no divergent block branch) in sub-passes of SUB
+  if (tid < EPB * Cfg::NT) {
+    const int le = tid / Cfg::NT;
+    const int64_t e = e0 + le;
+    const unsigned mask = s_mask[le];
+    if (e < g.e_end && mask) {
+      int a, c0;
+      chunk_of<NP, Cfg::CS>(tid - le * Cfg::NT, a, c0);
+      delta_chunk_uniform<DIM, NP, Cfg::CS, Cfg::REC, Cfg::SUB>(&s_st[le][0][0], mask, a, c0,
+                                                                g.scratch + (size_t)e * Cfg::NB * Cfg::D2);
+    }
+  }
 }
 
 // k_newton_warp (2D): the fused kernel with warp-owned elements (WarpCfg,
