@@ -224,6 +224,16 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def measured_traffic(config, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu capture (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
+            return json.load(f).get(config, {}).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
 def run_slabs(args, rank, world, dev, cfg):
     """N GPUs: one z-slab (y-slab in 2D) of the configuration's mesh per rank,
     interface-layer exchange over NCCL each step (paper_1805_04155_b200/dist.py).
@@ -278,6 +288,45 @@ def run_slabs(args, rank, world, dev, cfg):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t) / args.steps
     n_total = float(n_own)
+
+    # e2e: every step uploads this rank's E / Ep / Hard from pinned host memory
+    # and downloads its S, flag bytes and owned K rows (max over ranks)
+    e2e = None
+    if not args.no_e2e:
+        host_in = [x for x in (E, Ep0, Hard0) if x is not None]
+        h_in = [torch.empty_like(x, device="cpu").pin_memory() for x in host_in]
+        for h, x in zip(h_in, host_in):
+            h.copy_(x)
+        d_in = [torch.empty_like(x) for x in host_in]
+        S_, f_, K_ = eng.step(E, Ep0, Hard0)
+        h_out = [torch.empty_like(y, device="cpu").pin_memory() for y in (S_, f_, K_)]
+        bi = sum(x.numel() * x.element_size() for x in host_in)
+        bo = sum(y.numel() * y.element_size() for y in h_out)
+
+        def e2e_step():
+            for d, h in zip(d_in, h_in):
+                d.copy_(h, non_blocking=True)
+            outs = eng.step(*(d_in + [None] * (3 - len(d_in))))
+            for h, y in zip(h_out, outs):
+                h.copy_(y, non_blocking=True)
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        k2 = max(3, min(args.steps, 10))
+        ev0.record(stream)
+        for _ in range(k2):
+            e2e_step()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        t2 = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        tb = torch.tensor([bi, bo], dtype=torch.float64, device=dev)
+        dist.all_reduce(tb)
+        ms2 = float(t2) / k2
+        e2e = {"value": n_total / (ms2 * 1e-3), "unit": "ip/s", "h2d_bytes_per_step": int(tb[0]),
+               "d2h_bytes_per_step": int(tb[1]), "ms_per_step": ms2,
+               "how": "per rank: H2D of own E/Ep/Hard, step, D2H of own S/flags/K rows; all ranks summed"}
     npl = torch.tensor([float((eng.flags[p0:p1] & 1).sum())], dtype=torch.float64, device=dev)
     dist.all_reduce(npl)
     if rank == 0:
@@ -293,6 +342,7 @@ def run_slabs(args, rank, world, dev, cfg):
                        "l2": "inputs larger than L2"},
             "gpu_launches": 3 * args.steps,
             "clocks": clk.summary(),
+            "e2e": e2e,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -325,7 +375,10 @@ def main():
     import torch.distributed as dist
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # EPFEM_BENCH_SLABS=1: run the slab (multi-GPU) data path even at world
+    # size 1 (one-GPU check of the N>1 code under torchrun)
+    slabs = world > 1 or os.environ.get("EPFEM_BENCH_SLABS") == "1"
+    if slabs:
         dist.init_process_group("nccl", device_id=dev)
 
     from paper_1805_04155_b200 import build as B
@@ -333,7 +386,7 @@ def main():
     import paper_1805_04155_b200 as P
     from paper_1805_04155_b200.synthetic import CONFIGS, make_workload
     cfg = CONFIGS[args.config]
-    if world > 1 and cfg.model != "elastic":
+    if slabs and cfg.model != "elastic":
         return run_slabs(args, rank, world, dev, cfg)
     wl = make_workload(cfg, target=args.target, device=dev)
     cache, mat = wl.cache, wl.mat
@@ -541,7 +594,9 @@ def main():
                        "parallelism": f"replica x{world}" if world > 1 else "single GPU"},
             "gpu_launches": launches_per_step * args.steps,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+                         "unit": "GB/s", "frac": achieved / hbm_peak,
+                         "traffic": measured_traffic(args.config, dom),
+                         "traffic_source": "profiles/traffic.json (ncu --set full, bytes per launch)",
                          "algorithmic_bytes": dom_bytes, "kernel_ms": dom_ms,
                          "peak_source": peak_src},
             "roofline_step": {"algorithmic_bytes": step_bytes, "achieved": step_gbs,

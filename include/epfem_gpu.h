@@ -203,6 +203,23 @@ int epfem_constitutive_delta(epfem_ctx* ctx, const epfem_cache* cache, const epf
                              const epfem_constitutive_out* out);
 int epfem_assemble_rows(epfem_ctx* ctx, const epfem_cache* cache, double* K_values);
 
+/* Element-range forms for a mesh partition (multi-GPU slabs, dist.py): the
+ * reference has no partitioned entry point; these split
+ * epfem_constitutive_delta so a rank can update its own elements, receive
+ * its halo's flags + packed D from the neighbour, and build the halo's
+ * element deltas before epfem_assemble_rows.
+ * epfem_newton_range: (1) for elements [e_begin, e_end) only.  Every
+ *   per-point array (E, Ep_prev, Hard_prev, the material's per-point arrays,
+ *   out->S / flags / D) holds exactly the range's points, starting at point
+ *   e_begin * n_q; mat->n_int == (e_end - e_begin) * n_q.
+ * epfem_delta_range: element deltas of [e_begin, e_end) from a finished
+ *   update (flags + packed D over all n_int points of the cache). */
+int epfem_newton_range(epfem_ctx* ctx, const epfem_cache* cache, const epfem_material* mat,
+                       const double* E, const double* Ep_prev, const double* Hard_prev,
+                       const epfem_constitutive_out* out, int64_t e_begin, int64_t e_end);
+int epfem_delta_range(epfem_ctx* ctx, const epfem_cache* cache, int64_t n_int, const double* D,
+                      const uint8_t* flags, int64_t e_begin, int64_t e_end);
+
 /* K8: E = B u, 2D embedded in Voigt rows {0,1,3} (assembly.cpp:211-222). */
 int epfem_strains(epfem_ctx* ctx, const epfem_cache* cache, const double* u, double* E);
 /* K9: F = B^T (weight * S) (assembly.cpp:291-301). */

@@ -53,8 +53,8 @@ EXPORTS = [
     "epfem_dp_parameters", "epfem_constitutive", "epfem_cache_build", "epfem_cache_destroy",
     "epfem_cache_get_info", "epfem_cache_pattern", "epfem_cache_K_elast", "epfem_cache_geometry",
     "epfem_assemble_elastic", "epfem_assemble_tangent", "epfem_assemble_tangent_ds",
-    "epfem_newton_step", "epfem_constitutive_delta", "epfem_assemble_rows", "epfem_strains",
-    "epfem_internal_forces",
+    "epfem_newton_step", "epfem_constitutive_delta", "epfem_assemble_rows", "epfem_newton_range",
+    "epfem_delta_range", "epfem_strains", "epfem_internal_forces",
 ]
 
 _lib = None
@@ -95,6 +95,9 @@ def lib() -> C.CDLL:
     L.epfem_constitutive_delta.argtypes = [_P, _P, C.POINTER(Material), _P, _P, _P,
                                            C.POINTER(ConstitutiveOut)]
     L.epfem_assemble_rows.argtypes = [_P, _P, _P]
+    L.epfem_newton_range.argtypes = [_P, _P, C.POINTER(Material), _P, _P, _P,
+                                     C.POINTER(ConstitutiveOut), C.c_int64, C.c_int64]
+    L.epfem_delta_range.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_int64, C.c_int64]
     L.epfem_strains.argtypes = [_P, _P, _P, _P]
     L.epfem_internal_forces.argtypes = [_P, _P, _P, _P]
     _lib = L

@@ -96,6 +96,13 @@ bool aligned16(const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0
 
 }  // namespace
 
+// per-point pointer re-based so that the kernels' global point index m
+// addresses element e_begin's first point at offset 0 (epfem_newton_range)
+template <class T>
+static T* rebase(T* p, int64_t per_point, int64_t first_point) {
+  return p ? p - per_point * first_point : p;
+}
+
 extern "C" {
 
 const char* epfem_last_error(void) { return g_msg.c_str(); }
@@ -577,6 +584,65 @@ int epfem_constitutive_delta(epfem_ctx* ctx, const epfem_cache* c, const epfem_m
 
 int epfem_assemble_rows(epfem_ctx* ctx, const epfem_cache* c, double* K_values) {
   if (int rc = rows_part(ctx, c, K_values)) return rc;
+  return finish(ctx);
+}
+
+// per-point pointer re-based so that the kernels' global point index m
+// addresses element e_begin's first point at offset 0 (the arrays hold only
+// the range; the kernels never form m below the range)
+
+int epfem_newton_range(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
+                       const double* E, const double* Ep_prev, const double* Hard_prev,
+                       const epfem_constitutive_out* out, int64_t e_begin, int64_t e_end) {
+  if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
+  if (e_begin < 0 || e_end < e_begin || e_end > c->info.n_elements)
+    return fail(EPFEM_ERR_INVALID, "newton_range: element range out of bounds");
+  const int64_t nq = c->info.n_q, p0 = e_begin * nq;
+  if (!mat || mat->n_int != (e_end - e_begin) * nq)
+    return fail(EPFEM_ERR_INVALID, "newton_range: size mismatch");
+  ConstArgs a;
+  if (int rc = const_args(ctx, mat, E, Ep_prev, Hard_prev, out, &a)) return rc;
+  if (mat->n_int > 0 && (!out->S || !out->flags || !out->D))
+    return fail(EPFEM_ERR_INVALID, "newton_step: S, flags and D outputs are required");
+  if (out->DS || out->Ep || out->Hard || out->plastic_mask || out->smooth_mask || out->apex_mask ||
+      out->crit)
+    return fail(EPFEM_ERR_INVALID, "newton_step: only S, flags and D are produced");
+  if (e_end == e_begin) return finish(ctx);
+  a.n = e_end * nq;
+  a.E = rebase(a.E, 6, p0);
+  a.Ep = rebase(a.Ep, 6, p0);
+  a.Hard = rebase(a.Hard, 6, p0);
+  a.G = rebase(a.G, 1, p0);
+  a.K = rebase(a.K, 1, p0);
+  a.p1 = rebase(a.p1, 1, p0);
+  a.p2 = rebase(a.p2, 1, p0);
+  a.S = rebase(a.S, 6, p0);
+  a.flags = rebase(a.flags, 1, p0);
+  a.D = rebase(a.D, EPFEM_D_STRIDE, p0);
+  GatherArgs g = gather_args(c);
+  g.e_begin = e_begin;
+  g.e_end = e_end;
+  if (int rc = launch_newton_fused(mat->model, c->info.family, c->info.dim, a, g, ctx->stream)) return rc;
+  return finish(ctx);
+}
+
+int epfem_delta_range(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int, const double* D,
+                      const uint8_t* flags, int64_t e_begin, int64_t e_end) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
+  if (n_int != c->info.n_int) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: size mismatch");
+  if (e_begin < 0 || e_end < e_begin || e_end > c->info.n_elements)
+    return fail(EPFEM_ERR_INVALID, "delta_range: element range out of bounds");
+  if (e_end > e_begin && (!D || !flags))
+    return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null argument");
+  if (!aligned16(D)) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: D must be 16-byte aligned");
+  if (e_end == e_begin) return finish(ctx);
+  GatherArgs g = gather_args(c);
+  g.D = D;
+  g.flags = flags;
+  g.e_begin = e_begin;
+  g.e_end = e_end;
+  if (int rc = launch_delta(c->info.family, c->info.dim, G_TANGENT_PACKED, g, ctx->stream)) return rc;
   return finish(ctx);
 }
 

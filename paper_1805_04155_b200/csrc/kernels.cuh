@@ -81,6 +81,7 @@ int build_pattern(int family, int dim, int64_t n_nodes, int64_t n_e, const int32
 int launch_gather(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);
 int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);
 int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st);
+int launch_delta(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);  // pass 1 over [e_begin, e_end)
 int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
                         cudaStream_t st);
 size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements);

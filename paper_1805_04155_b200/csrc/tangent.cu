@@ -442,8 +442,7 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
   return 0;
 }
 
-int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st) {
-  if (a.n_nodes == 0) return 0;
+int launch_delta(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st) {
   bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
     constexpr int DIM = decltype(D)::value;
     constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
@@ -488,6 +487,12 @@ int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStrea
   });
   if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
   EPFEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st) {
+  if (a.n_nodes == 0) return 0;
+  if (int rc = launch_delta(family, dim, mode, a, st)) return rc;
   return launch_row_stream(family, dim, a, st);
 }
 

@@ -13,13 +13,17 @@ layers + one halo layer below (r > 0).  With the extended mesh every owned
 row has its full global column set, locally.
 
 Per Newton iteration:
-  1. constitutive update on the rank's own integration points (K1);
+  1. constitutive update + element deltas on the rank's own elements (K1 +
+     pass 1, fused);
   2. interface exchange: rank r sends the flag bytes + packed tangents of
      its TOP cell layer to rank r+1, which receives them as the plastic data
      of its halo layer (one grouped send/recv between neighbours: NCCL over
      NVLink on GPUs, gloo in the CPU tests);
-  3. tangent assembly on the extended slab (pass 1 + row stream); the owned
-     rows are complete and written exactly once.
+  3. element deltas of the halo layer from the received data, then the row
+     stream over the extended slab; the owned rows are complete and written
+     exactly once.
+Step 1 is the fused kernel of the single-GPU step restricted to the rank's
+own elements (epfem_newton_range), so a 1-rank run is bitwise the fused step.
 The exchange carries the producer-side data of the interface layer rather
 than partial K rows, so every rank assembles its rows with the single-GPU
 kernels and no remap/add kernel is needed; its volume, n_layer_points x
@@ -175,6 +179,16 @@ class DistributedTangent:
         self.own_values = (int(rp[r0]), int(rp[r1]))
 
     def step(self, E_own, Ep_own=None, Hard_own=None):
+        """One Newton iteration of this rank: fused constitutive update +
+        element deltas on its own elements (epfem_newton_range), interface
+        exchange, deltas of the halo elements from the received flags + D
+        (epfem_delta_range), then the row stream over the extended slab.
+        Returns this rank's S, flag bytes and owned K values."""
+        self.update_own(E_own, Ep_own, Hard_own)
+        exchange_interface(self.plan, self.flags, self.D, self.group)
+        return self.assemble()
+
+    def update_own(self, E_own, Ep_own=None, Hard_own=None):
         import ctypes as C
 
         from . import api
@@ -184,11 +198,19 @@ class DistributedTangent:
                                    api._ptr(self.D[p0:p1]))
         mv = self.mat_own.view()
         self.ctx.use_current_stream()
-        api._check(api.L.lib().epfem_constitutive(self.ctx.handle, C.byref(mv), api._ptr(E_own),
-                                                  api._ptr(Ep_own), api._ptr(Hard_own), C.byref(out)))
-        exchange_interface(self.plan, self.flags, self.D, self.group)
-        api._check(api.L.lib().epfem_assemble_tangent(self.ctx.handle, self.cache.handle,
-                                                      self.cache.n_int, api._ptr(self.D),
-                                                      api._ptr(self.flags), api._ptr(self.K)))
+        api._check(api.L.lib().epfem_newton_range(
+            self.ctx.handle, self.cache.handle, C.byref(mv), api._ptr(E_own), api._ptr(Ep_own),
+            api._ptr(Hard_own), C.byref(out), self.plan.halo_elems, self.plan.mesh.n_elements))
+
+    def assemble(self):
+        from . import api
+        lib = api.L.lib()
+        self.ctx.use_current_stream()
+        h_e = self.plan.halo_elems
+        if h_e:
+            api._check(lib.epfem_delta_range(self.ctx.handle, self.cache.handle, self.cache.n_int,
+                                             api._ptr(self.D), api._ptr(self.flags), 0, h_e))
+        api._check(lib.epfem_assemble_rows(self.ctx.handle, self.cache.handle, api._ptr(self.K)))
+        p0, p1 = self.plan.own_points
         v0, v1 = self.own_values
         return self.S[p0:p1], self.flags[p0:p1], self.K[v0:v1]

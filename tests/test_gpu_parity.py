@@ -329,6 +329,52 @@ def test_slab_data_path_on_one_rank(cuda, name):
     assert np.array_equal(_np(K).view(np.uint64), _np(K2).view(np.uint64))
 
 
+@pytest.mark.parametrize("name,world", [("cfg2", 2), ("cfg2", 3), ("cfg4", 2), ("cfg3", 3), ("cfg5", 2)])
+def test_slab_ranks_emulated_in_one_process(cuda, name, world):
+    """The N-rank data path (dist.py) with the NCCL exchange replaced by the
+    equivalent device copy, all ranks in one process one after another (no
+    rank waits on another): the owned K rows of all ranks, concatenated, are
+    bitwise the single-GPU fused step's K, and flags / S match per point."""
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.dist import DistributedTangent, make_plan
+    from paper_1805_04155_b200.synthetic import CONFIGS, calibrate, displacement
+    cfg = CONFIGS[name]
+    n = {"cfg2": 24, "cfg4": 6, "cfg3": 6, "cfg5": 4}[name]
+    mesh = cfg.mesh(n)
+    mat = cfg.material(mesh.n_int)
+    gc = P.build_assembly_cache(P.Mesh.from_structured(mesh, cuda), mat)
+    E1 = gc.strains(torch.from_numpy(displacement(mesh.coord, cfg.seed)).to(cuda))
+    s, frac = calibrate(E1, mat, 0.35)
+    E = (s * E1).contiguous()
+    eng = P.TangentEngine(gc, mat)
+    Sg, fg, Dg, Kg = eng.step(E)
+    eng.sync()
+    plans = [make_plan(cfg.family, cfg.dim, n, world, r) for r in range(world)]
+    dts = [DistributedTangent(p, cfg.material, cuda) for p in plans]
+    per_layer = plans[0].layer_elems
+    nq = plans[0].n_q
+    for p, dt in zip(plans, dts):
+        k0, k1 = p.own_layers
+        dt.update_own(E[k0 * per_layer * nq:k1 * per_layer * nq].contiguous())
+    for r in range(1, world):  # the exchange: top layer of r-1 -> halo of r
+        s0, s1 = plans[r - 1].send_points
+        h0, h1 = plans[r].halo_points
+        dts[r].flags[h0:h1] = dts[r - 1].flags[s0:s1]
+        dts[r].D[h0:h1] = dts[r - 1].D[s0:s1]
+    rp = _np(gc.row_ptr)
+    Kg_np = _np(Kg)
+    for p, dt in zip(plans, dts):
+        S, f, Kown = dt.assemble()
+        dt.ctx.sync()
+        k0, k1 = p.own_layers
+        q0, q1 = k0 * per_layer * nq, k1 * per_layer * nq
+        assert np.array_equal(_np(f), _np(fg[q0:q1])) and np.array_equal(_np(S), _np(Sg[q0:q1]))
+        g0, g1 = p.global_rows
+        want = Kg_np[rp[g0]:rp[g1]]
+        assert np.array_equal(_np(Kown).view(np.uint64), want.view(np.uint64)), (p.rank, g0, g1)
+    assert sum(p.global_rows[1] - p.global_rows[0] for p in plans) == gc.info.n_dofs
+
+
 # ---------------------------------------------------------------------------
 # full-size configurations: size-independent properties
 
