@@ -24,6 +24,10 @@
 // (delta.cuh).  The row stream (tangent.cu) then assembles K.
 #include "delta.cuh"
 
+#ifndef EPFEM_TSHARED
+#define EPFEM_TSHARED 0  // 1: 3D CTA phase 2 with T_a shared through shared memory (measured slower: the per-point barriers)
+#endif
+
 namespace epfem_gpu {
 
 namespace {
@@ -350,6 +354,13 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DeltaCfg<DIM, 
   }
   __syncthreads();
   if (tid < EPB && e0 + tid < g.e_end) g.emask[e0 + tid] = s_mask[tid];
+#if EPFEM_TSHARED
+  if constexpr (DIM == 3) {
+    __shared__ double s_T[EPB][NP][DIM * Cfg::NS];
+    delta_phase2_tshared<DIM, NP, NQ>(s_st, s_mask, s_T, tid, blockDim.x, e0, g.e_end, g.scratch);
+    return;
+  }
+#endif
   // phase 2: uniform chunks (no divergent block branch) in sub-passes of SUB
   if (tid < EPB * Cfg::NT) {
     const int le = tid / Cfg::NT;
@@ -468,6 +479,60 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
           ++n;
         }
       if (n) tma_store_wait_read();
+    }
+  }
+}
+
+// k_newton_warp3 (3D): warp-owned elements (EPW = 32 / NQ, all lanes busy in
+// phase 1 for Q1), ballot masks, phase 2 by row pairs (delta_pairs3) in
+// rounds of EPR elements.  No CTA barrier.
+#ifndef EPFEM_WARP3_MINB
+#define EPFEM_WARP3_MINB 4
+#endif
+template <int MODEL, int NP, int NQ>
+__global__ void __launch_bounds__(Pair3Cfg<NP, NQ>::THREADS, EPFEM_WARP3_MINB)
+    k_newton_warp3(ConstArgs c, GatherArgs g) {
+  pdl_trigger();
+  constexpr int DIM = 3;
+  using W = Pair3Cfg<NP, NQ>;
+  constexpr int EPW = W::EPW, REC = W::REC;
+  constexpr unsigned QMASK = NQ >= 32 ? 0xffffffffu : (1u << NQ) - 1u;
+  __shared__ double s_st[W::WPB][EPW * NQ * REC];
+  c.DS = nullptr;  // hot path: S, flags, packed D only
+  c.Ep_out = c.Hard_out = nullptr;
+  c.pm = c.sm = c.am = nullptr;
+  c.crit = nullptr;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t e0 = g.e_begin + ((int64_t)blockIdx.x * W::WPB + w) * EPW;
+  if (e0 >= g.e_end) return;  // warp-uniform
+  double* st_w = s_st[w];
+  bool plastic = false;
+  if (lane < EPW * NQ) {
+    const int le = lane / NQ, q = lane - le * NQ;
+    const int64_t e = e0 + le;
+    if (e < g.e_end) {
+      const int64_t m = e * NQ + q;
+      double* st = st_w + lane * REC;
+      auto stage = [&](auto&& f) {
+        stage_geometry<DIM, NP>(st, g.inv + m * W::D2, g.gradhat, q);
+        stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f);
+      };
+      plastic = eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
+    }
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, plastic);
+  __syncwarp();
+  if (lane < EPW && e0 + lane < g.e_end) g.emask[e0 + lane] = (bal >> (lane * NQ)) & QMASK;
+#pragma unroll 1
+  for (int r0 = 0; r0 < EPW; r0 += W::EPR) {
+    if (lane < W::EPR * W::PL) {
+      const int le = r0 + lane / W::PL, k = lane % W::PL;
+      if (le < EPW && e0 + le < g.e_end) {
+        const unsigned mask = (bal >> (le * NQ)) & QMASK;
+        if (mask)
+          delta_pairs3<NP, NQ>(st_w + le * NQ * REC, mask, k / 3, k % 3,
+                               g.scratch + (size_t)(e0 + le) * W::NB * W::D2);
+      }
     }
   }
 }
@@ -867,6 +932,12 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
     const char* v = getenv("EPFEM_FUSED");
     return (v && v[0] == 'm') ? 2 : 0;
   }();
+  // 3D tetrahedra: warp kernel with row-pair phase 2 by default (hexahedra
+  // keep the CTA kernel); EPFEM_FUSED=cta forces the CTA kernel
+  static const bool warp3 = [] {
+    const char* v = getenv("EPFEM_FUSED");
+    return !(v && v[0] == 'c' && v[1] == 't') && !getenv("EPFEM_NO_WARP3");
+  }();
   // warp-specialized producer / consumer kernel (2D): EPFEM_FUSED=ws
   static const bool ws = [] {
     const char* v = getenv("EPFEM_FUSED");
@@ -903,6 +974,26 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
           break;
       }
       return;
+    }
+    // (measured: P2 tet cfg3 3.61 vs 4.08 ms; Q1 hex cfg4 4.73 vs 4.17 ms -> CTA kernel for Q1)
+    if constexpr (DIM == 3 && NP < 20 && NP != 8) {
+      if (warp3) {
+        using W = Pair3Cfg<NP, NQ>;
+        const int64_t per = (int64_t)W::EPW * W::WPB;
+        const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
+        switch (model) {
+          case EPFEM_MODEL_VON_MISES:
+            k_newton_warp3<EPFEM_MODEL_VON_MISES, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, g);
+            break;
+          case EPFEM_MODEL_DRUCKER_PRAGER:
+            k_newton_warp3<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, g);
+            break;
+          default:
+            k_newton_warp3<EPFEM_MODEL_ELASTIC, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, g);
+            break;
+        }
+        return;
+      }
     }
     if constexpr (DIM == 2) {
       if (ws) {

@@ -25,6 +25,17 @@ __host__ __device__ constexpr int blk_index(int a, int b) {  // a <= b
   return a * (2 * NP - a + 1) / 2 + (b - a);
 }
 
+// (row a, first column c0) of phase-2 slot k of an element, chunks of CS
+template <int NP, int CS>
+__device__ __forceinline__ void chunk_of(int k, int& a, int& c0) {
+  a = 0;
+  while ((NP - a + CS - 1) / CS <= k) {
+    k -= (NP - a + CS - 1) / CS;
+    ++a;
+  }
+  c0 = a + k * CS;
+}
+
 template <int DIM, int NP, int NQ>
 struct DeltaCfg {
   static constexpr int NS = DIM == 3 ? 6 : 3;
@@ -51,8 +62,11 @@ struct DeltaCfg {
   // CTA-kernel phase 2 sub-pass width and minimum CTAs per SM (measured on
   // B200: 3D Q1 / P2 tet fastest at SUB = 2 with <= 102 registers; Q2-20 with
   // whole chunks and ptxas' own register choice; 2D: 1024 threads per SM)
+#ifndef EPFEM_MINB3
+#define EPFEM_MINB3 5
+#endif
   static constexpr int SUB = (DIM == 3 && NP < 20) ? 2 : 0;
-  static constexpr int MINB = DIM == 2 ? 1024 / THREADS : (NP < 20 ? 5 : 0);
+  static constexpr int MINB = DIM == 2 ? 1024 / THREADS : (NP < 20 ? EPFEM_MINB3 : 0);
 };
 
 // assembly row r -> Voigt row (2D plane strain uses {0,1,3}, assembly.cpp:92)
@@ -198,6 +212,111 @@ __device__ __forceinline__ void delta_phase2(
   }
 }
 
+// Phase 2 with T shared through shared memory (CTA kernel): the CTA walks
+// the union of its elements' plastic points; per point, step A forms every
+// T_a = B_a^T Dw once (thread per (element, node)) into s_T, a barrier, then
+// step B has each phase-2 thread (element, row a, CS-block chunk, uniform
+// length) add T_a B_b to its accumulators, and a second barrier.  Each T_a is
+// computed once instead of once per chunk of its row; the FMA sequence per
+// block entry is the one of delta_phase2, so the bits are identical.
+template <int DIM, int NP, int NQ>
+__device__ __forceinline__ void delta_phase2_tshared(
+    const double (*s_st)[NQ][DeltaCfg<DIM, NP, NQ>::REC], const unsigned* s_mask,
+    double (*s_T)[NP][DIM * DeltaCfg<DIM, NP, NQ>::NS], int tid, int nthreads, int64_t e0, int64_t e_end,
+    double* __restrict__ scratch) {
+  using Cfg = DeltaCfg<DIM, NP, NQ>;
+  constexpr int NS = Cfg::NS, D2 = Cfg::D2, NB = Cfg::NB, CS = Cfg::CS, NT = Cfg::NT, EPB = Cfg::EPB;
+  int le = 0, a = 0, c0 = 0;
+  unsigned mask = 0u;
+  if (tid < EPB * NT) {
+    le = tid / NT;
+    chunk_of<NP, CS>(tid - le * NT, a, c0);
+    if (e0 + le < e_end) mask = s_mask[le];
+  }
+  unsigned umask = 0u;
+#pragma unroll 1
+  for (int l = 0; l < EPB; ++l) umask |= s_mask[l];
+  double blk[CS][DIM][DIM];
+#pragma unroll
+  for (int b = 0; b < CS; ++b)
+#pragma unroll
+    for (int i = 0; i < DIM; ++i)
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) blk[b][i][j] = 0.0;
+#pragma unroll 1
+  while (umask) {
+    const int q = __ffs(umask) - 1;
+    umask &= umask - 1u;
+    // step A: T_a for every (element with q plastic, node a)
+    for (int t = tid; t < EPB * NP; t += nthreads) {
+      const int l2 = t / NP, a2 = t - l2 * NP;
+      if (!((s_mask[l2] >> q) & 1u)) continue;
+      const double* st = s_st[l2][q];
+      const double* dw = st + NP * DIM;
+      auto Dw = [&](int r, int c) {
+        const int lo = r < c ? r : c, hi = r < c ? c : r;
+        return dw[lo * NS - lo * (lo - 1) / 2 + (hi - lo)];
+      };
+      double ga[DIM];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) ga[i] = st[a2 * DIM + i];
+      double* T = s_T[l2][a2];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        if constexpr (DIM == 3) {
+          T[0 * NS + c] = __fma_rn(ga[2], Dw(5, c), __fma_rn(ga[1], Dw(3, c), __dmul_rn(ga[0], Dw(0, c))));
+          T[1 * NS + c] = __fma_rn(ga[2], Dw(4, c), __fma_rn(ga[0], Dw(3, c), __dmul_rn(ga[1], Dw(1, c))));
+          T[(DIM - 1) * NS + c] =
+              __fma_rn(ga[0], Dw(5, c), __fma_rn(ga[1], Dw(4, c), __dmul_rn(ga[2], Dw(2, c))));
+        } else {
+          T[0 * NS + c] = __fma_rn(ga[1], Dw(2, c), __dmul_rn(ga[0], Dw(0, c)));
+          T[1 * NS + c] = __fma_rn(ga[0], Dw(2, c), __dmul_rn(ga[1], Dw(1, c)));
+        }
+      }
+    }
+    __syncthreads();
+    // step B: the thread's chunk of block row a
+    if ((mask >> q) & 1u) {
+      const double* st = s_st[le][q];
+      const double* T = s_T[le][a];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) {
+        double Ti[NS];
+#pragma unroll
+        for (int c = 0; c < NS; ++c) Ti[c] = T[i * NS + c];
+#pragma unroll
+        for (int bb = 0; bb < CS; ++bb) {
+          const int b = c0 + bb < NP ? c0 + bb : NP - 1;  // clamped: result dropped below
+          const double* h = st + b * DIM;
+          const double h0 = h[0], h1 = h[1], h2 = DIM == 3 ? h[DIM - 1] : 0.0;
+          if constexpr (DIM == 3) {
+            blk[bb][i][0] = __fma_rn(Ti[5], h2, __fma_rn(Ti[3], h1, __fma_rn(Ti[0], h0, blk[bb][i][0])));
+            blk[bb][i][1] = __fma_rn(Ti[4], h2, __fma_rn(Ti[3], h0, __fma_rn(Ti[1], h1, blk[bb][i][1])));
+            blk[bb][i][DIM - 1] =
+                __fma_rn(Ti[5], h0, __fma_rn(Ti[4], h1, __fma_rn(Ti[2], h2, blk[bb][i][DIM - 1])));
+          } else {
+            blk[bb][i][0] = __fma_rn(Ti[2], h1, __fma_rn(Ti[0], h0, blk[bb][i][0]));
+            blk[bb][i][1] = __fma_rn(Ti[2], h0, __fma_rn(Ti[1], h1, blk[bb][i][1]));
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (!mask) return;
+  double* rec = scratch + (size_t)(e0 + le) * NB * D2;
+#pragma unroll
+  for (int bb = 0; bb < CS; ++bb) {
+    if (c0 + bb < NP) {
+      double* o = rec + blk_index<NP>(a, c0 + bb) * D2;
+#pragma unroll
+      for (int i = 0; i < DIM; ++i)
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) o[i * DIM + j] = blk[bb][i][j];
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Warp-synchronous variant (2D): a warp owns EPW whole elements, so phase 1
 // and phase 2 meet at a __syncwarp instead of a CTA barrier, and the plastic
@@ -326,17 +445,92 @@ __device__ __forceinline__ void delta_chunk_uniform1(const double* st_e, unsigne
   }
 }
 
-// (row a, first column c0) of phase-2 slot k of an element, chunks of CS
-template <int NP, int CS>
-__device__ __forceinline__ void chunk_of(int k, int& a, int& c0) {
-  a = 0;
-  while ((NP - a + CS - 1) / CS <= k) {
-    k -= (NP - a + CS - 1) / CS;
-    ++a;
-  }
-  c0 = a + k * CS;
-}
 
+
+// ---------------------------------------------------------------------------
+// 3D warp phase 2 by row pairs: lane (element, pair p, component i) owns row
+// i of the block rows a = p and a' = NP - 1 - p (a <= a'), i.e. (NP - a) +
+// (a + 1) = NP + 1 blocks whatever p is (balanced), and forms its own T rows
+// T_a[i][:] and T_a'[i][:] once per plastic point: every T entry and every
+// block entry is computed exactly once (the optimal n_p n_s g + n_p(n_p+1)/2 g
+// dim FMA per point).  Per-entry FMA sequences are those of delta_phase2, so
+// the bits are identical.  Accumulators are written straight to the element
+// record (no shared-memory staging of outputs).
+template <int NP, int NQ>
+struct Pair3Cfg {
+  static constexpr int DIM = 3, NS = 6, NSP = 21, D2 = 9;
+  static constexpr int NB = NP * (NP + 1) / 2;
+  static constexpr int REC = NP * DIM + NSP;
+  static constexpr int NPAIR = (NP + 1) / 2;
+  static constexpr int PL = 3 * NPAIR;          // phase-2 lanes per element
+  static constexpr int EPW = 32 / NQ;           // elements per warp (phase 1)
+  static constexpr int EPR = 32 / PL;           // elements per phase-2 round
+  static constexpr int NBLK = NP + 1;           // blocks per lane (a != a'); NP - a for a == a'
+  static constexpr int WPB = 4;
+  static constexpr int THREADS = 32 * WPB;
+};
+
+template <int NP, int NQ>
+__device__ __forceinline__ void delta_pairs3(const double* st_e, unsigned mask, int p, int i,
+                                             double* __restrict__ rec) {
+  using C = Pair3Cfg<NP, NQ>;
+  constexpr int NS = C::NS, REC = C::REC, D2 = C::D2, NBLK = C::NBLK;
+  const int a0 = p, a1 = NP - 1 - p;
+  const bool twin = a1 != a0;
+  // T row i: sum over the B column (node, i) nonzeros in delta_phase2's order
+  const int d0 = i, d1 = i == 2 ? 4 : 3, d2 = i == 0 ? 5 : (i == 1 ? 4 : 5);
+  const int e1 = i == 0 ? 1 : (i == 1 ? 0 : 1), e2 = i == 0 ? 2 : (i == 1 ? 2 : 0);
+  auto pk = [](int r, int c) {
+    const int lo = r < c ? r : c, hi = r < c ? c : r;
+    return lo * NS - lo * (lo - 1) / 2 + (hi - lo);
+  };
+  double acc[NBLK][3];
+#pragma unroll
+  for (int k = 0; k < NBLK; ++k) acc[k][0] = acc[k][1] = acc[k][2] = 0.0;
+  while (mask) {
+    const int q = __ffs(mask) - 1;
+    mask &= mask - 1u;
+    const double* st = st_e + q * REC;
+    const double* dw = st + NP * 3;
+    double T0[NS], T1[NS];
+    {
+      const double* g0 = st + a0 * 3;
+      const double* g1 = st + a1 * 3;
+      const double gA0 = g0[d0], gA1 = g0[e1], gA2 = g0[e2];
+      const double gB0 = g1[d0], gB1 = g1[e1], gB2 = g1[e2];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        const double w0 = dw[pk(d0, c)], w1 = dw[pk(d1, c)], w2 = dw[pk(d2, c)];
+        T0[c] = __fma_rn(gA2, w2, __fma_rn(gA1, w1, __dmul_rn(gA0, w0)));
+        T1[c] = __fma_rn(gB2, w2, __fma_rn(gB1, w1, __dmul_rn(gB0, w0)));
+      }
+    }
+    // blocks (a0, b) for b = a0 .. NP-1, then (a1, b) for b = a1 .. NP-1
+#pragma unroll
+    for (int k = 0; k < NBLK; ++k) {
+      const bool first = k < NP - a0;
+      const int b = first ? a0 + k : a1 + (k - (NP - a0));
+      const bool ok = first || (twin && k - (NP - a0) < NP - a1);
+      const double* T = first ? T0 : T1;
+      const double* h = st + (ok ? b : NP - 1) * 3;
+      const double h0 = h[0], h1 = h[1], h2 = h[2];
+      acc[k][0] = __fma_rn(T[5], h2, __fma_rn(T[3], h1, __fma_rn(T[0], h0, acc[k][0])));
+      acc[k][1] = __fma_rn(T[4], h2, __fma_rn(T[3], h0, __fma_rn(T[1], h1, acc[k][1])));
+      acc[k][2] = __fma_rn(T[5], h0, __fma_rn(T[4], h1, __fma_rn(T[2], h2, acc[k][2])));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NBLK; ++k) {
+    const bool first = k < NP - a0;
+    const int b = first ? a0 + k : a1 + (k - (NP - a0));
+    const bool ok = first || (twin && k - (NP - a0) < NP - a1);
+    if (!ok) continue;
+    double* o = rec + blk_index<NP>(first ? a0 : a1, b) * D2 + i * 3;
+    o[0] = acc[k][0];
+    o[1] = acc[k][1];
+    o[2] = acc[k][2];
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Tensor-core phase 2: dK_e = sum_q B_q^T (Dw_q B_q) on the FP64 tensor pipe
