@@ -172,6 +172,52 @@ def test_tangent_matches_oracle(cuda, oracle, family, dim):
             assert np.array_equal(gv.view(np.uint64), kel.view(np.uint64))
 
 
+@pytest.mark.parametrize("model", ["vm", "dp"])
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("family", FAMILIES)
+def test_fused_step_all_element_types(cuda, oracle, family, dim, model):
+    """The fused Newton step (each element type's default kernel: 2D warp,
+    3D tetrahedra warp / row pairs, 3D hexahedra CTA) vs the oracle's
+    evaluate_constitutive + assemble_tangent_stiffness on random strains,
+    and bitwise vs the separate constitutive + tangent calls."""
+    import paper_1805_04155_b200 as P
+    oc, gc, K, G = _caches(cuda, oracle, family, dim, 5.0, 0.2)
+    n = oc.n_int
+    E = np.random.default_rng(47).uniform(-1e-3, 1e-3, (n, 6))
+    if dim == 2:
+        E[:, [2, 4, 5]] = 0.0  # plane strain
+    if model == "vm":
+        a = 0.05
+        Y = float(np.median(oracle.constitutive_vm(E, None, None, G, K, a, 0.0)["crit"]))
+        mat = P.uniform_von_mises(n, K, G, a, Y)
+        ref = oracle.constitutive_vm(E, None, None, G, K, a, Y)
+    else:
+        eta, _ = P.dp_parameters(1.0, np.pi / 9)
+        # c at the median of rho / sqrt2 + eta p (constitutive.cpp:157-166): about half yields
+        tr = E[:, 0] + E[:, 1] + E[:, 2]
+        dev = E.copy()
+        dev[:, :3] -= tr[:, None] / 3.0
+        dev[:, 3:] *= 0.5
+        rho = 2.0 * G * np.sqrt(np.maximum(0.0, (E * dev).sum(1)))
+        c = float(np.median(rho / np.sqrt(2.0) + eta * K * tr))
+        mat = P.uniform_drucker_prager(n, K, G, eta, c)
+        ref = oracle.constitutive_dp(E, None, G, K, eta, c)
+    pl = ref["plastic"]
+    assert 0 < pl.sum() < n
+    Kref = oc.tangent(ref["DS"], pl)
+    Et = _t(E, cuda)
+    eng = P.TangentEngine(gc, mat)
+    S, flags, D, Kv = eng.step(Et)
+    eng.sync()
+    assert np.array_equal(_np(flags) & 1, pl)
+    assert np.array_equal(_np(S), ref["S"])
+    assert row_scaled_error(_np(Kv), Kref.data, Kref.indptr, oc.K_elast().data) <= 1e-12
+    sep = P.TangentEngine(gc, mat, fused=False)
+    S2, f2, D2, K2 = sep.step(Et)
+    sep.sync()
+    assert np.array_equal(_np(K2).view(np.uint64), _np(Kv).view(np.uint64))
+
+
 @pytest.mark.parametrize("dim", [2, 3])
 @pytest.mark.parametrize("family", FAMILIES)
 def test_strains_and_internal_forces(cuda, oracle, family, dim):
@@ -423,7 +469,7 @@ def test_full_size_pattern_and_properties(cuda, name):
 # ---------------------------------------------------------------------------
 # opt-in kernel variants (EPFEM_FUSED, read once per process): each in a
 # fresh interpreter, same bar as the default path
-@pytest.mark.parametrize("variant,name", [("mma", "cfg2"), ("mma", "cfg3"), ("mma", "cfg4"), ("ws", "cfg2"),
+@pytest.mark.parametrize("variant,name", [("mma", "cfg2"), ("mma", "cfg3"), ("mma", "cfg4"), ("ws", "cfg2"), ("cta", "cfg3"),
                                           ("cta", "cfg2"), ("pipe", "cfg2"), ("pipe", "cfg4")])
 def test_kernel_variants(cuda, oracle, variant, name):
     import subprocess
