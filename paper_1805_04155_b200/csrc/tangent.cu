@@ -22,6 +22,11 @@
 // contributions are therefore bitwise copies of K_elast.
 #include "delta.cuh"
 
+#ifndef EPFEM_K_EVICT_FIRST
+#define EPFEM_K_EVICT_FIRST 1  // 3D Q1 / P2: K_elast and K streamed through L2 with evict_first (measured
+                               // cfg3 row stream 3.08 -> 2.97 ms, cfg4 3.76 -> 3.66; neutral or worse in 2D / Q2-20)
+#endif
+
 namespace epfem_gpu {
 
 namespace {
@@ -229,7 +234,10 @@ __global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int
   if (tid == 0 && a1 > a0) {
     const unsigned bytes = (unsigned)((a1 - a0) * 8);
     mbar_expect_tx(&s_bar, bytes);
-    tma_load_1d(img_raw, a.base + a0, bytes, &s_bar);
+    if (EPFEM_K_EVICT_FIRST && DIM == 3 && NP < 20)
+      tma_load_1d_hint(img_raw, a.base + a0, bytes, &s_bar, l2_evict_first());
+    else
+      tma_load_1d(img_raw, a.base + a0, bytes, &s_bar);
   }
   // node offsets (cache data, independent of the producer kernel)
   for (int k = tid; k <= nloc; k += blockDim.x) {
@@ -299,7 +307,12 @@ __global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int
     const int64_t s0 = (v0 + 1) & ~int64_t(1), s1 = v1 & ~int64_t(1);
     if (v0 & 1) a.out[v0] = img[0];
     if ((v1 & 1) && v1 - 1 >= s0) a.out[v1 - 1] = img[v1 - 1 - v0];
-    if (s1 > s0) tma_store_1d_sync(a.out + s0, img + (s0 - v0), (unsigned)((s1 - s0) * 8));
+    if (s1 > s0) {
+      if (EPFEM_K_EVICT_FIRST && DIM == 3 && NP < 20)
+        tma_store_1d_sync_hint(a.out + s0, img + (s0 - v0), (unsigned)((s1 - s0) * 8), l2_evict_first());
+      else
+        tma_store_1d_sync(a.out + s0, img + (s0 - v0), (unsigned)((s1 - s0) * 8));
+    }
   }
 }
 
