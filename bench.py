@@ -482,6 +482,51 @@ def main():
             dom_bytes, dom_ms, dom = cons_b, tot_c / reps, "k_newton_fused (constitutive + element delta)"
     else:
         dom_bytes, dom_ms, dom = asm_b, ms_per_step, "k_gather<elastic> (K5)"
+    # the same step from nodal displacements with the
+    # strains formed inside the constitutive kernel, vs strains + step
+    from_u = None
+    if not elastic and cfg.dim == 2:
+        from paper_1805_04155_b200.synthetic import displacement
+        u = (wl.scale * torch.from_numpy(displacement(wl.mesh.coord, cfg.seed)).to(dev)).contiguous()
+        Etmp = torch.empty_like(E)
+        eng_u = P.TangentEngine(cache, mat, stream=stream)
+        with torch.cuda.stream(stream):
+            eng_u.capture_u(u, Ep0, Hard0)
+        g2 = torch.cuda.CUDAGraph()
+        s2 = torch.cuda.Stream(dev)
+        s2.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s2):
+            eng2 = P.TangentEngine(cache, mat, stream=s2)
+            lib_ = P.api.L.lib()
+            P.api._check(lib_.epfem_strains(eng2.ctx.handle, cache.handle, P.api._ptr(u), P.api._ptr(Etmp)))
+            eng2.step(Etmp, Ep0, Hard0)
+            with torch.cuda.graph(g2, stream=s2):
+                eng2.ctx.set_stream(torch.cuda.current_stream(dev))
+                P.api._check(lib_.epfem_strains(eng2.ctx.handle, cache.handle, P.api._ptr(u),
+                                                P.api._ptr(Etmp)))
+                eng2.step(Etmp, Ep0, Hard0)
+        torch.cuda.current_stream(dev).wait_stream(s2)
+
+        def t_graph(fn):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize(dev)
+            ev0.record(stream)
+            for _ in range(args.steps):
+                fn()
+            ev1.record(stream)
+            torch.cuda.synchronize(dev)
+            return ev0.elapsed_time(ev1) / args.steps
+
+        def run2():
+            with torch.cuda.stream(stream):
+                g2.replay()
+        t_u = t_graph(eng_u.replay)
+        t_2 = t_graph(run2)
+        from_u = {"newton_step_u_ms": t_u, "strains_plus_newton_step_ms": t_2,
+                  "value_from_u": n_int / (t_u * 1e-3),
+                  "how": "epfem_newton_step_u (E = B u inside the fused kernel, never stored) vs "
+                         "epfem_strains + epfem_newton_step, each one CUDA graph"}
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     step_bytes = cons_b + asm_b if not elastic else asm_b
     step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
@@ -606,6 +651,7 @@ def main():
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "step_from_displacements": from_u,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

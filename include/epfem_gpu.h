@@ -194,6 +194,13 @@ int epfem_assemble_tangent_ds(epfem_ctx* ctx, const epfem_cache* cache, int64_t 
 int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* cache, const epfem_material* mat,
                       const double* E, const double* Ep_prev, const double* Hard_prev,
                       const epfem_constitutive_out* out, double* K_values);
+/* The same step from nodal displacements: the strains
+ * E = B u (assembly.cpp:135-146, epfem_strains) are formed inside the
+ * constitutive kernel, never stored unless E_out != NULL (n_int x 6).  Same
+ * bits as epfem_strains followed by epfem_newton_step.  2D meshes. */
+int epfem_newton_step_u(epfem_ctx* ctx, const epfem_cache* cache, const epfem_material* mat,
+                        const double* u, const double* Ep_prev, const double* Hard_prev,
+                        const epfem_constitutive_out* out, double* E_out, double* K_values);
 /* The two halves of epfem_newton_step, for callers that overlap them with
  * other work: (1) constitutive update + element tangent deltas into the
  * cache's workspace, (2) K = K_elast + assembled deltas.  (2) must follow the

@@ -636,6 +636,16 @@ class TangentEngine:
                                           _ptr(self.D), _ptr(self.flags), _ptr(self.K)))
         return self.S, self.flags, self.D, self.K
 
+    def step_u(self, u: torch.Tensor, Ep: Optional[torch.Tensor] = None,
+               Hard: Optional[torch.Tensor] = None, E_out: Optional[torch.Tensor] = None):
+        """The step from nodal displacements (2D): E = B u is formed inside
+        the constitutive kernel (epfem_newton_step_u); same bits as
+        cache.strains(u) followed by step()."""
+        _check(L.lib().epfem_newton_step_u(self.ctx.handle, self.cache.handle, C.byref(self._mv),
+                                           _ptr(u), _ptr(Ep), _ptr(Hard), C.byref(self._out),
+                                           _ptr(E_out), _ptr(self.K)))
+        return self.S, self.flags, self.D, self.K
+
     def capture(self, E, Ep=None, Hard=None):
         """Record step() on fixed input buffers into a CUDA graph."""
         s = torch.cuda.Stream(self.device)
@@ -651,6 +661,23 @@ class TangentEngine:
         self.ctx.set_stream(self.stream)
         self.graph = g
         self._graph_inputs = (E, Ep, Hard)
+        return g
+
+    def capture_u(self, u, Ep=None, Hard=None, E_out=None):
+        """Record step_u() on fixed buffers into a CUDA graph (replay())."""
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.ctx.set_stream(s)
+            self.step_u(u, Ep, Hard, E_out)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                self.ctx.set_stream(torch.cuda.current_stream(self.device))
+                self.step_u(u, Ep, Hard, E_out)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        self.ctx.set_stream(self.stream)
+        self.graph = g
+        self._graph_inputs = (u, Ep, Hard, E_out)
         return g
 
     def replay(self):

@@ -30,7 +30,7 @@
 // element skip the arithmetic and copy K_elast bitwise.
 #include <cub/cub.cuh>
 
-#include "kernels.cuh"
+#include "delta.cuh"
 
 namespace epfem_gpu {
 
@@ -393,26 +393,10 @@ __global__ void k_strains(int64_t n_e, const int32_t* __restrict__ elem,
     for (int p = 0; p < NP; ++p) {
       const int32_t node = __ldg(elem + e * NP + p);
       double d[DIM], uu[DIM];
+      point_dphi<DIM>(Ji, gradhat + (q * NP + p) * DIM, d);
 #pragma unroll
-      for (int i = 0; i < DIM; ++i) {
-        double t = 0.0;
-#pragma unroll
-        for (int j = 0; j < DIM; ++j) t += Ji[j * DIM + i] * __ldg(gradhat + (q * NP + p) * DIM + j);
-        d[i] = t;
-        uu[i] = __ldg(u + (int64_t)DIM * node + i);
-      }
-      if constexpr (DIM == 3) {
-        s[0] += d[0] * uu[0];
-        s[1] += d[1] * uu[1];
-        s[2] += d[2] * uu[2];
-        s[3] += d[1] * uu[0] + d[0] * uu[1];
-        s[4] += d[2] * uu[1] + d[1] * uu[2];
-        s[5] += d[2] * uu[0] + d[0] * uu[2];
-      } else {
-        s[0] += d[0] * uu[0];
-        s[1] += d[1] * uu[1];
-        s[3] += d[1] * uu[0] + d[0] * uu[1];
-      }
+      for (int i = 0; i < DIM; ++i) uu[i] = __ldg(u + (int64_t)DIM * node + i);
+      strain_accumulate<DIM>(d, uu, s);
     }
     double2* o = reinterpret_cast<double2*>(E + 6 * m);
     o[0] = make_double2(s[0], s[1]);

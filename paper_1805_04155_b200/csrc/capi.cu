@@ -575,6 +575,26 @@ int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* c, const epfem_material
   return finish(ctx);
 }
 
+int epfem_newton_step_u(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
+                        const double* u, const double* Ep_prev, const double* Hard_prev,
+                        const epfem_constitutive_out* out, double* E_out, double* K_values) {
+  if (!K_values || !aligned16(K_values))
+    return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: K must be 16-byte aligned");
+  if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
+  if (c->info.n_int > 0 && !u) return fail(EPFEM_ERR_INVALID, "strains: null argument");
+  if (!aligned16(E_out)) return fail(EPFEM_ERR_INVALID, "strains: E must be 16-byte aligned");
+  ConstArgs a;
+  GatherArgs g;
+  // u stands in for E in the argument checks; the strain-fused kernel never reads c.E
+  if (int rc = delta_args(ctx, c, mat, u, Ep_prev, Hard_prev, out, &a, &g)) return rc;
+  a.E = nullptr;
+  g.u = u;
+  g.E_out = E_out;
+  if (int rc = launch_newton_fused_u(mat->model, c->info.family, c->info.dim, a, g, ctx->stream)) return rc;
+  if (int rc = rows_part(ctx, c, K_values)) return rc;
+  return finish(ctx);
+}
+
 int epfem_constitutive_delta(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
                              const double* E, const double* Ep_prev, const double* Hard_prev,
                              const epfem_constitutive_out* out) {

@@ -98,6 +98,18 @@ struct GlobalIn {  // pointers by value: never take the address of the kernel ar
   __device__ __forceinline__ void ep(int64_t q, double* v) const { load6(Ep, q, v); }
   __device__ __forceinline__ void hard(int64_t q, double* v) const { load6(H, q, v); }
 };
+// E from registers (strain-fused kernel), Ep / Hard from global memory
+struct RegEIn {
+  const double* e6;
+  const double* Ep;
+  const double* H;
+  __device__ __forceinline__ void e(int64_t, double* v) const {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) v[i] = e6[i];
+  }
+  __device__ __forceinline__ void ep(int64_t q, double* v) const { load6(Ep, q, v); }
+  __device__ __forceinline__ void hard(int64_t q, double* v) const { load6(H, q, v); }
+};
 struct SmemIn {
   const double* E;
   const double* Ep;
@@ -390,7 +402,7 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DeltaCfg<DIM, 
 #ifndef EPFEM_EARLY_GEOM
 #define EPFEM_EARLY_GEOM 1
 #endif
-template <int MODEL, int NP, int NQ>
+template <int MODEL, int NP, int NQ, bool FROM_U = false>
 __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
     k_newton_warp(ConstArgs c, GatherArgs g) {
   pdl_trigger();
@@ -418,6 +430,42 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
     if (e < g.e_end) {
       const int64_t m = e * NQ + q;
       double* st = st_w + lane * REC;
+      if constexpr (FROM_U) {
+        // K8 fused: dphi of every node (staged for phase 2 right away) and
+        // E = B u from the element's nodal displacements, in registers
+        double J[W::D2];
+        {
+          const double2* p2 = reinterpret_cast<const double2*>(g.inv + m * W::D2);
+#pragma unroll
+          for (int k = 0; k < W::D2 / 2; ++k) {
+            const double2 v = __ldg(p2 + k);
+            J[2 * k] = v.x;
+            J[2 * k + 1] = v.y;
+          }
+        }
+        double e6[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+        for (int p = 0; p < NP; ++p) {
+          const int32_t node = __ldg(g.elem + e * NP + p);
+          double d[DIM], uu[DIM];
+          point_dphi<DIM>(J, g.gradhat + (q * NP + p) * DIM, d);
+#pragma unroll
+          for (int i = 0; i < DIM; ++i) {
+            uu[i] = __ldg(g.u + (int64_t)DIM * node + i);
+            st[p * DIM + i] = d[i];
+          }
+          strain_accumulate<DIM>(d, uu, e6);
+        }
+        if (g.E_out) {
+          double2* o = reinterpret_cast<double2*>(g.E_out + 6 * m);
+          o[0] = make_double2(e6[0], e6[1]);
+          o[1] = make_double2(e6[2], e6[3]);
+          o[2] = make_double2(e6[4], e6[5]);
+        }
+        const double wq = __ldg(g.weight + m);
+        auto stage = [&](auto&& f) { stage_dw<DIM>(st + NP * DIM, wq, g, m, f); };
+        plastic = eval_point<MODEL>(c, m, RegEIn{e6, c.Ep, c.Hard}, stage);
+      } else {
 #if EPFEM_EARLY_GEOM
       // J^-1 and w are loaded with E / Ep / Hard, before the return map, so
       // plastic points do not pay a second dependent memory round trip
@@ -443,6 +491,7 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
       };
 #endif
       plastic = eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
+      }
     }
   }
   const unsigned bal = __ballot_sync(0xffffffffu, plastic);
@@ -905,6 +954,35 @@ static int launch_pipe(const ConstArgs& c, const GatherArgs& g, cudaStream_t st)
   const int64_t n_groups = (g.e_end - g.e_begin + Cfg::EPB - 1) / Cfg::EPB;
   const int64_t grid = std::min<int64_t>(n_groups, (int64_t)per_sm * num_sms);
   kern<<<(unsigned)grid, Cfg::THREADS, Tile::BYTES, st>>>(c, g, n_groups);
+  EPFEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int launch_newton_fused_u(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
+                          cudaStream_t st) {
+  if (g.e_end <= g.e_begin) return 0;
+  if (dim != 2) return fail(EPFEM_ERR_INVALID, "newton_step_u: 2D meshes only (3D: epfem_strains + epfem_newton_step)");
+  bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
+    constexpr int DIM = decltype(D)::value;
+    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
+    if constexpr (DIM == 2) {
+      using W = WarpCfg<DIM, NP, NQ>;
+      const int64_t per = (int64_t)W::EPW * W::WPB;
+      const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
+      switch (model) {
+        case EPFEM_MODEL_VON_MISES:
+          k_newton_warp<EPFEM_MODEL_VON_MISES, NP, NQ, true><<<blocks, W::THREADS, 0, st>>>(c, g);
+          break;
+        case EPFEM_MODEL_DRUCKER_PRAGER:
+          k_newton_warp<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ, true><<<blocks, W::THREADS, 0, st>>>(c, g);
+          break;
+        default:
+          k_newton_warp<EPFEM_MODEL_ELASTIC, NP, NQ, true><<<blocks, W::THREADS, 0, st>>>(c, g);
+          break;
+      }
+    }
+  });
+  if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
   EPFEM_CUDA_TRY(cudaGetLastError());
   return 0;
 }

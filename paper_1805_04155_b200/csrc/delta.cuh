@@ -98,6 +98,41 @@ __device__ __forceinline__ void stage_geometry(double* st, const double* inv_m,
   }
 }
 
+// K8 at one point: E = sum_p B_p u_p (assembly.cpp:135-146) from the
+// physical gradients dphi (as stage_geometry computes them) and the element's
+// nodal displacements; explicit roundings so every translation unit (K8
+// alone, the fused strain + Newton kernel) produces the same bits.  2D fills
+// Voigt rows {0, 1, 3}.
+template <int DIM>
+__device__ __forceinline__ void strain_accumulate(const double* d, const double* uu, double* s) {
+  if constexpr (DIM == 3) {
+    s[0] = __fma_rn(d[0], uu[0], s[0]);
+    s[1] = __fma_rn(d[1], uu[1], s[1]);
+    s[2] = __fma_rn(d[2], uu[2], s[2]);
+    s[3] = __fma_rn(d[0], uu[1], __fma_rn(d[1], uu[0], s[3]));
+    s[4] = __fma_rn(d[1], uu[2], __fma_rn(d[2], uu[1], s[4]));
+    s[5] = __fma_rn(d[0], uu[2], __fma_rn(d[2], uu[0], s[5]));
+  } else {
+    s[0] = __fma_rn(d[0], uu[0], s[0]);
+    s[1] = __fma_rn(d[1], uu[1], s[1]);
+    s[3] = __fma_rn(d[0], uu[1], __fma_rn(d[1], uu[0], s[3]));
+  }
+}
+// dphi_p at point q (same arithmetic as stage_geometry)
+template <int DIM>
+__device__ __forceinline__ void point_dphi(const double* J, const double* __restrict__ gh, double* d) {
+  double g[DIM];
+#pragma unroll
+  for (int j = 0; j < DIM; ++j) g[j] = __ldg(gh + j);
+#pragma unroll
+  for (int i = 0; i < DIM; ++i) {
+    double t = __dmul_rn(J[i], g[0]);
+#pragma unroll
+    for (int j = 1; j < DIM; ++j) t = __fma_rn(J[j * DIM + i], g[j], t);
+    d[i] = t;
+  }
+}
+
 // Dw(r, c) = w (D(R r, R c) - C(R r, R c)) packed upper triangle.  Dfun gives
 // the tangent entry D(i, j) in Voigt indices.
 template <int DIM, class Dfun>

@@ -56,6 +56,10 @@ struct GatherArgs {
   // sub-range processed by one launch (chunked, overlapped schedule)
   int64_t e_begin, e_end;  // elements of the delta / fused kernels
   int64_t n_begin, n_end;  // nodes of the row stream
+  // strain-fused Newton step (epfem_newton_step_u): nodal displacements in,
+  // optional strain output
+  const double* u;
+  double* E_out;
 };
 struct PatternOut {
   int64_t* n2e_ptr = nullptr;
@@ -82,6 +86,8 @@ int launch_gather(int family, int dim, int mode, const GatherArgs& a, cudaStream
 int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);
 int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st);
 int launch_delta(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);  // pass 1 over [e_begin, e_end)
+int launch_newton_fused_u(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
+                          cudaStream_t st);  // E = B u inside (GatherArgs::u)
 int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
                         cudaStream_t st);
 size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements);

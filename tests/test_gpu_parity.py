@@ -479,3 +479,39 @@ def test_kernel_variants(cuda, oracle, variant, name):
     r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "variant_check.py"), name,
                         str(n)], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg1"])
+def test_newton_step_from_displacements(cuda, name):
+    """epfem_newton_step_u (strains fused into the constitutive kernel,
+    SURVEY §8(f) rank 1) gives the bits of epfem_strains + epfem_newton_step,
+    and E_out the bits of epfem_strains; 3D meshes are refused."""
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.synthetic import CONFIGS, calibrate, displacement
+    cfg = CONFIGS[name]
+    mesh = cfg.mesh(REDUCED[name] * 2)
+    mat = cfg.material(mesh.n_int)
+    gc = P.build_assembly_cache(P.Mesh.from_structured(mesh, cuda), mat)
+    u1 = torch.from_numpy(displacement(mesh.coord, cfg.seed)).to(cuda)
+    E1 = gc.strains(u1)
+    s = calibrate(E1, mat, 0.3)[0] if cfg.model != "elastic" else 1.0
+    u = (s * u1).contiguous()
+    E = gc.strains(u)
+    e1, e2 = P.TangentEngine(gc, mat), P.TangentEngine(gc, mat)
+    S1, f1, D1, K1 = e1.step(E)
+    Eo = torch.empty_like(E)
+    S2, f2, D2, K2 = e2.step_u(u, E_out=Eo)
+    torch.cuda.synchronize()
+    assert np.array_equal(_np(Eo).view(np.uint64), _np(E).view(np.uint64))
+    assert np.array_equal(_np(f1), _np(f2)) and np.array_equal(_np(S1), _np(S2))
+    m = (_np(f1) & 1).astype(bool)
+    assert np.array_equal(_np(D1)[m], _np(D2)[m])
+    assert np.array_equal(_np(K1).view(np.uint64), _np(K2).view(np.uint64))
+    if cfg.model != "elastic":
+        assert 0.2 < m.mean() < 0.4
+    c3 = CONFIGS["cfg4"]
+    m3 = c3.mesh(3)
+    g3 = P.build_assembly_cache(P.Mesh.from_structured(m3, cuda), c3.material(m3.n_int))
+    with pytest.raises(P.Error, match="2D meshes only"):
+        P.TangentEngine(g3, c3.material(m3.n_int)).step_u(torch.zeros(g3.info.n_dofs, dtype=torch.float64,
+                                                                        device=cuda))
