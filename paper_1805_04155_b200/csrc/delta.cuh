@@ -158,6 +158,30 @@ __device__ __forceinline__ void stage_dw(double* dwst, double w, const GatherArg
     }
 }
 
+// Elastic assembly (K5) through the same two passes: Dw = w C, packed upper
+// triangle in assembly rows (stage_dw with D - C replaced by C).
+template <int DIM>
+__device__ __forceinline__ void stage_c(double* dwst, double w, const GatherArgs& a, int64_t m) {
+  constexpr int NS = DIM == 3 ? 6 : 3;
+  const bool uniform_c = a.shear == nullptr && a.bulk == nullptr;
+  double G2 = 0.0, Km = 0.0;
+  if (!uniform_c) {
+    G2 = 2.0 * (a.shear ? __ldg(a.shear + m) : a.shear_u);
+    Km = a.bulk ? __ldg(a.bulk + m) : a.bulk_u;
+  }
+  int k = 0;
+#pragma unroll
+  for (int r = 0; r < NS; ++r)
+#pragma unroll
+    for (int c = r; c < NS; ++c, ++k) {
+      const int ri = arow<DIM>(r), ci = arow<DIM>(c);
+      const double vol = (ri < 3 && ci < 3) ? 1.0 : 0.0;
+      const double dev = ((ri == ci) ? (ri < 3 ? 1.0 : 0.5) : 0.0) - vol / 3.0;
+      const double cel = uniform_c ? a.Cu[pk_index(ri, ci)] : __fma_rn(G2, dev, __dmul_rn(Km, vol));
+      dwst[k] = __dmul_rn(w, cel);
+    }
+}
+
 // Phase 2: thread (element le, row a, chunk starting at block c0 >= a)
 // accumulates the blocks (a, b), c0 <= b < c0 + CS, over the element's
 // plastic points from the staged records, then writes them to the workspace.

@@ -49,10 +49,14 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS) k_elem_delta_s
     const int64_t e = e0 + le;
     if (e >= a.e_end) continue;
     const int64_t m = e * NQ + q;
-    if (!(__ldg(a.flags + m) & 1)) continue;
+    if (MODE != G_ELASTIC && !(__ldg(a.flags + m) & 1)) continue;
     atomicOr(&s_mask[le], 1u << q);
     double* st = s_st[le][q];
     stage_geometry<DIM, NP>(st, a.inv + m * Cfg::D2, a.gradhat, q);
+    if (MODE == G_ELASTIC) {
+      stage_c<DIM>(st + NP * DIM, __ldg(a.weight + m), a, m);
+      continue;
+    }
     // packed-D loads first (independent), then the staged products
     double dv[NS][NS];
 #pragma unroll
@@ -103,8 +107,12 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS) k_delta_warp(Gath
     const int64_t e = e0 + le;
     if (e < a.e_end) {
       const int64_t m = e * NQ + q;
-      plastic = (__ldg(a.flags + m) & 1) != 0;
-      if (plastic) {
+      plastic = MODE == G_ELASTIC || (__ldg(a.flags + m) & 1) != 0;
+      if (MODE == G_ELASTIC) {
+        double* st = st_w + lane * REC;
+        stage_geometry<DIM, NP>(st, a.inv + m * W::D2, a.gradhat, q);
+        stage_c<DIM>(st + NP * DIM, __ldg(a.weight + m), a, m);
+      } else if (plastic) {
         double* st = st_w + lane * REC;
         double dv[NS][NS];
 #pragma unroll
@@ -169,8 +177,12 @@ __global__ void __launch_bounds__(MmaCfg<DIM, NP, NQ>::THREADS) k_delta_mma(Gath
     const int64_t e = e0 + le;
     if (e < a.e_end) {
       const int64_t m = e * NQ + q;
-      plastic = (__ldg(a.flags + m) & 1) != 0;
-      if (plastic) {
+      plastic = MODE == G_ELASTIC || (__ldg(a.flags + m) & 1) != 0;
+      if (MODE == G_ELASTIC) {
+        double* st = st_w + lane * REC;
+        stage_geometry<DIM, NP>(st, a.inv + m * M::D2, a.gradhat, q);
+        stage_c<DIM>(st + NP * DIM, __ldg(a.weight + m), a, m);
+      } else if (plastic) {
         double* st = st_w + lane * REC;
         double dv[NS][NS];
 #pragma unroll
@@ -231,7 +243,10 @@ __global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (tid == 0 && a1 > a0) {
+  const bool zero_base = a.base == nullptr;  // elastic assembly: K = sum of element blocks
+  if (zero_base)
+    for (int64_t k = tid; k < a1 - a0; k += blockDim.x) img_raw[k] = 0.0;
+  if (tid == 0 && a1 > a0 && !zero_base) {
     const unsigned bytes = (unsigned)((a1 - a0) * 8);
     mbar_expect_tx(&s_bar, bytes);
     if (EPFEM_K_EVICT_FIRST && DIM == 3 && NP < 20)
@@ -252,7 +267,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int
     s_item[k] = __ldcg(a.emask + it / NP) ? it : -1;
   }
   __syncthreads();
-  if (a1 > a0) mbar_wait(&s_bar, 0);
+  if (a1 > a0 && !zero_base) mbar_wait(&s_bar, 0);
   // Items are taken UB at a time: every lane first issues the loads of all
   // UB items (slot byte + workspace value), then applies the adds in item
   // order, so a node costs one memory round trip per UB items instead of
@@ -466,7 +481,7 @@ int launch_delta(int family, int dim, int mode, const GatherArgs& a, cudaStream_
       const char* v = getenv("EPFEM_FUSED");
       return (v && v[0] == 'm') ? 2 : 0;
     }();
-    if (mma == 2) {
+    if (mma == 2 && mode != G_ELASTIC) {
       if (a.n_elements > 0) {
         using M = MmaCfg<DIM, NP, NQ>;
         const int64_t per = (int64_t)M::EPW * M::WPB;
@@ -485,6 +500,8 @@ int launch_delta(int family, int dim, int mode, const GatherArgs& a, cudaStream_
         const unsigned blocks = (unsigned)((a.e_end - a.e_begin + per - 1) / per);
         if (mode == G_TANGENT_PACKED)
           k_delta_warp<NP, NQ, G_TANGENT_PACKED><<<blocks, W::THREADS, 0, st>>>(a);
+        else if (mode == G_ELASTIC)
+          k_delta_warp<NP, NQ, G_ELASTIC><<<blocks, W::THREADS, 0, st>>>(a);
         else
           k_delta_warp<NP, NQ, G_TANGENT_DS36><<<blocks, W::THREADS, 0, st>>>(a);
       }
@@ -494,6 +511,8 @@ int launch_delta(int family, int dim, int mode, const GatherArgs& a, cudaStream_
       const int64_t blocks = (a.e_end - a.e_begin + Cfg::EPB - 1) / Cfg::EPB;
       if (mode == G_TANGENT_PACKED)
         k_elem_delta_staged<DIM, NP, NQ, G_TANGENT_PACKED><<<(unsigned)blocks, Cfg::THREADS, 0, st>>>(a);
+      else if (mode == G_ELASTIC)
+        k_elem_delta_staged<DIM, NP, NQ, G_ELASTIC><<<(unsigned)blocks, Cfg::THREADS, 0, st>>>(a);
       else
         k_elem_delta_staged<DIM, NP, NQ, G_TANGENT_DS36><<<(unsigned)blocks, Cfg::THREADS, 0, st>>>(a);
     }

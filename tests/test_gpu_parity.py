@@ -515,3 +515,18 @@ def test_newton_step_from_displacements(cuda, name):
     with pytest.raises(P.Error, match="2D meshes only"):
         P.TangentEngine(g3, c3.material(m3.n_int)).step_u(torch.zeros(g3.info.n_dofs, dtype=torch.float64,
                                                                         device=cuda))
+
+
+@pytest.mark.parametrize("k5", ["gather", "rows"])
+def test_elastic_assembly_both_paths(cuda, oracle, k5):
+    """K5 through either implementation (EPFEM_K5, read once per process):
+    the pattern / K_elast / tangent tests of all 8 element types in a fresh
+    interpreter."""
+    import subprocess
+    import sys
+    env = dict(os.environ, EPFEM_K5=k5)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(os.path.dirname(__file__), "test_gpu_parity.py"),
+                        "-k", "pattern_and_elastic or tangent_matches_oracle or all_element_types"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
