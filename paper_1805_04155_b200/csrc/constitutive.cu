@@ -22,6 +22,8 @@
 // points the thread also stages dphi and w (D - C) for the element delta
 // straight from registers (D is never re-read).  Phase 2 builds dK_e
 // (delta.cuh).  The row stream (tangent.cu) then assembles K.
+#include <type_traits>
+
 #include "delta.cuh"
 
 #ifndef EPFEM_TSHARED
@@ -532,6 +534,110 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
   }
 }
 
+// k_newton_warp_pf (2D, EPFEM_FUSED=pf): k_newton_warp with two element
+// groups per warp; at entry lane 0 starts TMA bulk copies of the SECOND
+// group's E / Ep / Hard / J^-1 (contiguous: the group's points are) into
+// shared memory, so their latency hides behind the whole first group.
+constexpr int PFW = 3;  // warps per CTA (static shared memory < 48 KB)
+template <int MODEL, int NP, int NQ>
+__global__ void __launch_bounds__(32 * PFW, EPFEM_WARP_MINB * 4 / 3)
+    k_newton_warp_pf(ConstArgs c, GatherArgs g) {
+  pdl_trigger();
+  constexpr int DIM = 2;
+  using W = WarpCfg<DIM, NP, NQ>;
+  constexpr int EPW = W::EPW, REC = W::REC, PPG = EPW * NQ, D2 = W::D2;
+  constexpr unsigned QMASK = NQ >= 32 ? 0xffffffffu : (1u << NQ) - 1u;
+  constexpr int RECB = W::NB * W::D2;
+  constexpr int IN_E = 0, IN_EP = 6 * PPG, IN_H = 12 * PPG, IN_J = 18 * PPG, IN_SIZE = IN_J + D2 * PPG;
+  __shared__ double s_st[PFW][EPW * NQ * REC];
+  __shared__ __align__(16) double s_out[PFW][EPW * RECB];
+  __shared__ __align__(128) double s_in[PFW][IN_SIZE];
+  __shared__ uint64_t s_bar[PFW];
+  c.DS = nullptr;  // hot path: S, flags, packed D only
+  c.Ep_out = c.Hard_out = nullptr;
+  c.pm = c.sm = c.am = nullptr;
+  c.crit = nullptr;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t n_groups = (g.e_end - g.e_begin + EPW - 1) / EPW;
+  const int64_t grp0 = 2 * ((int64_t)blockIdx.x * PFW + w);
+  if (grp0 >= n_groups) return;  // warp-uniform
+  const bool has2 = grp0 + 1 < n_groups;
+  double* st_w = s_st[w];
+  double* in_w = s_in[w];
+  if (lane == 0) {
+    mbar_init(&s_bar[w], 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  if (has2 && lane == 0) {
+    const int64_t p0 = (g.e_begin + (grp0 + 1) * EPW) * NQ;
+    const unsigned np = (unsigned)min((int64_t)PPG, g.e_end * NQ - p0);
+    unsigned total = np * 48u + np * 8u * D2;
+    if (c.Ep) total += np * 48u;
+    if (c.Hard) total += np * 48u;
+    mbar_expect_tx(&s_bar[w], total);
+    tma_load_1d(in_w + IN_E, c.E + 6 * p0, np * 48u, &s_bar[w]);
+    if (c.Ep) tma_load_1d(in_w + IN_EP, c.Ep + 6 * p0, np * 48u, &s_bar[w]);
+    if (c.Hard) tma_load_1d(in_w + IN_H, c.Hard + 6 * p0, np * 48u, &s_bar[w]);
+    tma_load_1d(in_w + IN_J, g.inv + D2 * p0, np * 8u * D2, &s_bar[w]);
+  }
+  auto group = [&](int64_t grp, auto from_smem) {
+    constexpr bool SM = decltype(from_smem)::value;
+    const int64_t e0 = g.e_begin + grp * EPW;
+    bool plastic = false;
+    if (lane < PPG) {
+      const int le = lane / NQ, q = lane - le * NQ;
+      const int64_t e = e0 + le;
+      if (e < g.e_end) {
+        const int64_t m = e * NQ + q;
+        double* st = st_w + lane * REC;
+        double jinv[D2];
+#pragma unroll
+        for (int k = 0; k < D2; ++k) jinv[k] = SM ? in_w[IN_J + lane * D2 + k] : __ldg(g.inv + m * D2 + k);
+        const double wq = __ldg(g.weight + m);
+        auto stage = [&](auto&& f) {
+          stage_geometry<DIM, NP, true>(st, jinv, g.gradhat, q);
+          stage_dw<DIM>(st + NP * DIM, wq, g, m, f);
+        };
+        if constexpr (SM)
+          plastic = eval_point<MODEL>(c, m, SmemIn{in_w + IN_E, in_w + IN_EP, in_w + IN_H, lane}, stage);
+        else
+          plastic = eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, plastic);
+    __syncwarp();
+    if (lane < EPW && e0 + lane < g.e_end) g.emask[e0 + lane] = (bal >> (lane * NQ)) & QMASK;
+    if (lane < EPW * W::NT) {
+      const int le = lane / W::NT;
+      const unsigned mask = (bal >> (le * NQ)) & QMASK;
+      if (e0 + le < g.e_end && mask) {
+        int a, c0;
+        chunk_of<NP, W::CS>(lane - le * W::NT, a, c0);
+        delta_chunk_uniform<DIM, NP, W::CS, REC>(st_w + le * NQ * REC, mask, a, c0, s_out[w] + le * RECB);
+      }
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      int n = 0;
+      for (int le = 0; le < EPW; ++le)
+        if (e0 + le < g.e_end && ((bal >> (le * NQ)) & QMASK)) {
+          tma_store_1d(g.scratch + (size_t)(e0 + le) * RECB, s_out[w] + le * RECB,
+                       (unsigned)(RECB * sizeof(double)));
+          ++n;
+        }
+      if (n) tma_store_wait_read();
+    }
+    __syncwarp();  // staged records and output buffers are reused by the next group
+  };
+  group(grp0, std::false_type{});
+  if (has2) {
+    mbar_wait(&s_bar[w], 0);
+    group(grp0 + 1, std::true_type{});
+  }
+}
+
 // k_newton_warp3 (3D): warp-owned elements (EPW = 32 / NQ, all lanes busy in
 // phase 1 for Q1), ballot masks, phase 2 by row pairs (delta_pairs3) in
 // rounds of EPR elements.  No CTA barrier.
@@ -1016,6 +1122,11 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
     const char* v = getenv("EPFEM_FUSED");
     return !(v && v[0] == 'c' && v[1] == 't') && !getenv("EPFEM_NO_WARP3");
   }();
+  // two groups per warp with TMA prefetch of the second (2D): EPFEM_FUSED=pf
+  static const bool pf = [] {
+    const char* v = getenv("EPFEM_FUSED");
+    return v && v[0] == 'p' && v[1] == 'f';
+  }();
   // warp-specialized producer / consumer kernel (2D): EPFEM_FUSED=ws
   static const bool ws = [] {
     const char* v = getenv("EPFEM_FUSED");
@@ -1074,6 +1185,23 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
       }
     }
     if constexpr (DIM == 2) {
+      if (pf) {
+        using W = WarpCfg<DIM, NP, NQ>;
+        const int64_t per = 2 * (int64_t)W::EPW * PFW;
+        const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
+        switch (model) {
+          case EPFEM_MODEL_VON_MISES:
+            k_newton_warp_pf<EPFEM_MODEL_VON_MISES, NP, NQ><<<blocks, 32 * PFW, 0, st>>>(c, g);
+            break;
+          case EPFEM_MODEL_DRUCKER_PRAGER:
+            k_newton_warp_pf<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ><<<blocks, 32 * PFW, 0, st>>>(c, g);
+            break;
+          default:
+            k_newton_warp_pf<EPFEM_MODEL_ELASTIC, NP, NQ><<<blocks, 32 * PFW, 0, st>>>(c, g);
+            break;
+        }
+        return;
+      }
       if (ws) {
         switch (model) {
           case EPFEM_MODEL_VON_MISES: rc = launch_ws<EPFEM_MODEL_VON_MISES, NP, NQ>(c, g, st); break;

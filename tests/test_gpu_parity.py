@@ -469,7 +469,7 @@ def test_full_size_pattern_and_properties(cuda, name):
 # ---------------------------------------------------------------------------
 # opt-in kernel variants (EPFEM_FUSED, read once per process): each in a
 # fresh interpreter, same bar as the default path
-@pytest.mark.parametrize("variant,name", [("mma", "cfg2"), ("mma", "cfg3"), ("mma", "cfg4"), ("ws", "cfg2"), ("cta", "cfg3"),
+@pytest.mark.parametrize("variant,name", [("mma", "cfg2"), ("mma", "cfg3"), ("mma", "cfg4"), ("ws", "cfg2"), ("cta", "cfg3"), ("pf", "cfg2"),
                                           ("cta", "cfg2"), ("pipe", "cfg2"), ("pipe", "cfg4")])
 def test_kernel_variants(cuda, oracle, variant, name):
     import subprocess
