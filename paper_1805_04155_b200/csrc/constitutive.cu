@@ -26,6 +26,9 @@
 
 #include "delta.cuh"
 
+#ifndef EPFEM_CTA_PAIRS
+#define EPFEM_CTA_PAIRS 1
+#endif
 #ifndef EPFEM_TSHARED
 #define EPFEM_TSHARED 0  // 1: 3D CTA phase 2 with T_a shared through shared memory (measured slower: the per-point barriers)
 #endif
@@ -372,6 +375,22 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DeltaCfg<DIM, 
   if constexpr (DIM == 3) {
     __shared__ double s_T[EPB][NP][DIM * Cfg::NS];
     delta_phase2_tshared<DIM, NP, NQ>(s_st, s_mask, s_T, tid, blockDim.x, e0, g.e_end, g.scratch);
+    return;
+  }
+#endif
+#if EPFEM_CTA_PAIRS
+  // 3D (not Q2-20): phase 2 by balanced row pairs (delta_pairs3): every T
+  // entry and block entry computed once (cfg4: 1,404 instead of 2,592 FMA per
+  // plastic point)
+  if constexpr (DIM == 3 && NP < 20) {
+    using PC = Pair3Cfg<NP, NQ>;
+    for (int t = tid; t < EPB * PC::PL; t += blockDim.x) {
+      const int le = t / PC::PL, k = t - (t / PC::PL) * PC::PL;
+      const int64_t e = e0 + le;
+      const unsigned mask = s_mask[le];
+      if (e < g.e_end && mask)
+        delta_pairs3<NP, NQ>(&s_st[le][0][0], mask, k / 3, k % 3, g.scratch + (size_t)e * Cfg::NB * Cfg::D2);
+    }
     return;
   }
 #endif

@@ -60,10 +60,10 @@ struct DeltaCfg {
   static constexpr int EPB = (E1 < E2 ? E1 : E2) > 0 ? (E1 < E2 ? E1 : E2) : 1;
   static constexpr int THREADS = ((EPB * TPE + 31) / 32) * 32;
   // CTA-kernel phase 2 sub-pass width and minimum CTAs per SM (measured on
-  // B200: 3D Q1 / P2 tet fastest at SUB = 2 with <= 102 registers; Q2-20 with
+  // B200: 3D Q1 / P2 tet with row-pair phase 2 at <= 128 registers; Q2-20 with
   // whole chunks and ptxas' own register choice; 2D: 1024 threads per SM)
 #ifndef EPFEM_MINB3
-#define EPFEM_MINB3 5
+#define EPFEM_MINB3 4
 #endif
   static constexpr int SUB = (DIM == 3 && NP < 20) ? 2 : 0;
   static constexpr int MINB = DIM == 2 ? 1024 / THREADS : (NP < 20 ? EPFEM_MINB3 : 0);
