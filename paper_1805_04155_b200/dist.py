@@ -125,10 +125,22 @@ def make_plan(family: str, dim: int, n: int, world: int, rank: int) -> SlabPlan:
                     halo * per_layer, per_layer, nq)
 
 
-def exchange_interface(plan: SlabPlan, flags, D, group=None):
+def finish_exchange(pending):
+    """Complete exchange_interface(..., wait=False): wait (a stream wait for
+    NCCL) and copy any staged receive buffers into place."""
+    reqs, recv = pending
+    for req in reqs:
+        req.wait()
+    for dst, buf in recv:
+        if dst.data_ptr() != buf.data_ptr():
+            dst.copy_(buf)
+
+
+def exchange_interface(plan: SlabPlan, flags, D, group=None, wait=True):
     """Send the top layer's (flags, D) to rank + 1 and receive the halo
     layer's from rank - 1, in place (torch tensors on the process group's
-    device: CUDA with NCCL, CPU with gloo)."""
+    device: CUDA with NCCL, CPU with gloo).  wait=False returns the pending
+    exchange for finish_exchange()."""
     import torch.distributed as dist
     ops = []
     s0, s1 = plan.send_points
@@ -145,12 +157,10 @@ def exchange_interface(plan: SlabPlan, flags, D, group=None):
         ops.append(dist.P2POp(dist.irecv, rf, plan.rank - 1, group))
         ops.append(dist.P2POp(dist.irecv, rd, plan.rank - 1, group))
         recv = [(fb, rf), (db, rd)]
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
-    for dst, buf in recv:
-        if dst.data_ptr() != buf.data_ptr():
-            dst.copy_(buf)
+    reqs = dist.batch_isend_irecv(ops) if ops else []
+    if not wait:
+        return reqs, recv
+    finish_exchange((reqs, recv))
 
 
 class DistributedTangent:
@@ -169,6 +179,7 @@ class DistributedTangent:
         self.cache = api.build_assembly_cache(api.Mesh.from_structured(plan.mesh, device), self.mat_ext)
         p0, p1 = plan.own_points
         self.mat_own = mat_factory(p1 - p0)
+        self._mat_factory = mat_factory
         self.ctx = api.Context(device.index or 0, synchronous=False)
         self.S = torch.empty((n_ext, 6), dtype=torch.float64, device=device)
         self.flags = torch.zeros((n_ext,), dtype=torch.uint8, device=device)
@@ -183,24 +194,48 @@ class DistributedTangent:
         element deltas on its own elements (epfem_newton_range), interface
         exchange, deltas of the halo elements from the received flags + D
         (epfem_delta_range), then the row stream over the extended slab.
+        The top cell layer (the data rank + 1 needs) is updated first, so the
+        NCCL exchange — which torch runs on its own stream after the work
+        already queued — overlaps the update of the interior layers.
         Returns this rank's S, flag bytes and owned K values."""
-        self.update_own(E_own, Ep_own, Hard_own)
-        exchange_interface(self.plan, self.flags, self.D, self.group)
+        n_e = self.plan.mesh.n_elements
+        top = max(self.plan.halo_elems, n_e - self.plan.layer_elems)
+        if self.plan.rank + 1 < self.plan.world and top > self.plan.halo_elems:
+            self.update_own(E_own, Ep_own, Hard_own, (top, n_e))
+            reqs = exchange_interface(self.plan, self.flags, self.D, self.group, wait=False)
+            self.update_own(E_own, Ep_own, Hard_own, (self.plan.halo_elems, top))
+            finish_exchange(reqs)
+        else:
+            self.update_own(E_own, Ep_own, Hard_own)
+            exchange_interface(self.plan, self.flags, self.D, self.group)
         return self.assemble()
 
-    def update_own(self, E_own, Ep_own=None, Hard_own=None):
+    def update_own(self, E_own, Ep_own=None, Hard_own=None, elems=None):
+        """epfem_newton_range on own elements [e0, e1) (default: all own)."""
         import ctypes as C
 
         from . import api
-        p0, p1 = self.plan.own_points
+        h_e, n_e = self.plan.halo_elems, self.plan.mesh.n_elements
+        e0, e1 = elems if elems is not None else (h_e, n_e)
+        nq = self.plan.n_q
+        p0, q0, q1 = self.plan.own_points[0], e0 * nq, e1 * nq  # extended-mesh points
+        o0, o1 = q0 - p0, q1 - p0                                # offsets in the own arrays
         out = api.L.ConstitutiveOut()
-        out.S, out.flags, out.D = (api._ptr(self.S[p0:p1]), api._ptr(self.flags[p0:p1]),
-                                   api._ptr(self.D[p0:p1]))
-        mv = self.mat_own.view()
+        out.S, out.flags, out.D = (api._ptr(self.S[q0:q1]), api._ptr(self.flags[q0:q1]),
+                                   api._ptr(self.D[q0:q1]))
+        mat = self.mat_own if (o0, o1) == (0, self.mat_own.n_int) else self._mat_part(o1 - o0)
+        mv = mat.view()
+        sl = (lambda x: None if x is None else x[o0:o1])
         self.ctx.use_current_stream()
         api._check(api.L.lib().epfem_newton_range(
-            self.ctx.handle, self.cache.handle, C.byref(mv), api._ptr(E_own), api._ptr(Ep_own),
-            api._ptr(Hard_own), C.byref(out), self.plan.halo_elems, self.plan.mesh.n_elements))
+            self.ctx.handle, self.cache.handle, C.byref(mv), api._ptr(sl(E_own)), api._ptr(sl(Ep_own)),
+            api._ptr(sl(Hard_own)), C.byref(out), e0, e1))
+
+    def _mat_part(self, n):
+        cache = self.__dict__.setdefault("_mat_parts", {})
+        if n not in cache:
+            cache[n] = self._mat_factory(n)
+        return cache[n]
 
     def assemble(self):
         from . import api
