@@ -482,10 +482,10 @@ def main():
             dom_bytes, dom_ms, dom = cons_b, tot_c / reps, "k_newton_fused (constitutive + element delta)"
     else:
         dom_bytes, dom_ms, dom = asm_b, ms_per_step, "k_gather<elastic> (K5)"
-    # SURVEY §8(f) rank 1, 2D: the same step from nodal displacements with the
+    # SURVEY §8(f) rank 1: the same step from nodal displacements with the
     # strains formed inside the constitutive kernel, vs strains + step
     from_u = None
-    if not elastic and cfg.dim == 2:
+    if not elastic:
         from paper_1805_04155_b200.synthetic import displacement
         u = (wl.scale * torch.from_numpy(displacement(wl.mesh.coord, cfg.seed)).to(dev)).contiguous()
         Etmp = torch.empty_like(E)

@@ -197,7 +197,7 @@ int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* cache, const epfem_mate
 /* The same step from nodal displacements: the strains
  * E = B u (assembly.cpp:135-146, epfem_strains) are formed inside the
  * constitutive kernel, never stored unless E_out != NULL (n_int x 6).  Same
- * bits as epfem_strains followed by epfem_newton_step.  2D meshes. */
+ * bits as epfem_strains followed by epfem_newton_step. */
 int epfem_newton_step_u(epfem_ctx* ctx, const epfem_cache* cache, const epfem_material* mat,
                         const double* u, const double* Ep_prev, const double* Hard_prev,
                         const epfem_constitutive_out* out, double* E_out, double* K_values);

@@ -638,7 +638,7 @@ class TangentEngine:
 
     def step_u(self, u: torch.Tensor, Ep: Optional[torch.Tensor] = None,
                Hard: Optional[torch.Tensor] = None, E_out: Optional[torch.Tensor] = None):
-        """The step from nodal displacements (2D): E = B u is formed inside
+        """The step from nodal displacements: E = B u is formed inside
         the constitutive kernel (epfem_newton_step_u); same bits as
         cache.strains(u) followed by step()."""
         _check(L.lib().epfem_newton_step_u(self.ctx.handle, self.cache.handle, C.byref(self._mv),

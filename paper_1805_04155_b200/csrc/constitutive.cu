@@ -115,6 +115,37 @@ struct RegEIn {
   __device__ __forceinline__ void ep(int64_t q, double* v) const { load6(Ep, q, v); }
   __device__ __forceinline__ void hard(int64_t q, double* v) const { load6(H, q, v); }
 };
+// K8 at point m of element e for the strain-fused kernels: dphi of every
+// node into the staged record st (for phase 2), E = B u into e6 (and E_out).
+template <int DIM, int NP>
+__device__ __forceinline__ void strain_point(const GatherArgs& g, int64_t e, int q, int64_t m, double* st,
+                                             double* e6) {
+  constexpr int D2 = DIM * DIM;
+  double J[D2];
+#pragma unroll
+  for (int k = 0; k < D2; ++k) J[k] = __ldg(g.inv + m * D2 + k);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) e6[k] = 0.0;
+#pragma unroll 4
+  for (int p = 0; p < NP; ++p) {
+    const int32_t node = __ldg(g.elem + e * NP + p);
+    double d[DIM], uu[DIM];
+    point_dphi<DIM>(J, g.gradhat + (q * NP + p) * DIM, d);
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) {
+      uu[i] = __ldg(g.u + (int64_t)DIM * node + i);
+      st[p * DIM + i] = d[i];
+    }
+    strain_accumulate<DIM>(d, uu, e6);
+  }
+  if (g.E_out) {
+    double2* o = reinterpret_cast<double2*>(g.E_out + 6 * m);
+    o[0] = make_double2(e6[0], e6[1]);
+    o[1] = make_double2(e6[2], e6[3]);
+    o[2] = make_double2(e6[4], e6[5]);
+  }
+}
+
 struct SmemIn {
   const double* E;
   const double* Ep;
@@ -339,7 +370,7 @@ __global__ void __launch_bounds__(256) k_constitutive(ConstArgs a) {
 // minBlocks: 1024 threads/SM in 2D (caps at 64 registers, measured faster); 0 in 3D
 // leaves ptxas its own heuristic (126 registers; an explicit 1 gives 144 and
 // is ~15% slower on cfg4).
-template <int MODEL, int DIM, int NP, int NQ>
+template <int MODEL, int DIM, int NP, int NQ, bool FROM_U = false>
 __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DeltaCfg<DIM, NP, NQ>::MINB)
     k_newton_fused(ConstArgs c, GatherArgs g) {
   pdl_trigger();
@@ -362,12 +393,22 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DeltaCfg<DIM, 
     if (e >= g.e_end) continue;
     const int64_t m = e * NQ + q;
     double* st = s_st[le][q];
-    auto stage = [&](auto&& f) {
-      atomicOr(&s_mask[le], 1u << q);
-      stage_geometry<DIM, NP>(st, g.inv + m * Cfg::D2, g.gradhat, q);
-      stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f);
-    };
-    eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
+    if constexpr (FROM_U) {
+      double e6[6];
+      strain_point<DIM, NP>(g, e, q, m, st, e6);
+      auto stage = [&](auto&& f) {
+        atomicOr(&s_mask[le], 1u << q);
+        stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f);
+      };
+      eval_point<MODEL>(c, m, RegEIn{e6, c.Ep, c.Hard}, stage);
+    } else {
+      auto stage = [&](auto&& f) {
+        atomicOr(&s_mask[le], 1u << q);
+        stage_geometry<DIM, NP>(st, g.inv + m * Cfg::D2, g.gradhat, q);
+        stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f);
+      };
+      eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
+    }
   }
   __syncthreads();
   if (tid < EPB && e0 + tid < g.e_end) g.emask[e0 + tid] = s_mask[tid];
@@ -663,7 +704,7 @@ __global__ void __launch_bounds__(32 * PFW, EPFEM_WARP_MINB * 4 / 3)
 #ifndef EPFEM_WARP3_MINB
 #define EPFEM_WARP3_MINB 4
 #endif
-template <int MODEL, int NP, int NQ>
+template <int MODEL, int NP, int NQ, bool FROM_U = false>
 __global__ void __launch_bounds__(Pair3Cfg<NP, NQ>::THREADS, EPFEM_WARP3_MINB)
     k_newton_warp3(ConstArgs c, GatherArgs g) {
   pdl_trigger();
@@ -687,11 +728,18 @@ __global__ void __launch_bounds__(Pair3Cfg<NP, NQ>::THREADS, EPFEM_WARP3_MINB)
     if (e < g.e_end) {
       const int64_t m = e * NQ + q;
       double* st = st_w + lane * REC;
-      auto stage = [&](auto&& f) {
-        stage_geometry<DIM, NP>(st, g.inv + m * W::D2, g.gradhat, q);
-        stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f);
-      };
-      plastic = eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
+      if constexpr (FROM_U) {
+        double e6[6];
+        strain_point<DIM, NP>(g, e, q, m, st, e6);
+        auto stage = [&](auto&& f) { stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f); };
+        plastic = eval_point<MODEL>(c, m, RegEIn{e6, c.Ep, c.Hard}, stage);
+      } else {
+        auto stage = [&](auto&& f) {
+          stage_geometry<DIM, NP>(st, g.inv + m * W::D2, g.gradhat, q);
+          stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f);
+        };
+        plastic = eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
+      }
     }
   }
   const unsigned bal = __ballot_sync(0xffffffffu, plastic);
@@ -1086,10 +1134,39 @@ static int launch_pipe(const ConstArgs& c, const GatherArgs& g, cudaStream_t st)
 int launch_newton_fused_u(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
                           cudaStream_t st) {
   if (g.e_end <= g.e_begin) return 0;
-  if (dim != 2) return fail(EPFEM_ERR_INVALID, "newton_step_u: 2D meshes only (3D: epfem_strains + epfem_newton_step)");
   bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
     constexpr int DIM = decltype(D)::value;
     constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
+    if constexpr (DIM == 3 && NP < 20 && NP != 8) {  // tetrahedra: warp kernel (as launch_newton_fused)
+      using W = Pair3Cfg<NP, NQ>;
+      const int64_t per = (int64_t)W::EPW * W::WPB;
+      const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
+      switch (model) {
+        case EPFEM_MODEL_VON_MISES:
+          k_newton_warp3<EPFEM_MODEL_VON_MISES, NP, NQ, true><<<blocks, W::THREADS, 0, st>>>(c, g);
+          break;
+        case EPFEM_MODEL_DRUCKER_PRAGER:
+          k_newton_warp3<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ, true><<<blocks, W::THREADS, 0, st>>>(c, g);
+          break;
+        default:
+          k_newton_warp3<EPFEM_MODEL_ELASTIC, NP, NQ, true><<<blocks, W::THREADS, 0, st>>>(c, g);
+          break;
+      }
+    } else if constexpr (DIM == 3) {  // hexahedra: CTA kernel
+      using Cfg = DeltaCfg<DIM, NP, NQ>;
+      const unsigned blocks = (unsigned)((g.e_end - g.e_begin + Cfg::EPB - 1) / Cfg::EPB);
+      switch (model) {
+        case EPFEM_MODEL_VON_MISES:
+          k_newton_fused<EPFEM_MODEL_VON_MISES, DIM, NP, NQ, true><<<blocks, Cfg::THREADS, 0, st>>>(c, g);
+          break;
+        case EPFEM_MODEL_DRUCKER_PRAGER:
+          k_newton_fused<EPFEM_MODEL_DRUCKER_PRAGER, DIM, NP, NQ, true><<<blocks, Cfg::THREADS, 0, st>>>(c, g);
+          break;
+        default:
+          k_newton_fused<EPFEM_MODEL_ELASTIC, DIM, NP, NQ, true><<<blocks, Cfg::THREADS, 0, st>>>(c, g);
+          break;
+      }
+    }
     if constexpr (DIM == 2) {
       using W = WarpCfg<DIM, NP, NQ>;
       const int64_t per = (int64_t)W::EPW * W::WPB;
