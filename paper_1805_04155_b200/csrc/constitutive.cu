@@ -26,6 +26,9 @@
 
 #include "delta.cuh"
 
+#ifndef EPFEM_WARP_PAIRS
+#define EPFEM_WARP_PAIRS 1  // 2D warp kernel: phase 2 by row pairs
+#endif
 #ifndef EPFEM_CTA_PAIRS
 #define EPFEM_CTA_PAIRS 1
 #endif
@@ -559,7 +562,19 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
   const unsigned bal = __ballot_sync(0xffffffffu, plastic);
   __syncwarp();
   if (lane < EPW && e0 + lane < g.e_end) g.emask[e0 + lane] = (bal >> (lane * NQ)) & QMASK;
+#if EPFEM_WARP_PAIRS
+  // phase 2 by row pairs: lane (element, pair, component), 2 ceil(NP/2) lanes per element
+  constexpr int PL2 = 2 * ((NP + 1) / 2);
+  for (int t = lane; t < EPW * PL2; t += 32) {  // one round except for P1 (EPW = 10)
+    const int le = t / PL2, k = t - (t / PL2) * PL2;
+    const unsigned mask = (bal >> (le * NQ)) & QMASK;
+    if (e0 + le < g.e_end && mask)
+      delta_pairs2<NP>(st_w + le * NQ * REC, mask, k / 2, k % 2, REC, s_out[w] + le * RECB);
+  }
+  if (false) {
+#else
   if (EPFEM_EXP != 1 && lane < EPW * W::NT) {
+#endif
     const int le = lane / W::NT;
     const int64_t e = e0 + le;
     const unsigned mask = (bal >> (le * NQ)) & QMASK;

@@ -591,6 +591,64 @@ __device__ __forceinline__ void delta_pairs3(const double* st_e, unsigned mask, 
   }
 }
 
+// 2D row pairs (delta_pairs3's scheme with dim 2): lane (element, pair p,
+// component i) owns row i of block rows p and NP - 1 - p; 2 * ceil(NP / 2)
+// lanes per element (8 for Q2-8), NP + 1 blocks per lane, optimal FMA count.
+// Per-entry sequences are delta_phase2's, so the bits are identical.
+template <int NP>
+__device__ __forceinline__ void delta_pairs2(const double* st_e, unsigned mask, int p, int i, int REC,
+                                             double* __restrict__ rec) {
+  constexpr int NS = 3, D2 = 4, NBLK = NP + 1;
+  const int a0 = p, a1 = NP - 1 - p;
+  const bool twin = a1 != a0;
+  // T row i (delta_phase2): i = 0: g0 Dw(0, c) then g1 Dw(2, c); i = 1: g1 Dw(1, c) then g0 Dw(2, c)
+  auto pk = [](int r, int c) {
+    const int lo = r < c ? r : c, hi = r < c ? c : r;
+    return lo * NS - lo * (lo - 1) / 2 + (hi - lo);
+  };
+  double acc[NBLK][2];
+#pragma unroll
+  for (int k = 0; k < NBLK; ++k) acc[k][0] = acc[k][1] = 0.0;
+  while (mask) {
+    const int q = __ffs(mask) - 1;
+    mask &= mask - 1u;
+    const double* st = st_e + q * REC;
+    const double* dw = st + NP * 2;
+    double T0[NS], T1[NS];
+    {
+      const double gA0 = st[a0 * 2 + i], gA1 = st[a0 * 2 + (1 - i)];
+      const double gB0 = st[a1 * 2 + i], gB1 = st[a1 * 2 + (1 - i)];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        const double w0 = dw[pk(i, c)], w1 = dw[pk(2, c)];
+        T0[c] = __fma_rn(gA1, w1, __dmul_rn(gA0, w0));
+        T1[c] = __fma_rn(gB1, w1, __dmul_rn(gB0, w0));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NBLK; ++k) {
+      const bool first = k < NP - a0;
+      const int b = first ? a0 + k : a1 + (k - (NP - a0));
+      const bool ok = first || (twin && k - (NP - a0) < NP - a1);
+      const double* T = first ? T0 : T1;
+      const double* h = st + (ok ? b : NP - 1) * 2;
+      const double h0 = h[0], h1 = h[1];
+      acc[k][0] = __fma_rn(T[2], h1, __fma_rn(T[0], h0, acc[k][0]));
+      acc[k][1] = __fma_rn(T[2], h0, __fma_rn(T[1], h1, acc[k][1]));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NBLK; ++k) {
+    const bool first = k < NP - a0;
+    const int b = first ? a0 + k : a1 + (k - (NP - a0));
+    const bool ok = first || (twin && k - (NP - a0) < NP - a1);
+    if (!ok) continue;
+    double* o = rec + blk_index<NP>(first ? a0 : a1, b) * D2 + i * 2;
+    o[0] = acc[k][0];
+    o[1] = acc[k][1];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Tensor-core phase 2: dK_e = sum_q B_q^T (Dw_q B_q) on the FP64 tensor pipe
 // (mma.sync m8n8k4 f64, SASS DMMA.8x8x4; B200 runs it at the vector-FP64

@@ -134,14 +134,13 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS) k_delta_warp(Gath
   const unsigned bal = __ballot_sync(0xffffffffu, plastic);
   __syncwarp();
   if (lane < EPW && e0 + lane < a.e_end) a.emask[e0 + lane] = (bal >> (lane * NQ)) & QMASK;
-  if (lane < EPW * W::NT) {
-    const int le = lane / W::NT;
+  // phase 2 by row pairs (as k_newton_warp)
+  constexpr int PL2 = 2 * ((NP + 1) / 2);
+  for (int t = lane; t < EPW * PL2; t += 32) {
+    const int le = t / PL2, k = t - (t / PL2) * PL2;
     const unsigned mask = (bal >> (le * NQ)) & QMASK;
-    if (e0 + le < a.e_end && mask) {
-      int pa, c0;
-      chunk_of<NP, W::CS>(lane - le * W::NT, pa, c0);
-      delta_chunk_uniform<DIM, NP, W::CS, REC>(st_w + le * NQ * REC, mask, pa, c0, s_out[w] + le * RECB);
-    }
+    if (e0 + le < a.e_end && mask)
+      delta_pairs2<NP>(st_w + le * NQ * REC, mask, k / 2, k % 2, REC, s_out[w] + le * RECB);
   }
   fence_proxy_async_smem();
   __syncwarp();
