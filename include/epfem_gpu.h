@@ -172,6 +172,13 @@ int epfem_cache_K_elast(const epfem_cache* cache, const double** values);
 int epfem_cache_geometry(const epfem_cache* cache, const double** det,
                          const double** weight, const double** inv);
 
+/* The tangent workspace of the last step (introspection for tests): the
+ * symmetric element deltas dK_e (record_doubles per element, blocks (a, b),
+ * a <= b, row-major dim x dim) and the per-element plastic-point bitmask.
+ * Records of elements whose mask is 0 are stale. */
+int epfem_cache_workspace(const epfem_cache* cache, const double** records, const unsigned** emask,
+                          int64_t* record_doubles);
+
 /* K5 recomputed into K_values (nnz doubles) (assembly.cpp:258-260). */
 int epfem_assemble_elastic(epfem_ctx* ctx, const epfem_cache* cache, double* K_values);
 

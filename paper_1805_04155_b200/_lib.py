@@ -52,6 +52,7 @@ EXPORTS = [
     "epfem_ctx_set_sync", "epfem_ctx_sync", "epfem_ctx_destroy", "epfem_elastic_moduli",
     "epfem_dp_parameters", "epfem_constitutive", "epfem_cache_build", "epfem_cache_destroy",
     "epfem_cache_get_info", "epfem_cache_pattern", "epfem_cache_K_elast", "epfem_cache_geometry",
+    "epfem_cache_workspace",
     "epfem_assemble_elastic", "epfem_assemble_tangent", "epfem_assemble_tangent_ds",
     "epfem_newton_step", "epfem_newton_step_u", "epfem_constitutive_delta", "epfem_assemble_rows", "epfem_newton_range",
     "epfem_delta_range", "epfem_strains", "epfem_internal_forces",
@@ -87,6 +88,7 @@ def lib() -> C.CDLL:
     L.epfem_cache_pattern.argtypes = [_P, C.POINTER(_P), C.POINTER(_P)]
     L.epfem_cache_K_elast.argtypes = [_P, C.POINTER(_P)]
     L.epfem_cache_geometry.argtypes = [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P)]
+    L.epfem_cache_workspace.argtypes = [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_I64)]
     L.epfem_assemble_elastic.argtypes = [_P, _P, _P]
     L.epfem_assemble_tangent.argtypes = [_P, _P, _I64, _P, _P, _P]
     L.epfem_assemble_tangent_ds.argtypes = [_P, _P, _I64, _P, _P, _P]

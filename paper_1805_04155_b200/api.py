@@ -512,6 +512,17 @@ class AssemblyCache:
         _check(L.lib().epfem_cache_geometry(self._h, C.byref(det), C.byref(w), C.byref(inv)))
         return _tensor_view(w.value, self.n_int, torch.float64, self.device)
 
+    def workspace(self) -> tuple[torch.Tensor, torch.Tensor]:
+        """(records, emask) of the last tangent step: symmetric element deltas
+        (n_elements x record doubles) and the plastic-point bitmask per
+        element (records of elements with mask 0 are stale).  Copies."""
+        rec, em, nd = C.c_void_p(), C.c_void_p(), C.c_int64()
+        _check(L.lib().epfem_cache_workspace(self._h, C.byref(rec), C.byref(em), C.byref(nd)))
+        ne = self.info.n_elements
+        r = _tensor_view(rec.value, ne * nd.value, torch.float64, self.device).view(ne, nd.value)
+        m = _tensor_view(em.value, ne, torch.int32, self.device)
+        return r, m
+
     def strains(self, u: torch.Tensor) -> torch.Tensor:
         """E = B u, 6 x n_int with 2D rows {0,1,3} (assembly.cpp:211-222)."""
         if u.numel() != self.info.n_dofs or u.dtype != torch.float64:

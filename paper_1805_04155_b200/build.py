@@ -33,7 +33,7 @@ SOURCES = {
     "capi.cu": [],
     "tables.cpp": [],
 }
-HEADERS = ["common.cuh", "kernels.cuh", "delta.cuh", "tma.cuh"]
+HEADERS = ["common.cuh", "kernels.cuh", "delta.cuh", "tma.cuh", "rows.cuh"]
 
 
 def nvcc() -> str:

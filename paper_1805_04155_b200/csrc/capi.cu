@@ -2,7 +2,10 @@
 // assembly cache, argument validation with the reference's error texts, and
 // dispatch to the sm_100a kernels.  No CPU compute path exists: every entry
 // point fails with EPFEM_ERR_CUDA when no CUDA device is present.
+#include <algorithm>
 #include <chrono>
+#include <climits>
+#include <vector>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -60,6 +63,17 @@ struct epfem_cache {
   // needs exactly the element chunks 0..k (elements [echunk[j], echunk[j+1]))
   int n_chunks = 1;
   int64_t nchunk[kMaxChunks + 1] = {}, echunk[kMaxChunks + 1] = {};
+  // one-launch Newton step (k_newton_mega, 2D): item list, per-range group
+  // spans, per-group flags + ticket/generation words
+  int32_t* mega_sched = nullptr;
+  int32_t* mega_rlo = nullptr;
+  int32_t* mega_rhi = nullptr;
+  int* mega_flag = nullptr;
+  MegaSync* mega_sync = nullptr;
+  int64_t mega_items = 0;
+  int mega_group = 0;
+  int mega_npc = 0, mega_span = 0, mega_max_items = 0;  // node-range plan within one warp's slice
+  int mega_slice = 0, mega_workers = 0;                  // bytes of smem per warp, warps of the grid
 };
 
 namespace {
@@ -283,7 +297,8 @@ int epfem_cache_destroy(epfem_cache* c) {
   void* ptrs[] = {c->gradhat, c->wq,          c->elem,        c->det,          c->inv,
                   c->weight,  c->shear,       c->bulk,        c->pat.n2e_ptr,  c->pat.n2e,
                   c->pat.nbr_ptr, c->pat.row_ptr, c->pat.col_idx, c->pat.slot, c->K_elast,
-                  c->scratch, c->emask};
+                  c->scratch, c->emask, c->mega_sched, c->mega_rlo, c->mega_rhi, c->mega_flag,
+                  c->mega_sync};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -324,6 +339,73 @@ static GatherArgs gather_args(const epfem_cache* c) {
       g.Cu[pk_index(i, j)] = c->bulk_u * vol + 2.0 * c->shear_u * dev;
     }
   return g;
+}
+
+// Item list of the one-launch Newton step (k_newton_mega): producer groups
+// in element order, each node range placed after the last group it reads
+// plus SLACK groups (two rounds of the round-robin walk, so that the group
+// has usually finished when the range's worker gets there;
+// EPFEM_MEGA_SLACK overrides).  EPFEM_MEGA=1 enables the path.
+static int plan_mega(epfem_cache* c, cudaStream_t st) {
+  const epfem_cache_info& I = c->info;
+  int ge = 0;
+  // Opt-in (EPFEM_MEGA=1): measured on B200, cfg2, the one-launch step
+  // takes 0.55 ms against 0.357 ms for the two launches.  The warp-owned
+  // node ranges are latency-bound (0.50 ms for the row-stream role alone vs
+  // 0.169 ms for the CTA row stream) and the producer role loses ~35% to the
+  // persistent walk (0.283 vs 0.204 ms).  Kept, parity-tested, as the base
+  // for a CTA-granular consumer role.
+  static const bool off = [] {
+    const char* v = getenv("EPFEM_MEGA");
+    return !(v && v[0] == '1') || getenv("EPFEM_FUSED") != nullptr;
+  }();
+  int slice = 0, workers = 0;
+  if (off || I.n_nodes == 0 || I.n_elements == 0 || !mega_supported(I.family, I.dim, &ge, &slice, &workers))
+    return 0;
+  const int row_budget = getenv("EPFEM_MEGA_ROWB") ? atoi(getenv("EPFEM_MEGA_ROWB")) : slice;
+  if (int rc = plan_row_stream(I.n_nodes, I.dim, c->pat.nbr_ptr, c->pat.n2e_ptr, st, &c->mega_npc, &c->mega_span,
+                               &c->mega_max_items, row_budget))
+    return rc;
+  if (8 * ((size_t)c->mega_span + 2) + 4 * ((size_t)c->mega_max_items + 2 * ((size_t)c->mega_npc + 1)) >
+      (size_t)slice)
+    return 0;  // a single node's range does not fit a warp's slice: two-launch step
+  c->mega_slice = slice;
+  c->mega_workers = workers;
+  const int64_t n_groups = (I.n_elements + ge - 1) / ge;
+  const int64_t n_ranges = (I.n_nodes + c->mega_npc - 1) / c->mega_npc;
+  if (n_groups + n_ranges >= INT32_MAX) return 0;
+  int64_t slack = 2 * (int64_t)workers;  // two rounds of the worker walk
+  if (const char* v = getenv("EPFEM_MEGA_SLACK")) slack = atoi(v);
+  EPFEM_CUDA_TRY(cudaMalloc(&c->mega_rlo, sizeof(int32_t) * n_ranges));
+  EPFEM_CUDA_TRY(cudaMalloc(&c->mega_rhi, sizeof(int32_t) * n_ranges));
+  if (int rc = launch_range_groups(I.n_nodes, c->mega_npc, I.n_p, ge, c->pat.n2e_ptr, c->pat.n2e, c->mega_rlo,
+                                   c->mega_rhi, st))
+    return rc;
+  std::vector<int32_t> rhi(n_ranges);
+  EPFEM_CUDA_TRY(cudaMemcpyAsync(rhi.data(), c->mega_rhi, sizeof(int32_t) * n_ranges, cudaMemcpyDeviceToHost, st));
+  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+  std::vector<int32_t> order(n_ranges);
+  for (int64_t r = 0; r < n_ranges; ++r) order[r] = (int32_t)r;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return rhi[x] < rhi[y]; });
+  std::vector<int32_t> sched;
+  sched.reserve(n_groups + n_ranges);
+  size_t k = 0;
+  for (int64_t gi = 0; gi < n_groups; ++gi) {
+    sched.push_back((int32_t)gi);
+    while (k < order.size() && (int64_t)rhi[order[k]] + slack <= gi) sched.push_back(~order[k++]);
+  }
+  while (k < order.size()) sched.push_back(~order[k++]);
+  c->mega_items = (int64_t)sched.size();
+  c->mega_group = ge;
+  EPFEM_CUDA_TRY(cudaMalloc(&c->mega_sched, sizeof(int32_t) * sched.size()));
+  EPFEM_CUDA_TRY(cudaMemcpyAsync(c->mega_sched, sched.data(), sizeof(int32_t) * sched.size(),
+                                 cudaMemcpyHostToDevice, st));
+  EPFEM_CUDA_TRY(cudaMalloc(&c->mega_flag, sizeof(int) * n_groups));
+  EPFEM_CUDA_TRY(cudaMemsetAsync(c->mega_flag, 0, sizeof(int) * n_groups, st));
+  EPFEM_CUDA_TRY(cudaMalloc(&c->mega_sync, sizeof(MegaSync)));
+  EPFEM_CUDA_TRY(cudaMemsetAsync(c->mega_sync, 0, sizeof(MegaSync), st));
+  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));  // the host vectors go out of scope
+  return 0;
 }
 
 int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_material* mat,
@@ -436,6 +518,7 @@ int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_materi
   g.out = c->K_elast;
   if (int rc = elastic_assembly(g, I.family, I.dim, c->K_elast, st)) return bail(rc);
   CT(cudaEventRecord(ev[2], st));
+  if (int rc = plan_mega(c, st)) return bail(rc);
   CT(cudaStreamSynchronize(st));
   float ms_p = 0, ms_e = 0;
   cudaEventElapsedTime(&ms_p, ev[0], ev[1]);
@@ -460,6 +543,19 @@ int epfem_cache_pattern(const epfem_cache* c, const int64_t** row_ptr, const int
   if (!c) return fail(EPFEM_ERR_INVALID, "null cache");
   if (row_ptr) *row_ptr = c->pat.row_ptr;
   if (col_idx) *col_idx = c->pat.col_idx;
+  return 0;
+}
+
+int epfem_cache_workspace(const epfem_cache* c, const double** records, const unsigned** emask,
+                          int64_t* record_doubles) {
+  if (!c) return fail(EPFEM_ERR_INVALID, "null cache");
+  if (records) *records = c->scratch;
+  if (emask) *emask = c->emask;
+  if (record_doubles)
+    *record_doubles = c->info.n_elements > 0
+                          ? (int64_t)(tangent_workspace_doubles(c->info.family, c->info.dim, c->info.n_elements) /
+                                      (size_t)c->info.n_elements)
+                          : 0;
   return 0;
 }
 
@@ -595,6 +691,23 @@ int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* c, const epfem_material
     GatherArgs g;
     if (int rc = delta_args(ctx, c, mat, E, Ep_prev, Hard_prev, out, &a, &g)) return rc;
     if (int rc = overlapped_step(ctx, c, mat->model, a, g, K_values)) return rc;
+    return finish(ctx);
+  }
+  if (c && c->mega_items > 0) {
+    ConstArgs a;
+    GatherArgs g;
+    if (int rc = delta_args(ctx, c, mat, E, Ep_prev, Hard_prev, out, &a, &g)) return rc;
+    g.base = c->K_elast;
+    g.out = K_values;
+    g.npc = c->mega_npc;
+    g.max_span = c->mega_span;
+    g.max_items = c->mega_max_items;
+    static const int exp = getenv("EPFEM_MEGA_EXP") ? atoi(getenv("EPFEM_MEGA_EXP")) : 0;
+    MegaArgs m{c->mega_sched, c->mega_rlo, c->mega_rhi, c->mega_flag, c->mega_sync, c->mega_items,
+               c->mega_group, exp};
+    if (int rc = launch_newton_mega(mat->model, c->info.family, c->info.dim, a, g, m, c->mega_slice,
+                                    c->mega_workers, ctx->stream))
+      return rc;
     return finish(ctx);
   }
   if (int rc = delta_part(ctx, c, mat, E, Ep_prev, Hard_prev, out)) return rc;

@@ -22,9 +22,11 @@
 // points the thread also stages dphi and w (D - C) for the element delta
 // straight from registers (D is never re-read).  Phase 2 builds dK_e
 // (delta.cuh).  The row stream (tangent.cu) then assembles K.
+#include <algorithm>
+#include <climits>
 #include <type_traits>
 
-#include "delta.cuh"
+#include "rows.cuh"
 
 #ifndef EPFEM_WARP_PAIRS
 #define EPFEM_WARP_PAIRS 1  // 2D warp kernel: phase 2 by row pairs
@@ -467,27 +469,25 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DeltaCfg<DIM, 
 #ifndef EPFEM_EARLY_GEOM
 #define EPFEM_EARLY_GEOM 1
 #endif
-template <int MODEL, int NP, int NQ, bool FROM_U = false>
-__global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
-    k_newton_warp(ConstArgs c, GatherArgs g) {
-  pdl_trigger();
+// One warp's group of EPW elements starting at e0: st_w = the warp's staged
+// records (EPW * NQ * REC doubles), out_w = its element-record buffer
+// (EPW * RECB doubles, 16-byte aligned).  MEGA: the records leave through
+// plain coalesced stores (the one-launch step publishes them with a release
+// flag right after; no async-proxy writes to order).
+template <int MODEL, int NP, int NQ, bool FROM_U, bool MEGA>
+__device__ __forceinline__ void newton_warp_group(ConstArgs c, const GatherArgs& g, int64_t e0, double* st_w,
+                                                  double* out_w, int lane) {
   constexpr int DIM = 2;
   using W = WarpCfg<DIM, NP, NQ>;
   static_assert(W::EPW * NQ <= 32 && W::EPW * W::NT <= 32, "warp mapping");
   constexpr int EPW = W::EPW, REC = W::REC;
   constexpr unsigned QMASK = NQ >= 32 ? 0xffffffffu : (1u << NQ) - 1u;
   constexpr int RECB = W::NB * W::D2;  // doubles per element workspace record
-  __shared__ double s_st[W::WPB][EPW * NQ * REC];
-  __shared__ __align__(16) double s_out[W::WPB][EPW * RECB];
   c.DS = nullptr;  // hot path: S, flags, packed D only
   c.Ep_out = c.Hard_out = nullptr;
   c.pm = c.sm = c.am = nullptr;
   c.crit = nullptr;
-
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t e0 = g.e_begin + ((int64_t)blockIdx.x * W::WPB + w) * EPW;
   if (e0 >= g.e_end) return;  // warp-uniform
-  double* st_w = s_st[w];
   bool plastic = false;
   if (lane < EPW * NQ) {
     const int le = lane / NQ, q = lane - le * NQ;
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
     const int le = t / PL2, k = t - (t / PL2) * PL2;
     const unsigned mask = (bal >> (le * NQ)) & QMASK;
     if (e0 + le < g.e_end && mask)
-      delta_pairs2<NP>(st_w + le * NQ * REC, mask, k / 2, k % 2, REC, s_out[w] + le * RECB);
+      delta_pairs2<NP>(st_w + le * NQ * REC, mask, k / 2, k % 2, REC, out_w + le * RECB);
   }
   if (false) {
 #else
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
     if (e < g.e_end && mask) {
       int a, c0;
       chunk_of<NP, W::CS>(lane - le * W::NT, a, c0);
-      double* rec = s_out[w] + le * RECB;  // staged, then one bulk store per element
+      double* rec = out_w + le * RECB;  // staged, then one bulk store per element
       if (EPFEM_EXP == 2) {  // same stores, staged values instead of the products
         const double* st = st_w + le * NQ * REC;
         for (int bb = 0; bb < W::CS && c0 + bb < NP; ++bb)
@@ -593,20 +593,40 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
   }
   // the workspace records leave through the TMA unit: whole 1-KB-class
   // records instead of 8-byte scattered stores from every lane
-  if (EPFEM_EXP != 1) {
+  if (MEGA) {
+    __syncwarp();
+    for (int le = 0; le < EPW; ++le)
+      if (e0 + le < g.e_end && ((bal >> (le * NQ)) & QMASK)) {
+        const double2* s2 = reinterpret_cast<const double2*>(out_w + le * RECB);
+        double2* d2 = reinterpret_cast<double2*>(g.scratch + (size_t)(e0 + le) * RECB);
+        for (int k = lane; k < RECB / 2; k += 32) d2[k] = s2[k];
+      }
+  } else if (EPFEM_EXP != 1) {
     fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) {
       int n = 0;
       for (int le = 0; le < EPW; ++le)
         if (e0 + le < g.e_end && ((bal >> (le * NQ)) & QMASK)) {
-          tma_store_1d(g.scratch + (size_t)(e0 + le) * RECB, s_out[w] + le * RECB,
+          tma_store_1d(g.scratch + (size_t)(e0 + le) * RECB, out_w + le * RECB,
                        (unsigned)(RECB * sizeof(double)));
           ++n;
         }
       if (n) tma_store_wait_read();
     }
   }
+}
+
+template <int MODEL, int NP, int NQ, bool FROM_U = false>
+__global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
+    k_newton_warp(ConstArgs c, GatherArgs g) {
+  pdl_trigger();
+  using W = WarpCfg<2, NP, NQ>;
+  __shared__ double s_st[W::WPB][W::EPW * NQ * W::REC];
+  __shared__ __align__(16) double s_out[W::WPB][W::EPW * W::NB * W::D2];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t e0 = g.e_begin + ((int64_t)blockIdx.x * W::WPB + w) * W::EPW;
+  newton_warp_group<MODEL, NP, NQ, FROM_U, false>(c, g, e0, s_st[w], s_out[w], lane);
 }
 
 // k_newton_warp_pf (2D, EPFEM_FUSED=pf): k_newton_warp with two element
@@ -1200,6 +1220,215 @@ int launch_newton_fused_u(int model, int family, int dim, const ConstArgs& c, co
     }
   });
   if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
+  EPFEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// k_newton_mega (2D): the whole Newton step in ONE launch.  Every warp of a
+// cooperative (all CTAs co-resident) persistent grid is an independent
+// worker walking an ordered item list round-robin (worker w takes items w,
+// w + W, w + 2W, ...): producer items are k_newton_warp's element groups
+// (fused update + element deltas), consumer items are node ranges of the
+// row stream (rows.cuh, one warp per range).  The list puts every range
+// after all the groups it reads (plus a slack), so the smallest unfinished
+// item can always progress (its worker's earlier items are finished and the
+// groups it waits on have smaller positions): no deadlock.  The roles share
+// the SMs, so the latency-bound update and the bandwidth-bound row stream
+// overlap instead of running back to back, and the element records are
+// still L2-resident when read.  A group is published with a release store
+// of the launch generation (deferred to the worker's next item, so the
+// fence finds its stores drained); a range waits with acquire loads.  The
+// last CTA to finish bumps the generation: the launch is replayable (CUDA
+// graphs) without a memset.  Same per-entry arithmetic and add order as the
+// two-launch step, hence the same bits.
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int NP, int NQ>
+struct MegaCfg {
+  using W = WarpCfg<2, NP, NQ>;
+  static constexpr int ST = ((W::EPW * NQ * W::REC + 1) / 2) * 2;  // doubles (even: 16-B aligned)
+  static constexpr int OUT = W::EPW * W::NB * W::D2;
+  static constexpr int PRODUCER = ST + OUT;                        // doubles per warp
+};
+
+template <int MODEL, int NP, int NQ>
+__global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
+    k_newton_mega(ConstArgs c, GatherArgs g, MegaArgs m, int slice) {
+  using W = WarpCfg<2, NP, NQ>;
+  using MC = MegaCfg<NP, NQ>;
+  extern __shared__ __align__(128) double dyn[];
+  __shared__ uint64_t s_bar[W::WPB];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t workers = (int64_t)gridDim.x * W::WPB;
+  double* my = dyn + (size_t)w * slice;
+  const int gen = *((volatile int*)&m.sync->gen);  // bumped only after every CTA has finished
+  if (lane == 0) {
+    mbar_init(&s_bar[w], 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  unsigned parity = 0;
+  int pending = -1;  // produced group not yet published
+  auto publish = [&] {
+    if (pending >= 0 && lane == 0) {
+      __threadfence();
+      st_release_gpu(m.flag + pending, gen + 1);
+    }
+    pending = -1;
+  };
+  for (int64_t t = (int64_t)blockIdx.x * W::WPB + w; t < m.n_items; t += workers) {
+    const int item = __ldg(m.sched + t);
+    if (item >= 0) {
+      if (m.exp != 2) {
+        newton_warp_group<MODEL, NP, NQ, false, true>(c, g, (int64_t)item * W::EPW, my, my + MC::ST, lane);
+        __syncwarp();
+      }
+      publish();
+      pending = item;
+    } else {
+      publish();
+      if (m.exp == 1) continue;
+      const int r = ~item;
+      if (row_range<2, NP, NQ, 32, true>(
+              g, g.npc, r, my, &s_bar[w], parity,
+              [&] {
+                if (m.exp == 0) {
+                  const int lo = __ldg(m.rlo + r), hi = __ldg(m.rhi + r);
+                  for (int k = lo + lane; k <= hi; k += 32)
+                    while (ld_acquire_gpu(m.flag + k) != gen + 1) __nanosleep(32);
+                }
+                __syncwarp();
+              },
+              lane))
+        parity ^= 1u;
+    }
+    // this worker's generic smem writes are next overwritten by TMA
+    fence_proxy_async_smem();
+    __syncwarp();
+  }
+  publish();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&m.sync->finished, 1) == (int)gridDim.x - 1) {
+      m.sync->finished = 0;
+      atomicAdd(&m.sync->gen, 1);
+      __threadfence();
+    }
+  }
+}
+
+// per node range: the first and last producer group whose elements touch it
+__global__ void k_range_groups(int64_t n_nodes, int npc, int np, int group_elems,
+                               const int64_t* __restrict__ n2e_ptr, const int32_t* __restrict__ n2e,
+                               int32_t* rlo, int32_t* rhi) {
+  const int64_t n_ranges = (n_nodes + npc - 1) / npc;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_ranges;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n0 = r * npc, n1 = min(n0 + (int64_t)npc, n_nodes);
+    int lo = INT32_MAX, hi = -1;
+    for (int64_t a = n0; a < n1; ++a) {
+      const int64_t b = n2e_ptr[a], e = n2e_ptr[a + 1];
+      if (e > b) {  // a node's items are sorted by element
+        lo = min(lo, (int)(n2e[b] / np / group_elems));
+        hi = max(hi, (int)(n2e[e - 1] / np / group_elems));
+      }
+    }
+    rlo[r] = lo;
+    rhi[r] = hi;
+  }
+}
+
+// group_elems: elements per producer item (one warp group); slice_bytes:
+// the per-warp shared-memory slice (at least the producer's, sized so that
+// EPFEM_WARP_MINB CTAs fit an SM); workers: warps of the co-resident grid.
+bool mega_supported(int family, int dim, int* group_elems, int* slice_bytes, int* workers) {
+  bool ok = false;
+  dispatch_element(family, dim, [&](auto F, auto D) {
+    constexpr int DIM = decltype(D)::value;
+    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
+    if constexpr (DIM == 2) {
+      using W = WarpCfg<2, NP, NQ>;
+      *group_elems = W::EPW;
+      const int per_warp = ((200 * 1024 / EPFEM_WARP_MINB) / W::WPB) & ~127;
+      const int prod = (int)(MegaCfg<NP, NQ>::PRODUCER * sizeof(double));
+      *slice_bytes = per_warp > prod ? per_warp : prod;
+      if (const char* v = getenv("EPFEM_MEGA_SLICE")) *slice_bytes = atoi(v);  // tuning / debugging
+      int per_sm = 0, dev = 0, sms = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      auto kern = k_newton_mega<EPFEM_MODEL_VON_MISES, NP, NQ>;
+      const size_t smem = (size_t)*slice_bytes * W::WPB;
+      if (smem > 48 * 1024 &&
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W::THREADS, smem) != cudaSuccess ||
+          per_sm <= 0)
+        return;
+      *workers = per_sm * sms * W::WPB;
+      ok = true;
+    }
+  });
+  cudaGetLastError();
+  return ok;
+}
+
+int launch_range_groups(int64_t n_nodes, int npc, int np, int group_elems, const int64_t* n2e_ptr,
+                        const int32_t* n2e, int32_t* rlo, int32_t* rhi, cudaStream_t st) {
+  k_range_groups<<<256, 128, 0, st>>>(n_nodes, npc, np, group_elems, n2e_ptr, n2e, rlo, rhi);
+  EPFEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int launch_newton_mega(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g, const MegaArgs& m,
+                       int slice_bytes, int workers, cudaStream_t st) {
+  if (m.n_items <= 0) return 0;
+  int rc = 0;
+  bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
+    constexpr int DIM = decltype(D)::value;
+    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
+    if constexpr (DIM == 2) {
+      using W = WarpCfg<2, NP, NQ>;
+      const size_t smem = (size_t)slice_bytes * W::WPB;
+      const int slice = slice_bytes / (int)sizeof(double);
+      auto run = [&](auto kern) {
+        if (smem > 48 * 1024) {
+          cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          if (e != cudaSuccess) { rc = cuda_fail(e, "cudaFuncSetAttribute"); return; }
+        }
+        // cooperative: every CTA co-resident (the item walk relies on it)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(workers / W::WPB));
+        cfg.blockDim = dim3(W::THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, c, g, m, slice);
+        if (e != cudaSuccess) rc = cuda_fail(e, "one-launch Newton step");
+      };
+      switch (model) {
+        case EPFEM_MODEL_VON_MISES: run(k_newton_mega<EPFEM_MODEL_VON_MISES, NP, NQ>); break;
+        case EPFEM_MODEL_DRUCKER_PRAGER: run(k_newton_mega<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ>); break;
+        default: run(k_newton_mega<EPFEM_MODEL_ELASTIC, NP, NQ>); break;
+      }
+    } else {
+      rc = fail(EPFEM_ERR_INVALID, "one-launch Newton step: 2D meshes only");
+    }
+  });
+  if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
+  if (rc) return rc;
   EPFEM_CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -61,6 +61,27 @@ struct GatherArgs {
   const double* u;
   double* E_out;
 };
+// One-launch Newton step (k_newton_mega): an ordered item list of producer
+// groups (>= 0: one warp group of EPW elements through the fused update) and
+// node ranges (< 0: ~range through the row stream), walked round-robin by
+// the warps of a cooperative grid; a range sits after every group it reads;
+// per-group ready flags carry the launch generation.
+struct MegaSync {
+  int ticket;    // unused (static round-robin walk)
+  int finished;  // CTAs done in this launch
+  int gen;       // launch generation (flags of this launch read gen + 1)
+  int pad;
+};
+struct MegaArgs {
+  const int32_t* sched;  // item list
+  const int32_t* rlo;    // per node range: first / last producer group it reads
+  const int32_t* rhi;
+  int* flag;             // per producer group: generation that completed it
+  MegaSync* sync;
+  int64_t n_items;
+  int group_elems;       // elements per producer group
+  int exp;               // timing experiments (EPFEM_MEGA_EXP): 1 = ranges skipped, 2 = groups skipped, no waits
+};
 struct PatternOut {
   int64_t* n2e_ptr = nullptr;
   int32_t* n2e = nullptr;
@@ -90,9 +111,14 @@ int launch_newton_fused_u(int model, int family, int dim, const ConstArgs& c, co
                           cudaStream_t st);  // E = B u inside (GatherArgs::u)
 int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
                         cudaStream_t st);
+bool mega_supported(int family, int dim, int* group_elems, int* slice_bytes, int* workers);
+int launch_newton_mega(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
+                       const MegaArgs& m, int slice_bytes, int workers, cudaStream_t st);
+int launch_range_groups(int64_t n_nodes, int npc, int np, int group_elems, const int64_t* n2e_ptr,
+                        const int32_t* n2e, int32_t* rlo, int32_t* rhi, cudaStream_t st);
 size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements);
 int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
-                    cudaStream_t st, int* npc_out, int* span_out, int* items_out);
+                    cudaStream_t st, int* npc_out, int* span_out, int* items_out, int budget_bytes = 0);
 int plan_chunks(int64_t n_nodes, int64_t n_elements, int np, const int64_t* n2e_ptr,
                 const int32_t* n2e, int npc, int n_chunks, int64_t* nchunk, int64_t* echunk,
                 cudaStream_t st);

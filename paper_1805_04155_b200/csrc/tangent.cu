@@ -20,12 +20,7 @@
 // at the cached slots (one warp per node: a single writer per row); one TMA
 // bulk store writes the image to K[range].  Rows without plastic
 // contributions are therefore bitwise copies of K_elast.
-#include "delta.cuh"
-
-#ifndef EPFEM_K_EVICT_FIRST
-#define EPFEM_K_EVICT_FIRST 1  // 3D Q1 / P2: K_elast and K streamed through L2 with evict_first (measured
-                               // cfg3 row stream 3.08 -> 2.97 ms, cfg4 3.76 -> 3.66; neutral or worse in 2D / Q2-20)
-#endif
+#include "rows.cuh"
 
 namespace epfem_gpu {
 
@@ -212,122 +207,19 @@ __global__ void __launch_bounds__(MmaCfg<DIM, NP, NQ>::THREADS) k_delta_mma(Gath
 
 constexpr int kStreamThreads = 256;
 
-// The K_elast range [v0, v1) is read with ONE TMA bulk copy of the enclosing
-// 16-byte-aligned range into the shared image (the K_elast allocation is
-// padded by two doubles), overlapped with the item staging; the image goes
-// back to K with one TMA bulk store of the aligned interior plus at most two
-// edge doubles.
+// one CTA per node range (rows.cuh); programmatic dependent launch: the
+// K_elast load and node offsets overlap the producer's tail
 template <int DIM, int NP, int NQ>
 __global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int npc) {
   extern __shared__ __align__(128) double img_raw[];
   __shared__ uint64_t s_bar;
-  constexpr int NB = NP * (NP + 1) / 2;
-  constexpr int D2 = DIM * DIM;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t n0 = a.n_begin + (int64_t)blockIdx.x * npc;
-  const int64_t n1 = min(n0 + (int64_t)npc, a.n_end);
-  const int nloc = (int)(n1 - n0);
-  const int64_t v0 = __ldg(a.nbr_ptr + n0) * D2;
-  const int64_t v1 = __ldg(a.nbr_ptr + n1) * D2;
-  const int64_t a0 = v0 & ~int64_t(1), a1 = (v1 + 1) & ~int64_t(1);
-  const int64_t i_begin = __ldg(a.n2e_ptr + n0);
-  const int nitems = (int)(__ldg(a.n2e_ptr + n1) - i_begin);
-  // layout: [image (aligned to a0) | item (int) | iptr (int) | vptr (int)]
-  double* img = img_raw + (v0 - a0);  // img[k] <-> global v0 + k
-  int* s_item = reinterpret_cast<int*>(img_raw + a.max_span + 2);
-  int* s_iptr = s_item + a.max_items;
-  int* s_vptr = s_iptr + npc + 1;
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     mbar_init(&s_bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_init_fence();
   }
   __syncthreads();
-  const bool zero_base = a.base == nullptr;  // elastic assembly: K = sum of element blocks
-  if (zero_base)
-    for (int64_t k = tid; k < a1 - a0; k += blockDim.x) img_raw[k] = 0.0;
-  if (tid == 0 && a1 > a0 && !zero_base) {
-    const unsigned bytes = (unsigned)((a1 - a0) * 8);
-    mbar_expect_tx(&s_bar, bytes);
-    if (EPFEM_K_EVICT_FIRST && DIM == 3 && NP < 20)
-      tma_load_1d_hint(img_raw, a.base + a0, bytes, &s_bar, l2_evict_first());
-    else
-      tma_load_1d(img_raw, a.base + a0, bytes, &s_bar);
-  }
-  // node offsets (cache data, independent of the producer kernel)
-  for (int k = tid; k <= nloc; k += blockDim.x) {
-    s_iptr[k] = (int)(__ldg(a.n2e_ptr + n0 + k) - i_begin);
-    s_vptr[k] = (int)(__ldg(a.nbr_ptr + n0 + k) * D2 - v0);
-  }
-  // everything below reads the producer's emask / workspace
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  // stage the range's items (plastic ones kept, others -1)
-  for (int k = tid; k < nitems; k += blockDim.x) {
-    const int32_t it = __ldg(a.n2e + i_begin + k);
-    s_item[k] = __ldcg(a.emask + it / NP) ? it : -1;
-  }
-  __syncthreads();
-  if (a1 > a0 && !zero_base) mbar_wait(&s_bar, 0);
-  // Items are taken UB at a time: every lane first issues the loads of all
-  // UB items (slot byte + workspace value), then applies the adds in item
-  // order, so a node costs one memory round trip per UB items instead of
-  // one per item (the add order, hence the bits, is unchanged).
-  constexpr int KP = (NP * D2 + 31) / 32;
-  constexpr int UB = KP == 1 ? 4 : 1;  // 3D: wider rows already give ILP; registers matter more
-  for (int ln = warp; ln < nloc; ln += kStreamThreads / 32) {
-    const int ib = s_iptr[ln], ie = s_iptr[ln + 1];
-    const int row_len = (s_vptr[ln + 1] - s_vptr[ln]) / DIM;
-    double* seg = img + s_vptr[ln];
-    for (int kb = ib; kb < ie; kb += UB) {
-      double v[UB][KP];
-      int sl[UB][KP];
-#pragma unroll
-      for (int u = 0; u < UB; ++u) {
-        const int it = kb + u < ie ? s_item[kb + u] : -1;  // warp-uniform
-        const int64_t el = it / NP;
-        const int pa = it - (int)el * NP;
-        const double* rec = a.scratch + (size_t)el * NB * D2;
-#pragma unroll
-        for (int kk = 0; kk < KP; ++kk) {
-          const int k = lane + 32 * kk;
-          sl[u][kk] = -1;
-          if (it >= 0 && k < NP * D2) {
-            // lane <-> entry (pb, i, j) of block row pa; block (pb, pa) read
-            // transposed when pb < pa (branch-free addressing)
-            const int pb = k / D2, ij = k - pb * D2;
-            const int i = ij / DIM, j = ij - i * DIM;
-            const bool up = pa <= pb;
-            const int lo = up ? pa : pb, hi = up ? pb : pa;
-            const int src = blk_index<NP>(lo, hi) * D2 + (up ? ij : j * DIM + i);
-            sl[u][kk] = __ldg(a.slot + (int64_t)it * NP + pb);
-            v[u][kk] = __ldg(rec + src);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < UB; ++u)
-#pragma unroll
-        for (int kk = 0; kk < KP; ++kk)
-          if (sl[u][kk] >= 0) {
-            const int k = lane + 32 * kk;
-            const int ij = k % D2, i = ij / DIM, j = ij - i * DIM;
-            seg[i * row_len + sl[u][kk] * DIM + j] += v[u][kk];
-          }
-      __syncwarp();
-    }
-  }
-  fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
-  __syncthreads();
-  if (tid == 0 && v1 > v0) {
-    const int64_t s0 = (v0 + 1) & ~int64_t(1), s1 = v1 & ~int64_t(1);
-    if (v0 & 1) a.out[v0] = img[0];
-    if ((v1 & 1) && v1 - 1 >= s0) a.out[v1 - 1] = img[v1 - 1 - v0];
-    if (s1 > s0) {
-      if (EPFEM_K_EVICT_FIRST && DIM == 3 && NP < 20)
-        tma_store_1d_sync_hint(a.out + s0, img + (s0 - v0), (unsigned)((s1 - s0) * 8), l2_evict_first());
-      else
-        tma_store_1d_sync(a.out + s0, img + (s0 - v0), (unsigned)((s1 - s0) * 8));
-    }
-  }
+  row_range<DIM, NP, NQ, kStreamThreads, false>(a, npc, blockIdx.x, img_raw, &s_bar, 0u,
+                                               [] { asm volatile("griddepcontrol.wait;" ::: "memory"); });
 }
 
 __global__ void k_range_span(int64_t n_nodes, int npc, int d2, const int64_t* __restrict__ nbr_ptr,
@@ -404,12 +296,14 @@ size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements) {
 // Nodes per CTA for the row stream: the largest power of two <= 64 whose
 // widest value range and item list fit the shared-memory budget.
 int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
-                    cudaStream_t st, int* npc_out, int* span_out, int* items_out) {
+                    cudaStream_t st, int* npc_out, int* span_out, int* items_out, int budget_bytes) {
   // bytes of dynamic smem per CTA and the starting node count; EPFEM_ROW_KB /
-  // EPFEM_ROW_NPC override them for tuning runs
+  // EPFEM_ROW_NPC override them for tuning runs (budget_bytes > 0: the
+  // caller's budget, e.g. one warp's slice in the one-launch step)
   int budget = (dim == 2 ? 100 : 40) * 1024;  // measured optimum (2D: 32 nodes, Q1 hex: 16)
   int npc = 32;
   if (const char* v = getenv("EPFEM_ROW_KB")) budget = atoi(v) * 1024;
+  if (budget_bytes > 0) budget = budget_bytes;
   if (const char* v = getenv("EPFEM_ROW_NPC")) npc = atoi(v);
   int* d = nullptr;
   EPFEM_CUDA_TRY(cudaMalloc(&d, 2 * sizeof(int)));
@@ -438,8 +332,7 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
     constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
     const int64_t rblocks = (a.n_end - a.n_begin + a.npc - 1) / a.npc;
     if (rblocks <= 0) return;
-    const size_t smem = sizeof(double) * ((size_t)a.max_span + 2) +
-                        sizeof(int) * ((size_t)a.max_items + 2 * ((size_t)a.npc + 1));
+    const size_t smem = row_range_smem(a);
     auto kern = k_row_stream<DIM, NP, NQ>;
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

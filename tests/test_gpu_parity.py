@@ -477,11 +477,19 @@ def test_full_size_pattern_and_properties(cuda, name):
 # opt-in kernel variants (EPFEM_FUSED, read once per process): each in a
 # fresh interpreter, same bar as the default path
 @pytest.mark.parametrize("variant,name", [("mma", "cfg2"), ("mma", "cfg3"), ("mma", "cfg4"), ("ws", "cfg2"), ("cta", "cfg3"), ("pf", "cfg2"),
-                                          ("cta", "cfg2"), ("pipe", "cfg2"), ("pipe", "cfg4")])
+                                          ("cta", "cfg2"), ("pipe", "cfg2"), ("pipe", "cfg4"),
+                                          ("MEGA=1", "cfg2"), ("MEGA=1,MEGA_SLACK=0", "cfg2"),
+                                          ("MEGA=1,MEGA_SLACK=4", "cfg2")])
 def test_kernel_variants(cuda, oracle, variant, name):
+    """EPFEM_FUSED variants, and the one-launch step (MEGA=1), also with a
+    small MEGA_SLACK (node ranges right behind their producer groups in the
+    walk, so they wait on the ready flags)."""
     import subprocess
     import sys
-    env = dict(os.environ, EPFEM_FUSED=variant)
+    if "=" in variant:
+        env = dict(os.environ, **{"EPFEM_" + kv.split("=")[0]: kv.split("=")[1] for kv in variant.split(",")})
+    else:
+        env = dict(os.environ, EPFEM_FUSED=variant)
     n = {"cfg2": 24, "cfg3": 4, "cfg4": 6}[name]
     r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "variant_check.py"), name,
                         str(n)], env=env, capture_output=True, text=True, timeout=600)

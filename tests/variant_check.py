@@ -62,7 +62,8 @@ def main(name, n):
     S2, f2, D2, K2 = sep.step(Et)
     sep.sync()
     assert np.array_equal(K2.cpu().numpy().view(np.uint64), Kv.cpu().numpy().view(np.uint64))
-    print(f"OK {os.environ.get('EPFEM_FUSED', 'default')} {name} n={n} plastic={pl.mean():.2f} err={err:.2e}")
+    tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("EPFEM_")) or "default"
+    print(f"OK {tag} {name} n={n} plastic={pl.mean():.2f} err={err:.2e}")
 
 
 if __name__ == "__main__":
