@@ -4,7 +4,7 @@ and friends per kernel, averaged) and/or a --set full report (key raw
 metrics per profiled kernel).  Prints markdown.
 
     python tools/ncu_summary.py --launches gpurun_out/launches.csv
-    python tools/ncu_summary.py --report gpurun_out/prof.ncu-rep
+    python tools/ncu_summary.py --report gpurun_out/prof.ncu-rep   (or its --page raw --csv export)
 """
 import argparse
 import collections
@@ -22,6 +22,8 @@ KEYS = [
     ("launch__registers_per_thread", "regs/thread"),
     ("smsp__inst_executed.sum", "warp instructions"),
     ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "FP64 pipe %"),
+    ("launch__occupancy_limit_registers", "CTAs/SM (register limit)"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
     ("lts__t_bytes.sum", "L2 bytes"),
     ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall long-scoreboard"),
     ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "stall barrier"),
@@ -54,8 +56,11 @@ def launches(path):
 
 
 def report(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if path.endswith(".csv"):  # `ncu -i <rep> --page raw --csv` exported on the GPU box
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     print("| metric | " + " | ".join(f"`{r[hdr.index('Kernel Name')].split('(')[0][:48]}`"
