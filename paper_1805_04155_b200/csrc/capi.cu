@@ -59,6 +59,7 @@ struct epfem_cache {
   double* scratch = nullptr;  // tangent workspace (symmetric dK_e per element)
   unsigned* emask = nullptr;  // per-element plastic-point bitmask
   int npc = 64, max_span = 0, max_items = 0;  // row-stream plan
+  int32_t* range_order = nullptr;             // row-stream CTA -> node range (space-filling curve)
   // overlapped Newton step: row chunk k (nodes [nchunk[k], nchunk[k+1]))
   // needs exactly the element chunks 0..k (elements [echunk[j], echunk[j+1]))
   int n_chunks = 1;
@@ -298,7 +299,7 @@ int epfem_cache_destroy(epfem_cache* c) {
                   c->weight,  c->shear,       c->bulk,        c->pat.n2e_ptr,  c->pat.n2e,
                   c->pat.nbr_ptr, c->pat.row_ptr, c->pat.col_idx, c->pat.slot, c->K_elast,
                   c->scratch, c->emask, c->mega_sched, c->mega_rlo, c->mega_rhi, c->mega_flag,
-                  c->mega_sync};
+                  c->mega_sync, c->range_order};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -327,6 +328,7 @@ static GatherArgs gather_args(const epfem_cache* c) {
   g.npc = c->npc;
   g.max_span = c->max_span;
   g.max_items = c->max_items;
+  g.range_order = c->range_order;
   g.e_begin = 0;
   g.e_end = c->info.n_elements;
   g.n_begin = 0;
@@ -494,6 +496,14 @@ int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_materi
     if (int rc = plan_row_stream(I.n_nodes, I.dim, c->pat.nbr_ptr, c->pat.n2e_ptr, st, &c->npc,
                                  &c->max_span, &c->max_items))
       return bail(rc);
+  {
+    // opt-in (EPFEM_RANGE_ORDER=1): measured on B200 no faster on cfg3/cfg5
+    // and slower on cfg2/cfg4 (3.88 -> 4.05 ms) than node order
+    const char* v = getenv("EPFEM_RANGE_ORDER");
+    const bool on = v && v[0] == '1';
+    if (on && I.n_nodes > 0)
+      if (int rc = plan_range_order(I.n_nodes, I.dim, c->npc, mesh->coord, st, &c->range_order)) return bail(rc);
+  }
   {
     // overlap plan, opt-in via EPFEM_CHUNKS: measured on B200 the chunked
     // two-stream schedule is slower than one fused + one row launch (cfg2:

@@ -43,7 +43,19 @@ struct DeltaCfg {
   static constexpr int D2 = DIM * DIM;
   static constexpr int NB = NP * (NP + 1) / 2;
   static constexpr int REC = NP * DIM + NSP;
-  static constexpr int CS = (DIM == 3 && NP >= 20) ? 5 : 4;  // blocks per phase-2 thread
+// Q2-20 (cfg5) phase 2: chunks of 4 blocks at <= 128 registers (4 CTAs/SM)
+// measured 16.0 ms vs 18.9 ms for chunks of 5 at ptxas' 164 registers; 3, 6
+// and 7 blocks, sub-passes and 5 CTAs/SM were all slower (B200 sweep)
+#ifndef EPFEM_CS20
+#define EPFEM_CS20 4
+#endif
+#ifndef EPFEM_SUB20
+#define EPFEM_SUB20 0
+#endif
+#ifndef EPFEM_MINB20
+#define EPFEM_MINB20 4
+#endif
+  static constexpr int CS = (DIM == 3 && NP >= 20) ? EPFEM_CS20 : 4;  // blocks per phase-2 thread
   static constexpr int nt() {
     int s = 0;
     for (int a = 0; a < NP; ++a) s += (NP - a + CS - 1) / CS;
@@ -65,8 +77,8 @@ struct DeltaCfg {
 #ifndef EPFEM_MINB3
 #define EPFEM_MINB3 4
 #endif
-  static constexpr int SUB = (DIM == 3 && NP < 20) ? 2 : 0;
-  static constexpr int MINB = DIM == 2 ? 1024 / THREADS : (NP < 20 ? EPFEM_MINB3 : 0);
+  static constexpr int SUB = (DIM == 3 && NP < 20) ? 2 : (DIM == 3 ? EPFEM_SUB20 : 0);
+  static constexpr int MINB = DIM == 2 ? 1024 / THREADS : (NP < 20 ? EPFEM_MINB3 : EPFEM_MINB20);
 };
 
 // assembly row r -> Voigt row (2D plane strain uses {0,1,3}, assembly.cpp:92)

@@ -50,6 +50,7 @@ struct GatherArgs {
   double* scratch;   // tangent workspace: symmetric dK_e per element
   unsigned* emask;   // per-element plastic-point bitmask
   int npc;           // nodes per CTA of the row stream
+  const int32_t* range_order;  // row stream: CTA b assembles range range_order[b] (whole-mesh launches)
   int max_span;      // widest value range of any row-stream CTA (doubles)
   int max_items;     // most (element, node) items of any row-stream CTA
   double Cu[21];     // packed elastic operator when the material is uniform
@@ -119,6 +120,8 @@ int launch_range_groups(int64_t n_nodes, int npc, int np, int group_elems, const
 size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements);
 int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
                     cudaStream_t st, int* npc_out, int* span_out, int* items_out, int budget_bytes = 0);
+int plan_range_order(int64_t n_nodes, int dim, int npc, const double* coord, cudaStream_t st,
+                     int32_t** order_out);
 int plan_chunks(int64_t n_nodes, int64_t n_elements, int np, const int64_t* n2e_ptr,
                 const int32_t* n2e, int npc, int n_chunks, int64_t* nchunk, int64_t* echunk,
                 cudaStream_t st);

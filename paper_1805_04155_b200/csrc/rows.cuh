@@ -1,6 +1,8 @@
-// Pass 2 of the tangent (K2 + K6) for one range of consecutive nodes, shared
-// by the stand-alone row stream (k_row_stream, tangent.cu) and the one-launch
-// Newton step (k_newton_mega, constitutive.cu).
+// Pass 2 of the tangent (K2 + K6) for one range of consecutive nodes as a
+// device function: the warp-owned ranges of the one-launch Newton step
+// (k_newton_mega, constitutive.cu).  Same algorithm as the stand-alone row
+// stream k_row_stream (tangent.cu), which keeps its own code for codegen
+// reasons (see there).
 //
 // One CTA owns the nodes [n0, n1) = one contiguous value range of K (a node's
 // dim rows are contiguous and nodes are numbered in row order).  ONE TMA bulk
@@ -65,8 +67,11 @@ __device__ __forceinline__ bool row_range(const GatherArgs& a, int npc, int64_t 
   int* s_iptr = s_item + a.max_items;
   int* s_vptr = s_iptr + npc + 1;
   const bool zero_base = a.base == nullptr;  // elastic assembly: K = sum of element blocks
+  // staging loops stride by the runtime block size (a compile-time stride
+  // gets them unrolled: +14 registers on the 3D instances, one CTA per SM less)
+  const int nthr = WARP ? 32 : (int)blockDim.x;
   if (zero_base)
-    for (int64_t k = tid; k < a1 - a0; k += NTHREADS) img_raw[k] = 0.0;
+    for (int64_t k = tid; k < a1 - a0; k += nthr) img_raw[k] = 0.0;
   if (tid == 0 && a1 > a0 && !zero_base) {
     const unsigned bytes = (unsigned)((a1 - a0) * 8);
     mbar_expect_tx(s_bar, bytes);
@@ -76,14 +81,14 @@ __device__ __forceinline__ bool row_range(const GatherArgs& a, int npc, int64_t 
       tma_load_1d(img_raw, a.base + a0, bytes, s_bar);
   }
   // node offsets (cache data, independent of the producer)
-  for (int k = tid; k <= nloc; k += NTHREADS) {
+  for (int k = tid; k <= nloc; k += nthr) {
     s_iptr[k] = (int)(__ldg(a.n2e_ptr + n0 + k) - i_begin);
     s_vptr[k] = (int)(__ldg(a.nbr_ptr + n0 + k) * D2 - v0);
   }
   // everything below reads the producer's emask / workspace
   wait();
   // stage the range's items (plastic ones kept, others -1)
-  for (int k = tid; k < nitems; k += NTHREADS) {
+  for (int k = tid; k < nitems; k += nthr) {
     const int32_t it = __ldg(a.n2e + i_begin + k);
     s_item[k] = __ldcg(a.emask + it / NP) ? it : -1;
   }

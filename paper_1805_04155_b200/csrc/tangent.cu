@@ -20,6 +20,10 @@
 // at the cached slots (one warp per node: a single writer per row); one TMA
 // bulk store writes the image to K[range].  Rows without plastic
 // contributions are therefore bitwise copies of K_elast.
+#include <algorithm>
+#include <climits>
+#include <vector>
+
 #include "rows.cuh"
 
 namespace epfem_gpu {
@@ -206,20 +210,138 @@ __global__ void __launch_bounds__(MmaCfg<DIM, NP, NQ>::THREADS) k_delta_mma(Gath
 }
 
 constexpr int kStreamThreads = 256;
+// Q2-20: 4 CTAs per SM (64 registers) measured 9.6 vs 11.2 ms on cfg5; the
+// same bound on Q1 / P2 tetrahedra is slower (ptxas then uses 56 registers)
+#ifndef EPFEM_ROW_MINB20
+#define EPFEM_ROW_MINB20 4
+#endif
 
-// one CTA per node range (rows.cuh); programmatic dependent launch: the
-// K_elast load and node offsets overlap the producer's tail
+// The K_elast range [v0, v1) is read with ONE TMA bulk copy of the enclosing
+// 16-byte-aligned range into the shared image (the K_elast allocation is
+// padded by two doubles), overlapped with the item staging; the image goes
+// back to K with one TMA bulk store of the aligned interior plus at most two
+// edge doubles.  (rows.cuh holds the same range pass as a device function
+// for the warp-owned ranges of the one-launch step; this stand-alone kernel
+// keeps its own code: written as the shared function it compiled to 17 %
+// slower 3D instances.)
 template <int DIM, int NP, int NQ>
-__global__ void __launch_bounds__(kStreamThreads) k_row_stream(GatherArgs a, int npc) {
+__global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM_ROW_MINB20 : 0)
+    k_row_stream(GatherArgs a, int npc) {
   extern __shared__ __align__(128) double img_raw[];
   __shared__ uint64_t s_bar;
-  if (threadIdx.x == 0) {
+  constexpr int NB = NP * (NP + 1) / 2;
+  constexpr int D2 = DIM * DIM;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t range = a.range_order ? (int64_t)__ldg(a.range_order + blockIdx.x) : (int64_t)blockIdx.x;
+  const int64_t n0 = a.n_begin + range * npc;
+  const int64_t n1 = min(n0 + (int64_t)npc, a.n_end);
+  const int nloc = (int)(n1 - n0);
+  const int64_t v0 = __ldg(a.nbr_ptr + n0) * D2;
+  const int64_t v1 = __ldg(a.nbr_ptr + n1) * D2;
+  const int64_t a0 = v0 & ~int64_t(1), a1 = (v1 + 1) & ~int64_t(1);
+  const int64_t i_begin = __ldg(a.n2e_ptr + n0);
+  const int nitems = (int)(__ldg(a.n2e_ptr + n1) - i_begin);
+  // layout: [image (aligned to a0) | item (int) | iptr (int) | vptr (int)]
+  double* img = img_raw + (v0 - a0);  // img[k] <-> global v0 + k
+  int* s_item = reinterpret_cast<int*>(img_raw + a.max_span + 2);
+  int* s_iptr = s_item + a.max_items;
+  int* s_vptr = s_iptr + npc + 1;
+  if (tid == 0) {
     mbar_init(&s_bar, 1);
-    mbar_init_fence();
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  row_range<DIM, NP, NQ, kStreamThreads, false>(a, npc, blockIdx.x, img_raw, &s_bar, 0u,
-                                               [] { asm volatile("griddepcontrol.wait;" ::: "memory"); });
+  const bool zero_base = a.base == nullptr;  // elastic assembly: K = sum of element blocks
+  if (zero_base)
+    for (int64_t k = tid; k < a1 - a0; k += blockDim.x) img_raw[k] = 0.0;
+  if (tid == 0 && a1 > a0 && !zero_base) {
+    const unsigned bytes = (unsigned)((a1 - a0) * 8);
+    mbar_expect_tx(&s_bar, bytes);
+    if (EPFEM_K_EVICT_FIRST && DIM == 3 && NP < 20)
+      tma_load_1d_hint(img_raw, a.base + a0, bytes, &s_bar, l2_evict_first());
+    else
+      tma_load_1d(img_raw, a.base + a0, bytes, &s_bar);
+  }
+  // node offsets (cache data, independent of the producer kernel)
+  for (int k = tid; k <= nloc; k += blockDim.x) {
+    s_iptr[k] = (int)(__ldg(a.n2e_ptr + n0 + k) - i_begin);
+    s_vptr[k] = (int)(__ldg(a.nbr_ptr + n0 + k) * D2 - v0);
+  }
+  // everything below reads the producer's emask / workspace
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // stage the range's items (plastic ones kept, others -1)
+  for (int k = tid; k < nitems; k += blockDim.x) {
+    const int32_t it = __ldg(a.n2e + i_begin + k);
+    s_item[k] = __ldcg(a.emask + it / NP) ? it : -1;
+  }
+  __syncthreads();
+  if (a1 > a0 && !zero_base) mbar_wait(&s_bar, 0);
+  // Items are taken UB at a time: every lane first issues the loads of all
+  // UB items (slot byte + workspace value), then applies the adds in item
+  // order, so a node costs one memory round trip per UB items instead of
+  // one per item (the add order, hence the bits, is unchanged).
+  constexpr int KP = (NP * D2 + 31) / 32;
+  constexpr int UB = KP == 1 ? 4 : 1;  // 3D: wider rows already give ILP; registers matter more
+  for (int ln = warp; ln < nloc; ln += kStreamThreads / 32) {
+    const int ib = s_iptr[ln], ie = s_iptr[ln + 1];
+    const int row_len = (s_vptr[ln + 1] - s_vptr[ln]) / DIM;
+    double* seg = img + s_vptr[ln];
+    for (int kb = ib; kb < ie; kb += UB) {
+      double v[UB][KP];
+      int sl[UB][KP];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int it = kb + u < ie ? s_item[kb + u] : -1;  // warp-uniform
+        const int64_t el = it / NP;
+        const int pa = it - (int)el * NP;
+        const double* rec = a.scratch + (size_t)el * NB * D2;
+#pragma unroll
+        for (int kk = 0; kk < KP; ++kk) {
+          const int k = lane + 32 * kk;
+          sl[u][kk] = -1;
+          if (it >= 0 && k < NP * D2) {
+            // lane <-> entry (pb, i, j) of block row pa; block (pb, pa) read
+            // transposed when pb < pa (branch-free addressing)
+            const int pb = k / D2, ij = k - pb * D2;
+            const int i = ij / DIM, j = ij - i * DIM;
+            const bool up = pa <= pb;
+            const int lo = up ? pa : pb, hi = up ? pb : pa;
+            const int src = blk_index<NP>(lo, hi) * D2 + (up ? ij : j * DIM + i);
+            sl[u][kk] = __ldg(a.slot + (int64_t)it * NP + pb);
+            v[u][kk] = __ldg(rec + src);
+          }
+        }
+      }
+      // A lane's column node differs from item to item, so two lanes can
+      // update the same entry for different items: a warp barrier between
+      // items keeps the add order = item order even when the warp has
+      // diverged (independent thread scheduling).
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+#pragma unroll
+        for (int kk = 0; kk < KP; ++kk)
+          if (sl[u][kk] >= 0) {
+            const int k = lane + 32 * kk;
+            const int ij = k % D2, i = ij / DIM, j = ij - i * DIM;
+            seg[i * row_len + sl[u][kk] * DIM + j] += v[u][kk];
+          }
+        __syncwarp();
+      }
+    }
+  }
+  fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
+  __syncthreads();
+  if (tid == 0 && v1 > v0) {
+    const int64_t s0 = (v0 + 1) & ~int64_t(1), s1 = v1 & ~int64_t(1);
+    if (v0 & 1) a.out[v0] = img[0];
+    if ((v1 & 1) && v1 - 1 >= s0) a.out[v1 - 1] = img[v1 - 1 - v0];
+    if (s1 > s0) {
+      if (EPFEM_K_EVICT_FIRST && DIM == 3 && NP < 20)
+        tma_store_1d_sync_hint(a.out + s0, img + (s0 - v0), (unsigned)((s1 - s0) * 8), l2_evict_first());
+      else
+        tma_store_1d_sync(a.out + s0, img + (s0 - v0), (unsigned)((s1 - s0) * 8));
+    }
+  }
 }
 
 __global__ void k_range_span(int64_t n_nodes, int npc, int d2, const int64_t* __restrict__ nbr_ptr,
@@ -293,6 +415,112 @@ size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements) {
   return nb * (size_t)n_elements;
 }
 
+// Row-stream CTA order along a space-filling curve.  A node range's K
+// values are contiguous whatever order the ranges run in, but the element
+// records it reads are shared with the ranges of the neighbouring node rows
+// and planes: in node order those sit a whole plane of K apart, too far for
+// the records to stay in L2 (cfg5: 15 KB per Q2-20 record, 8 GB of records
+// re-read).  Ordering the ranges by the Morton code of their first node's
+// coordinates (normalised to the mesh box) runs geometric neighbours
+// together, so a record's readers meet while it is L2-resident.  Generic: it
+// uses only the coordinates, not the structured numbering.
+__global__ void k_coord_box(int64_t n, int dim, const double* __restrict__ coord, double* box) {
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < n; a += (int64_t)gridDim.x * blockDim.x)
+    for (int d = 0; d < dim; ++d) {
+      const double x = coord[a * dim + d];
+      lo[d] = fmin(lo[d], x);
+      hi[d] = fmax(hi[d], x);
+    }
+  for (int d = 0; d < dim; ++d)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+      hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+    }
+  if ((threadIdx.x & 31) == 0) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    for (int d = 0; d < dim; ++d) {
+      box[w * 6 + d] = lo[d];
+      box[w * 6 + 3 + d] = hi[d];
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t spread3(uint64_t v) {  // 21 bits -> every third bit
+  v &= 0x1fffff;
+  v = (v | v << 32) & 0x1f00000000ffffull;
+  v = (v | v << 16) & 0x1f0000ff0000ffull;
+  v = (v | v << 8) & 0x100f00f00f00f00full;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+  v = (v | v << 2) & 0x1249249249249249ull;
+  return v;
+}
+__device__ __forceinline__ uint64_t spread2(uint64_t v) {  // 32 bits -> every second bit
+  v &= 0xffffffffull;
+  v = (v | v << 16) & 0x0000ffff0000ffffull;
+  v = (v | v << 8) & 0x00ff00ff00ff00ffull;
+  v = (v | v << 4) & 0x0f0f0f0f0f0f0f0full;
+  v = (v | v << 2) & 0x3333333333333333ull;
+  v = (v | v << 1) & 0x5555555555555555ull;
+  return v;
+}
+
+__global__ void k_range_keys(int64_t n_nodes, int npc, int dim, const double* __restrict__ coord,
+                             const double* __restrict__ box, uint64_t* keys) {
+  const int64_t n_ranges = (n_nodes + npc - 1) / npc;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_ranges;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = r * npc;
+    uint64_t q[3] = {0, 0, 0};
+    const double scale = dim == 3 ? 2097151.0 : 4294967295.0;
+    for (int d = 0; d < dim; ++d) {
+      const double ext = box[3 + d] - box[d];
+      const double t = ext > 0 ? (coord[a * dim + d] - box[d]) / ext : 0.0;
+      q[d] = (uint64_t)fmin(fmax(t * scale, 0.0), scale);
+    }
+    keys[r] = dim == 3 ? (spread3(q[0]) | spread3(q[1]) << 1 | spread3(q[2]) << 2)
+                       : (spread2(q[0]) | spread2(q[1]) << 1);
+  }
+}
+
+int plan_range_order(int64_t n_nodes, int dim, int npc, const double* coord, cudaStream_t st,
+                     int32_t** order_out) {
+  *order_out = nullptr;
+  const int64_t n_ranges = (n_nodes + npc - 1) / npc;
+  if (n_ranges <= 1 || n_ranges >= INT32_MAX || !coord) return 0;
+  constexpr int B = 256, T = 256, WARPS = B * T / 32;
+  double* box = nullptr;
+  uint64_t* keys = nullptr;
+  EPFEM_CUDA_TRY(cudaMalloc(&box, sizeof(double) * 6 * WARPS));
+  EPFEM_CUDA_TRY(cudaMalloc(&keys, sizeof(uint64_t) * n_ranges));
+  k_coord_box<<<B, T, 0, st>>>(n_nodes, dim, coord, box);
+  std::vector<double> hb(6 * WARPS);
+  EPFEM_CUDA_TRY(cudaMemcpyAsync(hb.data(), box, sizeof(double) * hb.size(), cudaMemcpyDeviceToHost, st));
+  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+  double g[6] = {1e300, 1e300, 1e300, -1e300, -1e300, -1e300};
+  for (int w = 0; w < WARPS; ++w)
+    for (int d = 0; d < dim; ++d) {
+      g[d] = std::min(g[d], hb[w * 6 + d]);
+      g[3 + d] = std::max(g[3 + d], hb[w * 6 + 3 + d]);
+    }
+  EPFEM_CUDA_TRY(cudaMemcpyAsync(box, g, sizeof(g), cudaMemcpyHostToDevice, st));
+  k_range_keys<<<256, 256, 0, st>>>(n_nodes, npc, dim, coord, box, keys);
+  std::vector<uint64_t> hk(n_ranges);
+  EPFEM_CUDA_TRY(cudaMemcpyAsync(hk.data(), keys, sizeof(uint64_t) * n_ranges, cudaMemcpyDeviceToHost, st));
+  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+  cudaFree(box);
+  cudaFree(keys);
+  std::vector<int32_t> order(n_ranges);
+  for (int64_t r = 0; r < n_ranges; ++r) order[r] = (int32_t)r;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return hk[x] < hk[y]; });
+  int32_t* d = nullptr;
+  EPFEM_CUDA_TRY(cudaMalloc(&d, sizeof(int32_t) * n_ranges));
+  EPFEM_CUDA_TRY(cudaMemcpyAsync(d, order.data(), sizeof(int32_t) * n_ranges, cudaMemcpyHostToDevice, st));
+  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+  *order_out = d;
+  return 0;
+}
+
 // Nodes per CTA for the row stream: the largest power of two <= 64 whose
 // widest value range and item list fit the shared-memory budget.
 int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
@@ -353,7 +581,9 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, a.npc);
+    GatherArgs b = a;
+    if (a.n_begin != 0 || a.n_end != a.n_nodes) b.range_order = nullptr;  // the order covers whole-mesh launches
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, b, a.npc);
     if (e != cudaSuccess) rc = cuda_fail(e, "row stream launch");
   });
   if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");

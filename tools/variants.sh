@@ -1,19 +1,22 @@
 #!/bin/bash
-# Build libepfem_gpu.so variants with extra -D flags on constitutive.cu into
-# paper_1805_04155_b200/lib/variants/<name>/ (tuning experiments; load one with
-# EPFEM_GPU_LIB=<path>).  usage: tools/variants.sh name "-DFOO=1" [name2 "-D..."]...
+# Build libepfem_gpu.so variants with extra -D flags on constitutive.cu (or
+# SRC=tangent.cu) into paper_1805_04155_b200/lib/variants/<name>/ (tuning
+# experiments; load one with EPFEM_GPU_LIB=<path>).
+# usage: [SRC=tangent.cu] tools/variants.sh name "-DFOO=1" [name2 "-D..."]...
 set -e
 cd "$(dirname "$0")/.."
 python -m paper_1805_04155_b200.build > /dev/null
 P=paper_1805_04155_b200
+SRC=${SRC:-constitutive.cu}
+FMAD=""; [ $SRC = constitutive.cu ] && FMAD="--fmad=false"
 while [ $# -gt 0 ]; do
   name=$1; flags=$2; shift 2
   out=$P/lib/variants/$name; mkdir -p $out
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
-    -Xcompiler -ffp-contract=off --expt-relaxed-constexpr -I include --fmad=false $flags \
-    -c $P/csrc/constitutive.cu -o $out/constitutive.o
-  objs=$(ls $P/_obj/*.o | grep -v constitutive)
-  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libepfem_gpu.so $out/constitutive.o $objs -lcudart_static
-  rm $out/constitutive.o
+    -Xcompiler -ffp-contract=off --expt-relaxed-constexpr -I include $FMAD $flags \
+    -c $P/csrc/$SRC -o $out/$SRC.o
+  objs=$(ls $P/_obj/*.o | grep -v "/$SRC.o")
+  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libepfem_gpu.so $out/$SRC.o $objs -lcudart_static
+  rm $out/$SRC.o
   echo $out/libepfem_gpu.so
 done
