@@ -1326,6 +1326,87 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_newton_warp_ovl (2D): k_newton_warp made persistent for the overlapped
+// step.  The grid is sized below full occupancy (EPFEM_OVL_CTAS per SM) so
+// that the row stream's CTAs, launched with programmatic dependent launch,
+// share the SMs with it; each warp walks the element groups (warp-strided,
+// so groups complete roughly in order) and publishes every group with a
+// release store of the step generation (deferred to its next group, so the
+// fence finds the stores drained).  The trigger at entry lets the row
+// stream launch as soon as every producer CTA is resident, which is what
+// makes the row stream's flag waits deadlock-free.
+template <int MODEL, int NP, int NQ>
+__global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
+    k_newton_warp_ovl(ConstArgs c, GatherArgs g, OvlArgs o) {
+  pdl_trigger();
+  using W = WarpCfg<2, NP, NQ>;
+  __shared__ double s_st[W::WPB][W::EPW * NQ * W::REC];
+  __shared__ __align__(16) double s_out[W::WPB][W::EPW * W::NB * W::D2];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int gen = *((volatile int*)&o.sync->gen);
+  int pending = -1;
+  for (int64_t grp = (int64_t)blockIdx.x * W::WPB + w; grp < o.n_groups; grp += (int64_t)gridDim.x * W::WPB) {
+    newton_warp_group<MODEL, NP, NQ, false, true>(c, g, grp * W::EPW, s_st[w], s_out[w], lane);
+    __syncwarp();
+    if (pending >= 0 && lane == 0) {
+      __threadfence();
+      st_release_gpu(o.flag + pending, gen + 1);
+    }
+    pending = (int)grp;
+  }
+  if (pending >= 0 && lane == 0) {
+    __threadfence();
+    st_release_gpu(o.flag + pending, gen + 1);
+  }
+}
+
+bool ovl_supported(int family, int dim, int* group_elems) {
+  bool ok = false;
+  dispatch_element(family, dim, [&](auto F, auto D) {
+    constexpr int DIM = decltype(D)::value;
+    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
+    if constexpr (DIM == 2) {
+      *group_elems = WarpCfg<2, NP, NQ>::EPW;
+      ok = true;
+    }
+  });
+  return ok;
+}
+
+int launch_newton_ovl(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g, const OvlArgs& o,
+                      int ctas_per_sm, cudaStream_t st) {
+  if (o.n_groups <= 0) return 0;
+  int rc = 0;
+  bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
+    constexpr int DIM = decltype(D)::value;
+    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
+    if constexpr (DIM == 2) {
+      using W = WarpCfg<2, NP, NQ>;
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int64_t want = (o.n_groups + W::WPB - 1) / W::WPB;
+      const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)std::max(ctas_per_sm, 1) * sms);
+      switch (model) {
+        case EPFEM_MODEL_VON_MISES:
+          k_newton_warp_ovl<EPFEM_MODEL_VON_MISES, NP, NQ><<<grid, W::THREADS, 0, st>>>(c, g, o);
+          break;
+        case EPFEM_MODEL_DRUCKER_PRAGER:
+          k_newton_warp_ovl<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ><<<grid, W::THREADS, 0, st>>>(c, g, o);
+          break;
+        default: k_newton_warp_ovl<EPFEM_MODEL_ELASTIC, NP, NQ><<<grid, W::THREADS, 0, st>>>(c, g, o); break;
+      }
+    } else {
+      rc = fail(EPFEM_ERR_INVALID, "overlapped step: 2D meshes only");
+    }
+  });
+  if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
+  if (rc) return rc;
+  EPFEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 // per node range: the first and last producer group whose elements touch it
 __global__ void k_range_groups(int64_t n_nodes, int npc, int np, int group_elems,
                                const int64_t* __restrict__ n2e_ptr, const int32_t* __restrict__ n2e,

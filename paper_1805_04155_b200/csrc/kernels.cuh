@@ -83,6 +83,19 @@ struct MegaArgs {
   int group_elems;       // elements per producer group
   int exp;               // timing experiments (EPFEM_MEGA_EXP): 1 = ranges skipped, 2 = groups skipped, no waits
 };
+// Overlapped two-kernel Newton step (2D): a persistent fused update publishes
+// each warp group with a release flag; the row stream, launched with
+// programmatic dependent launch (so every producer CTA is already resident
+// when any of its CTAs starts), waits on the flags of the groups it reads
+// instead of on the whole producer grid.
+struct OvlArgs {
+  const int32_t* rlo;  // per node range: first / last producer group it reads
+  const int32_t* rhi;
+  int* flag;           // per producer group: generation that completed it
+  MegaSync* sync;      // finished counter + generation (bumped by the last row-stream CTA)
+  int64_t n_groups;
+  int group_elems;
+};
 struct PatternOut {
   int64_t* n2e_ptr = nullptr;
   int32_t* n2e = nullptr;
@@ -117,6 +130,10 @@ int launch_newton_mega(int model, int family, int dim, const ConstArgs& c, const
                        const MegaArgs& m, int slice_bytes, int workers, cudaStream_t st);
 int launch_range_groups(int64_t n_nodes, int npc, int np, int group_elems, const int64_t* n2e_ptr,
                         const int32_t* n2e, int32_t* rlo, int32_t* rhi, cudaStream_t st);
+bool ovl_supported(int family, int dim, int* group_elems);
+int launch_newton_ovl(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g, const OvlArgs& o,
+                      int ctas_per_sm, cudaStream_t st);
+int launch_row_stream_ovl(int family, int dim, const GatherArgs& a, const OvlArgs& o, cudaStream_t st);
 size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements);
 int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
                     cudaStream_t st, int* npc_out, int* span_out, int* items_out, int budget_bytes = 0);

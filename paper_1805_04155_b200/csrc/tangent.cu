@@ -224,9 +224,19 @@ constexpr int kStreamThreads = 256;
 // for the warp-owned ranges of the one-launch step; this stand-alone kernel
 // keeps its own code: written as the shared function it compiled to 17 %
 // slower 3D instances.)
-template <int DIM, int NP, int NQ>
+// FLAGS: the overlapped step (OvlArgs): wait on the ready flags of the
+// producer groups this range reads instead of griddepcontrol.wait, read the
+// element records with plain (coherent) loads, and let the last CTA bump the
+// generation.
+__device__ __forceinline__ int ld_acquire_gpu_i(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int DIM, int NP, int NQ, bool FLAGS = false>
 __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM_ROW_MINB20 : 0)
-    k_row_stream(GatherArgs a, int npc) {
+    k_row_stream(GatherArgs a, int npc, OvlArgs o) {
   extern __shared__ __align__(128) double img_raw[];
   __shared__ uint64_t s_bar;
   constexpr int NB = NP * (NP + 1) / 2;
@@ -268,7 +278,18 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
     s_vptr[k] = (int)(__ldg(a.nbr_ptr + n0 + k) * D2 - v0);
   }
   // everything below reads the producer's emask / workspace
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  int gen = 0;
+  if constexpr (FLAGS) {
+    gen = *((volatile int*)&o.sync->gen);
+    if (warp == 0) {
+      const int lo = __ldg(o.rlo + range), hi = __ldg(o.rhi + range);
+      for (int k = lo + lane; k <= hi; k += 32)
+        while (ld_acquire_gpu_i(o.flag + k) != gen + 1) __nanosleep(64);
+    }
+    __syncthreads();
+  } else {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   // stage the range's items (plastic ones kept, others -1)
   for (int k = tid; k < nitems; k += blockDim.x) {
     const int32_t it = __ldg(a.n2e + i_begin + k);
@@ -308,7 +329,7 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
             const int lo = up ? pa : pb, hi = up ? pb : pa;
             const int src = blk_index<NP>(lo, hi) * D2 + (up ? ij : j * DIM + i);
             sl[u][kk] = __ldg(a.slot + (int64_t)it * NP + pb);
-            v[u][kk] = __ldg(rec + src);
+            v[u][kk] = FLAGS ? rec[src] : __ldg(rec + src);  // FLAGS: written in this step's overlap
           }
         }
       }
@@ -340,6 +361,14 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
         tma_store_1d_sync_hint(a.out + s0, img + (s0 - v0), (unsigned)((s1 - s0) * 8), l2_evict_first());
       else
         tma_store_1d_sync(a.out + s0, img + (s0 - v0), (unsigned)((s1 - s0) * 8));
+    }
+  }
+  if constexpr (FLAGS) {
+    // every CTA of this grid has read gen once the counter completes
+    if (tid == 0 && atomicAdd(&o.sync->finished, 1) == (int)gridDim.x - 1) {
+      o.sync->finished = 0;
+      atomicAdd(&o.sync->gen, 1);
+      __threadfence();
     }
   }
 }
@@ -583,8 +612,49 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
     cfg.numAttrs = pdl ? 1 : 0;
     GatherArgs b = a;
     if (a.n_begin != 0 || a.n_end != a.n_nodes) b.range_order = nullptr;  // the order covers whole-mesh launches
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, b, a.npc);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, b, a.npc, OvlArgs{});
     if (e != cudaSuccess) rc = cuda_fail(e, "row stream launch");
+  });
+  if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
+  if (rc) return rc;
+  EPFEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// Row stream of the overlapped step: PDL launch (its CTAs start once every
+// producer CTA has started) waiting on per-group flags (k_row_stream<FLAGS>).
+int launch_row_stream_ovl(int family, int dim, const GatherArgs& a, const OvlArgs& o, cudaStream_t st) {
+  if (a.n_nodes == 0) return 0;
+  int rc = 0;
+  bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
+    constexpr int DIM = decltype(D)::value;
+    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
+    if constexpr (DIM == 2) {
+      const int64_t rblocks = (a.n_nodes + a.npc - 1) / a.npc;
+      const size_t smem = sizeof(double) * ((size_t)a.max_span + 2) +
+                          sizeof(int) * ((size_t)a.max_items + 2 * ((size_t)a.npc + 1));
+      auto kern = k_row_stream<DIM, NP, NQ, true>;
+      if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) { rc = cuda_fail(e, "cudaFuncSetAttribute"); return; }
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)rblocks);
+      cfg.blockDim = dim3(kStreamThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      GatherArgs b = a;
+      b.range_order = nullptr;  // flags are ordered by node range
+      cudaError_t e = cudaLaunchKernelEx(&cfg, kern, b, a.npc, o);
+      if (e != cudaSuccess) rc = cuda_fail(e, "overlapped row stream launch");
+    } else {
+      rc = fail(EPFEM_ERR_INVALID, "overlapped step: 2D meshes only");
+    }
   });
   if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
   if (rc) return rc;

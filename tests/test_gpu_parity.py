@@ -479,11 +479,14 @@ def test_full_size_pattern_and_properties(cuda, name):
 @pytest.mark.parametrize("variant,name", [("mma", "cfg2"), ("mma", "cfg3"), ("mma", "cfg4"), ("ws", "cfg2"), ("cta", "cfg3"), ("pf", "cfg2"),
                                           ("cta", "cfg2"), ("pipe", "cfg2"), ("pipe", "cfg4"),
                                           ("MEGA=1", "cfg2"), ("MEGA=1,MEGA_SLACK=0", "cfg2"),
-                                          ("MEGA=1,MEGA_SLACK=4", "cfg2")])
+                                          ("MEGA=1,MEGA_SLACK=4", "cfg2"), ("OVL=1", "cfg2"),
+                                          ("OVL=1,OVL_CTAS=1", "cfg2")])
 def test_kernel_variants(cuda, oracle, variant, name):
-    """EPFEM_FUSED variants, and the one-launch step (MEGA=1), also with a
-    small MEGA_SLACK (node ranges right behind their producer groups in the
-    walk, so they wait on the ready flags)."""
+    """EPFEM_FUSED variants; the one-launch step (MEGA=1), also with a small
+    MEGA_SLACK (node ranges right behind their producer groups in the walk,
+    so they wait on the ready flags); the overlapped two-kernel step (OVL=1),
+    also with one producer CTA per SM (row-stream CTAs far ahead of the
+    producers: flag waits)."""
     import subprocess
     import sys
     if "=" in variant:
