@@ -23,6 +23,8 @@
 // straight from registers (D is never re-read).  Phase 2 builds dK_e
 // (delta.cuh).  The row stream (tangent.cu) then assembles K.
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <climits>
 #include <type_traits>
 
@@ -372,6 +374,25 @@ __global__ void __launch_bounds__(256) k_constitutive(ConstArgs a) {
     eval_point<MODEL>(a, q, GlobalIn{a.E, a.Ep, a.Hard}, none);
 }
 
+// L2 prefetch of the per-point inputs of the elements [e_lo, e_hi) (E, Ep,
+// Hard, J^-1, w: all contiguous per element range), issued one occupancy
+// wave ahead by the fused kernels: the global-load latency of a CTA's first
+// phase (the top stall of the 2D kernel) becomes an L2 hit.
+template <int DIM, int NQ>
+__device__ __forceinline__ void prefetch_elements(const ConstArgs& c, const GatherArgs& g, int64_t e_lo,
+                                                  int64_t e_hi) {
+  e_lo = max(e_lo, g.e_begin);
+  e_hi = min(e_hi, g.e_end);
+  if (e_hi <= e_lo) return;
+  const int64_t m0 = e_lo * NQ, n = (e_hi - e_lo) * NQ;
+  const int k = threadIdx.x;
+  if (k == 0) l2_prefetch_bulk(c.E + 6 * m0, sizeof(double) * 6 * n);
+  if (k == 1) l2_prefetch_bulk(c.Ep ? c.Ep + 6 * m0 : nullptr, sizeof(double) * 6 * n);
+  if (k == 2) l2_prefetch_bulk(c.Hard ? c.Hard + 6 * m0 : nullptr, sizeof(double) * 6 * n);
+  if (k == 3) l2_prefetch_bulk(g.inv + DIM * DIM * m0, sizeof(double) * DIM * DIM * n);
+  if (k == 4) l2_prefetch_bulk(g.weight + m0, sizeof(double) * n);
+}
+
 // minBlocks: 1024 threads/SM in 2D (caps at 64 registers, measured faster); 0 in 3D
 // leaves ptxas its own heuristic (126 registers; an explicit 1 gives 144 and
 // is ~15% slower on cfg4).
@@ -381,6 +402,10 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DeltaCfg<DIM, 
   pdl_trigger();
   using Cfg = DeltaCfg<DIM, NP, NQ>;
   constexpr int EPB = Cfg::EPB;
+  if (!FROM_U && g.pf_dist > 0) {
+    const int64_t eb = g.e_begin + ((int64_t)blockIdx.x + g.pf_dist) * EPB;
+    prefetch_elements<DIM, NQ>(c, g, eb, eb + EPB);
+  }
   __shared__ double s_st[EPB][NQ][Cfg::REC];
   __shared__ unsigned s_mask[EPB];
   c.DS = nullptr;  // hot path: S, flags, packed D only
@@ -625,6 +650,10 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
   __shared__ double s_st[W::WPB][W::EPW * NQ * W::REC];
   __shared__ __align__(16) double s_out[W::WPB][W::EPW * W::NB * W::D2];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (!FROM_U && g.pf_dist > 0) {
+    const int64_t eb = g.e_begin + ((int64_t)blockIdx.x + g.pf_dist) * W::WPB * W::EPW;
+    prefetch_elements<2, NQ>(c, g, eb, eb + W::WPB * W::EPW);
+  }
   const int64_t e0 = g.e_begin + ((int64_t)blockIdx.x * W::WPB + w) * W::EPW;
   newton_warp_group<MODEL, NP, NQ, FROM_U, false>(c, g, e0, s_st[w], s_out[w], lane);
 }
@@ -753,6 +782,10 @@ __global__ void __launch_bounds__(Pair3Cfg<NP, NQ>::THREADS, EPFEM_WARP3_MINB)
   c.pm = c.sm = c.am = nullptr;
   c.crit = nullptr;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (!FROM_U && g.pf_dist > 0) {
+    const int64_t eb = g.e_begin + ((int64_t)blockIdx.x + g.pf_dist) * W::WPB * EPW;
+    prefetch_elements<DIM, NQ>(c, g, eb, eb + W::WPB * EPW);
+  }
   const int64_t e0 = g.e_begin + ((int64_t)blockIdx.x * W::WPB + w) * EPW;
   if (e0 >= g.e_end) return;  // warp-uniform
   double* st_w = s_st[w];
@@ -1514,6 +1547,29 @@ int launch_newton_mega(int model, int family, int dim, const ConstArgs& c, const
   return 0;
 }
 
+// Prefetch distance of the fused kernels, in CTAs: EPFEM_PF occupancy waves
+// times the CTAs resident on the device.  Opt-in (default 0): measured on
+// B200 neutral in 2D (cfg2 0.210 vs 0.213 ms at half a wave) and slower in 3D
+// (cfg3 4.34 vs 3.70 ms at one wave): the first-phase load stalls are
+// queueing under load, not DRAM latency an L2 hit would remove.
+static int prefetch_distance(const void* kern, int threads) {
+  static const double waves = getenv("EPFEM_PF") ? atof(getenv("EPFEM_PF")) : 0.0;
+  if (waves <= 0) return 0;
+  static std::mutex mu;
+  static std::map<const void*, int> resident;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = resident.find(kern);
+  if (it == resident.end()) {
+    int per_sm = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0) != cudaSuccess) per_sm = 0;
+    cudaGetLastError();
+    it = resident.emplace(kern, per_sm * sms).first;
+  }
+  return (int)(waves * it->second);
+}
+
 int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
                         cudaStream_t st) {
   if (g.e_end <= g.e_begin) return 0;
@@ -1591,15 +1647,17 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
         using W = Pair3Cfg<NP, NQ>;
         const int64_t per = (int64_t)W::EPW * W::WPB;
         const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
+        GatherArgs gp = g;
+        gp.pf_dist = prefetch_distance((const void*)k_newton_warp3<EPFEM_MODEL_VON_MISES, NP, NQ>, W::THREADS);
         switch (model) {
           case EPFEM_MODEL_VON_MISES:
-            k_newton_warp3<EPFEM_MODEL_VON_MISES, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, g);
+            k_newton_warp3<EPFEM_MODEL_VON_MISES, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, gp);
             break;
           case EPFEM_MODEL_DRUCKER_PRAGER:
-            k_newton_warp3<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, g);
+            k_newton_warp3<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, gp);
             break;
           default:
-            k_newton_warp3<EPFEM_MODEL_ELASTIC, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, g);
+            k_newton_warp3<EPFEM_MODEL_ELASTIC, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, gp);
             break;
         }
         return;
@@ -1635,30 +1693,34 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
         using W = WarpCfg<DIM, NP, NQ>;
         const int64_t per = (int64_t)W::EPW * W::WPB;
         const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
+        GatherArgs gp = g;
+        gp.pf_dist = prefetch_distance((const void*)k_newton_warp<EPFEM_MODEL_VON_MISES, NP, NQ>, W::THREADS);
         switch (model) {
           case EPFEM_MODEL_VON_MISES:
-            k_newton_warp<EPFEM_MODEL_VON_MISES, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, g);
+            k_newton_warp<EPFEM_MODEL_VON_MISES, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, gp);
             break;
           case EPFEM_MODEL_DRUCKER_PRAGER:
-            k_newton_warp<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, g);
+            k_newton_warp<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, gp);
             break;
           default:
-            k_newton_warp<EPFEM_MODEL_ELASTIC, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, g);
+            k_newton_warp<EPFEM_MODEL_ELASTIC, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, gp);
             break;
         }
         return;
       }
     }
     const unsigned blocks = (unsigned)((g.e_end - g.e_begin + Cfg::EPB - 1) / Cfg::EPB);
-    switch (model) {
+    GatherArgs gp = g;
+      gp.pf_dist = prefetch_distance((const void*)k_newton_fused<EPFEM_MODEL_VON_MISES, DIM, NP, NQ>, Cfg::THREADS);
+      switch (model) {
       case EPFEM_MODEL_VON_MISES:
-        k_newton_fused<EPFEM_MODEL_VON_MISES, DIM, NP, NQ><<<blocks, Cfg::THREADS, 0, st>>>(c, g);
+        k_newton_fused<EPFEM_MODEL_VON_MISES, DIM, NP, NQ><<<blocks, Cfg::THREADS, 0, st>>>(c, gp);
         break;
       case EPFEM_MODEL_DRUCKER_PRAGER:
-        k_newton_fused<EPFEM_MODEL_DRUCKER_PRAGER, DIM, NP, NQ><<<blocks, Cfg::THREADS, 0, st>>>(c, g);
+        k_newton_fused<EPFEM_MODEL_DRUCKER_PRAGER, DIM, NP, NQ><<<blocks, Cfg::THREADS, 0, st>>>(c, gp);
         break;
       default:
-        k_newton_fused<EPFEM_MODEL_ELASTIC, DIM, NP, NQ><<<blocks, Cfg::THREADS, 0, st>>>(c, g);
+        k_newton_fused<EPFEM_MODEL_ELASTIC, DIM, NP, NQ><<<blocks, Cfg::THREADS, 0, st>>>(c, gp);
         break;
     }
   });

@@ -61,6 +61,7 @@ struct GatherArgs {
   // optional strain output
   const double* u;
   double* E_out;
+  int pf_dist;  // fused kernels: CTA b prefetches (L2) the inputs of CTA b + pf_dist (0: off)
 };
 // One-launch Newton step (k_newton_mega): an ordered item list of producer
 // groups (>= 0: one warp group of EPW elements through the fused update) and

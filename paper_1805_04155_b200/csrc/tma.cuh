@@ -104,6 +104,17 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// TMA-engine prefetch of a global range into L2 (no registers, no shared
+// memory); the range is widened to 16-byte alignment
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, size_t bytes) {
+  if (!p || bytes == 0) return;
+  const uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)15, a1 = ((uintptr_t)p + bytes + 15) & ~(uintptr_t)15;
+  for (uintptr_t a = a0; a < a1; a += (1u << 20)) {  // size operand is 32-bit; chunk defensively
+    const unsigned n = (unsigned)((a1 - a < (1u << 20)) ? a1 - a : (1u << 20));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+  }
+}
+
 // make generic-proxy shared-memory writes visible to the async (TMA) proxy
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
