@@ -527,6 +527,53 @@ def main():
                   "value_from_u": n_int / (t_u * 1e-3),
                   "how": "epfem_newton_step_u (E = B u inside the fused kernel, never stored) vs "
                          "epfem_strains + epfem_newton_step, each one CUDA graph"}
+    # the step with the internal forces of its stresses
+    # (fused in 2D) vs the step followed by the stand-alone K9 kernel
+    with_f = None
+    if not elastic:
+        def graph_of(fn):
+            gs = torch.cuda.Stream(dev)
+            gs.wait_stream(torch.cuda.current_stream(dev))
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(gs):
+                fn(gs)
+                with torch.cuda.graph(gr, stream=gs):
+                    fn(torch.cuda.current_stream(dev))
+            torch.cuda.current_stream(dev).wait_stream(gs)
+            return gr
+        Fbuf = torch.empty((info.n_dofs,), dtype=torch.float64, device=dev)
+        eng_f = P.TangentEngine(cache, mat, stream=stream)
+        eng_s = P.TangentEngine(cache, mat, stream=stream)
+        lib_f = P.api.L.lib()
+
+        def fused_f(st):
+            eng_f.ctx.set_stream(st)
+            eng_f.step_f(E, Ep0, Hard0, Fbuf)
+
+        def sep_f(st):
+            eng_s.ctx.set_stream(st)
+            eng_s.step(E, Ep0, Hard0)
+            P.api._check(lib_f.epfem_internal_forces(eng_s.ctx.handle, cache.handle, P.api._ptr(eng_s.S),
+                                                     P.api._ptr(Fbuf)))
+        gf, gsep = graph_of(fused_f), graph_of(sep_f)
+
+        def t_replay(gr):
+            for _ in range(3):
+                with torch.cuda.stream(stream):
+                    gr.replay()
+            torch.cuda.synchronize(dev)
+            ev0.record(stream)
+            for _ in range(args.steps):
+                with torch.cuda.stream(stream):
+                    gr.replay()
+            ev1.record(stream)
+            torch.cuda.synchronize(dev)
+            return ev0.elapsed_time(ev1) / args.steps
+        t_f, t_sep = t_replay(gf), t_replay(gsep)
+        with_f = {"newton_step_f_ms": t_f, "step_plus_internal_forces_ms": t_sep,
+                  "value_with_forces": n_int / (t_f * 1e-3),
+                  "how": "epfem_newton_step_f (the step, then K9 in two passes: element force records, "
+                         "per-node fold) vs epfem_newton_step + epfem_internal_forces, each one CUDA graph"}
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     step_bytes = cons_b + asm_b if not elastic else asm_b
     step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
@@ -652,6 +699,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "step_from_displacements": from_u,
+            "step_with_internal_forces": with_f,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -208,6 +208,16 @@ int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* cache, const epfem_mate
 int epfem_newton_step_u(epfem_ctx* ctx, const epfem_cache* cache, const epfem_material* mat,
                         const double* u, const double* Ep_prev, const double* Hard_prev,
                         const epfem_constitutive_out* out, double* E_out, double* K_values);
+/* The same step with the internal forces of its stresses (SURVEY §8(f) rank
+ * 2; the reference computes them each iteration, solver.cpp:25):
+ * F_out (n_dofs) = B^T (weight * S) (internal_forces, assembly.cpp:215-225).
+ * epfem_newton_step followed by K9 (two passes: element force records, then
+ * a per-node fold); EPFEM_FORCES_FUSED=1 selects the fused 2D form (the
+ * constitutive kernel forms the records, the row stream folds them).  Either
+ * way bitwise the same F as epfem_internal_forces on out->S. */
+int epfem_newton_step_f(epfem_ctx* ctx, const epfem_cache* cache, const epfem_material* mat,
+                        const double* E, const double* Ep_prev, const double* Hard_prev,
+                        const epfem_constitutive_out* out, double* K_values, double* F_out);
 /* The two halves of epfem_newton_step, for callers that overlap them with
  * other work: (1) constitutive update + element tangent deltas into the
  * cache's workspace, (2) K = K_elast + assembled deltas.  (2) must follow the

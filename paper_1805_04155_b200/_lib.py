@@ -54,7 +54,7 @@ EXPORTS = [
     "epfem_cache_get_info", "epfem_cache_pattern", "epfem_cache_K_elast", "epfem_cache_geometry",
     "epfem_cache_workspace",
     "epfem_assemble_elastic", "epfem_assemble_tangent", "epfem_assemble_tangent_ds",
-    "epfem_newton_step", "epfem_newton_step_u", "epfem_constitutive_delta", "epfem_assemble_rows", "epfem_newton_range",
+    "epfem_newton_step", "epfem_newton_step_u", "epfem_newton_step_f", "epfem_constitutive_delta", "epfem_assemble_rows", "epfem_newton_range",
     "epfem_delta_range", "epfem_strains", "epfem_internal_forces",
 ]
 
@@ -95,6 +95,8 @@ def lib() -> C.CDLL:
     L.epfem_newton_step.argtypes = [_P, _P, C.POINTER(Material), _P, _P, _P,
                                     C.POINTER(ConstitutiveOut), _P]
     L.epfem_newton_step_u.argtypes = [_P, _P, C.POINTER(Material), _P, _P, _P,
+                                      C.POINTER(ConstitutiveOut), _P, _P]
+    L.epfem_newton_step_f.argtypes = [_P, _P, C.POINTER(Material), _P, _P, _P,
                                       C.POINTER(ConstitutiveOut), _P, _P]
     L.epfem_constitutive_delta.argtypes = [_P, _P, C.POINTER(Material), _P, _P, _P,
                                            C.POINTER(ConstitutiveOut)]

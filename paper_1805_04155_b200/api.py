@@ -657,6 +657,19 @@ class TangentEngine:
                                            _ptr(E_out), _ptr(self.K)))
         return self.S, self.flags, self.D, self.K
 
+    def step_f(self, E: torch.Tensor, Ep: Optional[torch.Tensor] = None,
+               Hard: Optional[torch.Tensor] = None, F: Optional[torch.Tensor] = None):
+        """step() plus the internal forces F = B^T (w S) of its stresses
+        (internal_forces, assembly.cpp:215-225; the reference forms them every
+        Newton iteration, solver.cpp:25): fused in 2D (epfem_newton_step_f),
+        bitwise cache.internal_forces(S).  Returns (S, flags, D, K, F)."""
+        if F is None:
+            F = torch.empty((self.cache.info.n_dofs,), dtype=torch.float64, device=self.device)
+        _check(L.lib().epfem_newton_step_f(self.ctx.handle, self.cache.handle, C.byref(self._mv),
+                                           _ptr(E), _ptr(Ep), _ptr(Hard), C.byref(self._out),
+                                           _ptr(self.K), _ptr(F)))
+        return self.S, self.flags, self.D, self.K, F
+
     def capture(self, E, Ep=None, Hard=None):
         """Record step() on fixed input buffers into a CUDA graph."""
         s = torch.cuda.Stream(self.device)

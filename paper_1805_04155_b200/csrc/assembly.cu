@@ -406,46 +406,61 @@ __global__ void k_strains(int64_t n_e, const int32_t* __restrict__ elem,
 }
 
 // K9 internal forces F = B^T (w S), one thread per node gathering its items.
+// K9 F = B^T (w S) in two passes (assembly.cpp:215-225).  Pass 1, thread per
+// (element, node p): the element's force record F_e[p] = sum_q w_q B_p(q)^T
+// S_q from zero in point order, with explicit roundings (dphi as
+// stage_geometry, delta.cuh).  Pass 2, thread per node: F[a] = the records of
+// the node's items summed from zero in item order.  The fused forces step
+// (epfem_newton_step_f) forms the same records in its constitutive kernel and
+// folds them in the row stream: the same bits.
 template <int DIM, int NP, int NQ>
-__global__ void k_internal_forces(int64_t n_nodes, const int64_t* __restrict__ n2e_ptr,
-                                  const int32_t* __restrict__ n2e,
-                                  const double* __restrict__ inv,
-                                  const double* __restrict__ weight,
-                                  const double* __restrict__ gradhat,
-                                  const double* __restrict__ S, double* __restrict__ F) {
-  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < n_nodes;
-       a += (int64_t)gridDim.x * blockDim.x) {
-    double f[DIM];
+__global__ void k_elem_forces(int64_t n_e, const double* __restrict__ inv, const double* __restrict__ weight,
+                              const double* __restrict__ gradhat, const double* __restrict__ S,
+                              double* __restrict__ fws) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_e * NP;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / NP;
+    const int p = (int)(t - e * NP);
+    double fe[DIM];
 #pragma unroll
-    for (int i = 0; i < DIM; ++i) f[i] = 0.0;
-    for (int64_t t = n2e_ptr[a]; t < n2e_ptr[a + 1]; ++t) {
-      const int32_t item = n2e[t];
-      const int64_t e = item / NP;
-      const int pa = item - (int)e * NP;
-      for (int q = 0; q < NQ; ++q) {
-        const int64_t m = e * NQ + q;
-        double g[DIM];
+    for (int i = 0; i < DIM; ++i) fe[i] = 0.0;
+    for (int q = 0; q < NQ; ++q) {
+      const int64_t m = e * NQ + q;
+      double g[DIM];
 #pragma unroll
-        for (int i = 0; i < DIM; ++i) {
-          double s = 0.0;
+      for (int i = 0; i < DIM; ++i) {
+        double s = __dmul_rn(__ldg(inv + m * DIM * DIM + i), __ldg(gradhat + (q * NP + p) * DIM));
 #pragma unroll
-          for (int j = 0; j < DIM; ++j) s += __ldg(inv + m * DIM * DIM + j * DIM + i) * __ldg(gradhat + (q * NP + pa) * DIM + j);
-          g[i] = s;
-        }
-        const double w = __ldg(weight + m);
-        const double* s6 = S + 6 * m;
-        if constexpr (DIM == 3) {
-          f[0] += w * (g[0] * s6[0] + g[1] * s6[3] + g[2] * s6[5]);
-          f[1] += w * (g[1] * s6[1] + g[0] * s6[3] + g[2] * s6[4]);
-          f[2] += w * (g[2] * s6[2] + g[1] * s6[4] + g[0] * s6[5]);
-        } else {
-          f[0] += w * (g[0] * s6[0] + g[1] * s6[3]);
-          f[1] += w * (g[1] * s6[1] + g[0] * s6[3]);
-        }
+        for (int j = 1; j < DIM; ++j)
+          s = __fma_rn(__ldg(inv + m * DIM * DIM + j * DIM + i), __ldg(gradhat + (q * NP + p) * DIM + j), s);
+        g[i] = s;
+      }
+      const double w = __ldg(weight + m);
+      const double* s6 = S + 6 * m;
+      if constexpr (DIM == 3) {
+        fe[0] = __fma_rn(w, __fma_rn(g[2], s6[5], __fma_rn(g[1], s6[3], __dmul_rn(g[0], s6[0]))), fe[0]);
+        fe[1] = __fma_rn(w, __fma_rn(g[2], s6[4], __fma_rn(g[0], s6[3], __dmul_rn(g[1], s6[1]))), fe[1]);
+        fe[2] = __fma_rn(w, __fma_rn(g[0], s6[5], __fma_rn(g[1], s6[4], __dmul_rn(g[2], s6[2]))), fe[2]);
+      } else {
+        fe[0] = __fma_rn(w, __fma_rn(g[1], s6[3], __dmul_rn(g[0], s6[0])), fe[0]);
+        fe[1] = __fma_rn(w, __fma_rn(g[0], s6[3], __dmul_rn(g[1], s6[1])), fe[1]);
       }
     }
 #pragma unroll
-    for (int i = 0; i < DIM; ++i) F[DIM * a + i] = f[i];
+    for (int i = 0; i < DIM; ++i) fws[t * DIM + i] = fe[i];
+  }
+}
+
+template <int DIM>
+__global__ void k_fold_forces(int64_t n_nodes, const int64_t* __restrict__ n2e_ptr, const int32_t* __restrict__ n2e,
+                              const double* __restrict__ fws, double* __restrict__ F) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_nodes * DIM;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = t / DIM;
+    const int i = (int)(t - a * DIM);
+    double f = 0.0;
+    for (int64_t k = n2e_ptr[a]; k < n2e_ptr[a + 1]; ++k) f = __dadd_rn(f, __ldg(fws + (int64_t)n2e[k] * DIM + i));
+    F[t] = f;
   }
 }
 
@@ -617,15 +632,17 @@ int launch_strains(int family, int dim, int64_t n_e, const int32_t* elem, const 
   return 0;
 }
 
-int launch_internal_forces(int family, int dim, int64_t n_nodes, const int64_t* n2e_ptr,
+int launch_internal_forces(int family, int dim, int64_t n_nodes, int64_t n_e, const int64_t* n2e_ptr,
                            const int32_t* n2e, const double* inv, const double* weight,
-                           const double* gradhat, const double* S, double* F_out,
+                           const double* gradhat, const double* S, double* fws, double* F_out,
                            cudaStream_t st, int num_sms) {
   bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
     constexpr int DIM = decltype(D)::value;
     constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
-    k_internal_forces<DIM, NP, NQ><<<grid_for(n_nodes, 128, num_sms), 128, 0, st>>>(
-        n_nodes, n2e_ptr, n2e, inv, weight, gradhat, S, F_out);
+    if (n_e > 0)
+      k_elem_forces<DIM, NP, NQ><<<grid_for(n_e * NP, 256, num_sms), 256, 0, st>>>(n_e, inv, weight, gradhat, S,
+                                                                                    fws);
+    k_fold_forces<DIM><<<grid_for(n_nodes * DIM, 256, num_sms), 256, 0, st>>>(n_nodes, n2e_ptr, n2e, fws, F_out);
   });
   if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
   EPFEM_CUDA_TRY(cudaGetLastError());

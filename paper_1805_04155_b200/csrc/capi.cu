@@ -60,6 +60,7 @@ struct epfem_cache {
   unsigned* emask = nullptr;  // per-element plastic-point bitmask
   int npc = 64, max_span = 0, max_items = 0;  // row-stream plan
   int32_t* range_order = nullptr;             // row-stream CTA -> node range (space-filling curve)
+  double* fws = nullptr;                      // element internal-force records (2D fused forces step)
   // overlapped Newton step: row chunk k (nodes [nchunk[k], nchunk[k+1]))
   // needs exactly the element chunks 0..k (elements [echunk[j], echunk[j+1]))
   int n_chunks = 1;
@@ -307,7 +308,8 @@ int epfem_cache_destroy(epfem_cache* c) {
                   c->weight,  c->shear,       c->bulk,        c->pat.n2e_ptr,  c->pat.n2e,
                   c->pat.nbr_ptr, c->pat.row_ptr, c->pat.col_idx, c->pat.slot, c->K_elast,
                   c->scratch, c->emask, c->mega_sched, c->mega_rlo, c->mega_rhi, c->mega_flag,
-                  c->mega_sync, c->range_order, c->ovl_rlo, c->ovl_rhi, c->ovl_flag, c->ovl_sync};
+                  c->mega_sync, c->range_order, c->ovl_rlo, c->ovl_rhi, c->ovl_flag, c->ovl_sync,
+                  c->fws};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -533,6 +535,7 @@ int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_materi
   CT(cudaMalloc(&c->scratch, sizeof(double) * std::max<size_t>(
                                  tangent_workspace_doubles(I.family, I.dim, I.n_elements), 1)));
   CT(cudaMalloc(&c->emask, sizeof(unsigned) * std::max<int64_t>(I.n_elements, 1)));
+  CT(cudaMalloc(&c->fws, sizeof(double) * std::max<size_t>((size_t)I.n_elements * I.n_p * I.dim, 1)));
   if (I.n_nodes > 0)
     if (int rc = plan_row_stream(I.n_nodes, I.dim, c->pat.nbr_ptr, c->pat.n2e_ptr, st, &c->npc,
                                  &c->max_span, &c->max_items))
@@ -779,6 +782,42 @@ int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* c, const epfem_material
   return finish(ctx);
 }
 
+int epfem_newton_step_f(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
+                        const double* E, const double* Ep_prev, const double* Hard_prev,
+                        const epfem_constitutive_out* out, double* K_values, double* F_out) {
+  if (!K_values || !aligned16(K_values))
+    return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: K must be 16-byte aligned");
+  if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
+  if (c->info.n_nodes > 0 && !F_out) return fail(EPFEM_ERR_INVALID, "internal_forces: null argument");
+  // The fused 2D form (the constitutive kernel forms the element force
+  // records, the row stream folds them) is opt-in, EPFEM_FORCES_FUSED=1:
+  // measured on B200, cfg2, it adds 0.10 ms to the step against 0.08 ms for
+  // the two-pass K9 after it (the records' point loop and the staging of
+  // every point sit on each warp's critical path).
+  const char* ff = getenv("EPFEM_FORCES_FUSED");
+  if (ff && ff[0] == '1' && forces_fused_supported(c->info.family, c->info.dim) && c->info.n_elements > 0) {
+    ConstArgs a;
+    GatherArgs g;
+    if (int rc = delta_args(ctx, c, mat, E, Ep_prev, Hard_prev, out, &a, &g)) return rc;
+    g.fws = c->fws;
+    if (int rc = launch_newton_forces(mat->model, c->info.family, c->info.dim, a, g, ctx->stream)) return rc;
+    GatherArgs r = gather_args(c);
+    r.base = c->K_elast;
+    r.out = K_values;
+    r.fws = c->fws;
+    r.F_out = F_out;
+    if (int rc = launch_row_stream(c->info.family, c->info.dim, r, ctx->stream)) return rc;
+    return finish(ctx);
+  }
+  if (int rc = epfem_newton_step(ctx, c, mat, E, Ep_prev, Hard_prev, out, K_values)) return rc;
+  if (c->info.n_nodes == 0) return 0;
+  if (int rc = launch_internal_forces(c->info.family, c->info.dim, c->info.n_nodes, c->info.n_elements, c->pat.n2e_ptr,
+                                      c->pat.n2e, c->inv, c->weight, c->gradhat, out->S, c->fws, F_out, ctx->stream,
+                                      ctx->num_sms))
+    return rc;
+  return finish(ctx);
+}
+
 int epfem_newton_step_u(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
                         const double* u, const double* Ep_prev, const double* Hard_prev,
                         const epfem_constitutive_out* out, double* E_out, double* K_values) {
@@ -885,9 +924,9 @@ int epfem_internal_forces(epfem_ctx* ctx, const epfem_cache* c, const double* S,
   if (int rc = check_ctx(ctx)) return rc;
   if (!c || !S || !F) return fail(EPFEM_ERR_INVALID, "internal_forces: null argument");
   if (c->info.n_nodes == 0) return 0;
-  if (int rc = launch_internal_forces(c->info.family, c->info.dim, c->info.n_nodes, c->pat.n2e_ptr,
-                                      c->pat.n2e, c->inv, c->weight, c->gradhat, S, F, ctx->stream,
-                                      ctx->num_sms))
+  if (int rc = launch_internal_forces(c->info.family, c->info.dim, c->info.n_nodes, c->info.n_elements,
+                                      c->pat.n2e_ptr, c->pat.n2e, c->inv, c->weight, c->gradhat, S, c->fws, F,
+                                      ctx->stream, ctx->num_sms))
     return rc;
   return finish(ctx);
 }

@@ -171,8 +171,14 @@ struct SmemIn {
 // The return map at point q (constitutive.cpp:76-196).  `sink(f)` is called
 // at plastic points with the tangent functor f(i, j) = D(i, j).  Returns the
 // plastic flag.
-template <int MODEL, class In, class Sink>
-__device__ __forceinline__ bool eval_point(const ConstArgs& a, int64_t q, const In& in, Sink& sink) {
+// `ssink(s6)` (optional) receives the stress at every point (the fused
+// internal-forces step stages w S for F = B^T (w S)).
+struct NoSSink {
+  __device__ __forceinline__ void operator()(const double*) const {}
+};
+template <int MODEL, class In, class Sink, class SSink = NoSSink>
+__device__ __forceinline__ bool eval_point(const ConstArgs& a, int64_t q, const In& in, Sink& sink,
+                                           SSink ssink = SSink{}) {
   const double G = a.G ? __ldg(a.G + q) : a.Gu;
   const double K = a.K ? __ldg(a.K + q) : a.Ku;
   double e[6], ep[6];
@@ -205,6 +211,7 @@ __device__ __forceinline__ bool eval_point(const ConstArgs& a, int64_t q, const 
       s6[i] = s;
     }
     if (a.S) store6(a.S, q, s6);
+    ssink(s6);
     if (a.flags) a.flags[q] = 0;
     if (a.pm) a.pm[q] = 0;
     if (a.sm) a.sm[q] = 0;
@@ -241,6 +248,7 @@ __device__ __forceinline__ bool eval_point(const ConstArgs& a, int64_t q, const 
     if (a.am) a.am[q] = 0;
     if (!plastic) {
       if (a.S) store6(a.S, q, sig);
+      ssink(sig);
       if (a.Ep_out) store6(a.Ep_out, q, ep);
       if (a.Hard_out) store6(a.Hard_out, q, h);
       write_tangent(a, q, false, [&](int i, int j) { return cel(K, G, i, j); });
@@ -255,6 +263,7 @@ __device__ __forceinline__ bool eval_point(const ConstArgs& a, int64_t q, const 
 #pragma unroll
     for (int i = 0; i < 6; ++i) out[i] = sig[i] - 2.0 * G * lam * nh[i];
     if (a.S) store6(a.S, q, out);
+    ssink(out);
     const double c4 = 4.0 * G * G / denom;
     const double cy = c4 * Y / ns;
     auto f = [&](int i, int j) {
@@ -299,6 +308,7 @@ __device__ __forceinline__ bool eval_point(const ConstArgs& a, int64_t q, const 
       if (a.sm) a.sm[q] = 0;
       if (a.am) a.am[q] = 0;
       if (a.S) store6(a.S, q, sig);
+      ssink(sig);
       if (a.Ep_out) store6(a.Ep_out, q, ep);
       write_tangent(a, q, false, [&](int i, int j) { return cel(K, G, i, j); });
       return false;
@@ -321,6 +331,7 @@ __device__ __forceinline__ bool eval_point(const ConstArgs& a, int64_t q, const 
 #pragma unroll
       for (int i = 0; i < 6; ++i) out[i] = sig[i] - lam * mh[i];
       if (a.S) store6(a.S, q, out);
+      ssink(out);
       const double c1 = 2.0 * sqrt2 * G * G * lam / rho;
       auto f = [&](int i, int j) {
         return cel(K, G, i, j) - c1 * (devop(i, j) - nh[i] * nh[j]) - mh[i] * mh[j] / dsm;
@@ -345,6 +356,7 @@ __device__ __forceinline__ bool eval_point(const ConstArgs& a, int64_t q, const 
 #pragma unroll
     for (int i = 0; i < 6; ++i) out[i] = (c / eta) * iota(i);
     if (a.S) store6(a.S, q, out);
+    ssink(out);
     auto f = [&](int, int) { return 0.0; };
     write_tangent(a, q, true, f);
     sink(f);
@@ -499,13 +511,19 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DeltaCfg<DIM, 
 // (EPW * RECB doubles, 16-byte aligned).  MEGA: the records leave through
 // plain coalesced stores (the one-launch step publishes them with a release
 // flag right after; no async-proxy writes to order).
-template <int MODEL, int NP, int NQ, bool FROM_U, bool MEGA>
+// FORCES (internal forces fused, epfem_newton_step_f): every point also
+// stages dphi and (w, S11, S22, S12) after its record (stride REC + 4), and
+// lane (element, node p) forms the element's internal-force record
+// F_e[p] = sum_q w_q B_p(q)^T S_q (the explicit-rounding sequence of
+// k_internal_forces) into g.fws; the row stream folds the records per node.
+template <int MODEL, int NP, int NQ, bool FROM_U, bool MEGA, bool FORCES = false>
 __device__ __forceinline__ void newton_warp_group(ConstArgs c, const GatherArgs& g, int64_t e0, double* st_w,
                                                   double* out_w, int lane) {
   constexpr int DIM = 2;
   using W = WarpCfg<DIM, NP, NQ>;
   static_assert(W::EPW * NQ <= 32 && W::EPW * W::NT <= 32, "warp mapping");
-  constexpr int EPW = W::EPW, REC = W::REC;
+  static_assert(!(FORCES && FROM_U), "the forces step reads E");
+  constexpr int EPW = W::EPW, REC0 = W::REC, REC = REC0 + (FORCES ? 4 : 0);
   constexpr unsigned QMASK = NQ >= 32 ? 0xffffffffu : (1u << NQ) - 1u;
   constexpr int RECB = W::NB * W::D2;  // doubles per element workspace record
   c.DS = nullptr;  // hot path: S, flags, packed D only
@@ -570,8 +588,9 @@ __device__ __forceinline__ void newton_warp_group(ConstArgs c, const GatherArgs&
         }
       }
       const double wq = __ldg(g.weight + m);
+      if constexpr (FORCES) stage_geometry<DIM, NP, true>(st, jinv, g.gradhat, q);
       auto stage = [&](auto&& f) {
-        stage_geometry<DIM, NP, true>(st, jinv, g.gradhat, q);
+        if constexpr (!FORCES) stage_geometry<DIM, NP, true>(st, jinv, g.gradhat, q);
         stage_dw<DIM>(st + NP * DIM, wq, g, m, f);
       };
 #else
@@ -580,7 +599,17 @@ __device__ __forceinline__ void newton_warp_group(ConstArgs c, const GatherArgs&
         stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f);
       };
 #endif
-      plastic = eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
+      if constexpr (FORCES) {
+        auto ss = [&](const double* s6) {
+          st[REC0] = wq;
+          st[REC0 + 1] = s6[0];
+          st[REC0 + 2] = s6[1];
+          st[REC0 + 3] = s6[3];
+        };
+        plastic = eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage, ss);
+      } else {
+        plastic = eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
+      }
       }
     }
   }
@@ -616,6 +645,24 @@ __device__ __forceinline__ void newton_warp_group(ConstArgs c, const GatherArgs&
       }
     }
   }
+  if constexpr (FORCES) {
+    // element internal-force records: lane (element, node p), points in order
+    for (int t = lane; t < EPW * NP; t += 32) {
+      const int le = t / NP, p = t - (t / NP) * NP;
+      if (e0 + le >= g.e_end) continue;
+      double f0 = 0.0, f1 = 0.0;
+#pragma unroll 1
+      for (int q = 0; q < NQ; ++q) {
+        const double* r = st_w + (le * NQ + q) * REC;
+        const double g0 = r[p * 2], g1 = r[p * 2 + 1];
+        const double w = r[REC0], s0 = r[REC0 + 1], s1 = r[REC0 + 2], s3 = r[REC0 + 3];
+        f0 = __fma_rn(w, __fma_rn(g1, s3, __dmul_rn(g0, s0)), f0);
+        f1 = __fma_rn(w, __fma_rn(g0, s3, __dmul_rn(g1, s1)), f1);
+      }
+      double2* o = reinterpret_cast<double2*>(g.fws + ((e0 + le) * NP + p) * DIM);
+      *o = make_double2(f0, f1);
+    }
+  }
   // the workspace records leave through the TMA unit: whole 1-KB-class
   // records instead of 8-byte scattered stores from every lane
   if (MEGA) {
@@ -642,12 +689,12 @@ __device__ __forceinline__ void newton_warp_group(ConstArgs c, const GatherArgs&
   }
 }
 
-template <int MODEL, int NP, int NQ, bool FROM_U = false>
+template <int MODEL, int NP, int NQ, bool FROM_U = false, bool FORCES = false>
 __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
     k_newton_warp(ConstArgs c, GatherArgs g) {
   pdl_trigger();
   using W = WarpCfg<2, NP, NQ>;
-  __shared__ double s_st[W::WPB][W::EPW * NQ * W::REC];
+  __shared__ double s_st[W::WPB][W::EPW * NQ * (W::REC + (FORCES ? 4 : 0))];
   __shared__ __align__(16) double s_out[W::WPB][W::EPW * W::NB * W::D2];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (!FROM_U && g.pf_dist > 0) {
@@ -655,7 +702,7 @@ __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
     prefetch_elements<2, NQ>(c, g, eb, eb + W::WPB * W::EPW);
   }
   const int64_t e0 = g.e_begin + ((int64_t)blockIdx.x * W::WPB + w) * W::EPW;
-  newton_warp_group<MODEL, NP, NQ, FROM_U, false>(c, g, e0, s_st[w], s_out[w], lane);
+  newton_warp_group<MODEL, NP, NQ, FROM_U, false, FORCES>(c, g, e0, s_st[w], s_out[w], lane);
 }
 
 // k_newton_warp_pf (2D, EPFEM_FUSED=pf): k_newton_warp with two element
@@ -1543,6 +1590,34 @@ int launch_newton_mega(int model, int family, int dim, const ConstArgs& c, const
   });
   if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
   if (rc) return rc;
+  EPFEM_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// Fused internal-forces step (2D warp kernel with FORCES).
+bool forces_fused_supported(int family, int dim) { return dim == 2 && family >= 0; }
+
+int launch_newton_forces(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g, cudaStream_t st) {
+  if (g.e_end <= g.e_begin) return 0;
+  bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
+    constexpr int DIM = decltype(D)::value;
+    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
+    if constexpr (DIM == 2) {
+      using W = WarpCfg<DIM, NP, NQ>;
+      const int64_t per = (int64_t)W::EPW * W::WPB;
+      const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
+      switch (model) {
+        case EPFEM_MODEL_VON_MISES:
+          k_newton_warp<EPFEM_MODEL_VON_MISES, NP, NQ, false, true><<<blocks, W::THREADS, 0, st>>>(c, g);
+          break;
+        case EPFEM_MODEL_DRUCKER_PRAGER:
+          k_newton_warp<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ, false, true><<<blocks, W::THREADS, 0, st>>>(c, g);
+          break;
+        default: k_newton_warp<EPFEM_MODEL_ELASTIC, NP, NQ, false, true><<<blocks, W::THREADS, 0, st>>>(c, g); break;
+      }
+    }
+  });
+  if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
   EPFEM_CUDA_TRY(cudaGetLastError());
   return 0;
 }

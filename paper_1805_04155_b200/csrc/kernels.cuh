@@ -62,6 +62,10 @@ struct GatherArgs {
   const double* u;
   double* E_out;
   int pf_dist;  // fused kernels: CTA b prefetches (L2) the inputs of CTA b + pf_dist (0: off)
+  // internal forces fused into the step (epfem_newton_step_f): per-element
+  // force records (n_elements x n_p x dim) and the assembled F (n_dofs)
+  double* fws;
+  double* F_out;
 };
 // One-launch Newton step (k_newton_mega): an ordered item list of producer
 // groups (>= 0: one warp group of EPW elements through the fused update) and
@@ -121,6 +125,8 @@ int build_pattern(int family, int dim, int64_t n_nodes, int64_t n_e, const int32
 int launch_gather(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);
 int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);
 int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st);
+bool forces_fused_supported(int family, int dim);
+int launch_newton_forces(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g, cudaStream_t st);
 int launch_delta(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);  // pass 1 over [e_begin, e_end)
 int launch_newton_fused_u(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
                           cudaStream_t st);  // E = B u inside (GatherArgs::u)
@@ -146,9 +152,9 @@ int plan_chunks(int64_t n_nodes, int64_t n_elements, int np, const int64_t* n2e_
 int launch_strains(int family, int dim, int64_t n_e, const int32_t* elem, const double* inv,
                    const double* gradhat, const double* u, double* E, cudaStream_t st,
                    int num_sms);
-int launch_internal_forces(int family, int dim, int64_t n_nodes, const int64_t* n2e_ptr,
+int launch_internal_forces(int family, int dim, int64_t n_nodes, int64_t n_e, const int64_t* n2e_ptr,
                            const int32_t* n2e, const double* inv, const double* weight,
-                           const double* gradhat, const double* S, double* F_out,
+                           const double* gradhat, const double* S, double* fws, double* F_out,
                            cudaStream_t st, int num_sms);
 
 

@@ -234,7 +234,10 @@ __device__ __forceinline__ int ld_acquire_gpu_i(const int* p) {
   return v;
 }
 
-template <int DIM, int NP, int NQ, bool FLAGS = false>
+// FORCES: also fold the element internal-force records (GatherArgs::fws,
+// written by the fused kernel) into F for the range's nodes, every item in
+// item order from zero (k_internal_forces' association, hence its bits).
+template <int DIM, int NP, int NQ, bool FLAGS = false, bool FORCES = false>
 __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM_ROW_MINB20 : 0)
     k_row_stream(GatherArgs a, int npc, OvlArgs o) {
   extern __shared__ __align__(128) double img_raw[];
@@ -295,6 +298,14 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
     const int32_t it = __ldg(a.n2e + i_begin + k);
     s_item[k] = __ldcg(a.emask + it / NP) ? it : -1;
   }
+  if constexpr (FORCES) {  // the range's force records, folded after the K adds
+    double* s_fv = reinterpret_cast<double*>(
+        (reinterpret_cast<uintptr_t>(s_vptr + npc + 1) + 15) & ~uintptr_t(15));
+    for (int k = tid; k < nitems * DIM; k += blockDim.x) {
+      const int it = __ldg(a.n2e + i_begin + k / DIM);
+      s_fv[k] = a.fws[(size_t)it * DIM + k % DIM];
+    }
+  }
   __syncthreads();
   if (a1 > a0 && !zero_base) mbar_wait(&s_bar, 0);
   // Items are taken UB at a time: every lane first issues the loads of all
@@ -348,6 +359,19 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
           }
         __syncwarp();
       }
+    }
+  }
+  if constexpr (FORCES) {
+    // the range's force records (item = (element, local node) = record
+    // index) staged by all threads, then one thread per (node, component)
+    // sums them in item order from zero
+    const double* s_fv = reinterpret_cast<const double*>(
+        (reinterpret_cast<uintptr_t>(s_vptr + npc + 1) + 15) & ~uintptr_t(15));
+    for (int t = tid; t < nloc * DIM; t += blockDim.x) {
+      const int ln = t / DIM, i = t - (t / DIM) * DIM;
+      double f = 0.0;
+      for (int k = s_iptr[ln]; k < s_iptr[ln + 1]; ++k) f = __dadd_rn(f, s_fv[k * DIM + i]);
+      a.F_out[(n0 + ln) * DIM + i] = f;
     }
   }
   fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
@@ -589,8 +613,8 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
     constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
     const int64_t rblocks = (a.n_end - a.n_begin + a.npc - 1) / a.npc;
     if (rblocks <= 0) return;
-    const size_t smem = row_range_smem(a);
-    auto kern = k_row_stream<DIM, NP, NQ>;
+    const size_t smem = row_range_smem(a) + (a.F_out ? 16 + sizeof(double) * DIM * (size_t)a.max_items : 0);
+    auto kern = a.F_out ? k_row_stream<DIM, NP, NQ, false, true> : k_row_stream<DIM, NP, NQ>;
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) { rc = cuda_fail(e, "cudaFuncSetAttribute"); return; }

@@ -542,3 +542,39 @@ def test_elastic_assembly_both_paths(cuda, oracle, k5):
                         "-k", "pattern_and_elastic or tangent_matches_oracle or all_element_types"],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+@pytest.mark.parametrize("name", ["cfg2", "cfg1", "cfg3", "cfg4", "cfg5"])
+def test_newton_step_with_internal_forces(cuda, oracle, name, fused, monkeypatch):
+    """epfem_newton_step_f (fused in 2D): S, flags, D
+    and K are the bits of epfem_newton_step, F the bits of K9
+    (epfem_internal_forces on the step's S), and F matches the oracle's
+    internal_forces (assembly.cpp:215-225) within 1e-12 of max |F|; for the
+    default (step + two-pass K9) and the fused 2D form (EPFEM_FORCES_FUSED)."""
+    import paper_1805_04155_b200 as P
+    monkeypatch.setenv("EPFEM_FORCES_FUSED", fused)
+    from paper_1805_04155_b200.synthetic import CONFIGS, calibrate, displacement
+    cfg = CONFIGS[name]
+    mesh = cfg.mesh(REDUCED[name])
+    mat = cfg.material(mesh.n_int)
+    gc = P.build_assembly_cache(P.Mesh.from_structured(mesh, cuda), mat)
+    u = torch.from_numpy(displacement(mesh.coord, cfg.seed)).to(cuda)
+    E1 = gc.strains(u)
+    s = calibrate(E1, mat, 0.3)[0] if cfg.model != "elastic" else 1.0
+    E = (s * E1).contiguous()
+    e1, e2 = P.TangentEngine(gc, mat), P.TangentEngine(gc, mat)
+    S1, f1, D1, K1 = e1.step(E)
+    S2, f2, D2, K2, F = e2.step_f(E)
+    torch.cuda.synchronize()
+    assert np.array_equal(_np(f1), _np(f2)) and np.array_equal(_np(S1), _np(S2))
+    m = (_np(f1) & 1).astype(bool)
+    assert np.array_equal(_np(D1)[m], _np(D2)[m])
+    assert np.array_equal(_np(K1).view(np.uint64), _np(K2).view(np.uint64))
+    F9 = P.internal_forces(gc, S2)
+    torch.cuda.synchronize()
+    assert np.array_equal(_np(F).view(np.uint64), _np(F9).view(np.uint64))
+    K, G = P.elastic_moduli(cfg.young, cfg.poisson)
+    oc = oracle.Cache(cfg.family, cfg.dim, mesh.coord, mesh.elem, G, K)
+    Fref = oc.internal_forces(_np(S2))
+    assert np.abs(_np(F) - Fref).max() <= 1e-12 * np.abs(Fref).max()
