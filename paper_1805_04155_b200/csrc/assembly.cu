@@ -465,6 +465,102 @@ __global__ void k_fold_forces(int64_t n_nodes, const int64_t* __restrict__ n2e_p
 }
 
 // ---------------------------------------------------------------------------
+// K5 for one-point P1 elements (cfg1), thread per node: the node's two (three)
+// K rows are formed from its elements in item order, each element block with
+// delta.cuh's explicit-rounding sequence (Dw = w C, T_a = B_a^T Dw, block =
+// T_a B_b), into a shared-memory image laid out exactly like K[v0, v1) of the
+// CTA's nodes (a node's rows are contiguous and nodes are numbered in row
+// order), which the CTA then writes out coalesced.  One launch, one wave on
+// cfg1 (66,049 nodes): the warp-per-node gather it replaces spent its time in
+// per-node dependent load chains.
+template <int DIM, int NP>
+__global__ void k_elastic_p1(GatherArgs a) {
+  extern __shared__ double img[];
+  constexpr int NS = DIM == 3 ? 6 : 3, D2 = DIM * DIM;
+  const int64_t first = (int64_t)blockIdx.x * blockDim.x;
+  const int64_t last = min(first + (int64_t)blockDim.x, a.n_nodes);
+  const int64_t v0 = __ldg(a.nbr_ptr + first) * D2, v1 = __ldg(a.nbr_ptr + last) * D2;
+  for (int64_t k = threadIdx.x; k < v1 - v0; k += blockDim.x) img[k] = 0.0;
+  __syncthreads();
+  const int64_t node = first + threadIdx.x;
+  if (node < last) {
+    const int64_t nb0 = __ldg(a.nbr_ptr + node);
+    const int row_len = DIM * (int)(__ldg(a.nbr_ptr + node + 1) - nb0);
+    double* seg = img + (nb0 * D2 - v0);
+    const bool uniform_c = a.shear == nullptr && a.bulk == nullptr;
+    for (int64_t t = __ldg(a.n2e_ptr + node); t < __ldg(a.n2e_ptr + node + 1); ++t) {
+      const int32_t item = __ldg(a.n2e + t);
+      const int64_t e = item / NP;  // one point per element: m = e
+      const int pa = item - (int)e * NP;
+      double J[D2];
+#pragma unroll
+      for (int k = 0; k < D2; ++k) J[k] = __ldg(a.inv + e * D2 + k);
+      const double w = __ldg(a.weight + e);
+      double G2 = 0.0, Km = 0.0;
+      if (!uniform_c) {
+        G2 = 2.0 * (a.shear ? __ldg(a.shear + e) : a.shear_u);
+        Km = a.bulk ? __ldg(a.bulk + e) : a.bulk_u;
+      }
+      double dw[NS][NS];
+#pragma unroll
+      for (int r = 0; r < NS; ++r)
+#pragma unroll
+        for (int c = r; c < NS; ++c) {  // stage_c (delta.cuh)
+          const int ri = arow<DIM>(r), ci = arow<DIM>(c);
+          const double vol = (ri < 3 && ci < 3) ? 1.0 : 0.0;
+          const double dev = ((ri == ci) ? (ri < 3 ? 1.0 : 0.5) : 0.0) - vol / 3.0;
+          const double cel = uniform_c ? a.Cu[pk_index(ri, ci)] : __fma_rn(G2, dev, __dmul_rn(Km, vol));
+          dw[r][c] = dw[c][r] = __dmul_rn(w, cel);
+        }
+      double d[NP][DIM];
+#pragma unroll
+      for (int p = 0; p < NP; ++p) point_dphi<DIM>(J, a.gradhat + p * DIM, d[p]);
+      double ga[DIM];
+#pragma unroll
+      for (int i = 0; i < DIM; ++i) ga[i] = d[0][i];
+#pragma unroll
+      for (int p = 1; p < NP; ++p)
+        if (p == pa)
+#pragma unroll
+          for (int i = 0; i < DIM; ++i) ga[i] = d[p][i];
+      double T[DIM][NS];  // delta_phase2's T_a
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        if constexpr (DIM == 3) {
+          T[0][c] = __fma_rn(ga[2], dw[5][c], __fma_rn(ga[1], dw[3][c], __dmul_rn(ga[0], dw[0][c])));
+          T[1][c] = __fma_rn(ga[2], dw[4][c], __fma_rn(ga[0], dw[3][c], __dmul_rn(ga[1], dw[1][c])));
+          T[DIM - 1][c] = __fma_rn(ga[0], dw[5][c], __fma_rn(ga[1], dw[4][c], __dmul_rn(ga[2], dw[2][c])));
+        } else {
+          T[0][c] = __fma_rn(ga[1], dw[2][c], __dmul_rn(ga[0], dw[0][c]));
+          T[1][c] = __fma_rn(ga[0], dw[2][c], __dmul_rn(ga[1], dw[1][c]));
+        }
+      }
+#pragma unroll
+      for (int pb = 0; pb < NP; ++pb) {
+        const int sl = __ldg(a.slot + (int64_t)item * NP + pb);
+        const double h0 = d[pb][0], h1 = d[pb][1], h2 = DIM == 3 ? d[pb][DIM - 1] : 0.0;
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) {
+          double b[DIM];
+          if constexpr (DIM == 3) {
+            b[0] = __fma_rn(T[i][5], h2, __fma_rn(T[i][3], h1, __fma_rn(T[i][0], h0, 0.0)));
+            b[1] = __fma_rn(T[i][4], h2, __fma_rn(T[i][3], h0, __fma_rn(T[i][1], h1, 0.0)));
+            b[DIM - 1] = __fma_rn(T[i][5], h0, __fma_rn(T[i][4], h1, __fma_rn(T[i][2], h2, 0.0)));
+          } else {
+            b[0] = __fma_rn(T[i][2], h1, __fma_rn(T[i][0], h0, 0.0));
+            b[1] = __fma_rn(T[i][2], h0, __fma_rn(T[i][1], h1, 0.0));
+          }
+#pragma unroll
+          for (int j = 0; j < DIM; ++j) seg[i * row_len + sl * DIM + j] += b[j];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int64_t k = threadIdx.x; k < v1 - v0; k += blockDim.x) a.out[v0 + k] = img[k];
+}
+
+// ---------------------------------------------------------------------------
 // Host launchers (called from capi.cu)
 
 static inline int grid_for(int64_t n, int threads, int num_sms) {
@@ -616,6 +712,24 @@ int launch_gather(int family, int dim, int mode, const GatherArgs& a, cudaStream
   if (rc) return rc;
   EPFEM_CUDA_TRY(cudaGetLastError());
   return 0;
+}
+
+// K5 for P1 meshes (k_elastic_p1); block size by dimension so that the
+// image (at most threads x max_seg doubles) fits the shared memory.
+int launch_elastic_p1(int family, int dim, const GatherArgs& a, cudaStream_t st) {
+  if (a.n_nodes == 0) return 0;
+  if (family != EPFEM_P1) return fail(EPFEM_ERR_INVALID, "elastic_p1: P1 elements only");
+  const int threads = dim == 2 ? 128 : 32;
+  const size_t smem = sizeof(double) * (size_t)a.max_seg * threads;
+  const int64_t blocks = (a.n_nodes + threads - 1) / threads;
+  auto run = [&](auto kern) -> int {
+    if (smem > 48 * 1024)
+      EPFEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)blocks, threads, smem, st>>>(a);
+    EPFEM_CUDA_TRY(cudaGetLastError());
+    return 0;
+  };
+  return dim == 2 ? run(k_elastic_p1<2, 3>) : run(k_elastic_p1<3, 4>);
 }
 
 int launch_strains(int family, int dim, int64_t n_e, const int32_t* elem, const double* inv,

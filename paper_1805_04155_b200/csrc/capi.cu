@@ -131,19 +131,20 @@ static T* rebase(T* p, int64_t per_point, int64_t first_point) {
 // point and a zero base: element blocks (k_delta_warp / k_elem_delta_staged in
 // elastic mode) then the row stream — measured 2.4x / 1.8x / 1.6x faster than
 // the one-pass row-block gather (k_gather) on cfg2 / cfg3 / cfg4.  P1
-// elements (one point, a 6x6 or 12x12 element matrix; cfg1) keep the gather,
-// whose single launch wins there (0.035 vs 0.047 ms).  EPFEM_K5=gather|rows
-// overrides.  The cache's K_elast and epfem_assemble_elastic use the same
-// path, so they agree bit for bit.
+// elements (one point, a 6x6 or 12x12 element matrix; cfg1) use the
+// thread-per-node k_elastic_p1 (one launch).  EPFEM_K5=gather|rows|p1
+// overrides (p1 on P1 meshes only).  The cache's K_elast and
+// epfem_assemble_elastic use the same path, so they agree bit for bit.
 static int elastic_assembly(const GatherArgs& g0, int family, int dim, double* out, cudaStream_t st) {
   static const int force = [] {
     const char* v = getenv("EPFEM_K5");
-    return v ? (v[0] == 'g' ? 1 : 2) : 0;
+    return v ? (v[0] == 'g' ? 1 : (v[0] == 'p' ? 3 : 2)) : 0;
   }();
   GatherArgs g = g0;
   g.out = out;
-  const bool gather = force ? force == 1 : family == EPFEM_P1;
-  if (gather) return launch_gather(family, dim, 0, g, st);
+  const int path = force ? force : (family == EPFEM_P1 ? 3 : 2);
+  if (path == 3 && family == EPFEM_P1) return launch_elastic_p1(family, dim, g, st);
+  if (path == 1) return launch_gather(family, dim, 0, g, st);
   g.base = nullptr;
   g.e_begin = 0;
   g.e_end = g.n_elements;

@@ -123,6 +123,7 @@ int launch_jacobians(int family, int dim, int64_t n_e, const int32_t* elem, cons
 int build_pattern(int family, int dim, int64_t n_nodes, int64_t n_e, const int32_t* elem,
                   cudaStream_t st, int num_sms, PatternOut* o);
 int launch_gather(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);
+int launch_elastic_p1(int family, int dim, const GatherArgs& a, cudaStream_t st);  // K5, P1 meshes
 int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);
 int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st);
 bool forces_fused_supported(int family, int dim);
