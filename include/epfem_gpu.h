@@ -66,7 +66,8 @@ enum epfem_status {
   EPFEM_ERR_ZERO_DEVIATOR = 3,  /* DP smooth return with zero deviator */
   EPFEM_ERR_CUDA = 4,           /* CUDA runtime / launch failure */
   EPFEM_ERR_NOMEM = 5,
-  EPFEM_ERR_UNSUPPORTED = 6     /* e.g. node valence > 255 */
+  EPFEM_ERR_UNSUPPORTED = 6,    /* e.g. node valence > 255 */
+  EPFEM_ERR_SOLVER = 7          /* restricted_solve above tolerance (reference: epfem::SolverError) */
 };
 
 /* epfem::ElementFamily order (reference_elements.hpp:10) */
@@ -249,6 +250,25 @@ int epfem_strains(epfem_ctx* ctx, const epfem_cache* cache, const double* u, dou
 /* K9: F = B^T (weight * S) (assembly.cpp:291-301). */
 int epfem_internal_forces(epfem_ctx* ctx, const epfem_cache* cache, const double* S,
                           double* F);
+
+/* Newton-loop linear algebra on any CSR matrix
+ * (row_ptr int64 n+1, col_idx int32, values), device pointers.
+ * epfem_restricted_solve: restricted_solve (linalg.cpp:37-121) with the
+ *   reference's LinearSolver::conjugate_gradient method: Jacobi-preconditioned
+ *   CG on K[free, free] (free_mask: one byte per row, NULL = all free),
+ *   stopping at |r| <= rel_tol |b_free|, at most max_iters iterations (<= 0:
+ *   10 n).  x (n) is zero on fixed rows.  EPFEM_ERR_SOLVER with the
+ *   reference's message ("restricted_solve: residual <r> above tolerance")
+ *   when the true residual |b - K x|_free / |b_free| exceeds rel_tol or is
+ *   not finite.  iters / residual (may be NULL) report the solve.
+ *   Deterministic (fixed-order reductions).
+ * epfem_energy_norm: sqrt(max(v . K v, 0)) (linalg.cpp:123-127). */
+int epfem_restricted_solve(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                           const double* values, const double* rhs, const uint8_t* free_mask,
+                           double rel_tol, int64_t max_iters, double* x, int64_t* iters,
+                           double* residual);
+int epfem_energy_norm(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                      const double* values, const double* v, double* out);
 
 #ifdef __cplusplus
 }

@@ -12,3 +12,7 @@ from .api import (  # noqa: F401
     internal_forces, unpack_D, uniform_drucker_prager, uniform_elastic, uniform_von_mises,
 )
 from .mesh import ElementType, StructuredMesh, structured_mesh  # noqa: F401
+from .solver import (  # noqa: F401
+    LinearSolver, NewtonResult, NewtonSettings, NonConvergenceError, SolveSettings, SolverError, energy_norm,
+    newton_solve, restricted_solve,
+)

@@ -55,7 +55,8 @@ EXPORTS = [
     "epfem_cache_workspace",
     "epfem_assemble_elastic", "epfem_assemble_tangent", "epfem_assemble_tangent_ds",
     "epfem_newton_step", "epfem_newton_step_u", "epfem_newton_step_f", "epfem_constitutive_delta", "epfem_assemble_rows", "epfem_newton_range",
-    "epfem_delta_range", "epfem_strains", "epfem_internal_forces",
+    "epfem_delta_range", "epfem_strains", "epfem_internal_forces", "epfem_restricted_solve",
+    "epfem_energy_norm",
 ]
 
 _lib = None
@@ -106,6 +107,9 @@ def lib() -> C.CDLL:
     L.epfem_delta_range.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_int64, C.c_int64]
     L.epfem_strains.argtypes = [_P, _P, _P, _P]
     L.epfem_internal_forces.argtypes = [_P, _P, _P, _P]
+    L.epfem_restricted_solve.argtypes = [_P, _I64, _P, _P, _P, _P, _P, _D, _I64, _P, C.POINTER(_I64),
+                                         C.POINTER(_D)]
+    L.epfem_energy_norm.argtypes = [_P, _I64, _P, _P, _P, _P, C.POINTER(_D)]
     _lib = L
     return L
 

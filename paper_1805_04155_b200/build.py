@@ -31,6 +31,7 @@ SOURCES = {
     "assembly.cu": [],
     "tangent.cu": [],
     "capi.cu": [],
+    "solve.cu": [],
     "tables.cpp": [],
 }
 HEADERS = ["common.cuh", "kernels.cuh", "delta.cuh", "tma.cuh", "rows.cuh"]

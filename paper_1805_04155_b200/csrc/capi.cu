@@ -932,4 +932,31 @@ int epfem_internal_forces(epfem_ctx* ctx, const epfem_cache* c, const double* S,
   return finish(ctx);
 }
 
+int epfem_restricted_solve(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                           const double* values, const double* rhs, const uint8_t* free_mask,
+                           double rel_tol, int64_t max_iters, double* x, int64_t* iters,
+                           double* residual) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (n < 0 || (n > 0 && (!row_ptr || !col_idx || !values || !rhs || !x)))
+    return fail(EPFEM_ERR_INVALID, "restricted_solve: dimension mismatch");
+  int64_t it = 0;
+  double res = 0.0;
+  if (int rc = cg_solve(n, row_ptr, col_idx, values, free_mask, rhs, x, rel_tol,
+                        max_iters > 0 ? max_iters : 10 * std::max<int64_t>(n, 1), ctx->stream, &it, &res))
+    return rc;
+  if (iters) *iters = it;
+  if (residual) *residual = res;
+  if (!std::isfinite(res) || res > rel_tol)
+    return fail(EPFEM_ERR_SOLVER, "restricted_solve: residual " + std::to_string(res) + " above tolerance");
+  return 0;
+}
+
+int epfem_energy_norm(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                      const double* values, const double* v, double* out) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!out || n < 0 || (n > 0 && (!row_ptr || !col_idx || !values || !v)))
+    return fail(EPFEM_ERR_INVALID, "energy_norm: dimension mismatch");
+  return energy_norm(n, row_ptr, col_idx, values, v, ctx->stream, out);
+}
+
 }  // extern "C"

@@ -142,6 +142,11 @@ bool ovl_supported(int family, int dim, int* group_elems);
 int launch_newton_ovl(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g, const OvlArgs& o,
                       int ctas_per_sm, cudaStream_t st);
 int launch_row_stream_ovl(int family, int dim, const GatherArgs& a, const OvlArgs& o, cudaStream_t st);
+int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, const uint8_t* mask,
+             const double* b, double* x_out, double rel_tol, int64_t max_iters, cudaStream_t st,
+             int64_t* iters_out, double* residual_out);
+int energy_norm(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, const double* x,
+                cudaStream_t st, double* out);
 size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements);
 int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
                     cudaStream_t st, int* npc_out, int* span_out, int* items_out, int budget_bytes = 0);

@@ -1,0 +1,248 @@
+// Newton-loop linear algebra on the device:
+// restricted_solve (linalg.cpp:37-121) as Jacobi-preconditioned conjugate
+// gradients on K[free, free] — the reference's LinearSolver::conjugate_gradient
+// (Eigen ConjugateGradient, DiagonalPreconditioner, tolerance rel_tol on
+// |r| / |b|, at most 10 m iterations) — and energy_norm (linalg.cpp:123-127).
+//
+// The restriction is never formed: the masked SpMV y = M (K (M x)), M =
+// diag(free), acts on the free block and leaves fixed dofs at zero, which is
+// exactly the reference's restrict / solve / scatter.  Every reduction is a
+// fixed two-stage tree (per-block partials, then one block over the partials
+// in order), so a solve is bitwise reproducible run to run.  The scalars
+// (alpha, beta, r.z) stay on the device; the host reads the residual every
+// kCheck iterations.
+#include <cmath>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace epfem_gpu {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kBlocks = 592;  // 4 x 148 SMs: partial-sum slots per reduction
+constexpr int kCheck = 8;     // iterations between host residual checks
+
+// warp per row: lanes stride the row's entries, fixed-order shuffle tree
+__global__ void __launch_bounds__(kThreads) k_spmv_masked(int64_t n, const int64_t* __restrict__ rp,
+                                                          const int32_t* __restrict__ ci,
+                                                          const double* __restrict__ v,
+                                                          const uint8_t* __restrict__ mask,
+                                                          const double* __restrict__ x, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; r < n;
+       r += ((int64_t)gridDim.x * kThreads) >> 5) {
+    double s = 0.0;
+    if (!mask || mask[r]) {
+      for (int64_t k = rp[r] + lane; k < rp[r + 1]; k += 32) {
+        const int32_t c = __ldg(ci + k);
+        if (!mask || __ldg(mask + c)) s = __fma_rn(__ldg(v + k), __ldg(x + c), s);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+    }
+    if (lane == 0) y[r] = s;
+  }
+}
+
+__device__ __forceinline__ double block_sum(double s, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) sh[w] = s;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < kThreads / 32; ++k) t = __dadd_rn(t, sh[k]);
+  __syncthreads();
+  return t;  // valid in thread 0
+}
+
+// partial[b] = sum over the block's grid-stride slice of a[i] * b[i] (two dots at once)
+__global__ void __launch_bounds__(kThreads) k_dot2(int64_t n, const double* __restrict__ a0,
+                                                   const double* __restrict__ b0, const double* __restrict__ a1,
+                                                   const double* __restrict__ b1, double* partial) {
+  __shared__ double sh[kThreads / 32];
+  double s0 = 0.0, s1 = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
+    s0 = __fma_rn(a0[i], b0[i], s0);
+    if (a1) s1 = __fma_rn(a1[i], b1[i], s1);
+  }
+  const double t0 = block_sum(s0, sh);
+  const double t1 = block_sum(s1, sh);
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = t0;
+    partial[2 * blockIdx.x + 1] = t1;
+  }
+}
+
+// scalar state: [0] r.z, [1] p.Ap, [2] r.r, [3] alpha, [4] beta, [5] b.b
+enum { S_RZ = 0, S_PAP = 1, S_RR = 2, S_ALPHA = 3, S_BETA = 4, S_BB = 5 };
+
+// sum the partials in order; mode 0: (r.z, r.r) -> beta; mode 1: p.Ap -> alpha;
+// mode 2: initial (r.z, b.b)
+__global__ void k_finish(const double* partial, int nb, double* sc, int mode) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double t0 = 0.0, t1 = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    t0 = __dadd_rn(t0, partial[2 * b]);
+    t1 = __dadd_rn(t1, partial[2 * b + 1]);
+  }
+  if (mode == 1) {
+    sc[S_PAP] = t0;
+    sc[S_ALPHA] = t0 != 0.0 ? sc[S_RZ] / t0 : 0.0;
+  } else if (mode == 0) {
+    sc[S_BETA] = sc[S_RZ] != 0.0 ? t0 / sc[S_RZ] : 0.0;
+    sc[S_RZ] = t0;
+    sc[S_RR] = t1;
+  } else {
+    sc[S_RZ] = t0;
+    sc[S_BB] = t1;
+    sc[S_RR] = t1;
+  }
+}
+
+// x = 0, r = M b, z = M r / d, p = z; diag d from the CSR (fixed dofs: 1)
+__global__ void k_cg_init(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                          const double* __restrict__ v, const uint8_t* __restrict__ mask,
+                          const double* __restrict__ b, double* x, double* r, double* z, double* p, double* d) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
+    double di = 0.0;
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+      if (ci[k] == i) di = v[k];
+    const bool f = !mask || mask[i];
+    // Eigen's DiagonalPreconditioner: 1 / diag, or 1 where the diagonal is 0
+    const double inv = di != 0.0 ? 1.0 / di : 1.0;
+    d[i] = inv;
+    const double ri = f ? b[i] : 0.0;
+    x[i] = 0.0;
+    r[i] = ri;
+    z[i] = f ? ri * inv : 0.0;
+    p[i] = z[i];
+  }
+}
+
+// x += alpha p; r -= alpha Ap; z = M r / d
+__global__ void k_cg_update(int64_t n, const double* __restrict__ sc, const uint8_t* __restrict__ mask,
+                            const double* __restrict__ d, const double* __restrict__ p,
+                            const double* __restrict__ Ap, double* x, double* r, double* z) {
+  const double alpha = sc[S_ALPHA];
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
+    x[i] = __fma_rn(alpha, p[i], x[i]);
+    const double ri = __fma_rn(-alpha, Ap[i], r[i]);
+    r[i] = ri;
+    z[i] = (!mask || mask[i]) ? ri * d[i] : 0.0;
+  }
+}
+
+// p = z + beta p
+__global__ void k_cg_dir(int64_t n, const double* __restrict__ sc, const double* __restrict__ z, double* p) {
+  const double beta = sc[S_BETA];
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads)
+    p[i] = __fma_rn(beta, p[i], z[i]);
+}
+
+// rb = M (b - Ap)
+__global__ void k_resid(int64_t n, const uint8_t* __restrict__ mask, const double* __restrict__ b,
+                        const double* __restrict__ Ap, double* rb) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads)
+    rb[i] = (!mask || mask[i]) ? b[i] - Ap[i] : 0.0;
+}
+
+unsigned grid_rows(int64_t n) {
+  const int64_t warps = (int64_t)kBlocks * (kThreads / 32);
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kThreads / 32 - 1) / (kThreads / 32),
+                                                          warps / (kThreads / 32)));
+}
+
+struct Work {  // device scratch of one solve
+  double *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *Ap = nullptr, *d = nullptr;
+  double *partial = nullptr, *sc = nullptr;
+  ~Work() {
+    for (double* q : {x, r, z, p, Ap, d, partial, sc})
+      if (q) cudaFree(q);
+  }
+};
+
+}  // namespace
+
+int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, const uint8_t* mask,
+             const double* b, double* x_out, double rel_tol, int64_t max_iters, cudaStream_t st,
+             int64_t* iters_out, double* residual_out) {
+  *iters_out = 0;
+  *residual_out = 0.0;
+  if (n == 0) return 0;
+  Work w;
+  for (double** q : {&w.x, &w.r, &w.z, &w.p, &w.Ap, &w.d})
+    EPFEM_CUDA_TRY(cudaMalloc(q, sizeof(double) * n));
+  EPFEM_CUDA_TRY(cudaMalloc(&w.partial, sizeof(double) * 2 * kBlocks));
+  EPFEM_CUDA_TRY(cudaMalloc(&w.sc, sizeof(double) * 8));
+  const unsigned gb = (unsigned)std::min<int64_t>(kBlocks, (n + kThreads - 1) / kThreads);
+  k_cg_init<<<gb, kThreads, 0, st>>>(n, rp, ci, v, mask, b, w.x, w.r, w.z, w.p, w.d);
+  k_dot2<<<gb, kThreads, 0, st>>>(n, w.r, w.z, w.r, w.r, w.partial);
+  k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 2);
+  double h[8];
+  EPFEM_CUDA_TRY(cudaMemcpyAsync(h, w.sc, sizeof(h), cudaMemcpyDeviceToHost, st));
+  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+  const double bnorm = std::sqrt(h[S_BB]);
+  int64_t it = 0;
+  double rn = bnorm;
+  if (bnorm > 0.0) {
+    while (it < max_iters) {
+      for (int k = 0; k < kCheck && it < max_iters; ++k, ++it) {
+        k_spmv_masked<<<grid_rows(n), kThreads, 0, st>>>(n, rp, ci, v, mask, w.p, w.Ap);
+        k_dot2<<<gb, kThreads, 0, st>>>(n, w.p, w.Ap, nullptr, nullptr, w.partial);
+        k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 1);
+        k_cg_update<<<gb, kThreads, 0, st>>>(n, w.sc, mask, w.d, w.p, w.Ap, w.x, w.r, w.z);
+        k_dot2<<<gb, kThreads, 0, st>>>(n, w.r, w.z, w.r, w.r, w.partial);
+        k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 0);
+        k_cg_dir<<<gb, kThreads, 0, st>>>(n, w.sc, w.z, w.p);
+      }
+      EPFEM_CUDA_TRY(cudaGetLastError());
+      EPFEM_CUDA_TRY(cudaMemcpyAsync(h, w.sc, sizeof(h), cudaMemcpyDeviceToHost, st));
+      EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+      rn = std::sqrt(std::max(h[S_RR], 0.0));
+      if (!(rn > rel_tol * bnorm)) break;  // also stops on NaN
+    }
+  }
+  // true residual |M (b - K x)| / |M b| (linalg.cpp:109-113)
+  k_spmv_masked<<<grid_rows(n), kThreads, 0, st>>>(n, rp, ci, v, mask, w.x, w.Ap);
+  k_resid<<<gb, kThreads, 0, st>>>(n, mask, b, w.Ap, w.z);
+  k_dot2<<<gb, kThreads, 0, st>>>(n, w.z, w.z, nullptr, nullptr, w.partial);
+  k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 1);
+  EPFEM_CUDA_TRY(cudaMemcpyAsync(x_out, w.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  EPFEM_CUDA_TRY(cudaMemcpyAsync(h, w.sc, sizeof(h), cudaMemcpyDeviceToHost, st));
+  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+  EPFEM_CUDA_TRY(cudaGetLastError());
+  *iters_out = it;
+  *residual_out = bnorm > 0.0 ? std::sqrt(std::max(h[S_PAP], 0.0)) / bnorm : 0.0;
+  return 0;
+}
+
+int energy_norm(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, const double* x,
+                cudaStream_t st, double* out) {
+  *out = 0.0;
+  if (n == 0) return 0;
+  double *y = nullptr, *partial = nullptr, *sc = nullptr;
+  EPFEM_CUDA_TRY(cudaMalloc(&y, sizeof(double) * n));
+  EPFEM_CUDA_TRY(cudaMalloc(&partial, sizeof(double) * 2 * kBlocks));
+  EPFEM_CUDA_TRY(cudaMalloc(&sc, sizeof(double) * 8));
+  const unsigned gb = (unsigned)std::min<int64_t>(kBlocks, (n + kThreads - 1) / kThreads);
+  k_spmv_masked<<<grid_rows(n), kThreads, 0, st>>>(n, rp, ci, v, nullptr, x, y);
+  k_dot2<<<gb, kThreads, 0, st>>>(n, x, y, nullptr, nullptr, partial);
+  double zero[8] = {1.0, 0, 0, 0, 0, 0, 0, 0};  // r.z = 1: alpha slot unused
+  EPFEM_CUDA_TRY(cudaMemcpyAsync(sc, zero, sizeof(zero), cudaMemcpyHostToDevice, st));
+  k_finish<<<1, 32, 0, st>>>(partial, gb, sc, 1);
+  double h[8];
+  EPFEM_CUDA_TRY(cudaMemcpyAsync(h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
+  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+  cudaFree(y);
+  cudaFree(partial);
+  cudaFree(sc);
+  EPFEM_CUDA_TRY(cudaGetLastError());
+  *out = std::sqrt(std::max(h[S_PAP], 0.0));  // linalg.cpp:123-127
+  return 0;
+}
+
+}  // namespace epfem_gpu

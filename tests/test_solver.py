@@ -1,0 +1,136 @@
+"""Newton-loop linear algebra and the Newton time step on the GPU (SURVEY
+§8(f) rank 3) against the reference's own tests (tests/test_linalg.cpp:90-162)
+and a restatement of newton_solve (solver.cpp:7-62) on the oracle with the
+reference's default direct solve."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def _csr(A, dev):
+    import scipy.sparse as sp
+    import paper_1805_04155_b200 as P
+    M = sp.csr_matrix(A)
+    M.sort_indices()
+    return P.CsrMatrix(torch.from_numpy(M.indptr.astype(np.int64)).to(dev),
+                       torch.from_numpy(M.indices.astype(np.int32)).to(dev),
+                       torch.from_numpy(M.data.astype(np.float64)).to(dev))
+
+
+def test_restricted_solve_trivial_cases(cuda):
+    """test_linalg.cpp:90-110: identity, and a decoupled 2x2 with one fixed dof."""
+    from paper_1805_04155_b200.solver import restricted_solve
+    x = restricted_solve(_csr(np.eye(3), cuda), torch.tensor([1.0, 0.0, 0.0], dtype=torch.float64, device=cuda),
+                         torch.ones(3, dtype=torch.bool, device=cuda)).cpu().numpy()
+    assert abs(x[0] - 1.0) < 1e-12 and np.abs(x[1:]).max() <= 1e-15
+    x2 = restricted_solve(_csr(np.diag([2.0, 2.0]), cuda), torch.tensor([2.0, 4.0], dtype=torch.float64, device=cuda),
+                          torch.tensor([True, False], device=cuda)).cpu().numpy()
+    assert abs(x2[0] - 1.0) < 1e-12 and x2[1] == 0.0
+
+
+def test_restricted_solve_random_spd(cuda):
+    """test_linalg.cpp:112-151: K = A^T A + 0.5 I, random free set, vs a dense solve."""
+    from paper_1805_04155_b200.solver import SolveSettings, LinearSolver, restricted_solve
+    rng = np.random.default_rng(23)
+    n = 20
+    A = rng.uniform(-1, 1, (n, n))
+    Kd = A.T @ A + 0.5 * np.eye(n)
+    rhs = rng.uniform(-1, 1, n)
+    mask = rng.uniform(size=n) < 0.7
+    mask[0] = True
+    x = restricted_solve(_csr(Kd, cuda), torch.from_numpy(rhs).to(cuda), torch.from_numpy(mask).to(cuda),
+                         SolveSettings(LinearSolver.conjugate_gradient, 1e-12)).cpu().numpy()
+    f = np.nonzero(mask)[0]
+    xf = np.linalg.solve(Kd[np.ix_(f, f)], rhs[f])
+    assert np.abs(x[f] - xf).max() <= 1e-9 * np.abs(xf).max()
+    assert np.all(x[~mask] == 0.0)
+    # deterministic: the same bits on a second solve
+    x2 = restricted_solve(_csr(Kd, cuda), torch.from_numpy(rhs).to(cuda), torch.from_numpy(mask).to(cuda),
+                          SolveSettings(LinearSolver.conjugate_gradient, 1e-12)).cpu().numpy()
+    assert np.array_equal(x.view(np.uint64), x2.view(np.uint64))
+
+
+def test_restricted_solve_reports_singular_systems(cuda):
+    """test_linalg.cpp:153-162: rank-deficient K, incompatible rhs -> SolverError."""
+    from paper_1805_04155_b200.solver import SolverError, restricted_solve
+    with pytest.raises(SolverError, match="restricted_solve: residual .* above tolerance"):
+        restricted_solve(_csr(np.ones((2, 2)), cuda), torch.tensor([1.0, -1.0], dtype=torch.float64, device=cuda))
+
+
+def test_energy_norm(cuda):
+    from paper_1805_04155_b200.solver import energy_norm
+    rng = np.random.default_rng(5)
+    A = rng.uniform(-1, 1, (12, 12))
+    Kd = A.T @ A
+    v = rng.uniform(-1, 1, 12)
+    e = energy_norm(_csr(Kd, cuda), torch.from_numpy(v).to(cuda))
+    assert abs(e - np.sqrt(v @ Kd @ v)) <= 1e-12 * np.sqrt(v @ Kd @ v)
+
+
+def _newton_ref(O, oc, mat_args, dirichlet, free, f_ext, eps, max_iters):
+    """solver.cpp:7-62 restated on the oracle (test infrastructure), with the
+    reference's default direct restricted solve (scipy spsolve on K[free, free])."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spl
+    G, K, a, Y = mat_args
+    Ke = oc.K_elast()
+    Kes = sp.csr_matrix((Ke.data, Ke.indices, Ke.indptr))
+
+    def en(v):
+        return np.sqrt(max(v @ (Kes @ v), 0.0))
+    u = dirichlet.copy()
+    fi = np.nonzero(free)[0]
+    for it in range(1, max_iters + 1):
+        E = oc.strains(u)
+        st = O.constitutive_vm(E, None, None, G, K, a, Y)
+        F = oc.internal_forces(st["S"])
+        Kt = oc.tangent(st["DS"], st["plastic"])
+        Ks = sp.csr_matrix((Kt.data, Kt.indices, Kt.indptr))
+        du = np.zeros_like(u)
+        du[fi] = spl.spsolve(Ks[fi][:, fi].tocsc(), (f_ext - F)[fi])
+        npv = en(u)
+        u = u + du
+        ncu = en(u)
+        if npv + ncu == 0.0 or en(du) <= eps * (npv + ncu):
+            st = O.constitutive_vm(oc.strains(u), None, None, G, K, a, Y)
+            return u, it, int(st["plastic"].sum())
+    raise AssertionError("reference Newton did not converge")
+
+
+def test_newton_solve_matches_reference(cuda, oracle):
+    """A 2D Q2-8 von Mises time step (cfg2's material): left edge clamped, the
+    right edge pulled by u_x = delta (yielding), GPU newton_solve (device CG,
+    rel_tol 1e-12) vs the restated reference with a direct solve: the same
+    number of Newton iterations and plastic points, u within 1e-8."""
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.solver import NewtonSettings, SolveSettings, newton_solve
+    from paper_1805_04155_b200.synthetic import CONFIGS
+    cfg = CONFIGS["cfg2"]
+    mesh = cfg.mesh(6)
+    mat = cfg.material(mesh.n_int)
+    K, G = P.elastic_moduli(cfg.young, cfg.poisson)
+    x = mesh.coord.reshape(-1, 2)
+    n_dofs = x.shape[0] * 2
+    dirichlet = np.zeros(n_dofs)
+    free = np.ones(n_dofs, bool)
+    left, right = np.isclose(x[:, 0], 0.0), np.isclose(x[:, 0], x[:, 0].max())
+    free[2 * np.nonzero(left)[0]] = False
+    free[2 * np.nonzero(left)[0] + 1] = False
+    free[2 * np.nonzero(right)[0]] = False
+    dirichlet[2 * np.nonzero(right)[0]] = 0.004 * x[:, 0].max()
+    f_ext = np.zeros(n_dofs)
+    gc = P.build_assembly_cache(P.Mesh.from_structured(mesh, cuda), mat)
+    res = newton_solve(gc, mat, P.IntegrationState.zero(mesh.n_int, device=cuda),
+                       torch.from_numpy(dirichlet), torch.from_numpy(free), torch.from_numpy(f_ext),
+                       NewtonSettings(eps_newton=1e-9, max_iters=25, linear=SolveSettings(rel_tol=1e-12)))
+    oc = oracle.Cache(cfg.family, cfg.dim, mesh.coord, mesh.elem, G, K)
+    u_ref, iters_ref, npl_ref = _newton_ref(oracle, oc, (G, K, cfg.p1, cfg.p2), dirichlet, free, f_ext, 1e-9, 25)
+    u = res.u.cpu().numpy()
+    assert 0 < npl_ref < mesh.n_int, npl_ref
+    assert res.record.newton_iters == iters_ref
+    assert res.record.n_plastic == npl_ref
+    assert np.abs(u - u_ref).max() <= 1e-8 * np.abs(u_ref).max()
+    assert np.all(u[~free] == dirichlet[~free])
