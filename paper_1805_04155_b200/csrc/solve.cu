@@ -143,6 +143,19 @@ __global__ void k_cg_dir(int64_t n, const double* __restrict__ sc, const double*
     p[i] = __fma_rn(beta, p[i], z[i]);
 }
 
+// restart from the true residual: r = M (b - K x) (Ap holds K x), z = M r / d, p = z
+__global__ void k_cg_restart(int64_t n, const uint8_t* __restrict__ mask, const double* __restrict__ b,
+                             const double* __restrict__ Ap, const double* __restrict__ d, double* r, double* z,
+                             double* p) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
+    const bool f = !mask || mask[i];
+    const double ri = f ? b[i] - Ap[i] : 0.0;
+    r[i] = ri;
+    z[i] = f ? ri * d[i] : 0.0;
+    p[i] = z[i];
+  }
+}
+
 // rb = M (b - Ap)
 __global__ void k_resid(int64_t n, const uint8_t* __restrict__ mask, const double* __restrict__ b,
                         const double* __restrict__ Ap, double* rb) {
@@ -187,36 +200,48 @@ int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, c
   EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
   const double bnorm = std::sqrt(h[S_BB]);
   int64_t it = 0;
-  double rn = bnorm;
-  if (bnorm > 0.0) {
-    while (it < max_iters) {
-      for (int k = 0; k < kCheck && it < max_iters; ++k, ++it) {
-        k_spmv_masked<<<grid_rows(n), kThreads, 0, st>>>(n, rp, ci, v, mask, w.p, w.Ap);
-        k_dot2<<<gb, kThreads, 0, st>>>(n, w.p, w.Ap, nullptr, nullptr, w.partial);
-        k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 1);
-        k_cg_update<<<gb, kThreads, 0, st>>>(n, w.sc, mask, w.d, w.p, w.Ap, w.x, w.r, w.z);
-        k_dot2<<<gb, kThreads, 0, st>>>(n, w.r, w.z, w.r, w.r, w.partial);
-        k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 0);
-        k_cg_dir<<<gb, kThreads, 0, st>>>(n, w.sc, w.z, w.p);
+  double res = 0.0;
+  // CG on the recurrence residual, then the true residual |M (b - K x)|; on
+  // recurrence drift (true residual above the tolerance although the
+  // recurrence met it) restart from the true residual, at most 3 times (the
+  // reference's direct solve refines likewise, linalg.cpp:97-103)
+  for (int restart = 0;; ++restart) {
+    if (bnorm > 0.0) {
+      while (it < max_iters) {
+        for (int k = 0; k < kCheck && it < max_iters; ++k, ++it) {
+          k_spmv_masked<<<grid_rows(n), kThreads, 0, st>>>(n, rp, ci, v, mask, w.p, w.Ap);
+          k_dot2<<<gb, kThreads, 0, st>>>(n, w.p, w.Ap, nullptr, nullptr, w.partial);
+          k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 1);
+          k_cg_update<<<gb, kThreads, 0, st>>>(n, w.sc, mask, w.d, w.p, w.Ap, w.x, w.r, w.z);
+          k_dot2<<<gb, kThreads, 0, st>>>(n, w.r, w.z, w.r, w.r, w.partial);
+          k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 0);
+          k_cg_dir<<<gb, kThreads, 0, st>>>(n, w.sc, w.z, w.p);
+        }
+        EPFEM_CUDA_TRY(cudaGetLastError());
+        EPFEM_CUDA_TRY(cudaMemcpyAsync(h, w.sc, sizeof(h), cudaMemcpyDeviceToHost, st));
+        EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+        const double rn = std::sqrt(std::max(h[S_RR], 0.0));
+        if (!(rn > rel_tol * bnorm)) break;  // also stops on NaN
       }
-      EPFEM_CUDA_TRY(cudaGetLastError());
-      EPFEM_CUDA_TRY(cudaMemcpyAsync(h, w.sc, sizeof(h), cudaMemcpyDeviceToHost, st));
-      EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
-      rn = std::sqrt(std::max(h[S_RR], 0.0));
-      if (!(rn > rel_tol * bnorm)) break;  // also stops on NaN
     }
+    // true residual |M (b - K x)| / |M b| (linalg.cpp:109-113)
+    k_spmv_masked<<<grid_rows(n), kThreads, 0, st>>>(n, rp, ci, v, mask, w.x, w.Ap);
+    k_resid<<<gb, kThreads, 0, st>>>(n, mask, b, w.Ap, w.z);
+    k_dot2<<<gb, kThreads, 0, st>>>(n, w.z, w.z, nullptr, nullptr, w.partial);
+    k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 1);
+    EPFEM_CUDA_TRY(cudaMemcpyAsync(h, w.sc, sizeof(h), cudaMemcpyDeviceToHost, st));
+    EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+    EPFEM_CUDA_TRY(cudaGetLastError());
+    res = bnorm > 0.0 ? std::sqrt(std::max(h[S_PAP], 0.0)) / bnorm : 0.0;
+    if (!(res > rel_tol) || restart == 3 || it >= max_iters || !std::isfinite(res)) break;
+    k_cg_restart<<<gb, kThreads, 0, st>>>(n, mask, b, w.Ap, w.d, w.r, w.z, w.p);
+    k_dot2<<<gb, kThreads, 0, st>>>(n, w.r, w.z, w.r, w.r, w.partial);
+    k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 2);  // r.z, r.r (the b.b slot is not read again)
   }
-  // true residual |M (b - K x)| / |M b| (linalg.cpp:109-113)
-  k_spmv_masked<<<grid_rows(n), kThreads, 0, st>>>(n, rp, ci, v, mask, w.x, w.Ap);
-  k_resid<<<gb, kThreads, 0, st>>>(n, mask, b, w.Ap, w.z);
-  k_dot2<<<gb, kThreads, 0, st>>>(n, w.z, w.z, nullptr, nullptr, w.partial);
-  k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 1);
   EPFEM_CUDA_TRY(cudaMemcpyAsync(x_out, w.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-  EPFEM_CUDA_TRY(cudaMemcpyAsync(h, w.sc, sizeof(h), cudaMemcpyDeviceToHost, st));
   EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
-  EPFEM_CUDA_TRY(cudaGetLastError());
   *iters_out = it;
-  *residual_out = bnorm > 0.0 ? std::sqrt(std::max(h[S_PAP], 0.0)) / bnorm : 0.0;
+  *residual_out = res;
   return 0;
 }
 

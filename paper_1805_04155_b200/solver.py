@@ -70,6 +70,7 @@ class TimeStepRecord:
     tangent_seconds: float = 0.0
     iterations: List[IterationSample] = field(default_factory=list)
     linear_iters: List[int] = field(default_factory=list)
+    ratios: List[float] = field(default_factory=list)  # |du|_e / (|u_prev|_e + |u|_e) per iteration
 
 
 @dataclass
@@ -169,11 +170,15 @@ def newton_solve(cache: AssemblyCache, mat: MaterialField, state_prev: Integrati
         u = u + du
         norm_curr = energy_norm(Ke, u, ctx=eng.ctx)
         denom = norm_prev + norm_curr
-        if denom == 0.0 or energy_norm(Ke, du, ctx=eng.ctx) <= settings.eps_newton * denom:
+        ndu = energy_norm(Ke, du, ctx=eng.ctx)
+        rec.ratios.append(ndu / denom if denom > 0.0 else 0.0)
+        if denom == 0.0 or ndu <= settings.eps_newton * denom:
             converged = True
             break
     if not converged:
-        raise NonConvergenceError(f"newton_solve: no convergence within {settings.max_iters} iterations")
+        err = NonConvergenceError(f"newton_solve: no convergence within {settings.max_iters} iterations")
+        err.record = rec
+        raise err
     state = evaluate_constitutive(cache.strains(u), state_prev, mat)
     rec.n_plastic = int(state.plastic_mask.sum().item())
     return NewtonResult(u=u, state=state, record=rec)
