@@ -80,15 +80,26 @@ __global__ void __launch_bounds__(kThreads) k_dot2(int64_t n, const double* __re
 // scalar state: [0] r.z, [1] p.Ap, [2] r.r, [3] alpha, [4] beta, [5] b.b
 enum { S_RZ = 0, S_PAP = 1, S_RR = 2, S_ALPHA = 3, S_BETA = 4, S_BB = 5 };
 
-// sum the partials in order; mode 0: (r.z, r.r) -> beta; mode 1: p.Ap -> alpha;
-// mode 2: initial (r.z, b.b)
-__global__ void k_finish(const double* partial, int nb, double* sc, int mode) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double t0 = 0.0, t1 = 0.0;
-  for (int b = 0; b < nb; ++b) {
-    t0 = __dadd_rn(t0, partial[2 * b]);
-    t1 = __dadd_rn(t1, partial[2 * b + 1]);
+// sum the partials with a fixed-order tree (one 1024-thread block, partial b
+// in slot b); mode 0: (r.z, r.r) -> beta; mode 1: p.Ap -> alpha; mode 2:
+// initial (r.z, b.b)
+constexpr int kFinish = 1024;
+static_assert(kBlocks <= kFinish, "one finishing block");
+__global__ void __launch_bounds__(kFinish) k_finish(const double* partial, int nb, double* sc, int mode) {
+  __shared__ double s0[kFinish], s1[kFinish];
+  const int t = threadIdx.x;
+  s0[t] = t < nb ? partial[2 * t] : 0.0;
+  s1[t] = t < nb ? partial[2 * t + 1] : 0.0;
+  __syncthreads();
+  for (int o = kFinish / 2; o > 0; o >>= 1) {
+    if (t < o) {
+      s0[t] = __dadd_rn(s0[t], s0[t + o]);
+      s1[t] = __dadd_rn(s1[t], s1[t + o]);
+    }
+    __syncthreads();
   }
+  if (t != 0) return;
+  const double t0 = s0[0], t1 = s1[0];
   if (mode == 1) {
     sc[S_PAP] = t0;
     sc[S_ALPHA] = t0 != 0.0 ? sc[S_RZ] / t0 : 0.0;
@@ -163,10 +174,10 @@ __global__ void k_resid(int64_t n, const uint8_t* __restrict__ mask, const doubl
     rb[i] = (!mask || mask[i]) ? b[i] - Ap[i] : 0.0;
 }
 
+// one warp per row (the row loop of a warp is a chain of dependent loads:
+// enough warps in flight is what hides it)
 unsigned grid_rows(int64_t n) {
-  const int64_t warps = (int64_t)kBlocks * (kThreads / 32);
-  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kThreads / 32 - 1) / (kThreads / 32),
-                                                          warps / (kThreads / 32)));
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kThreads / 32 - 1) / (kThreads / 32), 1 << 22));
 }
 
 struct Work {  // device scratch of one solve
@@ -181,11 +192,27 @@ struct Work {  // device scratch of one solve
 }  // namespace
 
 int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, const uint8_t* mask,
-             const double* b, double* x_out, double rel_tol, int64_t max_iters, cudaStream_t st,
+             const double* b, double* x_out, double rel_tol, int64_t max_iters, cudaStream_t caller,
              int64_t* iters_out, double* residual_out) {
   *iters_out = 0;
   *residual_out = 0.0;
   if (n == 0) return 0;
+  // the solve runs on a private stream ordered after the caller's work (the
+  // iteration chunks are captured into a graph, which the legacy default
+  // stream does not allow); it is host-synchronous on return
+  struct Stream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t e = nullptr;
+    ~Stream() {
+      if (s) cudaStreamDestroy(s);
+      if (e) cudaEventDestroy(e);
+    }
+  } ps;
+  EPFEM_CUDA_TRY(cudaStreamCreateWithFlags(&ps.s, cudaStreamNonBlocking));
+  EPFEM_CUDA_TRY(cudaEventCreateWithFlags(&ps.e, cudaEventDisableTiming));
+  EPFEM_CUDA_TRY(cudaEventRecord(ps.e, caller));
+  EPFEM_CUDA_TRY(cudaStreamWaitEvent(ps.s, ps.e, 0));
+  cudaStream_t st = ps.s;
   Work w;
   for (double** q : {&w.x, &w.r, &w.z, &w.p, &w.Ap, &w.d})
     EPFEM_CUDA_TRY(cudaMalloc(q, sizeof(double) * n));
@@ -194,11 +221,25 @@ int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, c
   const unsigned gb = (unsigned)std::min<int64_t>(kBlocks, (n + kThreads - 1) / kThreads);
   k_cg_init<<<gb, kThreads, 0, st>>>(n, rp, ci, v, mask, b, w.x, w.r, w.z, w.p, w.d);
   k_dot2<<<gb, kThreads, 0, st>>>(n, w.r, w.z, w.r, w.r, w.partial);
-  k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 2);
+  k_finish<<<1, kFinish, 0, st>>>(w.partial, gb, w.sc, 2);
   double h[8];
   EPFEM_CUDA_TRY(cudaMemcpyAsync(h, w.sc, sizeof(h), cudaMemcpyDeviceToHost, st));
   EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
   const double bnorm = std::sqrt(h[S_BB]);
+  auto iteration = [&] {
+    k_spmv_masked<<<grid_rows(n), kThreads, 0, st>>>(n, rp, ci, v, mask, w.p, w.Ap);
+    k_dot2<<<gb, kThreads, 0, st>>>(n, w.p, w.Ap, nullptr, nullptr, w.partial);
+    k_finish<<<1, kFinish, 0, st>>>(w.partial, gb, w.sc, 1);
+    k_cg_update<<<gb, kThreads, 0, st>>>(n, w.sc, mask, w.d, w.p, w.Ap, w.x, w.r, w.z);
+    k_dot2<<<gb, kThreads, 0, st>>>(n, w.r, w.z, w.r, w.r, w.partial);
+    k_finish<<<1, kFinish, 0, st>>>(w.partial, gb, w.sc, 0);
+    k_cg_dir<<<gb, kThreads, 0, st>>>(n, w.sc, w.z, w.p);
+  };
+  struct GraphExec {
+    cudaGraphExec_t e = nullptr;
+    ~GraphExec() { if (e) cudaGraphExecDestroy(e); }
+  } chunk_holder;
+  cudaGraphExec_t& chunk = chunk_holder.e;
   int64_t it = 0;
   double res = 0.0;
   // CG on the recurrence residual, then the true residual |M (b - K x)|; on
@@ -208,14 +249,25 @@ int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, c
   for (int restart = 0;; ++restart) {
     if (bnorm > 0.0) {
       while (it < max_iters) {
-        for (int k = 0; k < kCheck && it < max_iters; ++k, ++it) {
-          k_spmv_masked<<<grid_rows(n), kThreads, 0, st>>>(n, rp, ci, v, mask, w.p, w.Ap);
-          k_dot2<<<gb, kThreads, 0, st>>>(n, w.p, w.Ap, nullptr, nullptr, w.partial);
-          k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 1);
-          k_cg_update<<<gb, kThreads, 0, st>>>(n, w.sc, mask, w.d, w.p, w.Ap, w.x, w.r, w.z);
-          k_dot2<<<gb, kThreads, 0, st>>>(n, w.r, w.z, w.r, w.r, w.partial);
-          k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 0);
-          k_cg_dir<<<gb, kThreads, 0, st>>>(n, w.sc, w.z, w.p);
+        if (!chunk && max_iters - it >= kCheck) {
+          // kCheck iterations as one CUDA graph (seven launches each): the
+          // small systems of a Newton step are launch-bound otherwise
+          cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+          cudaStreamIsCapturing(st, &cs);
+          if (cs == cudaStreamCaptureStatusNone) {
+            EPFEM_CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            for (int k = 0; k < kCheck; ++k) iteration();
+            cudaGraph_t g = nullptr;
+            EPFEM_CUDA_TRY(cudaStreamEndCapture(st, &g));
+            EPFEM_CUDA_TRY(cudaGraphInstantiate(&chunk, g, 0));
+            cudaGraphDestroy(g);
+          }
+        }
+        if (chunk && max_iters - it >= kCheck) {
+          EPFEM_CUDA_TRY(cudaGraphLaunch(chunk, st));
+          it += kCheck;
+        } else {
+          for (int k = 0; k < kCheck && it < max_iters; ++k, ++it) iteration();
         }
         EPFEM_CUDA_TRY(cudaGetLastError());
         EPFEM_CUDA_TRY(cudaMemcpyAsync(h, w.sc, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -228,7 +280,7 @@ int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, c
     k_spmv_masked<<<grid_rows(n), kThreads, 0, st>>>(n, rp, ci, v, mask, w.x, w.Ap);
     k_resid<<<gb, kThreads, 0, st>>>(n, mask, b, w.Ap, w.z);
     k_dot2<<<gb, kThreads, 0, st>>>(n, w.z, w.z, nullptr, nullptr, w.partial);
-    k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 1);
+    k_finish<<<1, kFinish, 0, st>>>(w.partial, gb, w.sc, 1);
     EPFEM_CUDA_TRY(cudaMemcpyAsync(h, w.sc, sizeof(h), cudaMemcpyDeviceToHost, st));
     EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
     EPFEM_CUDA_TRY(cudaGetLastError());
@@ -236,7 +288,7 @@ int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, c
     if (!(res > rel_tol) || restart == 3 || it >= max_iters || !std::isfinite(res)) break;
     k_cg_restart<<<gb, kThreads, 0, st>>>(n, mask, b, w.Ap, w.d, w.r, w.z, w.p);
     k_dot2<<<gb, kThreads, 0, st>>>(n, w.r, w.z, w.r, w.r, w.partial);
-    k_finish<<<1, 32, 0, st>>>(w.partial, gb, w.sc, 2);  // r.z, r.r (the b.b slot is not read again)
+    k_finish<<<1, kFinish, 0, st>>>(w.partial, gb, w.sc, 2);  // r.z, r.r (the b.b slot is not read again)
   }
   EPFEM_CUDA_TRY(cudaMemcpyAsync(x_out, w.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
@@ -258,7 +310,7 @@ int energy_norm(int64_t n, const int64_t* rp, const int32_t* ci, const double* v
   k_dot2<<<gb, kThreads, 0, st>>>(n, x, y, nullptr, nullptr, partial);
   double zero[8] = {1.0, 0, 0, 0, 0, 0, 0, 0};  // r.z = 1: alpha slot unused
   EPFEM_CUDA_TRY(cudaMemcpyAsync(sc, zero, sizeof(zero), cudaMemcpyHostToDevice, st));
-  k_finish<<<1, 32, 0, st>>>(partial, gb, sc, 1);
+  k_finish<<<1, kFinish, 0, st>>>(partial, gb, sc, 1);
   double h[8];
   EPFEM_CUDA_TRY(cudaMemcpyAsync(h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
   EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
