@@ -134,3 +134,49 @@ def test_newton_solve_matches_reference(cuda, oracle):
     assert res.record.n_plastic == npl_ref
     assert np.abs(u - u_ref).max() <= 1e-8 * np.abs(u_ref).max()
     assert np.all(u[~free] == dirichlet[~free])
+
+
+def test_newton_iterates_follow_the_reference_when_diverging(cuda, oracle):
+    """A single too-large load step (16 x 16, the right edge pulled to 0.004
+    from the bare Dirichlet lift) is outside the semismooth Newton's basin for
+    the reference too: the GPU loop's stopping ratios |du|_e / (|u_prev|_e +
+    |u|_e) follow the restated reference's over the first iterations, and both
+    raise NonConvergenceError."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spl
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.synthetic import CONFIGS
+    cfg = CONFIGS["cfg2"]
+    mesh = cfg.mesh(16)
+    mat = cfg.material(mesh.n_int)
+    K, G = P.elastic_moduli(cfg.young, cfg.poisson)
+    x = mesh.coord
+    nd = x.shape[0] * 2
+    dirichlet, free = np.zeros(nd), np.ones(nd, bool)
+    left, right = np.isclose(x[:, 0], 0.0), np.isclose(x[:, 0], x[:, 0].max())
+    free[2 * np.nonzero(left)[0]] = free[2 * np.nonzero(left)[0] + 1] = False
+    free[2 * np.nonzero(right)[0]] = False
+    dirichlet[2 * np.nonzero(right)[0]] = 0.004
+    gc = P.build_assembly_cache(P.Mesh.from_structured(mesh, cuda), mat)
+    with pytest.raises(P.NonConvergenceError) as ex:
+        P.newton_solve(gc, mat, P.IntegrationState.zero(mesh.n_int, device=cuda), torch.from_numpy(dirichlet),
+                       torch.from_numpy(free), torch.zeros(nd, dtype=torch.float64),
+                       P.NewtonSettings(eps_newton=1e-9, max_iters=4, linear=P.SolveSettings(rel_tol=1e-12)))
+    gpu = ex.value.record.ratios
+    oc = oracle.Cache(cfg.family, cfg.dim, mesh.coord, mesh.elem, G, K)
+    Ke = oc.K_elast()
+    Kes = sp.csr_matrix((Ke.data, Ke.indices, Ke.indptr))
+    en = lambda v: np.sqrt(max(v @ (Kes @ v), 0.0))  # noqa: E731
+    u, fi, ref = dirichlet.copy(), np.nonzero(free)[0], []
+    for _ in range(4):
+        st = oracle.constitutive_vm(oc.strains(u), None, None, G, K, cfg.p1, cfg.p2)
+        F = oc.internal_forces(st["S"])
+        Kt = oc.tangent(st["DS"], st["plastic"])
+        Ks = sp.csr_matrix((Kt.data, Kt.indices, Kt.indptr))
+        du = np.zeros_like(u)
+        du[fi] = spl.spsolve(Ks[fi][:, fi].tocsc(), (-F)[fi])
+        a = en(u)
+        u = u + du
+        ref.append(en(du) / (a + en(u)))
+    assert len(gpu) == 4
+    assert np.allclose(gpu, ref, rtol=1e-6, atol=0), (gpu, ref)
