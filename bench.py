@@ -481,7 +481,7 @@ def main():
         else:
             dom_bytes, dom_ms, dom = cons_b, tot_c / reps, "k_newton_fused (constitutive + element delta)"
     else:
-        dom_bytes, dom_ms, dom = asm_b, ms_per_step, "k_gather<elastic> (K5)"
+        dom_bytes, dom_ms, dom = asm_b, ms_per_step, "k_elastic_p1 (K5, P1 meshes)"
     # the same step from nodal displacements with the
     # strains formed inside the constitutive kernel, vs strains + step
     from_u = None
