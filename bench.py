@@ -329,6 +329,17 @@ def run_slabs(args, rank, world, dev, cfg):
                "how": "per rank: H2D of own E/Ep/Hard, step, D2H of own S/flags/K rows; all ranks summed"}
     npl = torch.tensor([float((eng.flags[p0:p1] & 1).sum())], dtype=torch.float64, device=dev)
     dist.all_reduce(npl)
+    # whole-job algorithmic bytes from the owned shares, against
+    # world x the per-GPU HBM peak
+    v0, v1 = eng.own_values
+    n0, n1 = plan.own_nodes
+    e_own = (p1 - p0) // max(1, eng.cache.info.n_q)
+    cnt = torch.tensor([float(v1 - v0), float(n1 - n0), float(e_own)], dtype=torch.float64, device=dev)
+    dist.all_reduce(cnt)
+    cons_b, asm_b = algorithmic_bytes(cfg, int(n_total), int(npl), int(cnt[0]), int(cnt[1]), int(cnt[2]),
+                                      eng.cache.info.n_p)
+    hbm_peak, peak_src = load_peaks()
+    step_gbs = (cons_b + asm_b) / (ms_per_step * 1e-3) / 1e9
     if rank == 0:
         line = {
             "metric": METRIC, "value": n_total / (ms_per_step * 1e-3), "unit": "ip/s",
@@ -341,6 +352,10 @@ def run_slabs(args, rank, world, dev, cfg):
                        "parallelism": f"slab x{world} (one halo cell layer, NCCL interface exchange)",
                        "l2": "inputs larger than L2"},
             "gpu_launches": 3 * args.steps,
+            "roofline": {"bound": "hbm", "kernel": "whole step (fused update + halo deltas + row stream)",
+                         "achieved": step_gbs, "peak": hbm_peak * world, "unit": "GB/s",
+                         "frac": step_gbs / (hbm_peak * world), "traffic": None,
+                         "algorithmic_bytes": cons_b + asm_b, "peak_source": peak_src + f" x {world} GPUs"},
             "clocks": clk.summary(),
             "e2e": e2e,
         }
