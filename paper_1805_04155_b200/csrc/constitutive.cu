@@ -33,6 +33,10 @@
 #ifndef EPFEM_WARP_PAIRS
 #define EPFEM_WARP_PAIRS 1  // 2D warp kernel: phase 2 by row pairs
 #endif
+#ifndef EPFEM_HALFPAIRS20
+#define EPFEM_HALFPAIRS20 0  // Q2-20 CTA kernel with half row pairs (delta_pairs3_half): fewer FMA, but
+                             // measured slower on cfg5 (21.1 vs 16.0 ms; shared-memory loads per FMA)
+#endif
 #ifndef EPFEM_CTA_PAIRS
 #define EPFEM_CTA_PAIRS 1
 #endif
@@ -473,6 +477,22 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DeltaCfg<DIM, 
       const unsigned mask = s_mask[le];
       if (e < g.e_end && mask)
         delta_pairs3<NP, NQ>(&s_st[le][0][0], mask, k / 3, k % 3, g.scratch + (size_t)e * Cfg::NB * Cfg::D2);
+    }
+    return;
+  }
+#endif
+#if EPFEM_HALFPAIRS20
+  // Q2-20: row pairs split in halves (delta_pairs3_half): lane (element,
+  // pair, half, component)
+  if constexpr (DIM == 3 && NP >= 20) {
+    constexpr int PL = 6 * ((NP + 1) / 2);
+    for (int t = tid; t < EPB * PL; t += blockDim.x) {
+      const int le = t / PL, k = t - (t / PL) * PL;
+      const int64_t e = e0 + le;
+      const unsigned mask = s_mask[le];
+      if (e < g.e_end && mask)
+        delta_pairs3_half<NP, NQ>(&s_st[le][0][0], mask, k / 6, k % 3, (k / 3) % 2,
+                                  g.scratch + (size_t)e * Cfg::NB * Cfg::D2);
     }
     return;
   }

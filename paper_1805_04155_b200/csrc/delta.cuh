@@ -603,6 +603,77 @@ __device__ __forceinline__ void delta_pairs3(const double* st_e, unsigned mask, 
   }
 }
 
+// Q2-20 (cfg5): the row pair of delta_pairs3 split in two halves, lane (pair
+// p, component i, half h): half 0 owns the first ceil((NP+1)/2) blocks of the
+// pair (all in row a0 = p, so only T_a0 row i is formed), half 1 the rest
+// (the tail of row a0 and row a1).  33 instead of 63 accumulators per lane,
+// 7,290 FMA per plastic point against 9,720 for padded chunks of 4 (6,750
+// optimal).  Per-entry FMA sequences are those of delta_phase2: same bits.
+template <int NP, int NQ>
+__device__ __forceinline__ void delta_pairs3_half(const double* st_e, unsigned mask, int p, int i, int half,
+                                                  double* __restrict__ rec) {
+  using C = Pair3Cfg<NP, NQ>;
+  constexpr int NS = C::NS, REC = C::REC, D2 = C::D2, NBLK = C::NBLK;
+  constexpr int KH = (NBLK + 1) / 2;
+  static_assert(NP - (NP / 2 - 1) >= KH, "half 0 stays in row a0 for every pair");
+  const int a0 = p, a1 = NP - 1 - p;
+  const bool twin = a1 != a0;
+  const int k0 = half * KH;
+  const int d0 = i, d1 = i == 2 ? 4 : 3, d2 = i == 0 ? 5 : (i == 1 ? 4 : 5);
+  const int e1 = i == 0 ? 1 : (i == 1 ? 0 : 1), e2 = i == 0 ? 2 : (i == 1 ? 2 : 0);
+  auto pk = [](int r, int c) {
+    const int lo = r < c ? r : c, hi = r < c ? c : r;
+    return lo * NS - lo * (lo - 1) / 2 + (hi - lo);
+  };
+  double acc[KH][3];
+#pragma unroll
+  for (int k = 0; k < KH; ++k) acc[k][0] = acc[k][1] = acc[k][2] = 0.0;
+  while (mask) {
+    const int q = __ffs(mask) - 1;
+    mask &= mask - 1u;
+    const double* st = st_e + q * REC;
+    const double* dw = st + NP * 3;
+    double T0[NS], T1[NS];
+    {
+      const double* g0 = st + a0 * 3;
+      const double* g1 = st + a1 * 3;
+      const double gA0 = g0[d0], gA1 = g0[e1], gA2 = g0[e2];
+      const double gB0 = g1[d0], gB1 = g1[e1], gB2 = g1[e2];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        const double w0 = dw[pk(d0, c)], w1 = dw[pk(d1, c)], w2 = dw[pk(d2, c)];
+        T0[c] = __fma_rn(gA2, w2, __fma_rn(gA1, w1, __dmul_rn(gA0, w0)));
+        T1[c] = half ? __fma_rn(gB2, w2, __fma_rn(gB1, w1, __dmul_rn(gB0, w0))) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < KH; ++kk) {
+      const int k = k0 + kk;
+      const bool first = k < NP - a0;
+      const int b = first ? a0 + k : a1 + (k - (NP - a0));
+      const bool ok = k < NBLK && (first || (twin && k - (NP - a0) < NP - a1));
+      const double* T = first ? T0 : T1;
+      const double* h = st + (ok ? b : NP - 1) * 3;
+      const double h0 = h[0], h1 = h[1], h2 = h[2];
+      acc[kk][0] = __fma_rn(T[5], h2, __fma_rn(T[3], h1, __fma_rn(T[0], h0, acc[kk][0])));
+      acc[kk][1] = __fma_rn(T[4], h2, __fma_rn(T[3], h0, __fma_rn(T[1], h1, acc[kk][1])));
+      acc[kk][2] = __fma_rn(T[5], h0, __fma_rn(T[4], h1, __fma_rn(T[2], h2, acc[kk][2])));
+    }
+  }
+#pragma unroll
+  for (int kk = 0; kk < KH; ++kk) {
+    const int k = k0 + kk;
+    const bool first = k < NP - a0;
+    const int b = first ? a0 + k : a1 + (k - (NP - a0));
+    const bool ok = k < NBLK && (first || (twin && k - (NP - a0) < NP - a1));
+    if (!ok) continue;
+    double* o = rec + blk_index<NP>(first ? a0 : a1, b) * D2 + i * 3;
+    o[0] = acc[kk][0];
+    o[1] = acc[kk][1];
+    o[2] = acc[kk][2];
+  }
+}
+
 // 2D row pairs (delta_pairs3's scheme with dim 2): lane (element, pair p,
 // component i) owns row i of block rows p and NP - 1 - p; 2 * ceil(NP / 2)
 // lanes per element (8 for Q2-8), NP + 1 blocks per lane, optimal FMA count.
