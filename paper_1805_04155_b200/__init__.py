@@ -13,6 +13,6 @@ from .api import (  # noqa: F401
 )
 from .mesh import ElementType, StructuredMesh, structured_mesh  # noqa: F401
 from .solver import (  # noqa: F401
-    LinearSolver, NewtonResult, NewtonSettings, NonConvergenceError, SolveSettings, SolverError, energy_norm,
-    newton_solve, restricted_solve,
+    LinearSolver, NewtonResult, NewtonSettings, NonConvergenceError, SolveInfo, SolveSettings, SolverError,
+    energy_norm, newton_solve, restricted_solve,
 )

@@ -88,10 +88,19 @@ def _mask_u8(free_mask: Optional[torch.Tensor], n: int, device) -> Optional[torc
     return free_mask.to(device=device, dtype=torch.uint8).contiguous()
 
 
+@dataclass
+class SolveInfo:
+    """What a restricted_solve did: CG iterations and the true relative residual."""
+    iterations: int = 0
+    residual: float = 0.0
+
+
 def restricted_solve(K: CsrMatrix, rhs: torch.Tensor, free_mask: Optional[torch.Tensor] = None,
-                     settings: SolveSettings = SolveSettings(), ctx=None) -> torch.Tensor:
+                     settings: SolveSettings = SolveSettings(), ctx=None,
+                     info: Optional[SolveInfo] = None) -> torch.Tensor:
     """Solve K[free, free] x = rhs[free]; x is zero on fixed dofs (linalg.cpp:83-121).
-    Raises SolverError with the reference's message above tolerance."""
+    Raises SolverError with the reference's message above tolerance; `info`
+    (optional) receives the iteration count and the residual."""
     from .api import default_context
     n = K.n
     if rhs.numel() != n:
@@ -104,11 +113,12 @@ def restricted_solve(K: CsrMatrix, rhs: torch.Tensor, free_mask: Optional[torch.
     rc = L.lib().epfem_restricted_solve(ctx.handle, n, _ptr(K.row_ptr), _ptr(K.col_idx), _ptr(K.values),
                                         _ptr(rhs.contiguous()), _ptr(_mask_u8(free_mask, n, dev)),
                                         settings.rel_tol, 0, _ptr(x), C.byref(it), C.byref(res))
+    if info is not None:
+        info.iterations, info.residual = it.value, res.value
     if rc == 7:  # EPFEM_ERR_SOLVER
         raise SolverError(L.last_error(), res.value)
     if rc != 0:
         raise Error(L.last_error())
-    restricted_solve.last_iters = it.value
     return x
 
 
@@ -159,11 +169,12 @@ def newton_solve(cache: AssemblyCache, mat: MaterialField, state_prev: Integrati
         S, flags, D, Kv, F = eng.step_f(E, ep, hd, F)
         t1.record()
         Kt = CsrMatrix(cache.row_ptr, cache.col_idx, Kv)
-        du = restricted_solve(Kt, fext - F, free, settings.linear, ctx=eng.ctx)
+        lin = SolveInfo()
+        du = restricted_solve(Kt, fext - F, free, settings.linear, ctx=eng.ctx, info=lin)
         torch.cuda.synchronize(dev)
         n_pl = int((flags & 1).sum().item())
         rec.iterations.append(IterationSample(n_pl, t0.elapsed_time(t1) * 1e-3))
-        rec.linear_iters.append(restricted_solve.last_iters)
+        rec.linear_iters.append(lin.iterations)
         rec.tangent_seconds += rec.iterations[-1].tangent_seconds
         rec.newton_iters = it
         norm_prev = energy_norm(Ke, u, ctx=eng.ctx)
