@@ -59,9 +59,25 @@ __device__ __forceinline__ double cel(double K, double G, int i, int j) {
   return K * vol(i, j) + 2.0 * G * devop(i, j);
 }
 
+// Streamed per-point inputs.  EPFEM_LOAD_NA=1 skips L1 allocation
+// (ld.global.nc.L1::no_allocate) to keep the reference tables L1-resident:
+// measured slower (cfg2 fused 0.237 vs 0.215 ms): a lane's three 16-byte
+// loads share lines that the first one brought into L1.
+#ifndef EPFEM_LOAD_NA
+#define EPFEM_LOAD_NA 0
+#endif
+__device__ __forceinline__ double2 ld_stream2(const double2* p) {
+#if EPFEM_LOAD_NA
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+#else
+  return __ldg(p);
+#endif
+}
 __device__ __forceinline__ void load6(const double* p, int64_t q, double* v) {
   const double2* p2 = reinterpret_cast<const double2*>(p + 6 * q);
-  const double2 a = __ldg(p2), b = __ldg(p2 + 1), c = __ldg(p2 + 2);
+  const double2 a = ld_stream2(p2), b = ld_stream2(p2 + 1), c = ld_stream2(p2 + 2);
   v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y;
 }
 __device__ __forceinline__ void store6(double* p, int64_t q, const double* v) {
@@ -602,7 +618,7 @@ __device__ __forceinline__ void newton_warp_group(ConstArgs c, const GatherArgs&
         const double2* p2 = reinterpret_cast<const double2*>(g.inv + m * W::D2);
 #pragma unroll
         for (int k = 0; k < W::D2 / 2; ++k) {
-          const double2 v = __ldg(p2 + k);
+          const double2 v = ld_stream2(p2 + k);
           jinv[2 * k] = v.x;
           jinv[2 * k + 1] = v.y;
         }
