@@ -48,6 +48,25 @@ namespace epfem_gpu {
 
 namespace {
 
+// k_newton_fused's CTA shape: DeltaCfg's, except for Q1 hexahedra with the
+// row-pair phase 2.  There a CTA owns EPB_Q1 = 16 elements on 128 threads =
+// one thread per point, so no thread idles in phase 1, and phase 2's 12 row-pair
+// lanes per element run in rounds over the CTA (the loop is strided).  Measured
+// on B200, cfg4: 3.50 ms vs 3.88 ms for DeltaCfg's 10 elements on 120 threads,
+// where a quarter of the warp samples waited at the phase barrier (threads with
+// no point); 8 and 12 elements per CTA took 3.66 / 3.65 ms.  (For P2
+// tetrahedra the same shape does not beat the warp kernel: 3.87 vs 3.70 ms.)
+#ifndef EPFEM_EPB_Q1
+#define EPFEM_EPB_Q1 16
+#endif
+template <int DIM, int NP, int NQ>
+struct FusedCfg : DeltaCfg<DIM, NP, NQ> {
+  using Base = DeltaCfg<DIM, NP, NQ>;
+  static constexpr bool Q1 = DIM == 3 && NP == 8 && EPFEM_CTA_PAIRS && !EPFEM_TSHARED && EPFEM_EPB_Q1 > 0;
+  static constexpr int EPB = Q1 ? EPFEM_EPB_Q1 : Base::EPB;
+  static constexpr int THREADS = Q1 ? ((EPB * NQ + 31) / 32) * 32 : Base::THREADS;
+};
+
 __device__ __forceinline__ double iota(int i) { return i < 3 ? 1.0 : 0.0; }
 __device__ __forceinline__ double vol(int i, int j) { return iota(i) * iota(j); }
 // DEV = diag(1,1,1,1/2,1/2,1/2) - VOL/3 (voigt.hpp:62-69)
@@ -429,10 +448,10 @@ __device__ __forceinline__ void prefetch_elements(const ConstArgs& c, const Gath
 // leaves ptxas its own heuristic (126 registers; an explicit 1 gives 144 and
 // is ~15% slower on cfg4).
 template <int MODEL, int DIM, int NP, int NQ, bool FROM_U = false>
-__global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS, DeltaCfg<DIM, NP, NQ>::MINB)
+__global__ void __launch_bounds__(FusedCfg<DIM, NP, NQ>::THREADS, FusedCfg<DIM, NP, NQ>::MINB)
     k_newton_fused(ConstArgs c, GatherArgs g) {
   pdl_trigger();
-  using Cfg = DeltaCfg<DIM, NP, NQ>;
+  using Cfg = FusedCfg<DIM, NP, NQ>;
   constexpr int EPB = Cfg::EPB;
   if (!FROM_U && g.pf_dist > 0) {
     const int64_t eb = g.e_begin + ((int64_t)blockIdx.x + g.pf_dist) * EPB;
@@ -1304,7 +1323,7 @@ int launch_newton_fused_u(int model, int family, int dim, const ConstArgs& c, co
           break;
       }
     } else if constexpr (DIM == 3) {  // hexahedra: CTA kernel
-      using Cfg = DeltaCfg<DIM, NP, NQ>;
+      using Cfg = FusedCfg<DIM, NP, NQ>;
       const unsigned blocks = (unsigned)((g.e_end - g.e_begin + Cfg::EPB - 1) / Cfg::EPB);
       switch (model) {
         case EPFEM_MODEL_VON_MISES:
@@ -1820,18 +1839,19 @@ int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, cons
         return;
       }
     }
-    const unsigned blocks = (unsigned)((g.e_end - g.e_begin + Cfg::EPB - 1) / Cfg::EPB);
+    using FC = FusedCfg<DIM, NP, NQ>;
+    const unsigned blocks = (unsigned)((g.e_end - g.e_begin + FC::EPB - 1) / FC::EPB);
     GatherArgs gp = g;
-      gp.pf_dist = prefetch_distance((const void*)k_newton_fused<EPFEM_MODEL_VON_MISES, DIM, NP, NQ>, Cfg::THREADS);
+      gp.pf_dist = prefetch_distance((const void*)k_newton_fused<EPFEM_MODEL_VON_MISES, DIM, NP, NQ>, FC::THREADS);
       switch (model) {
       case EPFEM_MODEL_VON_MISES:
-        k_newton_fused<EPFEM_MODEL_VON_MISES, DIM, NP, NQ><<<blocks, Cfg::THREADS, 0, st>>>(c, gp);
+        k_newton_fused<EPFEM_MODEL_VON_MISES, DIM, NP, NQ><<<blocks, FC::THREADS, 0, st>>>(c, gp);
         break;
       case EPFEM_MODEL_DRUCKER_PRAGER:
-        k_newton_fused<EPFEM_MODEL_DRUCKER_PRAGER, DIM, NP, NQ><<<blocks, Cfg::THREADS, 0, st>>>(c, gp);
+        k_newton_fused<EPFEM_MODEL_DRUCKER_PRAGER, DIM, NP, NQ><<<blocks, FC::THREADS, 0, st>>>(c, gp);
         break;
       default:
-        k_newton_fused<EPFEM_MODEL_ELASTIC, DIM, NP, NQ><<<blocks, Cfg::THREADS, 0, st>>>(c, gp);
+        k_newton_fused<EPFEM_MODEL_ELASTIC, DIM, NP, NQ><<<blocks, FC::THREADS, 0, st>>>(c, gp);
         break;
     }
   });
