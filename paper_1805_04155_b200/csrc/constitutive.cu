@@ -59,12 +59,26 @@ namespace {
 #ifndef EPFEM_EPB_Q1
 #define EPFEM_EPB_Q1 16
 #endif
+// Tuning hook for Q2-20 (EPFEM_EPB_Q20 > 0): EPB_Q20 elements on
+// THREADS_Q20 threads at MINB_Q20 CTAs/SM, phase-2 chunks in rounds.
+#ifndef EPFEM_EPB_Q20
+#define EPFEM_EPB_Q20 0
+#endif
+#ifndef EPFEM_THREADS_Q20
+#define EPFEM_THREADS_Q20 64
+#endif
+#ifndef EPFEM_MINB_Q20
+#define EPFEM_MINB_Q20 6
+#endif
 template <int DIM, int NP, int NQ>
 struct FusedCfg : DeltaCfg<DIM, NP, NQ> {
   using Base = DeltaCfg<DIM, NP, NQ>;
   static constexpr bool Q1 = DIM == 3 && NP == 8 && EPFEM_CTA_PAIRS && !EPFEM_TSHARED && EPFEM_EPB_Q1 > 0;
-  static constexpr int EPB = Q1 ? EPFEM_EPB_Q1 : Base::EPB;
-  static constexpr int THREADS = Q1 ? ((EPB * NQ + 31) / 32) * 32 : Base::THREADS;
+  static constexpr bool Q20 = DIM == 3 && NP == 20 && !EPFEM_HALFPAIRS20 && !EPFEM_TSHARED && EPFEM_EPB_Q20 > 0;
+  static constexpr int EPB = Q1 ? EPFEM_EPB_Q1 : (Q20 ? EPFEM_EPB_Q20 : Base::EPB);
+  static constexpr int THREADS = Q1 ? ((EPB * NQ + 31) / 32) * 32 : (Q20 ? EPFEM_THREADS_Q20 : Base::THREADS);
+  static constexpr int MINB = Q20 ? EPFEM_MINB_Q20 : Base::MINB;
+  static constexpr bool ROUNDS = THREADS < EPB * Base::NT;  // chunk phase 2 needs more than one pass
 };
 
 __device__ __forceinline__ double iota(int i) { return i < 3 ? 1.0 : 0.0; }
@@ -533,7 +547,19 @@ __global__ void __launch_bounds__(FusedCfg<DIM, NP, NQ>::THREADS, FusedCfg<DIM, 
   }
 #endif
   // phase 2: uniform chunks (no divergent block branch) in sub-passes of SUB
-  if (tid < EPB * Cfg::NT) {
+  if constexpr (Cfg::ROUNDS) {
+    for (int t = tid; t < EPB * Cfg::NT; t += blockDim.x) {
+      const int le = t / Cfg::NT;
+      const int64_t e = e0 + le;
+      const unsigned mask = s_mask[le];
+      if (e < g.e_end && mask) {
+        int a, c0;
+        chunk_of<NP, Cfg::CS>(t - le * Cfg::NT, a, c0);
+        delta_chunk_uniform<DIM, NP, Cfg::CS, Cfg::REC, Cfg::SUB>(&s_st[le][0][0], mask, a, c0,
+                                                                  g.scratch + (size_t)e * Cfg::NB * Cfg::D2);
+      }
+    }
+  } else if (tid < EPB * Cfg::NT) {
     const int le = tid / Cfg::NT;
     const int64_t e = e0 + le;
     const unsigned mask = s_mask[le];
