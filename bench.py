@@ -18,6 +18,7 @@ port of the reference algorithm on a bounded sample, 1 host core.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -542,6 +543,11 @@ def main():
                   "value_from_u": n_int / (t_u * 1e-3),
                   "how": "epfem_newton_step_u (E = B u inside the fused kernel, never stored) vs "
                          "epfem_strains + epfem_newton_step, each one CUDA graph"}
+        # release this section's engines and graphs (cfg5: 16 GB of K each)
+        # before the next one allocates its own
+        del g2, eng2, eng_u, Etmp, u
+        gc.collect()
+        torch.cuda.empty_cache()
     # the step with the internal forces of its stresses
     # (fused in 2D) vs the step followed by the stand-alone K9 kernel
     with_f = None
@@ -589,6 +595,9 @@ def main():
                   "value_with_forces": n_int / (t_f * 1e-3),
                   "how": "epfem_newton_step_f (the step, then K9 in two passes: element force records, "
                          "per-node fold) vs epfem_newton_step + epfem_internal_forces, each one CUDA graph"}
+        del gf, gsep, eng_f, eng_s, Fbuf
+        gc.collect()
+        torch.cuda.empty_cache()
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     step_bytes = cons_b + asm_b if not elastic else asm_b
     step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9

@@ -59,16 +59,21 @@ namespace {
 #ifndef EPFEM_EPB_Q1
 #define EPFEM_EPB_Q1 16
 #endif
-// Tuning hook for Q2-20 (EPFEM_EPB_Q20 > 0): EPB_Q20 elements on
-// THREADS_Q20 threads at MINB_Q20 CTAs/SM, phase-2 chunks in rounds.
+// Q2-20: one element per 32-thread CTA (27 points on 27 lanes, then its 60
+// phase-2 chunks in two rounds over the warp) at up to 16 CTAs/SM (128
+// registers; shared memory admits 13).  Measured on B200, cfg5: fused 15.33 vs
+// 16.04 ms for DeltaCfg's 2 elements on 128 threads (54 of them busy in phase
+// 1); 2 elements on 64 threads: 15.69 ms.  The row stream after it is launched
+// without PDL (tangent.cu): its early CTAs slowed this many-CTA grid (step
+// 25.6 ms with PDL, 24.76 ms without).  EPFEM_EPB_Q20=0 restores DeltaCfg.
 #ifndef EPFEM_EPB_Q20
-#define EPFEM_EPB_Q20 0
+#define EPFEM_EPB_Q20 1
 #endif
 #ifndef EPFEM_THREADS_Q20
-#define EPFEM_THREADS_Q20 64
+#define EPFEM_THREADS_Q20 32
 #endif
 #ifndef EPFEM_MINB_Q20
-#define EPFEM_MINB_Q20 6
+#define EPFEM_MINB_Q20 16
 #endif
 template <int DIM, int NP, int NQ>
 struct FusedCfg : DeltaCfg<DIM, NP, NQ> {

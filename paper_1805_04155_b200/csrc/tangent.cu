@@ -623,7 +623,11 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
     // of the workspace (fused / delta kernel) drains; they load K_elast and
     // the item lists, then block in griddepcontrol.wait until the producer
     // grid has completed and flushed (a no-op after a normal launch).
-    static const bool pdl = getenv("EPFEM_NO_PDL") == nullptr;
+    // Not after Q2-20 producers: their one-element CTAs (constitutive.cu,
+    // FusedCfg) ran slower beside waiting row-stream CTAs (cfg5 step 25.6 vs
+    // 24.76 ms); on the other meshes PDL is neutral to slightly positive.
+    static const bool pdl_env = getenv("EPFEM_NO_PDL") == nullptr;
+    const bool pdl = pdl_env && !(DIM == 3 && NP >= 20);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)rblocks);
     cfg.blockDim = dim3(kStreamThreads);
