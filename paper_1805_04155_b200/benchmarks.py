@@ -1,0 +1,199 @@
+"""The paper's displacement-driven strip-footing benchmark over the GPU path
+(SURVEY §8(f) rank 4): the mesh with its Dirichlet data
+(``build_mesh_footing``, proj/src/mesh.cpp:262-293, with ``Mesh::free_mask`` /
+``dirichlet_values`` / ``constrain``, mesh.cpp:12-25,212-216) and the load
+driver ``run_dp_footing`` (proj/src/benchmarks.cpp:120-205): Drucker-Prager
+(E = 1e7, nu = 0.48, c0 = 450, phi = pi/9), adaptive footing displacement
+increments (halved on a Newton failure, doubled when the pressure settles),
+the normalised footing pressure per step.
+
+Every Newton time step runs on the device (``solver.newton_solve``); the
+reaction on the footing comes from ``internal_forces`` (K9).  The host holds
+only the mesh numbering and the Dirichlet tables, as the reference does.
+
+Not built here: ``run_elastic`` and ``run_vm_cyclic`` (benchmarks.cpp:36-118)
+need the Neumann traction faces and ``external_forces`` with face quadrature
+(mesh.cpp:296-321, assembly.cpp:303-348); see DESIGN.md §9.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+import torch
+
+from . import api as A
+from .mesh import StructuredMesh, structured_mesh
+from .solver import NewtonSettings, TimeStepRecord, newton_solve
+
+
+def default_layers(h: float) -> int:
+    """mesh.cpp:218-220: 3D extrusion layers tracking the in-plane density."""
+    return max(1, int(_lround(1.0 / h)))
+
+
+def _lround(x: float) -> int:
+    """std::lround: halves away from zero (Python's round() is to even)."""
+    return int(math.floor(x + 0.5)) if x >= 0 else -int(math.floor(-x + 0.5))
+
+
+@dataclass
+class BoundaryMesh:
+    """A structured mesh with the reference Mesh's Dirichlet data
+    (mesh.hpp:18-34): per node and direction, free or constrained, the fixed
+    value and the load pattern scaled by the load factor.  Arrays are
+    (n_nodes, dim), so ``reshape(-1)`` is the reference's dof order dim * j + i."""
+    mesh: StructuredMesh
+    free_dof: np.ndarray
+    dirichlet_fixed: np.ndarray
+    dirichlet_load: np.ndarray
+
+    @property
+    def dim(self) -> int:
+        return self.mesh.dim
+
+    @property
+    def n_nodes(self) -> int:
+        return self.mesh.n_nodes
+
+    @property
+    def n_dofs(self) -> int:
+        return self.mesh.n_dofs
+
+    def free_mask(self) -> np.ndarray:
+        """Mesh::free_mask (mesh.cpp:12-17)."""
+        return self.free_dof.reshape(-1).copy()
+
+    def dirichlet_values(self, load_scale: float) -> np.ndarray:
+        """Mesh::dirichlet_values (mesh.cpp:19-27): fixed + scale * load at
+        constrained dofs, zero at free ones."""
+        v = self.dirichlet_fixed + load_scale * self.dirichlet_load
+        return np.where(self.free_dof, 0.0, v).reshape(-1)
+
+    def constrain(self, direction: int, nodes: np.ndarray, fixed: float, load: float) -> None:
+        """constrain (mesh.cpp:212-216) on a node set; a later call overrides
+        an earlier one on the same (direction, node), as in the reference's
+        per-node sequence."""
+        self.free_dof[nodes, direction] = False
+        self.dirichlet_fixed[nodes, direction] = fixed
+        self.dirichlet_load[nodes, direction] = load
+
+
+def build_mesh_footing(level: int, family: str, dim: int, layers: int = -1) -> BoundaryMesh:
+    """build_mesh_footing (mesh.cpp:262-293): the 10 x 10 (x 1) half-domain
+    under a rigid rough strip footing of unit width at the top left.  Sides
+    slide (u1 = 0), the base slides (u2 = 0), the footing nodes carry
+    u2 = -u_D (load pattern -1) and u1 = 0; 3D fronts have u3 = 0."""
+    if level < 0:
+        raise A.Error("build_mesh_footing: level must be >= 0")
+    quadratic = family in ("P2", "Q2")
+    cells = (5 if quadratic else 10) << level
+    h = 10.0 / cells
+    nz, hz = 0, None
+    if dim == 3:
+        nz = layers if layers > 0 else default_layers(h)
+        hz = 1.0 / nz
+    m = structured_mesh(family, dim, cells, cells, nz, hx=h, hy=h, hz=hz)
+    n = m.n_nodes
+    bm = BoundaryMesh(m, np.ones((n, dim), bool), np.zeros((n, dim)), np.zeros((n, dim)))
+    amax, bmax, cmax = 2 * cells, 2 * cells, 2 * nz
+    a, b, c = m.fine[:, 0], m.fine[:, 1], m.fine[:, 2]
+    a_foot = _lround(2.0 / h)  # footing over x1 in [0, 1]: fine coordinate a <= 2 / hx
+    bm.constrain(0, np.nonzero((a == 0) | (a == amax))[0], 0.0, 0.0)
+    bm.constrain(1, np.nonzero(b == 0)[0], 0.0, 0.0)
+    foot = np.nonzero((b == bmax) & (a <= a_foot))[0]
+    bm.constrain(1, foot, 0.0, -1.0)  # u2 = -u_D under the footing
+    bm.constrain(0, foot, 0.0, 0.0)   # rough footing
+    if dim == 3:
+        bm.constrain(2, np.nonzero((c == 0) | (c == cmax))[0], 0.0, 0.0)
+    return bm
+
+
+@dataclass
+class BenchmarkConfig:
+    """benchmarks.hpp:7-19 (the footing's fields)."""
+    dim: int = 2
+    elem: str = "P1"
+    level: int = 1
+    layers: int = -1
+    newton: NewtonSettings = field(default_factory=NewtonSettings)
+    du0: float = 1e-3
+    u_max: float = 1.0
+    theta: float = 1e-3
+
+
+@dataclass
+class RunResults:
+    """benchmarks.hpp:26-37 (the footing's fields)."""
+    mesh: BoundaryMesh
+    records: List[TimeStepRecord] = field(default_factory=list)
+    u: Optional[torch.Tensor] = None
+    displacement_snapshots: list = field(default_factory=list)
+    n_int: int = 0
+    limit_pressure: float = 0.0
+    completed: bool = True
+
+
+def run_dp_footing(config: BenchmarkConfig, device="cuda") -> RunResults:
+    """run_dp_footing (benchmarks.cpp:120-205) with every Newton step on the GPU."""
+    bm = build_mesh_footing(config.level, config.elem, config.dim, config.layers)
+    res_all = RunResults(mesh=bm)
+    m = bm.mesh
+    bulk, shear = A.elastic_moduli(1e7, 0.48)
+    eta, cohesion = A.dp_parameters(450.0, math.pi / 9.0,
+                                    A.DPMode.three_d if m.dim == 3 else A.DPMode.plane_strain)
+    mat = A.uniform_drucker_prager(m.n_int, bulk, shear, eta, cohesion)
+    cache = A.build_assembly_cache(A.Mesh.from_structured(m, device), mat)
+    res_all.n_int = cache.n_int
+    dev = cache.device
+    n = bm.n_dofs
+    f_ext = torch.zeros(n, dtype=torch.float64, device=dev)
+    free = torch.from_numpy(bm.free_mask()).to(dev)
+    # footing dofs (x2) carry the load pattern; their reactions give the mean
+    # pressure over the unit footing area
+    footing = torch.from_numpy(m.dim * np.nonzero(bm.dirichlet_load[:, 1] != 0.0)[0] + 1).to(dev)
+    state = A.IntegrationState.zero(cache.n_int, device=dev)
+    u_prev = torch.zeros(n, dtype=torch.float64, device=dev)
+    u_d, du, p_prev, step, c0 = 0.0, config.du0, 0.0, 0, 450.0
+    halve_on_failure = config.newton.on_failure != "error"
+    while u_d < config.u_max - 1e-14:
+        increment = min(du, config.u_max - u_d)
+        solved = False
+        while True:
+            try:
+                dirichlet = torch.from_numpy(bm.dirichlet_values(u_d + increment))
+                res = newton_solve(cache, mat, state, dirichlet, free, f_ext, config.newton, u_prev)
+                solved = True
+                break
+            except A.Error:
+                if not halve_on_failure:
+                    raise
+                increment *= 0.5
+                if increment < 1e-9 * config.u_max:  # limit load reached
+                    break
+        if not solved:
+            res_all.completed = False
+            break
+        u_d += increment
+        du = increment
+        state = res.state
+        res_all.u = res.u
+        u_prev = res.u
+        F = A.internal_forces(cache, state.S)
+        reaction = 0.0
+        for f in F[footing].cpu().tolist():  # node order, one rounding per add (benchmarks.cpp:177-178)
+            reaction += f
+        pressure = -reaction  # footing area 1 x 1
+        step += 1
+        rec = res.record
+        rec.step, rec.load, rec.derived_scalar = step, u_d, pressure / c0
+        res_all.records.append(rec)
+        res_all.limit_pressure = pressure
+        if abs(pressure - p_prev) < config.theta * max(abs(pressure), 1e-300):
+            du *= 2.0
+        p_prev = pressure
+    if res_all.records:
+        res_all.displacement_snapshots.append((res_all.records[-1].step, res_all.u))
+    return res_all

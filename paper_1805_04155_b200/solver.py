@@ -51,10 +51,12 @@ class SolveSettings:
 
 @dataclass
 class NewtonSettings:
-    """solver.hpp:9-15."""
+    """solver.hpp:9-15.  ``on_failure`` ("halve_step" or "error") is read by
+    the load drivers (benchmarks.py), as in the reference."""
     eps_newton: float = 1e-10
     max_iters: int = 25
     linear: SolveSettings = field(default_factory=SolveSettings)
+    on_failure: str = "halve_step"
 
 
 @dataclass
@@ -65,6 +67,10 @@ class IterationSample:
 
 @dataclass
 class TimeStepRecord:
+    """solver.hpp:22-30 (+ the per-iteration CG counts and stopping ratios)."""
+    step: int = 0
+    load: float = 0.0            # zeta (traction scale) or u_D
+    derived_scalar: float = 0.0  # work (VM) or normalised pressure (DP)
     newton_iters: int = 0
     n_plastic: int = 0
     tangent_seconds: float = 0.0

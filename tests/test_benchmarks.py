@@ -1,0 +1,155 @@
+"""The strip-footing benchmark: the mesh and its
+Dirichlet data against the reference's per-node constraint loop
+(mesh.cpp:262-293) restated over the oracle's mesh numbering (CPU), and the
+load driver run_dp_footing (benchmarks.cpp:120-205) on the GPU against the
+same driver restated on the oracle with the reference's direct solves."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+
+def _footing_ref(O, level, family, dim, layers=-1):
+    """mesh.cpp:262-293 restated per node, in the reference's call order
+    (a later constrain on the same dof overrides an earlier one)."""
+    cells = (5 if family in ("P2", "Q2") else 10) << level
+    h = 10.0 / cells
+    nz = 0
+    if dim == 3:
+        nz = layers if layers > 0 else max(1, int(math.floor(1.0 / h + 0.5)))
+    coord, elem, fine = O.structured_mesh(family, dim, cells, cells, nz, h, h, (1.0 / nz if nz else None))
+    n = coord.shape[0]
+    free = np.ones((n, dim), bool)
+    fixed = np.zeros((n, dim))
+    load = np.zeros((n, dim))
+
+    def constrain(d, node, f, l):
+        free[node, d] = False
+        fixed[node, d] = f
+        load[node, d] = l
+    a_foot = int(math.floor(2.0 / h + 0.5))
+    amax, bmax, cmax = 2 * cells, 2 * cells, 2 * nz
+    for node in range(n):
+        a, b, c = (int(x) for x in fine[node])
+        if a == 0 or a == amax:
+            constrain(0, node, 0.0, 0.0)
+        if b == 0:
+            constrain(1, node, 0.0, 0.0)
+        if b == bmax and a <= a_foot:
+            constrain(1, node, 0.0, -1.0)
+            constrain(0, node, 0.0, 0.0)
+        if dim == 3 and (c == 0 or c == cmax):
+            constrain(2, node, 0.0, 0.0)
+    return coord, elem, free, fixed, load
+
+
+@pytest.mark.parametrize("family,dim,level", [("P1", 2, 0), ("P2", 2, 1), ("Q1", 2, 0), ("Q2", 2, 0),
+                                              ("P1", 3, 0), ("Q2", 3, 0)])
+def test_footing_mesh_matches_reference_loop(oracle, family, dim, level):
+    from paper_1805_04155_b200.benchmarks import build_mesh_footing
+    bm = build_mesh_footing(level, family, dim)
+    coord, elem, free, fixed, load = _footing_ref(oracle, level, family, dim)
+    assert np.array_equal(bm.mesh.coord, coord)
+    assert np.array_equal(bm.mesh.elem, elem)
+    assert np.array_equal(bm.free_dof, free)
+    assert np.array_equal(bm.dirichlet_fixed, fixed)
+    assert np.array_equal(bm.dirichlet_load, load)
+    # the footing is the unit segment x1 in [0, 1] of the top edge
+    foot = np.nonzero(load[:, 1] != 0.0)[0]
+    assert np.all(coord[foot, 1] == 10.0) and coord[foot, 0].max() == 1.0 and coord[foot, 0].min() == 0.0
+    # Mesh::free_mask / dirichlet_values: dof order dim * node + direction
+    v = bm.dirichlet_values(0.25)
+    assert np.array_equal(bm.free_mask(), free.reshape(-1))
+    assert np.all(v[dim * foot + 1] == -0.25)
+    assert np.all(v[free.reshape(-1)] == 0.0)
+    assert np.count_nonzero(v) == foot.size
+
+
+def test_footing_mesh_rejects_negative_level():
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.benchmarks import build_mesh_footing
+    with pytest.raises(P.Error, match="build_mesh_footing: level must be >= 0"):
+        build_mesh_footing(-1, "P1", 2)
+
+
+def _footing_driver_ref(O, bm, du0, u_max, theta, eps, max_iters):
+    """benchmarks.cpp:120-205 and solver.cpp:7-62 restated on the oracle, with
+    the reference's default direct restricted solve (no step failures
+    expected at these increments)."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spl
+    m = bm.mesh
+    K, G = O.elastic_moduli(1e7, 0.48)
+    eta, c = O.dp_parameters(450.0, math.pi / 9.0, three_d=(m.dim == 3))
+    oc = O.Cache(m.elem_type.family, m.dim, m.coord, m.elem, G, K)
+    Ke = oc.K_elast()
+    Kes = sp.csr_matrix((Ke.data, Ke.indices, Ke.indptr))
+
+    def en(v):
+        return np.sqrt(max(v @ (Kes @ v), 0.0))
+    free = bm.free_mask()
+    fi = np.nonzero(free)[0]
+    foot = m.dim * np.nonzero(bm.dirichlet_load[:, 1] != 0.0)[0] + 1
+    Ep = np.zeros((m.n_int, 6))
+    u_prev = np.zeros(bm.n_dofs)
+    u_d, du, p_prev, out = 0.0, du0, 0.0, []
+    while u_d < u_max - 1e-14:
+        inc = min(du, u_max - u_d)
+        u = bm.dirichlet_values(u_d + inc)
+        u[fi] = u_prev[fi]
+        for it in range(1, max_iters + 1):
+            st = O.constitutive_dp(oc.strains(u), Ep, G, K, eta, c)
+            F = oc.internal_forces(st["S"])
+            Kt = oc.tangent(st["DS"], st["plastic"])
+            Ks = sp.csr_matrix((Kt.data, Kt.indices, Kt.indptr))
+            d = np.zeros_like(u)
+            d[fi] = spl.spsolve(Ks[fi][:, fi].tocsc(), -F[fi])
+            npv = en(u)
+            u = u + d
+            ncu = en(u)
+            if npv + ncu == 0.0 or en(d) <= eps * (npv + ncu):
+                break
+        else:
+            raise AssertionError("reference Newton did not converge")
+        st = O.constitutive_dp(oc.strains(u), Ep, G, K, eta, c)
+        Ep = st["Ep"]
+        u_d += inc
+        du = inc
+        u_prev = u
+        F = oc.internal_forces(st["S"])
+        reaction = 0.0
+        for f in F[foot]:
+            reaction += f
+        p = -reaction
+        out.append((u_d, it, int(st["plastic"].sum()), p / 450.0))
+        if abs(p - p_prev) < theta * max(abs(p), 1e-300):
+            du *= 2.0
+        p_prev = p
+    return out, u_prev
+
+
+@pytest.mark.gpu
+def test_run_dp_footing_matches_reference_driver(cuda, oracle):
+    """Level-0 P1 footing, 6 footing increments of 1e-3 into plasticity: the
+    GPU driver (device CG at rel_tol 1e-12) and the restated reference driver
+    (direct solves) take the same load path and Newton iteration counts, with
+    the same plastic counts and normalised pressures within 1e-7."""
+    from paper_1805_04155_b200.benchmarks import BenchmarkConfig, run_dp_footing
+    from paper_1805_04155_b200.solver import NewtonSettings, SolveSettings
+    cfg = BenchmarkConfig(dim=2, elem="P1", level=0, du0=1e-3, u_max=6e-3, theta=1e-3,
+                          newton=NewtonSettings(eps_newton=1e-10, max_iters=25,
+                                                linear=SolveSettings(rel_tol=1e-12), on_failure="error"))
+    res = run_dp_footing(cfg, device=cuda)
+    ref, u_ref = _footing_driver_ref(oracle, res.mesh, cfg.du0, cfg.u_max, cfg.theta, 1e-10, 25)
+    assert res.completed and len(res.records) == len(ref)
+    assert ref[-1][2] > 0, "the footing must yield within the load path"
+    for rec, (load, iters, n_pl, p) in zip(res.records, ref):
+        assert rec.load == load
+        assert rec.newton_iters == iters
+        assert rec.n_plastic == n_pl
+        assert abs(rec.derived_scalar - p) <= 1e-7 * abs(p)
+    u = res.u.cpu().numpy()
+    assert np.abs(u - u_ref).max() <= 1e-8 * np.abs(u_ref).max()
+    assert abs(res.limit_pressure - res.records[-1].derived_scalar * 450.0) <= 1e-12 * abs(res.limit_pressure)
