@@ -11,9 +11,12 @@ Every Newton time step runs on the device (``solver.newton_solve``); the
 reaction on the footing comes from ``internal_forces`` (K9).  The host holds
 only the mesh numbering and the Dirichlet tables, as the reference does.
 
-Not built here: ``run_elastic`` and ``run_vm_cyclic`` (benchmarks.cpp:36-118)
-need the Neumann traction faces and ``external_forces`` with face quadrature
-(mesh.cpp:296-321, assembly.cpp:303-348); see DESIGN.md §9.
+The L-shaped elastic body (``build_mesh_elastic_body``, mesh.cpp:222-258)
+carries the two traction drivers: ``run_elastic`` (one elastic step under a
+volume force and a top traction, benchmarks.cpp:36-66) and ``run_vm_cyclic``
+(von Mises, traction cycled 0 -> 1 -> -1 -> 0, benchmarks.cpp:68-118).  Their
+external forces come from ``forces.external_forces`` (2D; 3D faces are not
+built, so the traction drivers are 2D here).
 """
 from __future__ import annotations
 
@@ -25,6 +28,7 @@ import numpy as np
 import torch
 
 from . import api as A
+from .forces import boundary_faces, constant_force, external_forces
 from .mesh import StructuredMesh, structured_mesh
 from .solver import NewtonSettings, TimeStepRecord, newton_solve
 
@@ -49,6 +53,7 @@ class BoundaryMesh:
     free_dof: np.ndarray
     dirichlet_fixed: np.ndarray
     dirichlet_load: np.ndarray
+    neumann_faces: list = field(default_factory=list)  # (element, local face), sorted
 
     @property
     def dim(self) -> int:
@@ -111,6 +116,41 @@ def build_mesh_footing(level: int, family: str, dim: int, layers: int = -1) -> B
     return bm
 
 
+def build_mesh_elastic_body(level: int, family: str, dim: int, layers: int = -1) -> BoundaryMesh:
+    """build_mesh_elastic_body (mesh.cpp:222-258): the 10 x 10 (x 1) square
+    without its bottom-left 5 x 5 block.  Left side: u1 = 0 (symmetry); bottom:
+    u2 = 0 and u1 = u_D (load pattern 1); 3D fronts u3 = 0; Neumann faces on
+    the top edge."""
+    if level < 0:
+        raise A.Error("build_mesh_elastic_body: level must be >= 0")
+    block = 5 << level
+    cells = 2 * block
+    h = 5.0 / block
+    nz, hz = 0, None
+    if dim == 3:
+        nz = layers if layers > 0 else default_layers(h)
+        hz = 1.0 / nz
+    active = np.ones((cells, cells), bool)
+    active[:block, :block] = False  # (j, i): remove the bottom-left block
+    m = structured_mesh(family, dim, cells, cells, nz, hx=h, hy=h, hz=hz, active=active)
+    n = m.n_nodes
+    bm = BoundaryMesh(m, np.ones((n, dim), bool), np.zeros((n, dim)), np.zeros((n, dim)))
+    a, b, c = m.fine[:, 0], m.fine[:, 1], m.fine[:, 2]
+    bmax, cmax = 2 * cells, 2 * nz
+    bm.constrain(0, np.nonzero(a == 0)[0], 0.0, 0.0)  # symmetry on the left
+    bottom = np.nonzero(b == 0)[0]
+    bm.constrain(1, bottom, 0.0, 0.0)                  # bottom: u.n = 0, u1 = u_D
+    bm.constrain(0, bottom, 0.0, 1.0)
+    if dim == 3:
+        bm.constrain(2, np.nonzero((c == 0) | (c == cmax))[0], 0.0, 0.0)
+        return bm  # 3D Neumann faces are not built (forces.py)
+    from .forces import FACE_NODES_2D
+    faces = FACE_NODES_2D[family]
+    bm.neumann_faces = [(e, f) for e, f in boundary_faces(m)
+                        if all(m.fine[m.elem[e, p], 1] == bmax for p in faces[f])]
+    return bm
+
+
 @dataclass
 class BenchmarkConfig:
     """benchmarks.hpp:7-19 (the footing's fields)."""
@@ -119,6 +159,7 @@ class BenchmarkConfig:
     level: int = 1
     layers: int = -1
     newton: NewtonSettings = field(default_factory=NewtonSettings)
+    n_steps: int = 40
     du0: float = 1e-3
     u_max: float = 1.0
     theta: float = 1e-3
@@ -131,9 +172,98 @@ class RunResults:
     records: List[TimeStepRecord] = field(default_factory=list)
     u: Optional[torch.Tensor] = None
     displacement_snapshots: list = field(default_factory=list)
+    hardening_snapshots: list = field(default_factory=list)  # (step, mean |Hard| per element)
     n_int: int = 0
     limit_pressure: float = 0.0
     completed: bool = True
+
+
+def vm_load_scale(t: float) -> float:
+    """benchmarks.cpp:31-35: 0 -> 1 on [0, 1], 1 -> -1 on [1, 3], -1 -> 0 on [3, 4]."""
+    if t <= 1.0:
+        return t
+    if t <= 3.0:
+        return 2.0 - t
+    return t - 4.0
+
+
+def _cell_mean_hardening(n_elements: int, Hard: torch.Tensor) -> np.ndarray:
+    """benchmarks.cpp:15-26: per element, the mean over its points of
+    stress_norm(Hard) (voigt.hpp:39-41), summed in point order."""
+    h = Hard.cpu().numpy().reshape(n_elements, -1, 6)
+    nrm = np.sqrt((h[..., 0] ** 2 + h[..., 1] ** 2 + h[..., 2] ** 2)
+                  + 2.0 * (h[..., 3] ** 2 + h[..., 4] ** 2 + h[..., 5] ** 2))
+    acc = np.zeros(n_elements)
+    for q in range(nrm.shape[1]):
+        acc = acc + nrm[:, q]
+    return acc / nrm.shape[1]
+
+
+def _traction_setup(config: BenchmarkConfig, mat_fn, device):
+    bm = build_mesh_elastic_body(config.level, config.elem, config.dim, config.layers)
+    m = bm.mesh
+    bulk, shear = A.elastic_moduli(206900.0, 0.29)
+    mat = mat_fn(m.n_int, bulk, shear)
+    cache = A.build_assembly_cache(A.Mesh.from_structured(m, device), mat)
+    return bm, m, mat, cache, cache.weight.cpu().numpy()
+
+
+def run_elastic(config: BenchmarkConfig, device="cuda") -> RunResults:
+    """run_elastic (benchmarks.cpp:36-66): one elastic step, unit volume force
+    and traction 200 in x2, u_D = 0.5 on the bottom segment."""
+    bm, m, mat, cache, w = _traction_setup(config, A.uniform_elastic, device)
+    out = RunResults(mesh=bm, n_int=cache.n_int)
+    dev = cache.device
+    e2 = [0.0] * m.dim
+    e2[1] = 1.0
+    t2 = [0.0] * m.dim
+    t2[1] = 200.0
+    f = external_forces(m, w, constant_force(e2), constant_force(t2), bm.neumann_faces)
+    ft = torch.from_numpy(f).to(dev)
+    res = newton_solve(cache, mat, A.IntegrationState.zero(cache.n_int, device=dev),
+                       torch.from_numpy(bm.dirichlet_values(0.5)), torch.from_numpy(bm.free_mask()), ft,
+                       config.newton)
+    rec = res.record
+    rec.step, rec.load, rec.derived_scalar = 1, 1.0, float(torch.dot(ft, res.u).item())
+    out.u = res.u
+    out.records.append(rec)
+    out.displacement_snapshots.append((1, res.u))
+    return out
+
+
+def run_vm_cyclic(config: BenchmarkConfig, device="cuda") -> RunResults:
+    """run_vm_cyclic (benchmarks.cpp:68-118): von Mises (a = 1e4,
+    Y = 450 sqrt(2/3)), traction scale zeta(t_k), t_k = 4k / n_steps, each
+    step a newton_solve from the committed state with a warm start; Newton
+    failure is an error; snapshots nearest t = 1, 2, 3, 4."""
+    bm, m, mat, cache, w = _traction_setup(
+        config, lambda n, k, g: A.uniform_von_mises(n, k, g, 1e4, 450.0 * math.sqrt(2.0 / 3.0)), device)
+    out = RunResults(mesh=bm, n_int=cache.n_int)
+    dev = cache.device
+    t2 = [0.0] * m.dim
+    t2[1] = 200.0
+    f_max = torch.from_numpy(external_forces(m, w, None, constant_force(t2), bm.neumann_faces)).to(dev)
+    dirichlet = torch.from_numpy(bm.dirichlet_values(0.0))
+    free = torch.from_numpy(bm.free_mask())
+    settings = NewtonSettings(eps_newton=config.newton.eps_newton, max_iters=config.newton.max_iters,
+                              linear=config.newton.linear, on_failure="error")
+    state = A.IntegrationState.zero(cache.n_int, device=dev)
+    u_prev = torch.zeros(bm.n_dofs, dtype=torch.float64, device=dev)
+    for k in range(1, config.n_steps + 1):
+        t = 4.0 * k / config.n_steps
+        zeta = vm_load_scale(t)
+        res = newton_solve(cache, mat, state, dirichlet, free, zeta * f_max, settings, u_prev)
+        state = res.state
+        out.u = res.u
+        u_prev = res.u
+        rec = res.record
+        rec.step, rec.load, rec.derived_scalar = k, zeta, float(torch.dot(f_max, res.u).item())
+        out.records.append(rec)
+        for j in range(1, 5):
+            if k == (j * config.n_steps + 2) // 4:
+                out.hardening_snapshots.append((k, _cell_mean_hardening(m.n_elements, state.Hard)))
+                out.displacement_snapshots.append((k, out.u))
+    return out
 
 
 def run_dp_footing(config: BenchmarkConfig, device="cuda") -> RunResults:

@@ -1,0 +1,162 @@
+"""External forces for the paper's load drivers (host side, one-time per
+driver, like the reference): ``external_forces`` (proj/src/assembly.cpp:231-296)
+with a volume force at the volume quadrature points (weights |det J| w_q from
+the device cache) and a traction on the mesh's Neumann faces with the face
+rule and the face restriction of the basis (reference_elements.cpp:87-115,
+117-135,196-244,392-412,466-498); ``boundary_faces`` (mesh.cpp:294-310).
+
+2D meshes (faces are segments).  3D faces (triangle / quadrilateral rules)
+are not built; ``external_forces`` raises for them.
+"""
+from __future__ import annotations
+
+import math
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import api as A
+from .mesh import StructuredMesh
+
+ForceField = Callable[[np.ndarray], np.ndarray]  # x (n, dim) -> value (n, dim)
+
+# face_nodes (reference_elements.cpp:466-498), 2D
+FACE_NODES_2D = {
+    "P1": [[0, 1], [1, 2], [2, 0]],
+    "P2": [[0, 1, 3], [1, 2, 4], [2, 0, 5]],
+    "Q1": [[0, 1], [1, 2], [2, 3], [3, 0]],
+    "Q2": [[0, 1, 4], [1, 2, 5], [2, 3, 6], [3, 0, 7]],
+}
+_QUAD_CORNERS = [(-1, -1), (1, -1), (1, 1), (-1, 1)]
+_QUAD_EDGES = [(0, -1), (1, 0), (0, 1), (-1, 0)]
+
+
+def constant_force(value) -> ForceField:
+    """constant_force (assembly.cpp:227-229)."""
+    v = np.asarray(value, dtype=np.float64)
+    return lambda x: np.broadcast_to(v, (x.shape[0], v.size))
+
+
+def gauss_segment(n: int):
+    """gauss_segment (reference_elements.cpp:20-44)."""
+    if n == 1:
+        return np.array([0.0]), np.array([2.0])
+    if n == 2:
+        g = 1.0 / math.sqrt(3.0)
+        return np.array([-g, g]), np.array([1.0, 1.0])
+    if n == 3:
+        g = math.sqrt(3.0 / 5.0)
+        return np.array([-g, 0.0, g]), np.array([5.0 / 9.0, 8.0 / 9.0, 5.0 / 9.0])
+    raise A.Error("unsupported segment rule")
+
+
+def _segment_basis(order: int, x: np.ndarray):
+    """segment_basis (reference_elements.cpp:87-115): values, d/dx (n_fp, m)."""
+    if order == 1:
+        return np.stack([0.5 * (1.0 - x), 0.5 * (1.0 + x)]), np.stack([np.full_like(x, -0.5), np.full_like(x, 0.5)])
+    return (np.stack([0.5 * x * (x - 1.0), 0.5 * x * (x + 1.0), 1.0 - x * x]),
+            np.stack([x - 0.5, x + 0.5, -2.0 * x]))
+
+
+def volume_rule_2d(family: str):
+    """quadrature_volume (reference_elements.cpp:345-372) in 2D: points (2, n_q), weights."""
+    if family == "P1":
+        return np.full((2, 1), 1.0 / 3.0), np.array([0.5])
+    if family == "P2":
+        return np.array([[0.5, 0.5, 0.0], [0.0, 0.5, 0.5]]), np.full(3, 1.0 / 6.0)
+    x1, w1 = gauss_segment(2 if family == "Q1" else 3)
+    n1 = x1.size
+    pts = np.zeros((2, n1 * n1))
+    w = np.zeros(n1 * n1)
+    for q in range(n1 * n1):  # tensor_rule: axis 0 fastest, weight = running product
+        idx, acc = q, 1.0
+        for i in range(2):
+            k = idx % n1
+            idx //= n1
+            pts[i, q] = x1[k]
+            acc *= w1[k]
+        w[q] = acc
+    return pts, w
+
+
+def volume_basis_values_2d(family: str, pts: np.ndarray) -> np.ndarray:
+    """Shape-function values (n_p, m) of the 2D bases (reference_elements.cpp:117-135,196-244)."""
+    x, y = pts[0], pts[1]
+    if family == "P1":
+        return np.stack([1.0 - x - y, x, y])
+    if family == "P2":
+        z = 1.0 - x - y
+        return np.stack([z * (2 * z - 1), x * (2 * x - 1), y * (2 * y - 1), 4 * z * x, 4 * x * y, 4 * z * y])
+    if family == "Q1":
+        return np.stack([0.25 * (1 + sx * x) * (1 + sy * y) for sx, sy in _QUAD_CORNERS])
+    vals = []
+    for sx, sy in _QUAD_CORNERS:
+        ax, ay = 1 + sx * x, 1 + sy * y
+        vals.append(0.25 * ax * ay * (sx * x + sy * y - 1))
+    for sx, sy in _QUAD_EDGES:
+        vals.append(0.5 * (1 - x * x) * (1 + sy * y) if sx == 0 else 0.5 * (1 + sx * x) * (1 - y * y))
+    return np.stack(vals)
+
+
+def boundary_faces(mesh: StructuredMesh) -> list:
+    """boundary_faces (mesh.cpp:294-310): the (element, face) pairs whose node
+    set occurs once, sorted."""
+    if mesh.dim != 2:
+        raise A.Error("boundary_faces: 3D faces are not built here")
+    faces = FACE_NODES_2D[mesh.elem_type.family]
+    table = {}
+    for e in range(mesh.n_elements):
+        for f, loc in enumerate(faces):
+            key = tuple(sorted(int(mesh.elem[e, p]) for p in loc))
+            ent = table.setdefault(key, [0, (e, f)])
+            ent[0] += 1
+    return sorted(v[1] for v in table.values() if v[0] == 1)
+
+
+def external_forces(mesh: StructuredMesh, weight: np.ndarray, volume_force: Optional[ForceField] = None,
+                    traction: Optional[ForceField] = None, neumann_faces: Optional[list] = None) -> np.ndarray:
+    """external_forces (assembly.cpp:231-296): f += w * value at every
+    (element, point, node, direction) in the reference's loop order (one
+    rounding per add, np.add.at is sequential in index order)."""
+    dim = mesh.dim
+    if dim != 2:
+        raise A.Error("external_forces: 3D meshes are not built here")
+    fam = mesh.elem_type.family
+    f = np.zeros(mesh.n_dofs)
+    coord, elem = mesh.coord, mesh.elem
+    if volume_force is not None:
+        pts, _ = volume_rule_2d(fam)
+        vals = volume_basis_values_2d(fam, pts)  # (n_p, n_q)
+        n_p, n_q = vals.shape
+        # x_q = sum_p N_p(q) x_p, accumulated over p in order
+        x = np.zeros((mesh.n_elements, n_q, dim))
+        for p in range(n_p):
+            x += vals[p][None, :, None] * coord[elem[:, p]][:, None, :]
+        value = np.asarray(volume_force(x.reshape(-1, dim)), dtype=np.float64).reshape(mesh.n_elements, n_q, dim)
+        w = weight.reshape(mesh.n_elements, n_q)[:, :, None] * vals.T[None, :, :]  # (e, q, p)
+        contrib = w[:, :, :, None] * value[:, :, None, :]                        # (e, q, p, i)
+        dofs = dim * elem[:, None, :, None] + np.arange(dim)[None, None, None, :]
+        dofs = np.broadcast_to(dofs, contrib.shape)
+        np.add.at(f, dofs.reshape(-1), contrib.reshape(-1))
+    if traction is not None:
+        if not neumann_faces:
+            raise A.Error("external_forces: traction given but mesh has no Neumann faces")
+        quadratic = fam in ("P2", "Q2")
+        fx, fw = gauss_segment({"P1": 1, "P2": 2, "Q1": 2, "Q2": 3}[fam])
+        vals, grads = _segment_basis(2 if quadratic else 1, fx)  # (n_fp, n_fq)
+        faces = FACE_NODES_2D[fam]
+        for e, fi in neumann_faces:
+            nodes = [int(elem[e, p]) for p in faces[fi]]
+            for q in range(fx.size):
+                x = np.zeros(dim)
+                t = np.zeros(dim)
+                for p, node in enumerate(nodes):
+                    x += vals[p, q] * coord[node]
+                    t += grads[p, q] * coord[node]
+                area = math.sqrt(t[0] * t[0] + t[1] * t[1])
+                value = np.asarray(traction(x[None, :]), dtype=np.float64).reshape(dim)
+                for p, node in enumerate(nodes):
+                    w = fw[q] * area * vals[p, q]
+                    for i in range(dim):
+                        f[dim * node + i] += w * value[i]
+    return f
