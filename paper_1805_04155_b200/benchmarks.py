@@ -327,3 +327,97 @@ def run_dp_footing(config: BenchmarkConfig, device="cuda") -> RunResults:
     if res_all.records:
         res_all.displacement_snapshots.append((res_all.records[-1].step, res_all.u))
     return res_all
+
+
+# ------------------------------------------------------------- mesh text I/O
+def _g17(x: float) -> str:
+    """operator<< on a double at precision(17) (printf %.17g)."""
+    return "%.17g" % x
+
+
+def write_mesh_text(bm: BoundaryMesh, path: str) -> None:
+    """write_mesh_text (mesh.cpp:323-355): header, nodes, elements, the
+    constrained dofs in (node, direction) order, the Neumann faces."""
+    m = bm.mesh
+    try:
+        out = open(path, "w")
+    except OSError:
+        raise A.Error("write_mesh_text: cannot open " + path) from None
+    with out:
+        w = out.write
+        w("epfem-mesh 1\n")
+        w(f"dim {m.dim}\n")
+        w(f"elem {m.elem_type.family}\n")
+        w(f"nodes {m.n_nodes}\n")
+        for n in range(m.n_nodes):
+            w(str(n) + "".join(" " + _g17(float(v)) for v in m.coord[n]) + "\n")
+        w(f"elements {m.n_elements} {m.elem.shape[1]}\n")
+        for e in range(m.n_elements):
+            w(str(e) + "".join(f" {int(v)}" for v in m.elem[e]) + "\n")
+        con = np.argwhere(~bm.free_dof)  # row-major: node, then direction
+        w(f"dirichlet {con.shape[0]}\n")
+        for n, i in con:
+            w(f"{n} {i} {_g17(float(bm.dirichlet_fixed[n, i]))} {_g17(float(bm.dirichlet_load[n, i]))}\n")
+        w(f"neumann {len(bm.neumann_faces)}\n")
+        for e, f in bm.neumann_faces:
+            w(f"{e} {f}\n")
+
+
+def read_mesh_text(path: str) -> BoundaryMesh:
+    """read_mesh_text (mesh.cpp:357-410), with its error messages.  The mesh
+    carries no fine-grid indices (``fine`` is None)."""
+    from .mesh import ElementType, node_count
+    try:
+        toks = open(path).read().split()
+    except OSError:
+        raise A.Error("read_mesh_text: cannot open " + path) from None
+    pos = 0
+
+    def nxt(conv=str):
+        nonlocal pos
+        if pos >= len(toks):
+            raise A.Error("read_mesh_text: truncated file " + path)
+        pos += 1
+        try:
+            return conv(toks[pos - 1])
+        except ValueError:
+            raise A.Error("read_mesh_text: truncated file " + path) from None
+    if len(toks) < 2 or toks[0] != "epfem-mesh" or toks[1] != "1":
+        raise A.Error("read_mesh_text: unrecognized header in " + path)
+    pos = 2
+    nxt()
+    dim = nxt(int)
+    nxt()
+    family = nxt()
+    if family not in ("P1", "P2", "Q1", "Q2"):
+        raise A.Error("unknown element family: " + family)
+    t = ElementType(family, dim)
+    nxt()
+    n_nodes = nxt(int)
+    coord = np.zeros((n_nodes, dim))
+    for _ in range(n_nodes):
+        nid = nxt(int)
+        for i in range(dim):
+            coord[nid, i] = nxt(float)
+    nxt()
+    n_elems, n_p = nxt(int), nxt(int)
+    if n_p != node_count(t):
+        raise A.Error("read_mesh_text: node count mismatch for element type")
+    elem = np.zeros((n_elems, n_p), np.int32)
+    for _ in range(n_elems):
+        eid = nxt(int)
+        for p in range(n_p):
+            v = nxt(int)
+            if v < 0 or v >= n_nodes:
+                raise A.Error("read_mesh_text: node index out of range")
+            elem[eid, p] = v
+    m = StructuredMesh(t, coord, elem, None, (0, 0, 0))
+    bm = BoundaryMesh(m, np.ones((n_nodes, dim), bool), np.zeros((n_nodes, dim)), np.zeros((n_nodes, dim)))
+    nxt()
+    for _ in range(nxt(int)):
+        n, d, fx, ld = nxt(int), nxt(int), nxt(float), nxt(float)
+        bm.constrain(d, np.array([n]), fx, ld)
+    nxt()
+    for _ in range(nxt(int)):
+        bm.neumann_faces.append((nxt(int), nxt(int)))
+    return bm

@@ -312,3 +312,53 @@ def test_run_elastic_and_vm_cyclic_match_reference_drivers(cuda, oracle):
         assert abs(rec.derived_scalar - fmax @ u_r) <= 1e-9 * max(abs(fmax @ u_r), 1e-30)
     assert np.abs(cy.u.cpu().numpy() - ref[-1][2]).max() <= 1e-8 * np.abs(ref[-1][2]).max()
     assert [k for k, _ in cy.hardening_snapshots] == [2, 4, 6, 8]
+
+
+# ------------------------------------------------------------- mesh text I/O
+@pytest.mark.parametrize("builder,family,dim", [("footing", "P2", 2), ("body", "Q2", 2), ("footing", "Q1", 3)])
+def test_mesh_text_round_trip(tmp_path, builder, family, dim):
+    """write_mesh_text / read_mesh_text (mesh.cpp:323-410): every array comes
+    back bit for bit (%.17g round-trips doubles)."""
+    from paper_1805_04155_b200.benchmarks import (build_mesh_elastic_body, build_mesh_footing, read_mesh_text,
+                                                  write_mesh_text)
+    bm = (build_mesh_footing if builder == "footing" else build_mesh_elastic_body)(0, family, dim)
+    p = str(tmp_path / "m.txt")
+    write_mesh_text(bm, p)
+    rb = read_mesh_text(p)
+    assert rb.mesh.elem_type == bm.mesh.elem_type
+    assert np.array_equal(rb.mesh.coord, bm.mesh.coord) and np.array_equal(rb.mesh.elem, bm.mesh.elem)
+    assert np.array_equal(rb.free_dof, bm.free_dof)
+    assert np.array_equal(rb.dirichlet_fixed, bm.dirichlet_fixed)
+    assert np.array_equal(rb.dirichlet_load, bm.dirichlet_load)
+    assert rb.neumann_faces == bm.neumann_faces
+
+
+def test_mesh_text_format_and_errors(tmp_path):
+    """The reference's text layout on a 1-cell P1 mesh (h = 0.1), and its
+    error messages for a bad header, a wrong node count, an out-of-range node
+    and a truncated file."""
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.benchmarks import BoundaryMesh, read_mesh_text, write_mesh_text
+    m = P.structured_mesh("P1", 2, 1, 1, hx=0.1, hy=0.1)
+    bm = BoundaryMesh(m, np.ones((4, 2), bool), np.zeros((4, 2)), np.zeros((4, 2)))
+    bm.constrain(1, np.array([0, 1]), 0.0, 0.0)
+    bm.constrain(0, np.array([3]), 0.25, -1.0)
+    bm.neumann_faces = [(1, 0)]
+    p = tmp_path / "m.txt"
+    write_mesh_text(bm, str(p))
+    lines = p.read_text().splitlines()
+    assert lines[:4] == ["epfem-mesh 1", "dim 2", "elem P1", "nodes 4"]
+    assert lines[4:8] == ["0 0 0", "1 0.10000000000000001 0", "2 0 0.10000000000000001",
+                          "3 0.10000000000000001 0.10000000000000001"]
+    assert lines[8] == "elements 2 3"
+    assert lines[9:11] == ["0 " + " ".join(map(str, m.elem[0])), "1 " + " ".join(map(str, m.elem[1]))]
+    assert lines[11:] == ["dirichlet 3", "0 1 0 0", "1 1 0 0", "3 0 0.25 -1", "neumann 1", "1 0"]
+    bad = tmp_path / "bad.txt"
+    for text, msg in [("epfem-mesh 2\n", "unrecognized header"),
+                      (p.read_text().replace("elements 2 3", "elements 2 4"), "node count mismatch"),
+                      (p.read_text().replace("\n1 " + " ".join(map(str, m.elem[1])), "\n1 0 1 7"),
+                       "node index out of range"),
+                      ("\n".join(lines[:12]) + "\n", "truncated file")]:
+        bad.write_text(text)
+        with pytest.raises(P.Error, match=msg):
+            read_mesh_text(str(bad))
