@@ -15,8 +15,7 @@ The L-shaped elastic body (``build_mesh_elastic_body``, mesh.cpp:222-258)
 carries the two traction drivers: ``run_elastic`` (one elastic step under a
 volume force and a top traction, benchmarks.cpp:36-66) and ``run_vm_cyclic``
 (von Mises, traction cycled 0 -> 1 -> -1 -> 0, benchmarks.cpp:68-118).  Their
-external forces come from ``forces.external_forces`` (2D; 3D faces are not
-built, so the traction drivers are 2D here).
+external forces come from ``forces.external_forces`` (2D and 3D).
 """
 from __future__ import annotations
 
@@ -143,9 +142,8 @@ def build_mesh_elastic_body(level: int, family: str, dim: int, layers: int = -1)
     bm.constrain(0, bottom, 0.0, 1.0)
     if dim == 3:
         bm.constrain(2, np.nonzero((c == 0) | (c == cmax))[0], 0.0, 0.0)
-        return bm  # 3D Neumann faces are not built (forces.py)
-    from .forces import FACE_NODES_2D
-    faces = FACE_NODES_2D[family]
+    from .forces import face_nodes
+    faces = face_nodes(family, dim)
     bm.neumann_faces = [(e, f) for e, f in boundary_faces(m)
                         if all(m.fine[m.elem[e, p], 1] == bmax for p in faces[f])]
     return bm

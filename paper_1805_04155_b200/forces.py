@@ -5,8 +5,9 @@ the device cache) and a traction on the mesh's Neumann faces with the face
 rule and the face restriction of the basis (reference_elements.cpp:87-115,
 117-135,196-244,392-412,466-498); ``boundary_faces`` (mesh.cpp:294-310).
 
-2D meshes (faces are segments).  3D faces (triangle / quadrilateral rules)
-are not built; ``external_forces`` raises for them.
+2D faces are segments (Gauss rules, segment basis); 3D faces use the 2D
+volume rule and basis of the same family (triangles for tetrahedra,
+quadrilaterals for hexahedra) with the area element |t1 x t2|.
 """
 from __future__ import annotations
 
@@ -27,7 +28,25 @@ FACE_NODES_2D = {
     "Q1": [[0, 1], [1, 2], [2, 3], [3, 0]],
     "Q2": [[0, 1, 4], [1, 2, 5], [2, 3, 6], [3, 0, 7]],
 }
+FACE_NODES_3D = {
+    "P1": [[0, 2, 1], [0, 1, 3], [1, 2, 3], [0, 3, 2]],
+    "P2": [[0, 2, 1, 6, 5, 4], [0, 1, 3, 4, 7, 9], [1, 2, 3, 5, 8, 7], [0, 3, 2, 9, 8, 6]],
+    "Q1": [[0, 1, 2, 3], [4, 5, 6, 7], [0, 1, 5, 4], [1, 2, 6, 5], [2, 3, 7, 6], [3, 0, 4, 7]],
+    "Q2": [[0, 1, 2, 3, 8, 9, 10, 11], [4, 5, 6, 7, 12, 13, 14, 15], [0, 1, 5, 4, 8, 17, 12, 16],
+           [1, 2, 6, 5, 9, 18, 13, 17], [2, 3, 7, 6, 10, 19, 14, 18], [3, 0, 4, 7, 11, 16, 15, 19]],
+}
+
+
+def face_nodes(family: str, dim: int) -> list:
+    """face_nodes (reference_elements.cpp:466-498)."""
+    return (FACE_NODES_2D if dim == 2 else FACE_NODES_3D)[family]
+
+
 _QUAD_CORNERS = [(-1, -1), (1, -1), (1, 1), (-1, 1)]
+_HEX_CORNERS = [(-1, -1, -1), (1, -1, -1), (1, 1, -1), (-1, 1, -1),
+                (-1, -1, 1), (1, -1, 1), (1, 1, 1), (-1, 1, 1)]
+_HEX_EDGES = [(0, -1, -1), (1, 0, -1), (0, 1, -1), (-1, 0, -1), (0, -1, 1), (1, 0, 1),
+              (0, 1, 1), (-1, 0, 1), (-1, -1, 0), (1, -1, 0), (1, 1, 0), (-1, 1, 0)]
 _QUAD_EDGES = [(0, -1), (1, 0), (0, 1), (-1, 0)]
 
 
@@ -98,12 +117,87 @@ def volume_basis_values_2d(family: str, pts: np.ndarray) -> np.ndarray:
     return np.stack(vals)
 
 
+def volume_basis_grads_2d(family: str, pts: np.ndarray) -> np.ndarray:
+    """Reference gradients (2, n_p, m) of the 2D bases (reference_elements.cpp:117-135,196-244)."""
+    x, y = pts[0], pts[1]
+    one, zero = np.ones_like(x), np.zeros_like(x)
+    if family == "P1":
+        return np.stack([np.stack([-one, one, zero]), np.stack([-one, zero, one])])
+    if family == "P2":
+        z = 1.0 - x - y
+        return np.stack([np.stack([1 - 4 * z, 4 * x - 1, zero, 4 * (z - x), 4 * y, -4 * y]),
+                         np.stack([1 - 4 * z, zero, 4 * y - 1, -4 * x, 4 * x, 4 * (z - y)])])
+    if family == "Q1":
+        return np.stack([np.stack([0.25 * sx * (1 + sy * y) for sx, sy in _QUAD_CORNERS]),
+                         np.stack([0.25 * sy * (1 + sx * x) for sx, sy in _QUAD_CORNERS])])
+    gx, gy = [], []
+    for sx, sy in _QUAD_CORNERS:
+        ax, ay = 1 + sx * x, 1 + sy * y
+        r = sx * x + sy * y - 1
+        gx.append(0.25 * sx * (ay * r + ax * ay))
+        gy.append(0.25 * sy * (ax * r + ax * ay))
+    for sx, sy in _QUAD_EDGES:
+        if sx == 0:
+            gx.append(-x * (1 + sy * y))
+            gy.append(0.5 * sy * (1 - x * x))
+        else:
+            gx.append(0.5 * sx * (1 - y * y))
+            gy.append(-y * (1 + sx * x))
+    return np.stack([np.stack(gx), np.stack(gy)])
+
+
+def volume_rule_3d(family: str):
+    """quadrature_volume (reference_elements.cpp:20-84,345-372) in 3D: points (3, n_q), weights."""
+    if family == "P1":
+        return np.full((3, 1), 0.25), np.array([1.0 / 6.0])
+    if family == "P2":  # the reference's 11-point tetrahedron rule (Keast), its literals
+        a, b, f, g = 0.399403576166799, 0.100596423833201, 0.071428571428571, 0.785714285714286
+        w1, w2, w3 = -0.013155555555555, 0.007622222222222, 0.024888888888888
+        pts = np.array([[0.25, f, g, f, f, a, b, b, a, a, b],
+                        [0.25, f, f, g, f, b, a, b, a, b, a],
+                        [0.25, f, f, f, g, b, b, a, b, a, a]])
+        return pts, np.array([w1, w2, w2, w2, w2, w3, w3, w3, w3, w3, w3])
+    x1, w1 = gauss_segment(2 if family == "Q1" else 3)
+    n1 = x1.size
+    pts = np.zeros((3, n1 ** 3))
+    w = np.zeros(n1 ** 3)
+    for q in range(n1 ** 3):
+        idx, acc = q, 1.0
+        for i in range(3):
+            k = idx % n1
+            idx //= n1
+            pts[i, q] = x1[k]
+            acc *= w1[k]
+        w[q] = acc
+    return pts, w
+
+
+def volume_basis_values_3d(family: str, pts: np.ndarray) -> np.ndarray:
+    """Shape-function values (n_p, m) of the 3D bases (reference_elements.cpp:137-194,246-304)."""
+    x, y, z = pts[0], pts[1], pts[2]
+    if family == "P1":
+        return np.stack([1.0 - x - y - z, x, y, z])
+    if family == "P2":
+        x0 = 1.0 - x - y - z
+        return np.stack([x0 * (2 * x0 - 1), x * (2 * x - 1), y * (2 * y - 1), z * (2 * z - 1), 4 * x0 * x,
+                         4 * x * y, 4 * x0 * y, 4 * x * z, 4 * y * z, 4 * x0 * z])
+    if family == "Q1":
+        return np.stack([0.125 * (1 + sx * x) * (1 + sy * y) * (1 + sz * z) for sx, sy, sz in _HEX_CORNERS])
+    vals = []
+    for sx, sy, sz in _HEX_CORNERS:
+        ax, ay, az = 1 + sx * x, 1 + sy * y, 1 + sz * z
+        vals.append(0.125 * ax * ay * az * (sx * x + sy * y + sz * z - 2))
+    c = (x, y, z)
+    for e in _HEX_EDGES:
+        v = [1 - c[i] * c[i] if e[i] == 0 else 1 + e[i] * c[i] for i in range(3)]
+        vals.append(0.25 * v[0] * v[1] * v[2])
+    return np.stack(vals)
+
+
 def boundary_faces(mesh: StructuredMesh) -> list:
     """boundary_faces (mesh.cpp:294-310): the (element, face) pairs whose node
     set occurs once, sorted."""
-    if mesh.dim != 2:
-        raise A.Error("boundary_faces: 3D faces are not built here")
-    faces = FACE_NODES_2D[mesh.elem_type.family]
+    faces = face_nodes(mesh.elem_type.family, mesh.dim)
     table = {}
     for e in range(mesh.n_elements):
         for f, loc in enumerate(faces):
@@ -119,14 +213,16 @@ def external_forces(mesh: StructuredMesh, weight: np.ndarray, volume_force: Opti
     (element, point, node, direction) in the reference's loop order (one
     rounding per add, np.add.at is sequential in index order)."""
     dim = mesh.dim
-    if dim != 2:
-        raise A.Error("external_forces: 3D meshes are not built here")
     fam = mesh.elem_type.family
     f = np.zeros(mesh.n_dofs)
     coord, elem = mesh.coord, mesh.elem
     if volume_force is not None:
-        pts, _ = volume_rule_2d(fam)
-        vals = volume_basis_values_2d(fam, pts)  # (n_p, n_q)
+        if dim == 2:
+            pts, _ = volume_rule_2d(fam)
+            vals = volume_basis_values_2d(fam, pts)  # (n_p, n_q)
+        else:
+            pts, _ = volume_rule_3d(fam)
+            vals = volume_basis_values_3d(fam, pts)
         n_p, n_q = vals.shape
         # x_q = sum_p N_p(q) x_p, accumulated over p in order
         x = np.zeros((mesh.n_elements, n_q, dim))
@@ -141,19 +237,31 @@ def external_forces(mesh: StructuredMesh, weight: np.ndarray, volume_force: Opti
     if traction is not None:
         if not neumann_faces:
             raise A.Error("external_forces: traction given but mesh has no Neumann faces")
-        quadratic = fam in ("P2", "Q2")
-        fx, fw = gauss_segment({"P1": 1, "P2": 2, "Q1": 2, "Q2": 3}[fam])
-        vals, grads = _segment_basis(2 if quadratic else 1, fx)  # (n_fp, n_fq)
-        faces = FACE_NODES_2D[fam]
+        if dim == 2:
+            quadratic = fam in ("P2", "Q2")
+            fx, fw = gauss_segment({"P1": 1, "P2": 2, "Q1": 2, "Q2": 3}[fam])
+            vals, g1 = _segment_basis(2 if quadratic else 1, fx)  # (n_fp, n_fq)
+            grads = g1[None]                                      # (dim - 1, n_fp, n_fq)
+        else:
+            fpts, fw = volume_rule_2d(fam)
+            vals = volume_basis_values_2d(fam, fpts)
+            grads = volume_basis_grads_2d(fam, fpts)
+        faces = face_nodes(fam, dim)
         for e, fi in neumann_faces:
             nodes = [int(elem[e, p]) for p in faces[fi]]
-            for q in range(fx.size):
+            for q in range(fw.size):
                 x = np.zeros(dim)
-                t = np.zeros(dim)
+                t = np.zeros((dim - 1, dim))
                 for p, node in enumerate(nodes):
                     x += vals[p, q] * coord[node]
-                    t += grads[p, q] * coord[node]
-                area = math.sqrt(t[0] * t[0] + t[1] * t[1])
+                    for k in range(dim - 1):
+                        t[k] += grads[k, p, q] * coord[node]
+                if dim == 3:
+                    a, b = t[0], t[1]
+                    cr = (a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0])
+                    area = math.sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2])
+                else:
+                    area = math.sqrt(t[0, 0] * t[0, 0] + t[0, 1] * t[0, 1])
                 value = np.asarray(traction(x[None, :]), dtype=np.float64).reshape(dim)
                 for p, node in enumerate(nodes):
                     w = fw[q] * area * vals[p, q]

@@ -156,17 +156,18 @@ def test_run_dp_footing_matches_reference_driver(cuda, oracle):
 
 
 # ---------------------------------------------------------------- elastic body
-def _elastic_body_ref(O, level, family):
-    """mesh.cpp:222-258 restated per node (2D) over the oracle's numbering."""
+def _elastic_body_ref(O, level, family, dim=2):
+    """mesh.cpp:222-258 restated per node over the oracle's numbering."""
     block = 5 << level
     cells, h = 2 * block, 5.0 / block
+    nz = max(1, int(math.floor(1.0 / h + 0.5))) if dim == 3 else 0
     active = np.ones((cells, cells), np.uint8)
     active[:block, :block] = 0
-    coord, elem, fine = O.structured_mesh(family, 2, cells, cells, 0, h, h, None, active)
+    coord, elem, fine = O.structured_mesh(family, dim, cells, cells, nz, h, h, (1.0 / nz if nz else None), active)
     n = coord.shape[0]
-    free = np.ones((n, 2), bool)
-    fixed = np.zeros((n, 2))
-    load = np.zeros((n, 2))
+    free = np.ones((n, dim), bool)
+    fixed = np.zeros((n, dim))
+    load = np.zeros((n, dim))
 
     def constrain(d, node, f, l):
         free[node, d] = False
@@ -179,7 +180,35 @@ def _elastic_body_ref(O, level, family):
         if b == 0:
             constrain(1, node, 0.0, 0.0)
             constrain(0, node, 0.0, 1.0)
+        if dim == 3 and fine[node, 2] in (0, 2 * nz):
+            constrain(2, node, 0.0, 0.0)
     return coord, elem, free, fixed, load
+
+
+@pytest.mark.parametrize("family", ["P1", "P2", "Q1", "Q2"])
+def test_elastic_body_3d_mesh_and_forces(oracle, family):
+    """3D body (one layer): mesh and Dirichlet data equal the reference's
+    loop; Neumann faces lie on the top face; a unit volume force sums to the
+    volume (75) and the traction 200 to 200 x 10 x 1 (face rule = the 2D
+    volume rule, area element |t1 x t2|)."""
+    from paper_1805_04155_b200.benchmarks import build_mesh_elastic_body
+    from paper_1805_04155_b200.forces import constant_force, external_forces, face_nodes
+    bm = build_mesh_elastic_body(0, family, 3)
+    coord, elem, free, fixed, load = _elastic_body_ref(oracle, 0, family, 3)
+    m = bm.mesh
+    assert np.array_equal(m.coord, coord) and np.array_equal(m.elem, elem)
+    assert np.array_equal(bm.free_dof, free)
+    assert np.array_equal(bm.dirichlet_fixed, fixed) and np.array_equal(bm.dirichlet_load, load)
+    assert len(bm.neumann_faces) == (20 if family in ("P1", "P2") else 10)
+    for e, f in bm.neumann_faces:
+        assert np.all(coord[elem[e, face_nodes(family, 3)[f]], 1] == 10.0)
+    K, G = oracle.elastic_moduli(206900.0, 0.29)
+    w = oracle.Cache(family, 3, coord, elem, G, K).arrays()[1]
+    fv = external_forces(m, np.asarray(w), constant_force([0.0, 1.0, 0.0]))
+    assert abs(fv[1::3].sum() - 75.0) <= 1e-11 * 75.0 and np.all(fv[0::3] == 0.0) and np.all(fv[2::3] == 0.0)
+    ft = external_forces(m, np.asarray(w), None, constant_force([0.0, 200.0, 0.0]), bm.neumann_faces)
+    assert abs(ft[1::3].sum() - 2000.0) <= 1e-11 * 2000.0
+    assert np.all(ft[1::3][coord[:, 1] != 10.0] == 0.0)
 
 
 @pytest.mark.parametrize("family,level", [("P1", 0), ("P2", 0), ("Q1", 1), ("Q2", 0)])
@@ -231,7 +260,7 @@ def _traction_driver_ref(O, bm, model, f_steps, dirichlet, eps, max_iters):
     import scipy.sparse.linalg as spl
     m = bm.mesh
     K, G = O.elastic_moduli(206900.0, 0.29)
-    oc = O.Cache(m.elem_type.family, 2, m.coord, m.elem, G, K)
+    oc = O.Cache(m.elem_type.family, m.dim, m.coord, m.elem, G, K)
     Ke = oc.K_elast()
     Kes = sp.csr_matrix((Ke.data, Ke.indices, Ke.indptr))
 
@@ -272,23 +301,25 @@ def _traction_driver_ref(O, bm, model, f_steps, dirichlet, eps, max_iters):
 
 
 @pytest.mark.gpu
-def test_run_elastic_and_vm_cyclic_match_reference_drivers(cuda, oracle):
+@pytest.mark.parametrize("family,dim", [("Q2", 2), ("Q1", 3)])
+def test_run_elastic_and_vm_cyclic_match_reference_drivers(cuda, oracle, family, dim):
     """run_elastic and run_vm_cyclic (8 steps, traction to +-1 and back) on the
-    level-0 Q2-8 body vs the same drivers restated on the oracle with direct
+    level-0 Q2-8 (2D) and Q1 (3D, one layer) bodies vs the same drivers restated on the oracle with direct
     solves: plastic counts per step equal, Newton iterations within one (see
     below), u within 1e-8, the traction work f.u within 1e-9."""
     from paper_1805_04155_b200.benchmarks import (BenchmarkConfig, run_elastic, run_vm_cyclic,
                                                   vm_load_scale)
     from paper_1805_04155_b200.solver import NewtonSettings, SolveSettings
     ns = NewtonSettings(eps_newton=1e-10, max_iters=25, linear=SolveSettings(rel_tol=1e-12))
-    cfg = BenchmarkConfig(dim=2, elem="Q2", level=0, n_steps=8, newton=ns)
+    cfg = BenchmarkConfig(dim=dim, elem=family, level=0, n_steps=8, newton=ns)
     el = run_elastic(cfg, device=cuda)
     bm = el.mesh
     from paper_1805_04155_b200.forces import constant_force, external_forces
     K, G = oracle.elastic_moduli(206900.0, 0.29)
-    w = oracle.Cache("Q2", 2, bm.mesh.coord, bm.mesh.elem, G, K).arrays()[1]
-    f = external_forces(bm.mesh, np.asarray(w), constant_force([0.0, 1.0]), constant_force([0.0, 200.0]),
-                        bm.neumann_faces)
+    w = oracle.Cache(family, dim, bm.mesh.coord, bm.mesh.elem, G, K).arrays()[1]
+    e2 = [0.0, 1.0, 0.0][:dim]
+    t2 = [0.0, 200.0, 0.0][:dim]
+    f = external_forces(bm.mesh, np.asarray(w), constant_force(e2), constant_force(t2), bm.neumann_faces)
     (it, npl, u_ref), = _traction_driver_ref(oracle, bm, "elastic", [f], bm.dirichlet_values(0.5), 1e-10, 25)
     u = el.u.cpu().numpy()
     assert el.records[0].newton_iters == it and npl == 0
@@ -296,7 +327,7 @@ def test_run_elastic_and_vm_cyclic_match_reference_drivers(cuda, oracle):
     assert abs(el.records[0].derived_scalar - f @ u_ref) <= 1e-9 * abs(f @ u_ref)
 
     cy = run_vm_cyclic(cfg, device=cuda)
-    fmax = external_forces(bm.mesh, np.asarray(w), None, constant_force([0.0, 200.0]), bm.neumann_faces)
+    fmax = external_forces(bm.mesh, np.asarray(w), None, constant_force(t2), bm.neumann_faces)
     zetas = [vm_load_scale(4.0 * k / 8) for k in range(1, 9)]
     ref = _traction_driver_ref(oracle, bm, "vm", [z * fmax for z in zetas], bm.dirichlet_values(0.0), 1e-10, 25)
     assert len(cy.records) == 8 and [r.load for r in cy.records] == zetas
