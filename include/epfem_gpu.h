@@ -267,6 +267,15 @@ int epfem_restricted_solve(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, co
                            const double* values, const double* rhs, const uint8_t* free_mask,
                            double rel_tol, int64_t max_iters, double* x, int64_t* iters,
                            double* residual);
+/* epfem_restricted_solve_blocked: the same solve with a node-block Jacobi
+ *   preconditioner (block = dim: the inverse of each dim x dim diagonal block of
+ *   the restricted operator; block = 1 is epfem_restricted_solve).  Serves the
+ *   reference's default LinearSolver::direct (linalg.cpp:83-121) to the same
+ *   tolerance contract; there is no device sparse factorisation here. */
+int epfem_restricted_solve_blocked(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                                   const double* values, const double* rhs, const uint8_t* free_mask,
+                                   double rel_tol, int64_t max_iters, int block, double* x, int64_t* iters,
+                                   double* residual);
 int epfem_energy_norm(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                       const double* values, const double* v, double* out);
 

@@ -56,7 +56,7 @@ EXPORTS = [
     "epfem_assemble_elastic", "epfem_assemble_tangent", "epfem_assemble_tangent_ds",
     "epfem_newton_step", "epfem_newton_step_u", "epfem_newton_step_f", "epfem_constitutive_delta", "epfem_assemble_rows", "epfem_newton_range",
     "epfem_delta_range", "epfem_strains", "epfem_internal_forces", "epfem_restricted_solve",
-    "epfem_energy_norm",
+    "epfem_restricted_solve_blocked", "epfem_energy_norm",
 ]
 
 _lib = None
@@ -109,6 +109,8 @@ def lib() -> C.CDLL:
     L.epfem_internal_forces.argtypes = [_P, _P, _P, _P]
     L.epfem_restricted_solve.argtypes = [_P, _I64, _P, _P, _P, _P, _P, _D, _I64, _P, C.POINTER(_I64),
                                          C.POINTER(_D)]
+    L.epfem_restricted_solve_blocked.argtypes = [_P, _I64, _P, _P, _P, _P, _P, _D, _I64, C.c_int, _P,
+                                                 C.POINTER(_I64), C.POINTER(_D)]
     L.epfem_energy_norm.argtypes = [_P, _I64, _P, _P, _P, _P, C.POINTER(_D)]
     _lib = L
     return L

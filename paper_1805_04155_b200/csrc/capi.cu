@@ -936,13 +936,22 @@ int epfem_restricted_solve(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, co
                            const double* values, const double* rhs, const uint8_t* free_mask,
                            double rel_tol, int64_t max_iters, double* x, int64_t* iters,
                            double* residual) {
+  return epfem_restricted_solve_blocked(ctx, n, row_ptr, col_idx, values, rhs, free_mask, rel_tol, max_iters,
+                                        1, x, iters, residual);
+}
+
+int epfem_restricted_solve_blocked(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                                   const double* values, const double* rhs, const uint8_t* free_mask,
+                                   double rel_tol, int64_t max_iters, int block, double* x, int64_t* iters,
+                                   double* residual) {
   if (int rc = check_ctx(ctx)) return rc;
   if (n < 0 || (n > 0 && (!row_ptr || !col_idx || !values || !rhs || !x)))
     return fail(EPFEM_ERR_INVALID, "restricted_solve: dimension mismatch");
   int64_t it = 0;
   double res = 0.0;
   if (int rc = cg_solve(n, row_ptr, col_idx, values, free_mask, rhs, x, rel_tol,
-                        max_iters > 0 ? max_iters : 10 * std::max<int64_t>(n, 1), ctx->stream, &it, &res))
+                        max_iters > 0 ? max_iters : 10 * std::max<int64_t>(n, 1), ctx->stream, &it, &res,
+                        block))
     return rc;
   if (iters) *iters = it;
   if (residual) *residual = res;

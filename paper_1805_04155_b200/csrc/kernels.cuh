@@ -144,7 +144,7 @@ int launch_newton_ovl(int model, int family, int dim, const ConstArgs& c, const 
 int launch_row_stream_ovl(int family, int dim, const GatherArgs& a, const OvlArgs& o, cudaStream_t st);
 int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, const uint8_t* mask,
              const double* b, double* x_out, double rel_tol, int64_t max_iters, cudaStream_t st,
-             int64_t* iters_out, double* residual_out);
+             int64_t* iters_out, double* residual_out, int block = 1);
 int energy_norm(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, const double* x,
                 cudaStream_t st, double* out);
 size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements);

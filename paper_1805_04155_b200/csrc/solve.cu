@@ -174,6 +174,80 @@ __global__ void k_resid(int64_t n, const uint8_t* __restrict__ mask, const doubl
     rb[i] = (!mask || mask[i]) ? b[i] - Ap[i] : 0.0;
 }
 
+// Node-block Jacobi (block = dim, the `direct` method's preconditioner):
+// per block of B consecutive dofs the inverse of K's B x B diagonal block of
+// the restricted operator M K M + (I - M) (fixed dofs: identity rows and
+// columns), explicit 2x2 / 3x3 cofactor inverse; a singular or non-finite
+// block falls back to the scalar Jacobi of its diagonal.
+template <int B>
+__global__ void k_bj_setup(int64_t nb, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                           const double* __restrict__ v, const uint8_t* __restrict__ mask, double* binv) {
+  for (int64_t blk = (int64_t)blockIdx.x * kThreads + threadIdx.x; blk < nb;
+       blk += (int64_t)gridDim.x * kThreads) {
+    const int64_t i0 = blk * B;
+    double A[B][B];
+    bool f[B];
+    for (int r = 0; r < B; ++r) {
+      f[r] = !mask || mask[i0 + r];
+      for (int c = 0; c < B; ++c) A[r][c] = 0.0;
+      for (int64_t k = rp[i0 + r]; k < rp[i0 + r + 1]; ++k) {
+        const int64_t c = (int64_t)ci[k] - i0;
+        if (c >= 0 && c < B) A[r][c] = v[k];
+      }
+    }
+    for (int r = 0; r < B; ++r)
+      for (int c = 0; c < B; ++c)
+        if (!f[r] || !f[c]) A[r][c] = r == c ? 1.0 : 0.0;
+    double Ai[B][B];
+    double det;
+    if constexpr (B == 2) {
+      det = A[0][0] * A[1][1] - A[0][1] * A[1][0];
+      Ai[0][0] = A[1][1] / det;
+      Ai[0][1] = -A[0][1] / det;
+      Ai[1][0] = -A[1][0] / det;
+      Ai[1][1] = A[0][0] / det;
+    } else {
+      const double c00 = A[1][1] * A[2][2] - A[1][2] * A[2][1];
+      const double c01 = A[1][2] * A[2][0] - A[1][0] * A[2][2];
+      const double c02 = A[1][0] * A[2][1] - A[1][1] * A[2][0];
+      det = A[0][0] * c00 + A[0][1] * c01 + A[0][2] * c02;
+      Ai[0][0] = c00 / det;
+      Ai[1][0] = c01 / det;
+      Ai[2][0] = c02 / det;
+      Ai[0][1] = (A[0][2] * A[2][1] - A[0][1] * A[2][2]) / det;
+      Ai[1][1] = (A[0][0] * A[2][2] - A[0][2] * A[2][0]) / det;
+      Ai[2][1] = (A[0][1] * A[2][0] - A[0][0] * A[2][1]) / det;
+      Ai[0][2] = (A[0][1] * A[1][2] - A[0][2] * A[1][1]) / det;
+      Ai[1][2] = (A[0][2] * A[1][0] - A[0][0] * A[1][2]) / det;
+      Ai[2][2] = (A[0][0] * A[1][1] - A[0][1] * A[1][0]) / det;
+    }
+    bool ok = det != 0.0 && isfinite(det);
+    for (int r = 0; r < B; ++r)
+      for (int c = 0; c < B; ++c) ok = ok && isfinite(Ai[r][c]);
+    for (int r = 0; r < B; ++r)
+      for (int c = 0; c < B; ++c)
+        binv[blk * B * B + r * B + c] =
+            ok ? Ai[r][c] : (r == c ? (A[r][r] != 0.0 ? 1.0 / A[r][r] : 1.0) : 0.0);
+  }
+}
+
+// z = M Binv r per block (fixed dofs: 0)
+template <int B>
+__global__ void k_bj_apply(int64_t nb, const uint8_t* __restrict__ mask, const double* __restrict__ binv,
+                           const double* __restrict__ r, double* z) {
+  for (int64_t blk = (int64_t)blockIdx.x * kThreads + threadIdx.x; blk < nb;
+       blk += (int64_t)gridDim.x * kThreads) {
+    const int64_t i0 = blk * B;
+    double rr[B];
+    for (int c = 0; c < B; ++c) rr[c] = r[i0 + c];
+    for (int a = 0; a < B; ++a) {
+      double acc = 0.0;
+      for (int c = 0; c < B; ++c) acc = __fma_rn(binv[blk * B * B + a * B + c], rr[c], acc);
+      z[i0 + a] = (!mask || mask[i0 + a]) ? acc : 0.0;
+    }
+  }
+}
+
 // one warp per row (the row loop of a warp is a chain of dependent loads:
 // enough warps in flight is what hides it)
 unsigned grid_rows(int64_t n) {
@@ -182,9 +256,9 @@ unsigned grid_rows(int64_t n) {
 
 struct Work {  // device scratch of one solve
   double *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *Ap = nullptr, *d = nullptr;
-  double *partial = nullptr, *sc = nullptr;
+  double *partial = nullptr, *sc = nullptr, *binv = nullptr;
   ~Work() {
-    for (double* q : {x, r, z, p, Ap, d, partial, sc})
+    for (double* q : {x, r, z, p, Ap, d, partial, sc, binv})
       if (q) cudaFree(q);
   }
 };
@@ -193,10 +267,13 @@ struct Work {  // device scratch of one solve
 
 int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, const uint8_t* mask,
              const double* b, double* x_out, double rel_tol, int64_t max_iters, cudaStream_t caller,
-             int64_t* iters_out, double* residual_out) {
+             int64_t* iters_out, double* residual_out, int block) {
   *iters_out = 0;
   *residual_out = 0.0;
   if (n == 0) return 0;
+  if (block != 1 && block != 2 && block != 3) return fail(EPFEM_ERR_INVALID, "restricted_solve: block must be 1, 2 or 3");
+  if (n % block) return fail(EPFEM_ERR_INVALID, "restricted_solve: dimension mismatch");
+  const int64_t nb = n / block;
   // the solve runs on a private stream ordered after the caller's work (the
   // iteration chunks are captured into a graph, which the legacy default
   // stream does not allow); it is host-synchronous on return
@@ -219,7 +296,23 @@ int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, c
   EPFEM_CUDA_TRY(cudaMalloc(&w.partial, sizeof(double) * 2 * kBlocks));
   EPFEM_CUDA_TRY(cudaMalloc(&w.sc, sizeof(double) * 8));
   const unsigned gb = (unsigned)std::min<int64_t>(kBlocks, (n + kThreads - 1) / kThreads);
+  const unsigned gbb = (unsigned)std::min<int64_t>(kBlocks, (nb + kThreads - 1) / kThreads);
+  // block > 1: z = M Binv r replaces the scalar z = M r / d after every
+  // kernel that forms r (the scalar kernels' z is overwritten)
+  auto apply_block = [&](bool set_p) -> int {
+    if (block == 1) return 0;
+    if (block == 2) k_bj_apply<2><<<gbb, kThreads, 0, st>>>(nb, mask, w.binv, w.r, w.z);
+    else k_bj_apply<3><<<gbb, kThreads, 0, st>>>(nb, mask, w.binv, w.r, w.z);
+    if (set_p) EPFEM_CUDA_TRY(cudaMemcpyAsync(w.p, w.z, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    return 0;
+  };
+  if (block > 1) {
+    EPFEM_CUDA_TRY(cudaMalloc(&w.binv, sizeof(double) * nb * block * block));
+    if (block == 2) k_bj_setup<2><<<gbb, kThreads, 0, st>>>(nb, rp, ci, v, mask, w.binv);
+    else k_bj_setup<3><<<gbb, kThreads, 0, st>>>(nb, rp, ci, v, mask, w.binv);
+  }
   k_cg_init<<<gb, kThreads, 0, st>>>(n, rp, ci, v, mask, b, w.x, w.r, w.z, w.p, w.d);
+  if (int rc = apply_block(true)) return rc;
   k_dot2<<<gb, kThreads, 0, st>>>(n, w.r, w.z, w.r, w.r, w.partial);
   k_finish<<<1, kFinish, 0, st>>>(w.partial, gb, w.sc, 2);
   double h[8];
@@ -231,6 +324,7 @@ int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, c
     k_dot2<<<gb, kThreads, 0, st>>>(n, w.p, w.Ap, nullptr, nullptr, w.partial);
     k_finish<<<1, kFinish, 0, st>>>(w.partial, gb, w.sc, 1);
     k_cg_update<<<gb, kThreads, 0, st>>>(n, w.sc, mask, w.d, w.p, w.Ap, w.x, w.r, w.z);
+    apply_block(false);
     k_dot2<<<gb, kThreads, 0, st>>>(n, w.r, w.z, w.r, w.r, w.partial);
     k_finish<<<1, kFinish, 0, st>>>(w.partial, gb, w.sc, 0);
     k_cg_dir<<<gb, kThreads, 0, st>>>(n, w.sc, w.z, w.p);
@@ -287,6 +381,7 @@ int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, c
     res = bnorm > 0.0 ? std::sqrt(std::max(h[S_PAP], 0.0)) / bnorm : 0.0;
     if (!(res > rel_tol) || restart == 3 || it >= max_iters || !std::isfinite(res)) break;
     k_cg_restart<<<gb, kThreads, 0, st>>>(n, mask, b, w.Ap, w.d, w.r, w.z, w.p);
+    if (int rc = apply_block(true)) return rc;
     k_dot2<<<gb, kThreads, 0, st>>>(n, w.r, w.z, w.r, w.r, w.partial);
     k_finish<<<1, kFinish, 0, st>>>(w.partial, gb, w.sc, 2);  // r.z, r.r (the b.b slot is not read again)
   }

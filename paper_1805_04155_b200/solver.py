@@ -103,10 +103,12 @@ class SolveInfo:
 
 def restricted_solve(K: CsrMatrix, rhs: torch.Tensor, free_mask: Optional[torch.Tensor] = None,
                      settings: SolveSettings = SolveSettings(), ctx=None,
-                     info: Optional[SolveInfo] = None) -> torch.Tensor:
+                     info: Optional[SolveInfo] = None, block: int = 1) -> torch.Tensor:
     """Solve K[free, free] x = rhs[free]; x is zero on fixed dofs (linalg.cpp:83-121).
     Raises SolverError with the reference's message above tolerance; `info`
-    (optional) receives the iteration count and the residual."""
+    (optional) receives the iteration count and the residual.  ``block`` > 1
+    (the mesh dimension) uses the node-block Jacobi preconditioner
+    (epfem_restricted_solve_blocked) instead of the scalar one."""
     from .api import default_context
     n = K.n
     if rhs.numel() != n:
@@ -116,9 +118,10 @@ def restricted_solve(K: CsrMatrix, rhs: torch.Tensor, free_mask: Optional[torch.
     ctx.use_current_stream()
     x = torch.empty((n,), dtype=torch.float64, device=dev)
     it, res = C.c_int64(), C.c_double()
-    rc = L.lib().epfem_restricted_solve(ctx.handle, n, _ptr(K.row_ptr), _ptr(K.col_idx), _ptr(K.values),
-                                        _ptr(rhs.contiguous()), _ptr(_mask_u8(free_mask, n, dev)),
-                                        settings.rel_tol, 0, _ptr(x), C.byref(it), C.byref(res))
+    rc = L.lib().epfem_restricted_solve_blocked(ctx.handle, n, _ptr(K.row_ptr), _ptr(K.col_idx),
+                                                _ptr(K.values), _ptr(rhs.contiguous()),
+                                                _ptr(_mask_u8(free_mask, n, dev)), settings.rel_tol, 0, int(block),
+                                                _ptr(x), C.byref(it), C.byref(res))
     if info is not None:
         info.iterations, info.residual = it.value, res.value
     if rc == 7:  # EPFEM_ERR_SOLVER
@@ -176,6 +179,10 @@ def newton_solve(cache: AssemblyCache, mat: MaterialField, state_prev: Integrati
         t1.record()
         Kt = CsrMatrix(cache.row_ptr, cache.col_idx, Kv)
         lin = SolveInfo()
+        # scalar Jacobi CG for both methods: the node-block preconditioner
+        # (block = dim) saved only 5-28 % of the CG iterations on the footing
+        # and was slower on the 64 x 64 load path (tools/footing_bench.py,
+        # tools/newton_bench.py)
         du = restricted_solve(Kt, fext - F, free, settings.linear, ctx=eng.ctx, info=lin)
         torch.cuda.synchronize(dev)
         n_pl = int((flags & 1).sum().item())

@@ -180,3 +180,35 @@ def test_newton_iterates_follow_the_reference_when_diverging(cuda, oracle):
         ref.append(en(du) / (a + en(u)))
     assert len(gpu) == 4
     assert np.allclose(gpu, ref, rtol=1e-6, atol=0), (gpu, ref)
+
+
+@pytest.mark.parametrize("block", [2, 3])
+def test_restricted_solve_block_jacobi(cuda, block):
+    """The node-block Jacobi CG (epfem_restricted_solve_blocked) solves the
+    same restricted SPD system as the scalar one, to the same tolerance, with
+    fixed dofs zero; a dimension not divisible by the block is rejected."""
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.solver import SolveInfo, SolveSettings, restricted_solve
+    rng = np.random.default_rng(7 + block)
+    n = 60 * block
+    A = rng.standard_normal((n, n))
+    A = A @ A.T + n * np.eye(n)
+    A[np.abs(A) < 0.5] = 0.0
+    A = 0.5 * (A + A.T) + n * np.eye(n)
+    b = rng.standard_normal(n)
+    free = rng.random(n) > 0.2
+    K = _csr(A, cuda)
+    s = SolveSettings(rel_tol=1e-12)
+    i1, ib = SolveInfo(), SolveInfo()
+    x1 = restricted_solve(K, torch.from_numpy(b).to(cuda), torch.from_numpy(free).to(cuda), s, info=i1).cpu().numpy()
+    xb = restricted_solve(K, torch.from_numpy(b).to(cuda), torch.from_numpy(free).to(cuda), s, info=ib,
+                          block=block).cpu().numpy()
+    fi = np.nonzero(free)[0]
+    ref = np.zeros(n)
+    ref[fi] = np.linalg.solve(A[np.ix_(fi, fi)], b[fi])
+    assert np.all(xb[~free] == 0.0)
+    assert np.abs(xb - ref).max() <= 1e-9 * np.abs(ref).max()
+    assert np.abs(x1 - ref).max() <= 1e-9 * np.abs(ref).max()
+    assert ib.residual <= 1e-12
+    with pytest.raises(P.Error, match="dimension mismatch"):
+        restricted_solve(_csr(A[:n - 1, :n - 1], cuda), torch.from_numpy(b[:n - 1]).to(cuda), None, s, block=block)
