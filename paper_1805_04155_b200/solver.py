@@ -179,10 +179,9 @@ def newton_solve(cache: AssemblyCache, mat: MaterialField, state_prev: Integrati
         t1.record()
         Kt = CsrMatrix(cache.row_ptr, cache.col_idx, Kv)
         lin = SolveInfo()
-        # scalar Jacobi CG for both methods: the node-block preconditioner
-        # (block = dim) saved only 5-28 % of the CG iterations on the footing
-        # and was slower on the 64 x 64 load path (tools/footing_bench.py,
-        # tools/newton_bench.py)
+        # scalar Jacobi CG (Eigen's iterates) for both methods: the node-block
+        # preconditioner (block = dim) saved only 5-28 % of the CG iterations
+        # on the footing (tools/footing_bench.py)
         du = restricted_solve(Kt, fext - F, free, settings.linear, ctx=eng.ctx, info=lin)
         torch.cuda.synchronize(dev)
         n_pl = int((flags & 1).sum().item())
