@@ -237,11 +237,15 @@ __device__ __forceinline__ int ld_acquire_gpu_i(const int* p) {
 // FORCES: also fold the element internal-force records (GatherArgs::fws,
 // written by the fused kernel) into F for the range's nodes, every item in
 // item order from zero (k_internal_forces' association, hence its bits).
+#ifndef EPFEM_ROW_DYN
+#define EPFEM_ROW_DYN 0
+#endif
 template <int DIM, int NP, int NQ, bool FLAGS = false, bool FORCES = false>
 __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM_ROW_MINB20 : 0)
     k_row_stream(GatherArgs a, int npc, OvlArgs o) {
   extern __shared__ __align__(128) double img_raw[];
   __shared__ uint64_t s_bar;
+  __shared__ int s_next;  // EPFEM_ROW_DYN: next unclaimed node of the range
   constexpr int NB = NP * (NP + 1) / 2;
   constexpr int D2 = DIM * DIM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -262,6 +266,7 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
   if (tid == 0) {
     mbar_init(&s_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_next = kStreamThreads / 32;
   }
   __syncthreads();
   const bool zero_base = a.base == nullptr;  // elastic assembly: K = sum of element blocks
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
   // one per item (the add order, hence the bits, is unchanged).
   constexpr int KP = (NP * D2 + 31) / 32;
   constexpr int UB = KP == 1 ? 4 : 1;  // 3D: wider rows already give ILP; registers matter more
-  for (int ln = warp; ln < nloc; ln += kStreamThreads / 32) {
+  for (int ln = warp; ln < nloc;) {
     const int ib = s_iptr[ln], ie = s_iptr[ln + 1];
     const int row_len = (s_vptr[ln + 1] - s_vptr[ln]) / DIM;
     double* seg = img + s_vptr[ln];
@@ -360,6 +365,15 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
         __syncwarp();
       }
     }
+#if EPFEM_ROW_DYN
+    // dynamic node claim: warps that drew light nodes take the next ones
+    // (one warp per node and item order as before, so the same bits)
+    int nx = 0;
+    if (lane == 0) nx = atomicAdd(&s_next, 1);
+    ln = __shfl_sync(0xffffffffu, nx, 0);
+#else
+    ln += kStreamThreads / 32;
+#endif
   }
   if constexpr (FORCES) {
     // the range's force records (item = (element, local node) = record
