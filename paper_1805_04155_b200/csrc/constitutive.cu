@@ -75,14 +75,23 @@ namespace {
 #ifndef EPFEM_MINB_Q20
 #define EPFEM_MINB_Q20 16
 #endif
+// Tuning hook for the 2D CTA kernel (EPFEM_FUSED=cta): EPB_2D elements on
+// one thread per point at MINB_2D CTAs/SM, phase 2 in rounds.
+#ifndef EPFEM_EPB_2D
+#define EPFEM_EPB_2D 0
+#endif
+#ifndef EPFEM_MINB_2D
+#define EPFEM_MINB_2D 4
+#endif
 template <int DIM, int NP, int NQ>
 struct FusedCfg : DeltaCfg<DIM, NP, NQ> {
   using Base = DeltaCfg<DIM, NP, NQ>;
+  static constexpr bool D2C = DIM == 2 && EPFEM_EPB_2D > 0;
   static constexpr bool Q1 = DIM == 3 && NP == 8 && EPFEM_CTA_PAIRS && !EPFEM_TSHARED && EPFEM_EPB_Q1 > 0;
   static constexpr bool Q20 = DIM == 3 && NP == 20 && !EPFEM_HALFPAIRS20 && !EPFEM_TSHARED && EPFEM_EPB_Q20 > 0;
-  static constexpr int EPB = Q1 ? EPFEM_EPB_Q1 : (Q20 ? EPFEM_EPB_Q20 : Base::EPB);
-  static constexpr int THREADS = Q1 ? ((EPB * NQ + 31) / 32) * 32 : (Q20 ? EPFEM_THREADS_Q20 : Base::THREADS);
-  static constexpr int MINB = Q20 ? EPFEM_MINB_Q20 : Base::MINB;
+  static constexpr int EPB = Q1 ? EPFEM_EPB_Q1 : (Q20 ? EPFEM_EPB_Q20 : (D2C ? EPFEM_EPB_2D : Base::EPB));
+  static constexpr int THREADS = (Q1 || D2C) ? ((EPB * NQ + 31) / 32) * 32 : (Q20 ? EPFEM_THREADS_Q20 : Base::THREADS);
+  static constexpr int MINB = Q20 ? EPFEM_MINB_Q20 : (D2C ? EPFEM_MINB_2D : Base::MINB);
   static constexpr bool ROUNDS = THREADS < EPB * Base::NT;  // chunk phase 2 needs more than one pass
 };
 
