@@ -207,6 +207,15 @@ def boundary_faces(mesh: StructuredMesh) -> list:
     return sorted(v[1] for v in table.values() if v[0] == 1)
 
 
+def boundary_nodes(mesh: StructuredMesh) -> list:
+    """boundary_nodes (mesh.cpp:312-321): the nodes of the boundary faces, ascending."""
+    faces = face_nodes(mesh.elem_type.family, mesh.dim)
+    on = np.zeros(mesh.n_nodes, bool)
+    for e, f in boundary_faces(mesh):
+        on[mesh.elem[e, faces[f]]] = True
+    return np.nonzero(on)[0].tolist()
+
+
 def external_forces(mesh: StructuredMesh, weight: np.ndarray, volume_force: Optional[ForceField] = None,
                     traction: Optional[ForceField] = None, neumann_faces: Optional[list] = None) -> np.ndarray:
     """external_forces (assembly.cpp:231-296): f += w * value at every

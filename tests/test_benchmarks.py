@@ -393,3 +393,21 @@ def test_mesh_text_format_and_errors(tmp_path):
         bad.write_text(text)
         with pytest.raises(P.Error, match=msg):
             read_mesh_text(str(bad))
+
+
+@pytest.mark.parametrize("family,dim", [("P1", 2), ("Q2", 2), ("P2", 3), ("Q2", 3)])
+def test_boundary_nodes_of_a_box(family, dim):
+    """boundary_faces / boundary_nodes (mesh.cpp:294-321) on a structured box:
+    the boundary nodes are exactly those on the box's faces, and every
+    boundary face lies in one of them."""
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.forces import boundary_faces, boundary_nodes, face_nodes
+    m = P.structured_mesh(family, dim, 3, 2, 2 if dim == 3 else 0)
+    x = m.coord
+    on = np.zeros(m.n_nodes, bool)
+    for d in range(dim):
+        on |= (x[:, d] == 0.0) | (x[:, d] == x[:, d].max())
+    assert boundary_nodes(m) == np.nonzero(on)[0].tolist()
+    for e, f in boundary_faces(m):
+        fx = x[m.elem[e, face_nodes(family, dim)[f]]]
+        assert any(np.all(fx[:, d] == v) for d in range(dim) for v in (0.0, x[:, d].max()))
