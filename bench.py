@@ -215,7 +215,7 @@ def run_reference(args, rank, world):
     line = {
         "metric": METRIC, "value": value, "unit": "ip/s", "impl": "reference",
         "n_gpus": world, "steps": len(vals), "warmup": args.warmup,
-        "ms_per_step": 1e3 * n_int / value, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * n_int / value, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config},
         "cpu_baseline": {"value": value, "unit": "ip/s", "cores": cores, "kind": "port",
@@ -698,7 +698,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "ip/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "element": f"{cfg.family} {cfg.dim}D",
                        "mesh": f"{cfg.n}^{cfg.dim}", "model": cfg.model,
