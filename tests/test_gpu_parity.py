@@ -578,3 +578,44 @@ def test_newton_step_with_internal_forces(cuda, oracle, name, fused, monkeypatch
     oc = oracle.Cache(cfg.family, cfg.dim, mesh.coord, mesh.elem, G, K)
     Fref = oc.internal_forces(_np(S2))
     assert np.abs(_np(F) - Fref).max() <= 1e-12 * np.abs(Fref).max()
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("family", FAMILIES)
+def test_single_cell_mesh_all_plastic(cuda, oracle, family, dim):
+    """Edge case: a one-cell mesh (one element, or the cell's 2 / 6 simplices;
+    a CTA or warp group far from full) with every point plastic: flags and S
+    bitwise, K within 1e-12 row-scaled of the oracle."""
+    import paper_1805_04155_b200 as P
+    coord, elem, _ = oracle.structured_mesh(family, dim, 1, 1, 1 if dim == 3 else 0)
+    K, G = oracle.elastic_moduli(206900.0, 0.29)
+    oc = oracle.Cache(family, dim, coord, elem, G, K)
+    mesh = P.Mesh(P.ElementType(family, dim), _t(coord, cuda), _t(elem, cuda, torch.int32))
+    n = oc.n_int
+    E = np.random.default_rng(5).uniform(-1e-3, 1e-3, (n, 6))
+    if dim == 2:
+        E[:, [2, 4, 5]] = 0.0
+    a = 1.0e4
+    Y = 0.5 * float(oracle.constitutive_vm(E, None, None, G, K, a, 0.0)["crit"].min())
+    ref = oracle.constitutive_vm(E, None, None, G, K, a, Y)
+    assert ref["plastic"].all()
+    mat = P.uniform_von_mises(n, K, G, a, Y)
+    gc = P.build_assembly_cache(mesh, mat)
+    eng = P.TangentEngine(gc, mat)
+    S, flags, D, Kv = eng.step(_t(E, cuda))
+    eng.sync()
+    assert np.array_equal(_np(flags) & 1, ref["plastic"])
+    assert np.array_equal(_np(S), ref["S"])
+    Kref = oc.tangent(ref["DS"], ref["plastic"])
+    assert row_scaled_error(_np(Kv), Kref.data, Kref.indptr, oc.K_elast().data) <= 1e-12
+
+
+def test_empty_constitutive_batch(cuda):
+    """Edge case: zero integration points (the reference's 6 x 0 Mat) returns
+    empty outputs without a launch error."""
+    import paper_1805_04155_b200 as P
+    K, G = P.elastic_moduli(206900.0, 0.29)
+    mat = P.uniform_von_mises(0, K, G, 1.0e4, 450.0)
+    st = P.evaluate_constitutive(torch.zeros((0, 6), dtype=torch.float64, device=cuda),
+                                 P.IntegrationState.zero(0, device=cuda), mat)
+    assert st.S.shape[0] == 0 and st.plastic_mask.numel() == 0
