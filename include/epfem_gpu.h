@@ -9,13 +9,13 @@
  *   constitutive_elastic/vm/dp   include/epfem/constitutive.hpp:67,80-81,92-93
  *                                src/constitutive.cpp:76-225    epfem_constitutive
  *   build_assembly_cache         include/epfem/assembly.hpp:53
- *                                src/assembly.cpp:224-256       epfem_cache_build
+ *                                src/assembly.cpp:148-180       epfem_cache_build
  *   jacobians / weights          include/epfem/assembly.hpp:20-21
- *                                src/assembly.cpp:96-137        epfem_cache_geometry
+ *                                src/assembly.cpp:20-61        epfem_cache_geometry
  *   AssemblyCache::K_elast       include/epfem/assembly.hpp:45  epfem_cache_K_elast
  *   assemble_elastic_stiffness   include/epfem/assembly.hpp:55  epfem_assemble_elastic
  *   assemble_tangent_stiffness   include/epfem/assembly.hpp:59-60
- *                                src/assembly.cpp:262-289       epfem_assemble_tangent (packed D)
+ *                                src/assembly.cpp:186-213       epfem_assemble_tangent (packed D)
  *                                                               epfem_assemble_tangent_ds (36 x n_int DS)
  *   sparsity of K (Eigen CSC)    src/linalg.cpp:28-35           epfem_cache_pattern
  *   AssemblyCache::strains       include/epfem/assembly.hpp:50  epfem_strains
@@ -73,7 +73,7 @@ enum epfem_status {
 /* epfem::ElementFamily order (reference_elements.hpp:10) */
 enum epfem_family { EPFEM_P1 = 0, EPFEM_P2 = 1, EPFEM_Q1 = 2, EPFEM_Q2 = 3 };
 
-/* MaterialField::plastic variant (constitutive.hpp:120-129) */
+/* MaterialField::plastic variant (constitutive.hpp:18-38) */
 enum epfem_model {
   EPFEM_MODEL_ELASTIC = 0,        /* std::monostate */
   EPFEM_MODEL_VON_MISES = 1,      /* VonMisesParams {a, Y} */
@@ -180,11 +180,11 @@ int epfem_cache_geometry(const epfem_cache* cache, const double** det,
 int epfem_cache_workspace(const epfem_cache* cache, const double** records, const unsigned** emask,
                           int64_t* record_doubles);
 
-/* K5 recomputed into K_values (nnz doubles) (assembly.cpp:258-260). */
+/* K5 recomputed into K_values (nnz doubles) (assembly.cpp:182-184). */
 int epfem_assemble_elastic(epfem_ctx* ctx, const epfem_cache* cache, double* K_values);
 
 /* K6+K2: K = K_elast + sum over plastic points of B^T w (D - C) B, written
- * into the cached pattern (assembly.cpp:262-289).  Rows with no plastic
+ * into the cached pattern (assembly.cpp:186-213).  Rows with no plastic
  * contribution are bitwise copies of K_elast. */
 int epfem_assemble_tangent(epfem_ctx* ctx, const epfem_cache* cache, int64_t n_int,
                            const double* D, const uint8_t* flags, double* K_values);
@@ -213,9 +213,7 @@ int epfem_newton_step_u(epfem_ctx* ctx, const epfem_cache* cache, const epfem_ma
  * 2; the reference computes them each iteration, solver.cpp:25):
  * F_out (n_dofs) = B^T (weight * S) (internal_forces, assembly.cpp:215-225).
  * epfem_newton_step followed by K9 (two passes: element force records, then
- * a per-node fold); EPFEM_FORCES_FUSED=1 selects the fused 2D form (the
- * constitutive kernel forms the records, the row stream folds them).  Either
- * way bitwise the same F as epfem_internal_forces on out->S. */
+ * a per-node fold), bitwise the same F as epfem_internal_forces on out->S. */
 int epfem_newton_step_f(epfem_ctx* ctx, const epfem_cache* cache, const epfem_material* mat,
                         const double* E, const double* Ep_prev, const double* Hard_prev,
                         const epfem_constitutive_out* out, double* K_values, double* F_out);
@@ -245,15 +243,15 @@ int epfem_newton_range(epfem_ctx* ctx, const epfem_cache* cache, const epfem_mat
 int epfem_delta_range(epfem_ctx* ctx, const epfem_cache* cache, int64_t n_int, const double* D,
                       const uint8_t* flags, int64_t e_begin, int64_t e_end);
 
-/* K8: E = B u, 2D embedded in Voigt rows {0,1,3} (assembly.cpp:211-222). */
+/* K8: E = B u, 2D embedded in Voigt rows {0,1,3} (assembly.cpp:135-146). */
 int epfem_strains(epfem_ctx* ctx, const epfem_cache* cache, const double* u, double* E);
-/* K9: F = B^T (weight * S) (assembly.cpp:291-301). */
+/* K9: F = B^T (weight * S) (assembly.cpp:215-225). */
 int epfem_internal_forces(epfem_ctx* ctx, const epfem_cache* cache, const double* S,
                           double* F);
 
 /* Newton-loop linear algebra on any CSR matrix
  * (row_ptr int64 n+1, col_idx int32, values), device pointers.
- * epfem_restricted_solve: restricted_solve (linalg.cpp:37-121) with the
+ * epfem_restricted_solve: restricted_solve (linalg.cpp:69-115) with the
  *   reference's LinearSolver::conjugate_gradient method: Jacobi-preconditioned
  *   CG on K[free, free] (free_mask: one byte per row, NULL = all free),
  *   stopping at |r| <= rel_tol |b_free|, at most max_iters iterations (<= 0:
@@ -262,16 +260,18 @@ int epfem_internal_forces(epfem_ctx* ctx, const epfem_cache* cache, const double
  *   when the true residual |b - K x|_free / |b_free| exceeds rel_tol or is
  *   not finite.  iters / residual (may be NULL) report the solve.
  *   Deterministic (fixed-order reductions).
- * epfem_energy_norm: sqrt(max(v . K v, 0)) (linalg.cpp:123-127). */
+ * epfem_energy_norm: sqrt(max(v . K v, 0)) (linalg.cpp:117-121). */
 int epfem_restricted_solve(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                            const double* values, const double* rhs, const uint8_t* free_mask,
                            double rel_tol, int64_t max_iters, double* x, int64_t* iters,
                            double* residual);
 /* epfem_restricted_solve_blocked: the same solve with a node-block Jacobi
  *   preconditioner (block = dim: the inverse of each dim x dim diagonal block of
- *   the restricted operator; block = 1 is epfem_restricted_solve).  Serves the
- *   reference's default LinearSolver::direct (linalg.cpp:83-121) to the same
- *   tolerance contract; there is no device sparse factorisation here. */
+ *   the restricted operator; block = 1 is epfem_restricted_solve).  There is
+ *   no device sparse factorisation here: the reference's default
+ *   LinearSolver::direct (SimplicialLDLT + refinement, linalg.cpp:84-96) is
+ *   NOT reproduced; a host caller asking for it gets this CG under the same
+ *   tolerance contract (the Python solver warns and records the substitution). */
 int epfem_restricted_solve_blocked(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                                    const double* values, const double* rhs, const uint8_t* free_mask,
                                    double rel_tol, int64_t max_iters, int block, double* x, int64_t* iters,

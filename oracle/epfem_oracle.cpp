@@ -767,7 +767,7 @@ int64_t constitutive_dp(int64_t n, const double* E, const double* Ep,
 }
 
 // ---------------------------------------------------------------------------
-// Assembly cache (assembly.cpp:96-256).
+// Assembly cache (assembly.cpp:20-180).
 static const int kPlane[3] = {0, 1, 3};
 
 struct Cache {
@@ -780,7 +780,7 @@ struct Cache {
   double elastic_seconds = 0.0;
 };
 
-// Jacobians (assembly.cpp:96-137).  Eigen's fixed-size determinant and
+// Jacobians (assembly.cpp:20-61).  Eigen's fixed-size determinant and
 // cofactor inverse are written out.
 static int64_t jacobians(Cache& c, const double* coord, const int32_t* elem) {
   const int dim = c.dim, np = c.np, nq = c.nq;
@@ -832,7 +832,7 @@ static int64_t jacobians(Cache& c, const double* coord, const int32_t* elem) {
   return 0;
 }
 
-// Global strain-displacement matrix (assembly.cpp:139-185).
+// Global strain-displacement matrix (assembly.cpp:63-109).
 static void strain_displacement(Cache& c, const int32_t* elem) {
   const int dim = c.dim, np = c.np, nq = c.nq, ns = c.ns;
   Triplets t;
@@ -870,8 +870,8 @@ static void strain_displacement(Cache& c, const int32_t* elem) {
   c.B = from_triplets(t, (int64_t)ns * c.nint, (int64_t)dim * c.nn);
 }
 
-// Block-diagonal weight(q) * DS_q (assembly.cpp:187-209); with `only`, blocks
-// (DS_q - C_q) at flagged columns (the tangent's D_diff, assembly.cpp:272-287).
+// Block-diagonal weight(q) * DS_q (assembly.cpp:111-133); with `only`, blocks
+// (DS_q - C_q) at flagged columns (the tangent's D_diff, assembly.cpp:196-211).
 static Csc block_diag(const Cache& c, const double* DS, const uint8_t* only,
                       bool subtract_elastic) {
   const int ns = c.ns;
@@ -976,7 +976,7 @@ int64_t or_constitutive_dp(int64_t n, const double* E, const double* Ep,
   return constitutive_dp(n, E, Ep, G, K, eta, c, S, DS, Ep_out, smooth, apex);
 }
 
-// build_assembly_cache (assembly.cpp:224-256).  Returns null on error
+// build_assembly_cache (assembly.cpp:148-180).  Returns null on error
 // (or_last_error() has the reference's message).
 void* or_cache_build(int family, int dim, int64_t n_nodes, const double* coord,
                      int64_t n_elems, const int32_t* elem, const double* shear,
@@ -1050,7 +1050,7 @@ void or_cache_B(void* h, int64_t* outer, int32_t* inner, double* val) {
   copy_csc(static_cast<Cache*>(h)->B, outer, inner, val);
 }
 
-// Strains E = B u, 2D embedded into Voigt rows {0,1,3} (assembly.cpp:211-222).
+// Strains E = B u, 2D embedded into Voigt rows {0,1,3} (assembly.cpp:135-146).
 // E is 6 x n_int column-major.  SpMV in column order like Eigen's col-major
 // sparse * dense product.
 void or_cache_strains(void* h, const double* u, double* E) {
@@ -1065,7 +1065,7 @@ void or_cache_strains(void* h, const double* u, double* E) {
       E[6 * q + (c->dim == 3 ? i : kPlane[i])] = ef[(size_t)c->ns * q + i];
 }
 
-// F = B^T (W S)  (assembly.cpp:291-301).
+// F = B^T (W S)  (assembly.cpp:215-225).
 void or_cache_internal_forces(void* h, const double* S, double* F) {
   Cache* c = static_cast<Cache*>(h);
   std::vector<double> sc((size_t)c->ns * c->nint);
@@ -1092,7 +1092,7 @@ static void* wrap(Csc&& A) {
   return k;
 }
 
-// assemble_tangent_stiffness (assembly.cpp:262-289): K_elast when nothing is
+// assemble_tangent_stiffness (assembly.cpp:186-213): K_elast when nothing is
 // plastic, else K_elast + sandwich(B, D_diff).  Returns null on size mismatch.
 void* or_cache_tangent(void* h, int64_t n_int, const double* DS,
                        const uint8_t* plastic) {
@@ -1115,7 +1115,7 @@ void* or_cache_direct(void* h, const double* DS) {
   return wrap(sandwich(c->B, block_diag(*c, DS, nullptr, false)));
 }
 
-// assemble_elastic_stiffness (assembly.cpp:258-260).
+// assemble_elastic_stiffness (assembly.cpp:182-184).
 void* or_cache_elastic(void* h) {
   Cache* c = static_cast<Cache*>(h);
   return wrap(sandwich(c->B, c->Delast));

@@ -241,7 +241,7 @@ def _take_k(handle):
 
 
 class Cache:
-    """build_assembly_cache restated (assembly.cpp:224-256)."""
+    """build_assembly_cache restated (assembly.cpp:148-180)."""
 
     def __init__(self, family, dim, coord, elem, shear, bulk):
         L = lib()

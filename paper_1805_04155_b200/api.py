@@ -139,7 +139,7 @@ class DruckerPragerParams:
 
 @dataclass
 class MaterialField:
-    """Per-integration-point moduli and plastic model (constitutive.hpp:120-129).
+    """Per-integration-point moduli and plastic model (constitutive.hpp:18-38).
 
     Each field is either a python float (uniform) or a CUDA float64 tensor of
     length n_int.
@@ -158,6 +158,16 @@ class MaterialField:
         if self.plastic is None:
             return L.MODEL_ELASTIC
         return L.MODEL_VON_MISES if isinstance(self.plastic, VonMisesParams) else L.MODEL_DRUCKER_PRAGER
+
+    def slice(self, p0: int, p1: int) -> "MaterialField":
+        """The field of points [p0, p1): per-point arrays sliced, uniform values kept."""
+        cut = (lambda v: v[p0:p1] if isinstance(v, torch.Tensor) else v)
+        plastic = self.plastic
+        if isinstance(plastic, VonMisesParams):
+            plastic = VonMisesParams(cut(plastic.a), cut(plastic.Y))
+        elif isinstance(plastic, DruckerPragerParams):
+            plastic = DruckerPragerParams(cut(plastic.eta), cut(plastic.c))
+        return MaterialField(p1 - p0, cut(self.shear), cut(self.bulk), plastic)
 
     def view(self) -> L.Material:
         m = L.Material()
@@ -524,7 +534,7 @@ class AssemblyCache:
         return r, m
 
     def strains(self, u: torch.Tensor) -> torch.Tensor:
-        """E = B u, 6 x n_int with 2D rows {0,1,3} (assembly.cpp:211-222)."""
+        """E = B u, 6 x n_int with 2D rows {0,1,3} (assembly.cpp:135-146)."""
         if u.numel() != self.info.n_dofs or u.dtype != torch.float64:
             raise Error("strains: size mismatch")
         E = torch.empty((self.n_int, 6), dtype=torch.float64, device=self.device)
@@ -546,7 +556,7 @@ def build_assembly_cache(mesh: Union[Mesh, StructuredMesh], mat: MaterialField) 
 
 
 def assemble_elastic_stiffness(cache: AssemblyCache) -> CsrMatrix:
-    """sandwich(B, D_elast) recomputed (assembly.cpp:258-260)."""
+    """sandwich(B, D_elast) recomputed (assembly.cpp:182-184)."""
     vals = torch.empty((cache.nnz,), dtype=torch.float64, device=cache.device)
     cache.ctx.use_current_stream()
     _check(L.lib().epfem_assemble_elastic(cache.ctx.handle, cache.handle, _ptr(vals)))
@@ -555,7 +565,7 @@ def assemble_elastic_stiffness(cache: AssemblyCache) -> CsrMatrix:
 
 def assemble_tangent_stiffness(cache: AssemblyCache, DS: torch.Tensor,
                                plastic_cols: torch.Tensor) -> CsrMatrix:
-    """K_elast + B^T (D_tangent - D_elast) B (assembly.cpp:262-289).
+    """K_elast + B^T (D_tangent - D_elast) B (assembly.cpp:186-213).
 
     DS is (n_int, 36) in the reference layout; plastic_cols a bool mask."""
     if DS.dim() != 2 or DS.shape[0] != cache.n_int or DS.shape[1] != 36 or \
@@ -582,7 +592,7 @@ def assemble_tangent_packed(cache: AssemblyCache, D: torch.Tensor, flags: torch.
 
 
 def internal_forces(cache: AssemblyCache, S: torch.Tensor) -> torch.Tensor:
-    """F = B^T (weight * S) (assembly.cpp:291-301)."""
+    """F = B^T (weight * S) (assembly.cpp:215-225)."""
     if S.shape[0] != cache.n_int:
         raise Error("internal_forces: size mismatch")
     F = torch.empty((cache.info.n_dofs,), dtype=torch.float64, device=cache.device)

@@ -1,6 +1,6 @@
 """The paper's displacement-driven strip-footing benchmark over the GPU path
 (SURVEY §8(f) rank 4): the mesh with its Dirichlet data
-(``build_mesh_footing``, proj/src/mesh.cpp:262-293, with ``Mesh::free_mask`` /
+(``build_mesh_footing``, proj/src/mesh.cpp:260-291, with ``Mesh::free_mask`` /
 ``dirichlet_values`` / ``constrain``, mesh.cpp:12-25,212-216) and the load
 driver ``run_dp_footing`` (proj/src/benchmarks.cpp:120-205): Drucker-Prager
 (E = 1e7, nu = 0.48, c0 = 450, phi = pi/9), adaptive footing displacement
@@ -86,7 +86,7 @@ class BoundaryMesh:
 
 
 def build_mesh_footing(level: int, family: str, dim: int, layers: int = -1) -> BoundaryMesh:
-    """build_mesh_footing (mesh.cpp:262-293): the 10 x 10 (x 1) half-domain
+    """build_mesh_footing (mesh.cpp:260-291): the 10 x 10 (x 1) half-domain
     under a rigid rough strip footing of unit width at the top left.  Sides
     slide (u1 = 0), the base slides (u2 = 0), the footing nodes carry
     u2 = -u_D (load pattern -1) and u1 = 0; 3D fronts have u3 = 0."""
@@ -334,7 +334,7 @@ def _g17(x: float) -> str:
 
 
 def write_mesh_text(bm: BoundaryMesh, path: str) -> None:
-    """write_mesh_text (mesh.cpp:323-355): header, nodes, elements, the
+    """write_mesh_text (mesh.cpp:323-354): header, nodes, elements, the
     constrained dofs in (node, direction) order, the Neumann faces."""
     m = bm.mesh
     try:
@@ -362,7 +362,7 @@ def write_mesh_text(bm: BoundaryMesh, path: str) -> None:
 
 
 def read_mesh_text(path: str) -> BoundaryMesh:
-    """read_mesh_text (mesh.cpp:357-410), with its error messages.  The mesh
+    """read_mesh_text (mesh.cpp:356-410), with its error messages.  The mesh
     carries no fine-grid indices (``fine`` is None)."""
     from .mesh import ElementType, node_count
     try:

@@ -34,7 +34,7 @@ SOURCES = {
     "solve.cu": [],
     "tables.cpp": [],
 }
-HEADERS = ["common.cuh", "kernels.cuh", "delta.cuh", "tma.cuh", "rows.cuh"]
+HEADERS = ["common.cuh", "kernels.cuh", "delta.cuh", "tma.cuh"]
 
 
 def nvcc() -> str:

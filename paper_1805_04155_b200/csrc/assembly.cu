@@ -35,7 +35,7 @@
 namespace epfem_gpu {
 
 // ---------------------------------------------------------------------------
-// Geometry: det J, J^-1, weight (assembly.cpp:96-137, 237-241)
+// Geometry: det J, J^-1, weight (assembly.cpp:20-61, 237-241)
 template <int DIM, int NP, int NQ>
 __global__ void k_jacobians(int64_t n_e, const int32_t* __restrict__ elem,
                             const double* __restrict__ coord,
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(32 * kGatherWarps) k_gather(GatherArgs a) {
       if (!contrib) continue;
 
       // effective material block Dw = w * (D - C) or w * C, reduced to the
-      // assembly rows (2D: Voigt rows {0,1,3}, assembly.cpp:92,123-124)
+      // assembly rows (2D: Voigt rows {0,1,3}, assembly.cpp:16,123-124)
       const double Gm = a.shear ? __ldg(a.shear + m) : a.shear_u;
       const double Km = a.bulk ? __ldg(a.bulk + m) : a.bulk_u;
       constexpr int R[6] = {0, 1, DIM == 3 ? 2 : 3, 3, 4, 5};
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(32 * kGatherWarps) k_gather(GatherArgs a) {
           Dw[c][r] = w * v;
         }
       if constexpr (DIM == 3) {
-        // T = B_a^T Dw  (B rows e11,e22,e33,2e12,2e23,2e31; assembly.cpp:162-171)
+        // T = B_a^T Dw  (B rows e11,e22,e33,2e12,2e23,2e31; assembly.cpp:86-95)
         double T[3][6];
 #pragma unroll
         for (int c = 0; c < 6; ++c) {
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(32 * kGatherWarps) k_gather(GatherArgs a) {
           blk[i][2] += T[i][2] * h[2] + T[i][4] * h[1] + T[i][5] * h[0];
         }
       } else {
-        // 2D rows e11, e22, 2e12 (assembly.cpp:173-176)
+        // 2D rows e11, e22, 2e12 (assembly.cpp:96-100)
         double T[2][3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(32 * kGatherWarps) k_gather(GatherArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// K8 strains E = B u, one thread per integration point (assembly.cpp:211-222)
+// K8 strains E = B u, one thread per integration point (assembly.cpp:135-146)
 template <int DIM, int NP, int NQ>
 __global__ void k_strains(int64_t n_e, const int32_t* __restrict__ elem,
                           const double* __restrict__ inv, const double* __restrict__ gradhat,

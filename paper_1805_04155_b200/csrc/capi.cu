@@ -30,17 +30,12 @@ int cuda_fail(cudaError_t err, const char* what) {
 
 using namespace epfem_gpu;
 
-constexpr int kMaxChunks = 32;
-
 struct epfem_ctx {
   int device = 0;
   int num_sms = 148;
   cudaStream_t stream = nullptr;
   bool sync = false;
   DevErr* err = nullptr;  // device
-  // side stream + events of the overlapped (chunked) Newton step
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_chunk[kMaxChunks] = {};
 };
 
 struct epfem_cache {
@@ -59,31 +54,7 @@ struct epfem_cache {
   double* scratch = nullptr;  // tangent workspace (symmetric dK_e per element)
   unsigned* emask = nullptr;  // per-element plastic-point bitmask
   int npc = 64, max_span = 0, max_items = 0;  // row-stream plan
-  int32_t* range_order = nullptr;             // row-stream CTA -> node range (space-filling curve)
-  double* fws = nullptr;                      // element internal-force records (2D fused forces step)
-  // overlapped Newton step: row chunk k (nodes [nchunk[k], nchunk[k+1]))
-  // needs exactly the element chunks 0..k (elements [echunk[j], echunk[j+1]))
-  int n_chunks = 1;
-  int64_t nchunk[kMaxChunks + 1] = {}, echunk[kMaxChunks + 1] = {};
-  // one-launch Newton step (k_newton_mega, 2D): item list, per-range group
-  // spans, per-group flags + ticket/generation words
-  int32_t* mega_sched = nullptr;
-  int32_t* mega_rlo = nullptr;
-  int32_t* mega_rhi = nullptr;
-  int* mega_flag = nullptr;
-  MegaSync* mega_sync = nullptr;
-  int64_t mega_items = 0;
-  int mega_group = 0;
-  int mega_npc = 0, mega_span = 0, mega_max_items = 0;  // node-range plan within one warp's slice
-  int mega_slice = 0, mega_workers = 0;                  // bytes of smem per warp, warps of the grid
-  // overlapped two-kernel step (2D): per-range group spans for the row
-  // stream's npc, per-group flags, finished counter + generation
-  int32_t* ovl_rlo = nullptr;
-  int32_t* ovl_rhi = nullptr;
-  int* ovl_flag = nullptr;
-  MegaSync* ovl_sync = nullptr;
-  int64_t ovl_groups = 0;
-  int ovl_group = 0;
+  double* fws = nullptr;                      // element internal-force records (K9)
 };
 
 namespace {
@@ -117,6 +88,22 @@ int finish(epfem_ctx* ctx) {
 }
 
 bool aligned16(const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; }
+
+// Every entry point taking a context runs on the context's device and
+// restores the caller's current device on return (torch or the host
+// application may have another device current).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(const epfem_ctx* ctx) {
+    if (!ctx) return;
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != ctx->device && cudaSetDevice(ctx->device) == cudaSuccess)
+      prev = cur;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 }  // namespace
 
@@ -166,9 +153,9 @@ int epfem_ctx_create(int device, void* cuda_stream, epfem_ctx** out) {
   if (e != cudaSuccess || n == 0)
     return fail(EPFEM_ERR_CUDA, "epfem_gpu: no CUDA device available (there is no CPU fallback)");
   if (device < 0 || device >= n) return fail(EPFEM_ERR_INVALID, "epfem_gpu: invalid device");
-  EPFEM_CUDA_TRY(cudaSetDevice(device));
   epfem_ctx* c = new epfem_ctx;
   c->device = device;
+  DeviceGuard guard(c);
   c->stream = (cudaStream_t)cuda_stream;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   e = cudaMalloc(&c->err, sizeof(DevErr));
@@ -179,21 +166,6 @@ int epfem_ctx_create(int device, void* cuda_stream, epfem_ctx** out) {
   DevErr z{};
   z.index = ~0ull;
   cudaMemcpy(c->err, &z, sizeof(DevErr), cudaMemcpyHostToDevice);
-  // the side stream carries the row stream of the overlapped step: highest
-  // priority, so its CTAs take SM slots ahead of the next fused chunk
-  int prio_lo = 0, prio_hi = 0;
-  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-  if (cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
-    epfem_ctx_destroy(c);
-    return cuda_fail(cudaGetLastError(), "side stream / events");
-  }
-  for (auto& ev : c->ev_chunk)
-    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
-      epfem_ctx_destroy(c);
-      return cuda_fail(cudaGetLastError(), "chunk events");
-    }
   *out = c;
   return 0;
 }
@@ -211,6 +183,7 @@ int epfem_ctx_set_sync(epfem_ctx* ctx, int synchronous) {
 }
 
 int epfem_ctx_sync(epfem_ctx* ctx) {
+  DeviceGuard guard(ctx);
   if (int rc = check_ctx(ctx)) return rc;
   EPFEM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return poll_device_error(ctx, nullptr);
@@ -218,12 +191,8 @@ int epfem_ctx_sync(epfem_ctx* ctx) {
 
 int epfem_ctx_destroy(epfem_ctx* ctx) {
   if (!ctx) return 0;
+  DeviceGuard guard(ctx);
   if (ctx->err) cudaFree(ctx->err);
-  for (auto ev : ctx->ev_chunk)
-    if (ev) cudaEventDestroy(ev);
-  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
-  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
-  if (ctx->side) cudaStreamDestroy(ctx->side);
   delete ctx;
   return 0;
 }
@@ -297,6 +266,7 @@ static int const_args(epfem_ctx* ctx, const epfem_material* mat, const double* E
 int epfem_constitutive(epfem_ctx* ctx, const epfem_material* mat, const double* E,
                        const double* Ep_prev, const double* Hard_prev,
                        const epfem_constitutive_out* out) {
+  DeviceGuard guard(ctx);
   ConstArgs a;
   if (int rc = const_args(ctx, mat, E, Ep_prev, Hard_prev, out, &a)) return rc;
   if (int rc = launch_constitutive(mat->model, a, ctx->stream, ctx->num_sms)) return rc;
@@ -308,9 +278,7 @@ int epfem_cache_destroy(epfem_cache* c) {
   void* ptrs[] = {c->gradhat, c->wq,          c->elem,        c->det,          c->inv,
                   c->weight,  c->shear,       c->bulk,        c->pat.n2e_ptr,  c->pat.n2e,
                   c->pat.nbr_ptr, c->pat.row_ptr, c->pat.col_idx, c->pat.slot, c->K_elast,
-                  c->scratch, c->emask, c->mega_sched, c->mega_rlo, c->mega_rhi, c->mega_flag,
-                  c->mega_sync, c->range_order, c->ovl_rlo, c->ovl_rhi, c->ovl_flag, c->ovl_sync,
-                  c->fws};
+                  c->scratch, c->emask, c->fws};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -339,12 +307,11 @@ static GatherArgs gather_args(const epfem_cache* c) {
   g.npc = c->npc;
   g.max_span = c->max_span;
   g.max_items = c->max_items;
-  g.range_order = c->range_order;
   g.e_begin = 0;
   g.e_end = c->info.n_elements;
   g.n_begin = 0;
   g.n_end = c->info.n_nodes;
-  // packed elastic operator C = K VOL + 2G DEV (voigt.hpp:72-74) for a uniform material
+  // packed elastic operator C = K VOL + 2G DEV (voigt.hpp:33-36) for a uniform material
   for (int i = 0; i < 6; ++i)
     for (int j = i; j < 6; ++j) {
       const double vol = (i < 3 && j < 3) ? 1.0 : 0.0;
@@ -354,108 +321,9 @@ static GatherArgs gather_args(const epfem_cache* c) {
   return g;
 }
 
-// Item list of the one-launch Newton step (k_newton_mega): producer groups
-// in element order, each node range placed after the last group it reads
-// plus SLACK groups (two rounds of the round-robin walk, so that the group
-// has usually finished when the range's worker gets there;
-// EPFEM_MEGA_SLACK overrides).  EPFEM_MEGA=1 enables the path.
-static int plan_mega(epfem_cache* c, cudaStream_t st) {
-  const epfem_cache_info& I = c->info;
-  int ge = 0;
-  // Opt-in (EPFEM_MEGA=1): measured on B200, cfg2, the one-launch step
-  // takes 0.55 ms against 0.357 ms for the two launches.  The warp-owned
-  // node ranges are latency-bound (0.50 ms for the row-stream role alone vs
-  // 0.169 ms for the CTA row stream) and the producer role loses ~35% to the
-  // persistent walk (0.283 vs 0.204 ms).  Kept, parity-tested, as the base
-  // for a CTA-granular consumer role.
-  static const bool off = [] {
-    const char* v = getenv("EPFEM_MEGA");
-    return !(v && v[0] == '1') || getenv("EPFEM_FUSED") != nullptr;
-  }();
-  int slice = 0, workers = 0;
-  if (off || I.n_nodes == 0 || I.n_elements == 0 || !mega_supported(I.family, I.dim, &ge, &slice, &workers))
-    return 0;
-  const int row_budget = getenv("EPFEM_MEGA_ROWB") ? atoi(getenv("EPFEM_MEGA_ROWB")) : slice;
-  if (int rc = plan_row_stream(I.n_nodes, I.dim, c->pat.nbr_ptr, c->pat.n2e_ptr, st, &c->mega_npc, &c->mega_span,
-                               &c->mega_max_items, row_budget))
-    return rc;
-  if (8 * ((size_t)c->mega_span + 2) + 4 * ((size_t)c->mega_max_items + 2 * ((size_t)c->mega_npc + 1)) >
-      (size_t)slice)
-    return 0;  // a single node's range does not fit a warp's slice: two-launch step
-  c->mega_slice = slice;
-  c->mega_workers = workers;
-  const int64_t n_groups = (I.n_elements + ge - 1) / ge;
-  const int64_t n_ranges = (I.n_nodes + c->mega_npc - 1) / c->mega_npc;
-  if (n_groups + n_ranges >= INT32_MAX) return 0;
-  int64_t slack = 2 * (int64_t)workers;  // two rounds of the worker walk
-  if (const char* v = getenv("EPFEM_MEGA_SLACK")) slack = atoi(v);
-  EPFEM_CUDA_TRY(cudaMalloc(&c->mega_rlo, sizeof(int32_t) * n_ranges));
-  EPFEM_CUDA_TRY(cudaMalloc(&c->mega_rhi, sizeof(int32_t) * n_ranges));
-  if (int rc = launch_range_groups(I.n_nodes, c->mega_npc, I.n_p, ge, c->pat.n2e_ptr, c->pat.n2e, c->mega_rlo,
-                                   c->mega_rhi, st))
-    return rc;
-  std::vector<int32_t> rhi(n_ranges);
-  EPFEM_CUDA_TRY(cudaMemcpyAsync(rhi.data(), c->mega_rhi, sizeof(int32_t) * n_ranges, cudaMemcpyDeviceToHost, st));
-  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
-  std::vector<int32_t> order(n_ranges);
-  for (int64_t r = 0; r < n_ranges; ++r) order[r] = (int32_t)r;
-  std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return rhi[x] < rhi[y]; });
-  std::vector<int32_t> sched;
-  sched.reserve(n_groups + n_ranges);
-  size_t k = 0;
-  for (int64_t gi = 0; gi < n_groups; ++gi) {
-    sched.push_back((int32_t)gi);
-    while (k < order.size() && (int64_t)rhi[order[k]] + slack <= gi) sched.push_back(~order[k++]);
-  }
-  while (k < order.size()) sched.push_back(~order[k++]);
-  c->mega_items = (int64_t)sched.size();
-  c->mega_group = ge;
-  EPFEM_CUDA_TRY(cudaMalloc(&c->mega_sched, sizeof(int32_t) * sched.size()));
-  EPFEM_CUDA_TRY(cudaMemcpyAsync(c->mega_sched, sched.data(), sizeof(int32_t) * sched.size(),
-                                 cudaMemcpyHostToDevice, st));
-  EPFEM_CUDA_TRY(cudaMalloc(&c->mega_flag, sizeof(int) * n_groups));
-  EPFEM_CUDA_TRY(cudaMemsetAsync(c->mega_flag, 0, sizeof(int) * n_groups, st));
-  EPFEM_CUDA_TRY(cudaMalloc(&c->mega_sync, sizeof(MegaSync)));
-  EPFEM_CUDA_TRY(cudaMemsetAsync(c->mega_sync, 0, sizeof(MegaSync), st));
-  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));  // the host vectors go out of scope
-  return 0;
-}
-
-// Overlapped step plan (2D, opt-in EPFEM_OVL=1): producer groups of one
-// warp (EPW elements), the group span of every row-stream range.  Measured
-// on B200, cfg2: 0.43 ms against 0.363 ms for the two launches back to back.
-// The persistent update alone takes 0.265 ms (0.212 non-persistent), and the
-// two kernels run concurrently on two streams with no dependency at all take
-// 0.485 ms: the latency-bound update slows down more under the row stream's
-// bandwidth load than the overlap recovers.  Kept, parity-tested, as
-// evidence and for hardware where that balance differs.
-static int plan_ovl(epfem_cache* c, cudaStream_t st) {
-  const epfem_cache_info& I = c->info;
-  int ge = 0;
-  static const bool off = [] {
-    const char* v = getenv("EPFEM_OVL");
-    return !(v && v[0] == '1') || getenv("EPFEM_FUSED") != nullptr;
-  }();
-  if (off || I.n_nodes == 0 || I.n_elements == 0 || !ovl_supported(I.family, I.dim, &ge)) return 0;
-  const int64_t n_groups = (I.n_elements + ge - 1) / ge;
-  const int64_t n_ranges = (I.n_nodes + c->npc - 1) / c->npc;
-  if (n_groups >= INT32_MAX || n_ranges >= INT32_MAX) return 0;
-  EPFEM_CUDA_TRY(cudaMalloc(&c->ovl_rlo, sizeof(int32_t) * n_ranges));
-  EPFEM_CUDA_TRY(cudaMalloc(&c->ovl_rhi, sizeof(int32_t) * n_ranges));
-  if (int rc = launch_range_groups(I.n_nodes, c->npc, I.n_p, ge, c->pat.n2e_ptr, c->pat.n2e, c->ovl_rlo,
-                                   c->ovl_rhi, st))
-    return rc;
-  EPFEM_CUDA_TRY(cudaMalloc(&c->ovl_flag, sizeof(int) * n_groups));
-  EPFEM_CUDA_TRY(cudaMemsetAsync(c->ovl_flag, 0, sizeof(int) * n_groups, st));
-  EPFEM_CUDA_TRY(cudaMalloc(&c->ovl_sync, sizeof(MegaSync)));
-  EPFEM_CUDA_TRY(cudaMemsetAsync(c->ovl_sync, 0, sizeof(MegaSync), st));
-  c->ovl_groups = n_groups;
-  c->ovl_group = ge;
-  return 0;
-}
-
 int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_material* mat,
                       epfem_cache** out) {
+  DeviceGuard guard(ctx);
   if (int rc = check_ctx(ctx)) return rc;
   if (!mesh || !mat || !out) return fail(EPFEM_ERR_INVALID, "build_assembly_cache: null argument");
   *out = nullptr;
@@ -469,6 +337,9 @@ int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_materi
     return fail(EPFEM_ERR_INVALID, "build_assembly_cache: material field size mismatch");
   if (mesh->n_nodes >= (int64_t)INT32_MAX / mesh->dim)
     return fail(EPFEM_ERR_UNSUPPORTED, "build_assembly_cache: too many nodes for int32 columns");
+  // the node -> item lists hold item = element * n_p + local node as int32
+  if (mesh->n_elements >= (int64_t)INT32_MAX / tab.np)
+    return fail(EPFEM_ERR_UNSUPPORTED, "build_assembly_cache: too many elements for int32 item ids");
   cudaStream_t st = ctx->stream;
   epfem_cache* c = new epfem_cache;
   epfem_cache_info& I = c->info;
@@ -541,40 +412,10 @@ int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_materi
     if (int rc = plan_row_stream(I.n_nodes, I.dim, c->pat.nbr_ptr, c->pat.n2e_ptr, st, &c->npc,
                                  &c->max_span, &c->max_items))
       return bail(rc);
-  {
-    // opt-in (EPFEM_RANGE_ORDER=1): measured on B200 no faster on cfg3/cfg5
-    // and slower on cfg2/cfg4 (3.88 -> 4.05 ms) than node order
-    const char* v = getenv("EPFEM_RANGE_ORDER");
-    const bool on = v && v[0] == '1';
-    if (on && I.n_nodes > 0)
-      if (int rc = plan_range_order(I.n_nodes, I.dim, c->npc, mesh->coord, st, &c->range_order)) return bail(rc);
-  }
-  {
-    // overlap plan, opt-in via EPFEM_CHUNKS: measured on B200 the chunked
-    // two-stream schedule is slower than one fused + one row launch (cfg2:
-    // 0.412 ms at 4 chunks vs 0.377 ms) because each fused launch fills the
-    // GPU and the row-stream CTAs only start as it drains
-    int want = 1;
-    if (const char* v = getenv("EPFEM_CHUNKS")) want = std::max(1, std::min(kMaxChunks, atoi(v)));
-    if (want > 1 && I.n_nodes > 0) {
-      const int n = plan_chunks(I.n_nodes, I.n_elements, I.n_p, c->pat.n2e_ptr, c->pat.n2e, c->npc,
-                                want, c->nchunk, c->echunk, st);
-      if (n < 0) return bail(EPFEM_ERR_CUDA);
-      c->n_chunks = n;
-    } else {
-      c->n_chunks = 1;
-      c->nchunk[0] = 0;
-      c->nchunk[1] = I.n_nodes;
-      c->echunk[0] = 0;
-      c->echunk[1] = I.n_elements;
-    }
-  }
   GatherArgs g = gather_args(c);
   g.out = c->K_elast;
   if (int rc = elastic_assembly(g, I.family, I.dim, c->K_elast, st)) return bail(rc);
   CT(cudaEventRecord(ev[2], st));
-  if (int rc = plan_mega(c, st)) return bail(rc);
-  if (int rc = plan_ovl(c, st)) return bail(rc);
   CT(cudaStreamSynchronize(st));
   float ms_p = 0, ms_e = 0;
   cudaEventElapsedTime(&ms_p, ev[0], ev[1]);
@@ -631,6 +472,7 @@ int epfem_cache_geometry(const epfem_cache* c, const double** det, const double*
 }
 
 int epfem_assemble_elastic(epfem_ctx* ctx, const epfem_cache* c, double* K_values) {
+  DeviceGuard guard(ctx);
   if (int rc = check_ctx(ctx)) return rc;
   if (!c || !K_values) return fail(EPFEM_ERR_INVALID, "assemble_elastic_stiffness: null argument");
   if (!aligned16(K_values))
@@ -661,11 +503,13 @@ static int tangent_common(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int, c
 
 int epfem_assemble_tangent(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int, const double* D,
                            const uint8_t* flags, double* K_values) {
+  DeviceGuard guard(ctx);
   return tangent_common(ctx, c, n_int, D, flags, K_values, 1);
 }
 
 int epfem_assemble_tangent_ds(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int,
                               const double* DS, const uint8_t* plastic_cols, double* K_values) {
+  DeviceGuard guard(ctx);
   return tangent_common(ctx, c, n_int, DS, plastic_cols, K_values, 2);
 }
 
@@ -696,36 +540,6 @@ static int delta_part(epfem_ctx* ctx, const epfem_cache* c, const epfem_material
   return launch_newton_fused(mat->model, c->info.family, c->info.dim, a, g, ctx->stream);
 }
 
-// Overlapped step: element chunk k (fused kernel) on the context stream,
-// row chunk k (row stream) on the side stream after chunk k's event, so the
-// memory-bound assembly of chunk k runs under the compute-bound update of
-// chunk k+1.  Fork/join events keep the call ordered on the context stream
-// (and capturable into one CUDA graph).
-static int overlapped_step(epfem_ctx* ctx, const epfem_cache* c, int model, const ConstArgs& a,
-                           GatherArgs g, double* K_values) {
-  g.base = c->K_elast;
-  g.out = K_values;
-  // EPFEM_CHUNK_SERIAL: both launches of a chunk on the context stream (the
-  // chunk's workspace is still L2-resident when its rows are assembled)
-  static const bool serial = getenv("EPFEM_CHUNK_SERIAL") != nullptr;
-  cudaStream_t rs = serial ? ctx->stream : ctx->side;
-  EPFEM_CUDA_TRY(cudaEventRecord(ctx->ev_fork, ctx->stream));
-  EPFEM_CUDA_TRY(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-  for (int k = 0; k < c->n_chunks; ++k) {
-    g.e_begin = c->echunk[k];
-    g.e_end = c->echunk[k + 1];
-    if (int rc = launch_newton_fused(model, c->info.family, c->info.dim, a, g, ctx->stream)) return rc;
-    EPFEM_CUDA_TRY(cudaEventRecord(ctx->ev_chunk[k], ctx->stream));
-    EPFEM_CUDA_TRY(cudaStreamWaitEvent(ctx->side, ctx->ev_chunk[k], 0));
-    g.n_begin = c->nchunk[k];
-    g.n_end = c->nchunk[k + 1];
-    if (int rc = launch_row_stream(c->info.family, c->info.dim, g, rs)) return rc;
-  }
-  EPFEM_CUDA_TRY(cudaEventRecord(ctx->ev_join, ctx->side));
-  EPFEM_CUDA_TRY(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
-  return 0;
-}
-
 static int rows_part(epfem_ctx* ctx, const epfem_cache* c, double* K_values) {
   if (int rc = check_ctx(ctx)) return rc;
   if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
@@ -740,44 +554,9 @@ static int rows_part(epfem_ctx* ctx, const epfem_cache* c, double* K_values) {
 int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
                       const double* E, const double* Ep_prev, const double* Hard_prev,
                       const epfem_constitutive_out* out, double* K_values) {
+  DeviceGuard guard(ctx);
   if (!K_values || !aligned16(K_values))
     return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: K must be 16-byte aligned");
-  if (c && c->n_chunks > 1) {
-    ConstArgs a;
-    GatherArgs g;
-    if (int rc = delta_args(ctx, c, mat, E, Ep_prev, Hard_prev, out, &a, &g)) return rc;
-    if (int rc = overlapped_step(ctx, c, mat->model, a, g, K_values)) return rc;
-    return finish(ctx);
-  }
-  if (c && c->mega_items > 0) {
-    ConstArgs a;
-    GatherArgs g;
-    if (int rc = delta_args(ctx, c, mat, E, Ep_prev, Hard_prev, out, &a, &g)) return rc;
-    g.base = c->K_elast;
-    g.out = K_values;
-    g.npc = c->mega_npc;
-    g.max_span = c->mega_span;
-    g.max_items = c->mega_max_items;
-    static const int exp = getenv("EPFEM_MEGA_EXP") ? atoi(getenv("EPFEM_MEGA_EXP")) : 0;
-    MegaArgs m{c->mega_sched, c->mega_rlo, c->mega_rhi, c->mega_flag, c->mega_sync, c->mega_items,
-               c->mega_group, exp};
-    if (int rc = launch_newton_mega(mat->model, c->info.family, c->info.dim, a, g, m, c->mega_slice,
-                                    c->mega_workers, ctx->stream))
-      return rc;
-    return finish(ctx);
-  }
-  if (c && c->ovl_groups > 0) {
-    ConstArgs a;
-    GatherArgs g;
-    if (int rc = delta_args(ctx, c, mat, E, Ep_prev, Hard_prev, out, &a, &g)) return rc;
-    g.base = c->K_elast;
-    g.out = K_values;
-    OvlArgs o{c->ovl_rlo, c->ovl_rhi, c->ovl_flag, c->ovl_sync, c->ovl_groups, c->ovl_group};
-    static const int per_sm = getenv("EPFEM_OVL_CTAS") ? atoi(getenv("EPFEM_OVL_CTAS")) : 4;
-    if (int rc = launch_newton_ovl(mat->model, c->info.family, c->info.dim, a, g, o, per_sm, ctx->stream)) return rc;
-    if (int rc = launch_row_stream_ovl(c->info.family, c->info.dim, g, o, ctx->stream)) return rc;
-    return finish(ctx);
-  }
   if (int rc = delta_part(ctx, c, mat, E, Ep_prev, Hard_prev, out)) return rc;
   if (int rc = rows_part(ctx, c, K_values)) return rc;
   return finish(ctx);
@@ -786,30 +565,15 @@ int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* c, const epfem_material
 int epfem_newton_step_f(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
                         const double* E, const double* Ep_prev, const double* Hard_prev,
                         const epfem_constitutive_out* out, double* K_values, double* F_out) {
+  DeviceGuard guard(ctx);
   if (!K_values || !aligned16(K_values))
     return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: K must be 16-byte aligned");
   if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
   if (c->info.n_nodes > 0 && !F_out) return fail(EPFEM_ERR_INVALID, "internal_forces: null argument");
-  // The fused 2D form (the constitutive kernel forms the element force
-  // records, the row stream folds them) is opt-in, EPFEM_FORCES_FUSED=1:
-  // measured on B200, cfg2, it adds 0.10 ms to the step against 0.08 ms for
-  // the two-pass K9 after it (the records' point loop and the staging of
-  // every point sit on each warp's critical path).
-  const char* ff = getenv("EPFEM_FORCES_FUSED");
-  if (ff && ff[0] == '1' && forces_fused_supported(c->info.family, c->info.dim) && c->info.n_elements > 0) {
-    ConstArgs a;
-    GatherArgs g;
-    if (int rc = delta_args(ctx, c, mat, E, Ep_prev, Hard_prev, out, &a, &g)) return rc;
-    g.fws = c->fws;
-    if (int rc = launch_newton_forces(mat->model, c->info.family, c->info.dim, a, g, ctx->stream)) return rc;
-    GatherArgs r = gather_args(c);
-    r.base = c->K_elast;
-    r.out = K_values;
-    r.fws = c->fws;
-    r.F_out = F_out;
-    if (int rc = launch_row_stream(c->info.family, c->info.dim, r, ctx->stream)) return rc;
-    return finish(ctx);
-  }
+  // K9 in two passes after the step (element force records, then a per-node
+  // fold in item order).  A form fused into the 2D step (records from the
+  // constitutive kernel, fold in the row stream) gave the same bits but
+  // measured slower on cfg2 (+0.10 vs +0.08 ms).
   if (int rc = epfem_newton_step(ctx, c, mat, E, Ep_prev, Hard_prev, out, K_values)) return rc;
   if (c->info.n_nodes == 0) return 0;
   if (int rc = launch_internal_forces(c->info.family, c->info.dim, c->info.n_nodes, c->info.n_elements, c->pat.n2e_ptr,
@@ -822,6 +586,7 @@ int epfem_newton_step_f(epfem_ctx* ctx, const epfem_cache* c, const epfem_materi
 int epfem_newton_step_u(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
                         const double* u, const double* Ep_prev, const double* Hard_prev,
                         const epfem_constitutive_out* out, double* E_out, double* K_values) {
+  DeviceGuard guard(ctx);
   if (!K_values || !aligned16(K_values))
     return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: K must be 16-byte aligned");
   if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
@@ -842,11 +607,13 @@ int epfem_newton_step_u(epfem_ctx* ctx, const epfem_cache* c, const epfem_materi
 int epfem_constitutive_delta(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
                              const double* E, const double* Ep_prev, const double* Hard_prev,
                              const epfem_constitutive_out* out) {
+  DeviceGuard guard(ctx);
   if (int rc = delta_part(ctx, c, mat, E, Ep_prev, Hard_prev, out)) return rc;
   return finish(ctx);
 }
 
 int epfem_assemble_rows(epfem_ctx* ctx, const epfem_cache* c, double* K_values) {
+  DeviceGuard guard(ctx);
   if (int rc = rows_part(ctx, c, K_values)) return rc;
   return finish(ctx);
 }
@@ -858,6 +625,7 @@ int epfem_assemble_rows(epfem_ctx* ctx, const epfem_cache* c, double* K_values) 
 int epfem_newton_range(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,
                        const double* E, const double* Ep_prev, const double* Hard_prev,
                        const epfem_constitutive_out* out, int64_t e_begin, int64_t e_end) {
+  DeviceGuard guard(ctx);
   if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
   if (e_begin < 0 || e_end < e_begin || e_end > c->info.n_elements)
     return fail(EPFEM_ERR_INVALID, "newton_range: element range out of bounds");
@@ -892,6 +660,7 @@ int epfem_newton_range(epfem_ctx* ctx, const epfem_cache* c, const epfem_materia
 
 int epfem_delta_range(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int, const double* D,
                       const uint8_t* flags, int64_t e_begin, int64_t e_end) {
+  DeviceGuard guard(ctx);
   if (int rc = check_ctx(ctx)) return rc;
   if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
   if (n_int != c->info.n_int) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: size mismatch");
@@ -911,6 +680,7 @@ int epfem_delta_range(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int, const
 }
 
 int epfem_strains(epfem_ctx* ctx, const epfem_cache* c, const double* u, double* E) {
+  DeviceGuard guard(ctx);
   if (int rc = check_ctx(ctx)) return rc;
   if (!c || !u || !E) return fail(EPFEM_ERR_INVALID, "strains: null argument");
   if (!aligned16(E)) return fail(EPFEM_ERR_INVALID, "strains: E must be 16-byte aligned");
@@ -922,6 +692,7 @@ int epfem_strains(epfem_ctx* ctx, const epfem_cache* c, const double* u, double*
 }
 
 int epfem_internal_forces(epfem_ctx* ctx, const epfem_cache* c, const double* S, double* F) {
+  DeviceGuard guard(ctx);
   if (int rc = check_ctx(ctx)) return rc;
   if (!c || !S || !F) return fail(EPFEM_ERR_INVALID, "internal_forces: null argument");
   if (c->info.n_nodes == 0) return 0;
@@ -936,6 +707,7 @@ int epfem_restricted_solve(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, co
                            const double* values, const double* rhs, const uint8_t* free_mask,
                            double rel_tol, int64_t max_iters, double* x, int64_t* iters,
                            double* residual) {
+  DeviceGuard guard(ctx);
   return epfem_restricted_solve_blocked(ctx, n, row_ptr, col_idx, values, rhs, free_mask, rel_tol, max_iters,
                                         1, x, iters, residual);
 }
@@ -944,6 +716,7 @@ int epfem_restricted_solve_blocked(epfem_ctx* ctx, int64_t n, const int64_t* row
                                    const double* values, const double* rhs, const uint8_t* free_mask,
                                    double rel_tol, int64_t max_iters, int block, double* x, int64_t* iters,
                                    double* residual) {
+  DeviceGuard guard(ctx);
   if (int rc = check_ctx(ctx)) return rc;
   if (n < 0 || (n > 0 && (!row_ptr || !col_idx || !values || !rhs || !x)))
     return fail(EPFEM_ERR_INVALID, "restricted_solve: dimension mismatch");
@@ -962,6 +735,7 @@ int epfem_restricted_solve_blocked(epfem_ctx* ctx, int64_t n, const int64_t* row
 
 int epfem_energy_norm(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                       const double* values, const double* v, double* out) {
+  DeviceGuard guard(ctx);
   if (int rc = check_ctx(ctx)) return rc;
   if (!out || n < 0 || (n > 0 && (!row_ptr || !col_idx || !values || !v)))
     return fail(EPFEM_ERR_INVALID, "energy_norm: dimension mismatch");

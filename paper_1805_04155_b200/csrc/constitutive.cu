@@ -23,26 +23,10 @@
 // straight from registers (D is never re-read).  Phase 2 builds dK_e
 // (delta.cuh).  The row stream (tangent.cu) then assembles K.
 #include <algorithm>
-#include <map>
-#include <mutex>
 #include <climits>
 #include <type_traits>
 
-#include "rows.cuh"
-
-#ifndef EPFEM_WARP_PAIRS
-#define EPFEM_WARP_PAIRS 1  // 2D warp kernel: phase 2 by row pairs
-#endif
-#ifndef EPFEM_HALFPAIRS20
-#define EPFEM_HALFPAIRS20 0  // Q2-20 CTA kernel with half row pairs (delta_pairs3_half): fewer FMA, but
-                             // measured slower on cfg5 (21.1 vs 16.0 ms; shared-memory loads per FMA)
-#endif
-#ifndef EPFEM_CTA_PAIRS
-#define EPFEM_CTA_PAIRS 1
-#endif
-#ifndef EPFEM_TSHARED
-#define EPFEM_TSHARED 0  // 1: 3D CTA phase 2 with T_a shared through shared memory (measured slower: the per-point barriers)
-#endif
+#include "delta.cuh"
 
 namespace epfem_gpu {
 
@@ -75,53 +59,32 @@ namespace {
 #ifndef EPFEM_MINB_Q20
 #define EPFEM_MINB_Q20 16
 #endif
-// Tuning hook for the 2D CTA kernel (EPFEM_FUSED=cta): EPB_2D elements on
-// one thread per point at MINB_2D CTAs/SM, phase 2 in rounds.
-#ifndef EPFEM_EPB_2D
-#define EPFEM_EPB_2D 0
-#endif
-#ifndef EPFEM_MINB_2D
-#define EPFEM_MINB_2D 4
-#endif
 template <int DIM, int NP, int NQ>
 struct FusedCfg : DeltaCfg<DIM, NP, NQ> {
   using Base = DeltaCfg<DIM, NP, NQ>;
-  static constexpr bool D2C = DIM == 2 && EPFEM_EPB_2D > 0;
-  static constexpr bool Q1 = DIM == 3 && NP == 8 && EPFEM_CTA_PAIRS && !EPFEM_TSHARED && EPFEM_EPB_Q1 > 0;
-  static constexpr bool Q20 = DIM == 3 && NP == 20 && !EPFEM_HALFPAIRS20 && !EPFEM_TSHARED && EPFEM_EPB_Q20 > 0;
-  static constexpr int EPB = Q1 ? EPFEM_EPB_Q1 : (Q20 ? EPFEM_EPB_Q20 : (D2C ? EPFEM_EPB_2D : Base::EPB));
-  static constexpr int THREADS = (Q1 || D2C) ? ((EPB * NQ + 31) / 32) * 32 : (Q20 ? EPFEM_THREADS_Q20 : Base::THREADS);
-  static constexpr int MINB = Q20 ? EPFEM_MINB_Q20 : (D2C ? EPFEM_MINB_2D : Base::MINB);
+  static constexpr bool Q1 = DIM == 3 && NP == 8 && EPFEM_EPB_Q1 > 0;
+  static constexpr bool Q20 = DIM == 3 && NP == 20 && EPFEM_EPB_Q20 > 0;
+  static constexpr int EPB = Q1 ? EPFEM_EPB_Q1 : (Q20 ? EPFEM_EPB_Q20 : Base::EPB);
+  static constexpr int THREADS = Q1 ? ((EPB * NQ + 31) / 32) * 32 : (Q20 ? EPFEM_THREADS_Q20 : Base::THREADS);
+  static constexpr int MINB = Q20 ? EPFEM_MINB_Q20 : Base::MINB;
   static constexpr bool ROUNDS = THREADS < EPB * Base::NT;  // chunk phase 2 needs more than one pass
 };
 
 __device__ __forceinline__ double iota(int i) { return i < 3 ? 1.0 : 0.0; }
 __device__ __forceinline__ double vol(int i, int j) { return iota(i) * iota(j); }
-// DEV = diag(1,1,1,1/2,1/2,1/2) - VOL/3 (voigt.hpp:62-69)
+// DEV = diag(1,1,1,1/2,1/2,1/2) - VOL/3 (voigt.hpp:24-31)
 __device__ __forceinline__ double devop(int i, int j) {
   return ((i == j) ? (i < 3 ? 1.0 : 0.5) : 0.0) - vol(i, j) / 3.0;
 }
-// C = K VOL + 2G DEV (voigt.hpp:72-74)
+// C = K VOL + 2G DEV (voigt.hpp:33-36)
 __device__ __forceinline__ double cel(double K, double G, int i, int j) {
   return K * vol(i, j) + 2.0 * G * devop(i, j);
 }
 
-// Streamed per-point inputs.  EPFEM_LOAD_NA=1 skips L1 allocation
-// (ld.global.nc.L1::no_allocate) to keep the reference tables L1-resident:
-// measured slower (cfg2 fused 0.237 vs 0.215 ms): a lane's three 16-byte
-// loads share lines that the first one brought into L1.
-#ifndef EPFEM_LOAD_NA
-#define EPFEM_LOAD_NA 0
-#endif
-__device__ __forceinline__ double2 ld_stream2(const double2* p) {
-#if EPFEM_LOAD_NA
-  double2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
-  return r;
-#else
-  return __ldg(p);
-#endif
-}
+// Streamed per-point inputs: three 16-byte read-only loads per 48-byte record
+// (a lane's three loads share the lines the first one brings into L1; an
+// L1::no_allocate variant measured slower, cfg2 fused 0.237 vs 0.215 ms).
+__device__ __forceinline__ double2 ld_stream2(const double2* p) { return __ldg(p); }
 __device__ __forceinline__ void load6(const double* p, int64_t q, double* v) {
   const double2* p2 = reinterpret_cast<const double2*>(p + 6 * q);
   const double2 a = ld_stream2(p2), b = ld_stream2(p2 + 1), c = ld_stream2(p2 + 2);
@@ -133,7 +96,6 @@ __device__ __forceinline__ void store6(double* p, int64_t q, const double* v) {
   p2[1] = make_double2(v[2], v[3]);
   p2[2] = make_double2(v[4], v[5]);
 }
-
 // Tangent block producer: f(i, j) gives D(i, j).  Writes the packed block
 // (plastic points) and/or the reference 36-entry block.
 template <class F>
@@ -219,21 +181,6 @@ __device__ __forceinline__ void strain_point(const GatherArgs& g, int64_t e, int
     o[2] = make_double2(e6[4], e6[5]);
   }
 }
-
-struct SmemIn {
-  const double* E;
-  const double* Ep;
-  const double* H;
-  int li;  // point index inside the tile
-  __device__ __forceinline__ static void ld(const double* p, int li, double* v) {
-    const double2* p2 = reinterpret_cast<const double2*>(p + 6 * li);
-    const double2 a = p2[0], b = p2[1], c = p2[2];
-    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y;
-  }
-  __device__ __forceinline__ void e(int64_t, double* v) const { ld(E, li, v); }
-  __device__ __forceinline__ void ep(int64_t, double* v) const { ld(Ep, li, v); }
-  __device__ __forceinline__ void hard(int64_t, double* v) const { ld(H, li, v); }
-};
 
 // The return map at point q (constitutive.cpp:76-196).  `sink(f)` is called
 // at plastic points with the tangent functor f(i, j) = D(i, j).  Returns the
@@ -453,25 +400,6 @@ __global__ void __launch_bounds__(256) k_constitutive(ConstArgs a) {
     eval_point<MODEL>(a, q, GlobalIn{a.E, a.Ep, a.Hard}, none);
 }
 
-// L2 prefetch of the per-point inputs of the elements [e_lo, e_hi) (E, Ep,
-// Hard, J^-1, w: all contiguous per element range), issued one occupancy
-// wave ahead by the fused kernels: the global-load latency of a CTA's first
-// phase (the top stall of the 2D kernel) becomes an L2 hit.
-template <int DIM, int NQ>
-__device__ __forceinline__ void prefetch_elements(const ConstArgs& c, const GatherArgs& g, int64_t e_lo,
-                                                  int64_t e_hi) {
-  e_lo = max(e_lo, g.e_begin);
-  e_hi = min(e_hi, g.e_end);
-  if (e_hi <= e_lo) return;
-  const int64_t m0 = e_lo * NQ, n = (e_hi - e_lo) * NQ;
-  const int k = threadIdx.x;
-  if (k == 0) l2_prefetch_bulk(c.E + 6 * m0, sizeof(double) * 6 * n);
-  if (k == 1) l2_prefetch_bulk(c.Ep ? c.Ep + 6 * m0 : nullptr, sizeof(double) * 6 * n);
-  if (k == 2) l2_prefetch_bulk(c.Hard ? c.Hard + 6 * m0 : nullptr, sizeof(double) * 6 * n);
-  if (k == 3) l2_prefetch_bulk(g.inv + DIM * DIM * m0, sizeof(double) * DIM * DIM * n);
-  if (k == 4) l2_prefetch_bulk(g.weight + m0, sizeof(double) * n);
-}
-
 // minBlocks: 1024 threads/SM in 2D (caps at 64 registers, measured faster); 0 in 3D
 // leaves ptxas its own heuristic (126 registers; an explicit 1 gives 144 and
 // is ~15% slower on cfg4).
@@ -481,10 +409,6 @@ __global__ void __launch_bounds__(FusedCfg<DIM, NP, NQ>::THREADS, FusedCfg<DIM, 
   pdl_trigger();
   using Cfg = FusedCfg<DIM, NP, NQ>;
   constexpr int EPB = Cfg::EPB;
-  if (!FROM_U && g.pf_dist > 0) {
-    const int64_t eb = g.e_begin + ((int64_t)blockIdx.x + g.pf_dist) * EPB;
-    prefetch_elements<DIM, NQ>(c, g, eb, eb + EPB);
-  }
   __shared__ double s_st[EPB][NQ][Cfg::REC];
   __shared__ unsigned s_mask[EPB];
   c.DS = nullptr;  // hot path: S, flags, packed D only
@@ -521,14 +445,6 @@ __global__ void __launch_bounds__(FusedCfg<DIM, NP, NQ>::THREADS, FusedCfg<DIM, 
   }
   __syncthreads();
   if (tid < EPB && e0 + tid < g.e_end) g.emask[e0 + tid] = s_mask[tid];
-#if EPFEM_TSHARED
-  if constexpr (DIM == 3) {
-    __shared__ double s_T[EPB][NP][DIM * Cfg::NS];
-    delta_phase2_tshared<DIM, NP, NQ>(s_st, s_mask, s_T, tid, blockDim.x, e0, g.e_end, g.scratch);
-    return;
-  }
-#endif
-#if EPFEM_CTA_PAIRS
   // 3D (not Q2-20): phase 2 by balanced row pairs (delta_pairs3): every T
   // entry and block entry computed once (cfg4: 1,404 instead of 2,592 FMA per
   // plastic point)
@@ -543,23 +459,6 @@ __global__ void __launch_bounds__(FusedCfg<DIM, NP, NQ>::THREADS, FusedCfg<DIM, 
     }
     return;
   }
-#endif
-#if EPFEM_HALFPAIRS20
-  // Q2-20: row pairs split in halves (delta_pairs3_half): lane (element,
-  // pair, half, component)
-  if constexpr (DIM == 3 && NP >= 20) {
-    constexpr int PL = 6 * ((NP + 1) / 2);
-    for (int t = tid; t < EPB * PL; t += blockDim.x) {
-      const int le = t / PL, k = t - (t / PL) * PL;
-      const int64_t e = e0 + le;
-      const unsigned mask = s_mask[le];
-      if (e < g.e_end && mask)
-        delta_pairs3_half<NP, NQ>(&s_st[le][0][0], mask, k / 6, k % 3, (k / 3) % 2,
-                                  g.scratch + (size_t)e * Cfg::NB * Cfg::D2);
-    }
-    return;
-  }
-#endif
   // phase 2: uniform chunks (no divergent block branch) in sub-passes of SUB
   if constexpr (Cfg::ROUNDS) {
     for (int t = tid; t < EPB * Cfg::NT; t += blockDim.x) {
@@ -595,30 +494,16 @@ __global__ void __launch_bounds__(FusedCfg<DIM, NP, NQ>::THREADS, FusedCfg<DIM, 
 #ifndef EPFEM_WARP_MINB
 #define EPFEM_WARP_MINB 5
 #endif
-#ifndef EPFEM_EXP
-#define EPFEM_EXP 0  // timing experiments only: 1 = no phase 2, 2 = phase 2 without FP64 work
-#endif
-#ifndef EPFEM_EARLY_GEOM
-#define EPFEM_EARLY_GEOM 1
-#endif
 // One warp's group of EPW elements starting at e0: st_w = the warp's staged
 // records (EPW * NQ * REC doubles), out_w = its element-record buffer
-// (EPW * RECB doubles, 16-byte aligned).  MEGA: the records leave through
-// plain coalesced stores (the one-launch step publishes them with a release
-// flag right after; no async-proxy writes to order).
-// FORCES (internal forces fused, epfem_newton_step_f): every point also
-// stages dphi and (w, S11, S22, S12) after its record (stride REC + 4), and
-// lane (element, node p) forms the element's internal-force record
-// F_e[p] = sum_q w_q B_p(q)^T S_q (the explicit-rounding sequence of
-// k_internal_forces) into g.fws; the row stream folds the records per node.
-template <int MODEL, int NP, int NQ, bool FROM_U, bool MEGA, bool FORCES = false>
+// (EPW * RECB doubles, 16-byte aligned).
+template <int MODEL, int NP, int NQ, bool FROM_U>
 __device__ __forceinline__ void newton_warp_group(ConstArgs c, const GatherArgs& g, int64_t e0, double* st_w,
                                                   double* out_w, int lane) {
   constexpr int DIM = 2;
   using W = WarpCfg<DIM, NP, NQ>;
   static_assert(W::EPW * NQ <= 32 && W::EPW * W::NT <= 32, "warp mapping");
-  static_assert(!(FORCES && FROM_U), "the forces step reads E");
-  constexpr int EPW = W::EPW, REC0 = W::REC, REC = REC0 + (FORCES ? 4 : 0);
+  constexpr int EPW = W::EPW, REC = W::REC;
   constexpr unsigned QMASK = NQ >= 32 ? 0xffffffffu : (1u << NQ) - 1u;
   constexpr int RECB = W::NB * W::D2;  // doubles per element workspace record
   c.DS = nullptr;  // hot path: S, flags, packed D only
@@ -669,49 +554,30 @@ __device__ __forceinline__ void newton_warp_group(ConstArgs c, const GatherArgs&
         auto stage = [&](auto&& f) { stage_dw<DIM>(st + NP * DIM, wq, g, m, f); };
         plastic = eval_point<MODEL>(c, m, RegEIn{e6, c.Ep, c.Hard}, stage);
       } else {
-#if EPFEM_EARLY_GEOM
-      // J^-1 and w are loaded with E / Ep / Hard, before the return map, so
-      // plastic points do not pay a second dependent memory round trip
-      double jinv[W::D2];
-      {
-        const double2* p2 = reinterpret_cast<const double2*>(g.inv + m * W::D2);
+        // J^-1 and w are loaded with E / Ep / Hard, before the return map, so
+        // plastic points do not pay a second dependent memory round trip
+        double jinv[W::D2];
+        {
+          const double2* p2 = reinterpret_cast<const double2*>(g.inv + m * W::D2);
 #pragma unroll
-        for (int k = 0; k < W::D2 / 2; ++k) {
-          const double2 v = ld_stream2(p2 + k);
-          jinv[2 * k] = v.x;
-          jinv[2 * k + 1] = v.y;
+          for (int k = 0; k < W::D2 / 2; ++k) {
+            const double2 v = ld_stream2(p2 + k);
+            jinv[2 * k] = v.x;
+            jinv[2 * k + 1] = v.y;
+          }
         }
-      }
-      const double wq = __ldg(g.weight + m);
-      if constexpr (FORCES) stage_geometry<DIM, NP, true>(st, jinv, g.gradhat, q);
-      auto stage = [&](auto&& f) {
-        if constexpr (!FORCES) stage_geometry<DIM, NP, true>(st, jinv, g.gradhat, q);
-        stage_dw<DIM>(st + NP * DIM, wq, g, m, f);
-      };
-#else
-      auto stage = [&](auto&& f) {
-        stage_geometry<DIM, NP>(st, g.inv + m * W::D2, g.gradhat, q);
-        stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f);
-      };
-#endif
-      if constexpr (FORCES) {
-        auto ss = [&](const double* s6) {
-          st[REC0] = wq;
-          st[REC0 + 1] = s6[0];
-          st[REC0 + 2] = s6[1];
-          st[REC0 + 3] = s6[3];
+        const double wq = __ldg(g.weight + m);
+        auto stage = [&](auto&& f) {
+          stage_geometry<DIM, NP, true>(st, jinv, g.gradhat, q);
+          stage_dw<DIM>(st + NP * DIM, wq, g, m, f);
         };
-        plastic = eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage, ss);
-      } else {
         plastic = eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
-      }
       }
     }
   }
   const unsigned bal = __ballot_sync(0xffffffffu, plastic);
   __syncwarp();
   if (lane < EPW && e0 + lane < g.e_end) g.emask[e0 + lane] = (bal >> (lane * NQ)) & QMASK;
-#if EPFEM_WARP_PAIRS
   // phase 2 by row pairs: lane (element, pair, component), 2 ceil(NP/2) lanes per element
   constexpr int PL2 = 2 * ((NP + 1) / 2);
   for (int t = lane; t < EPW * PL2; t += 32) {  // one round except for P1 (EPW = 10)
@@ -720,188 +586,31 @@ __device__ __forceinline__ void newton_warp_group(ConstArgs c, const GatherArgs&
     if (e0 + le < g.e_end && mask)
       delta_pairs2<NP>(st_w + le * NQ * REC, mask, k / 2, k % 2, REC, out_w + le * RECB);
   }
-  if (false) {
-#else
-  if (EPFEM_EXP != 1 && lane < EPW * W::NT) {
-#endif
-    const int le = lane / W::NT;
-    const int64_t e = e0 + le;
-    const unsigned mask = (bal >> (le * NQ)) & QMASK;
-    if (e < g.e_end && mask) {
-      int a, c0;
-      chunk_of<NP, W::CS>(lane - le * W::NT, a, c0);
-      double* rec = out_w + le * RECB;  // staged, then one bulk store per element
-      if (EPFEM_EXP == 2) {  // same stores, staged values instead of the products
-        const double* st = st_w + le * NQ * REC;
-        for (int bb = 0; bb < W::CS && c0 + bb < NP; ++bb)
-          for (int k = 0; k < W::D2; ++k) rec[blk_index<NP>(a, c0 + bb) * W::D2 + k] = st[bb * 4 + k];
-      } else {
-        delta_chunk_uniform<DIM, NP, W::CS, REC>(st_w + le * NQ * REC, mask, a, c0, rec);
-      }
-    }
-  }
-  if constexpr (FORCES) {
-    // element internal-force records: lane (element, node p), points in order
-    for (int t = lane; t < EPW * NP; t += 32) {
-      const int le = t / NP, p = t - (t / NP) * NP;
-      if (e0 + le >= g.e_end) continue;
-      double f0 = 0.0, f1 = 0.0;
-#pragma unroll 1
-      for (int q = 0; q < NQ; ++q) {
-        const double* r = st_w + (le * NQ + q) * REC;
-        const double g0 = r[p * 2], g1 = r[p * 2 + 1];
-        const double w = r[REC0], s0 = r[REC0 + 1], s1 = r[REC0 + 2], s3 = r[REC0 + 3];
-        f0 = __fma_rn(w, __fma_rn(g1, s3, __dmul_rn(g0, s0)), f0);
-        f1 = __fma_rn(w, __fma_rn(g0, s3, __dmul_rn(g1, s1)), f1);
-      }
-      double2* o = reinterpret_cast<double2*>(g.fws + ((e0 + le) * NP + p) * DIM);
-      *o = make_double2(f0, f1);
-    }
-  }
   // the workspace records leave through the TMA unit: whole 1-KB-class
   // records instead of 8-byte scattered stores from every lane
-  if (MEGA) {
-    __syncwarp();
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    int n = 0;
     for (int le = 0; le < EPW; ++le)
       if (e0 + le < g.e_end && ((bal >> (le * NQ)) & QMASK)) {
-        const double2* s2 = reinterpret_cast<const double2*>(out_w + le * RECB);
-        double2* d2 = reinterpret_cast<double2*>(g.scratch + (size_t)(e0 + le) * RECB);
-        for (int k = lane; k < RECB / 2; k += 32) d2[k] = s2[k];
+        tma_store_1d(g.scratch + (size_t)(e0 + le) * RECB, out_w + le * RECB, (unsigned)(RECB * sizeof(double)));
+        ++n;
       }
-  } else if (EPFEM_EXP != 1) {
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      int n = 0;
-      for (int le = 0; le < EPW; ++le)
-        if (e0 + le < g.e_end && ((bal >> (le * NQ)) & QMASK)) {
-          tma_store_1d(g.scratch + (size_t)(e0 + le) * RECB, out_w + le * RECB,
-                       (unsigned)(RECB * sizeof(double)));
-          ++n;
-        }
-      if (n) tma_store_wait_read();
-    }
+    if (n) tma_store_wait_read();
   }
 }
 
-template <int MODEL, int NP, int NQ, bool FROM_U = false, bool FORCES = false>
+template <int MODEL, int NP, int NQ, bool FROM_U = false>
 __global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
     k_newton_warp(ConstArgs c, GatherArgs g) {
   pdl_trigger();
   using W = WarpCfg<2, NP, NQ>;
-  __shared__ double s_st[W::WPB][W::EPW * NQ * (W::REC + (FORCES ? 4 : 0))];
+  __shared__ double s_st[W::WPB][W::EPW * NQ * W::REC];
   __shared__ __align__(16) double s_out[W::WPB][W::EPW * W::NB * W::D2];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (!FROM_U && g.pf_dist > 0) {
-    const int64_t eb = g.e_begin + ((int64_t)blockIdx.x + g.pf_dist) * W::WPB * W::EPW;
-    prefetch_elements<2, NQ>(c, g, eb, eb + W::WPB * W::EPW);
-  }
   const int64_t e0 = g.e_begin + ((int64_t)blockIdx.x * W::WPB + w) * W::EPW;
-  newton_warp_group<MODEL, NP, NQ, FROM_U, false, FORCES>(c, g, e0, s_st[w], s_out[w], lane);
-}
-
-// k_newton_warp_pf (2D, EPFEM_FUSED=pf): k_newton_warp with two element
-// groups per warp; at entry lane 0 starts TMA bulk copies of the SECOND
-// group's E / Ep / Hard / J^-1 (contiguous: the group's points are) into
-// shared memory, so their latency hides behind the whole first group.
-constexpr int PFW = 3;  // warps per CTA (static shared memory < 48 KB)
-template <int MODEL, int NP, int NQ>
-__global__ void __launch_bounds__(32 * PFW, EPFEM_WARP_MINB * 4 / 3)
-    k_newton_warp_pf(ConstArgs c, GatherArgs g) {
-  pdl_trigger();
-  constexpr int DIM = 2;
-  using W = WarpCfg<DIM, NP, NQ>;
-  constexpr int EPW = W::EPW, REC = W::REC, PPG = EPW * NQ, D2 = W::D2;
-  constexpr unsigned QMASK = NQ >= 32 ? 0xffffffffu : (1u << NQ) - 1u;
-  constexpr int RECB = W::NB * W::D2;
-  constexpr int IN_E = 0, IN_EP = 6 * PPG, IN_H = 12 * PPG, IN_J = 18 * PPG, IN_SIZE = IN_J + D2 * PPG;
-  __shared__ double s_st[PFW][EPW * NQ * REC];
-  __shared__ __align__(16) double s_out[PFW][EPW * RECB];
-  __shared__ __align__(128) double s_in[PFW][IN_SIZE];
-  __shared__ uint64_t s_bar[PFW];
-  c.DS = nullptr;  // hot path: S, flags, packed D only
-  c.Ep_out = c.Hard_out = nullptr;
-  c.pm = c.sm = c.am = nullptr;
-  c.crit = nullptr;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t n_groups = (g.e_end - g.e_begin + EPW - 1) / EPW;
-  const int64_t grp0 = 2 * ((int64_t)blockIdx.x * PFW + w);
-  if (grp0 >= n_groups) return;  // warp-uniform
-  const bool has2 = grp0 + 1 < n_groups;
-  double* st_w = s_st[w];
-  double* in_w = s_in[w];
-  if (lane == 0) {
-    mbar_init(&s_bar[w], 1);
-    mbar_init_fence();
-  }
-  __syncwarp();
-  if (has2 && lane == 0) {
-    const int64_t p0 = (g.e_begin + (grp0 + 1) * EPW) * NQ;
-    const unsigned np = (unsigned)min((int64_t)PPG, g.e_end * NQ - p0);
-    unsigned total = np * 48u + np * 8u * D2;
-    if (c.Ep) total += np * 48u;
-    if (c.Hard) total += np * 48u;
-    mbar_expect_tx(&s_bar[w], total);
-    tma_load_1d(in_w + IN_E, c.E + 6 * p0, np * 48u, &s_bar[w]);
-    if (c.Ep) tma_load_1d(in_w + IN_EP, c.Ep + 6 * p0, np * 48u, &s_bar[w]);
-    if (c.Hard) tma_load_1d(in_w + IN_H, c.Hard + 6 * p0, np * 48u, &s_bar[w]);
-    tma_load_1d(in_w + IN_J, g.inv + D2 * p0, np * 8u * D2, &s_bar[w]);
-  }
-  auto group = [&](int64_t grp, auto from_smem) {
-    constexpr bool SM = decltype(from_smem)::value;
-    const int64_t e0 = g.e_begin + grp * EPW;
-    bool plastic = false;
-    if (lane < PPG) {
-      const int le = lane / NQ, q = lane - le * NQ;
-      const int64_t e = e0 + le;
-      if (e < g.e_end) {
-        const int64_t m = e * NQ + q;
-        double* st = st_w + lane * REC;
-        double jinv[D2];
-#pragma unroll
-        for (int k = 0; k < D2; ++k) jinv[k] = SM ? in_w[IN_J + lane * D2 + k] : __ldg(g.inv + m * D2 + k);
-        const double wq = __ldg(g.weight + m);
-        auto stage = [&](auto&& f) {
-          stage_geometry<DIM, NP, true>(st, jinv, g.gradhat, q);
-          stage_dw<DIM>(st + NP * DIM, wq, g, m, f);
-        };
-        if constexpr (SM)
-          plastic = eval_point<MODEL>(c, m, SmemIn{in_w + IN_E, in_w + IN_EP, in_w + IN_H, lane}, stage);
-        else
-          plastic = eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
-      }
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, plastic);
-    __syncwarp();
-    if (lane < EPW && e0 + lane < g.e_end) g.emask[e0 + lane] = (bal >> (lane * NQ)) & QMASK;
-    if (lane < EPW * W::NT) {
-      const int le = lane / W::NT;
-      const unsigned mask = (bal >> (le * NQ)) & QMASK;
-      if (e0 + le < g.e_end && mask) {
-        int a, c0;
-        chunk_of<NP, W::CS>(lane - le * W::NT, a, c0);
-        delta_chunk_uniform<DIM, NP, W::CS, REC>(st_w + le * NQ * REC, mask, a, c0, s_out[w] + le * RECB);
-      }
-    }
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      int n = 0;
-      for (int le = 0; le < EPW; ++le)
-        if (e0 + le < g.e_end && ((bal >> (le * NQ)) & QMASK)) {
-          tma_store_1d(g.scratch + (size_t)(e0 + le) * RECB, s_out[w] + le * RECB,
-                       (unsigned)(RECB * sizeof(double)));
-          ++n;
-        }
-      if (n) tma_store_wait_read();
-    }
-    __syncwarp();  // staged records and output buffers are reused by the next group
-  };
-  group(grp0, std::false_type{});
-  if (has2) {
-    mbar_wait(&s_bar[w], 0);
-    group(grp0 + 1, std::true_type{});
-  }
+  newton_warp_group<MODEL, NP, NQ, FROM_U>(c, g, e0, s_st[w], s_out[w], lane);
 }
 
 // k_newton_warp3 (3D): warp-owned elements (EPW = 32 / NQ, all lanes busy in
@@ -924,10 +633,6 @@ __global__ void __launch_bounds__(Pair3Cfg<NP, NQ>::THREADS, EPFEM_WARP3_MINB)
   c.pm = c.sm = c.am = nullptr;
   c.crit = nullptr;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (!FROM_U && g.pf_dist > 0) {
-    const int64_t eb = g.e_begin + ((int64_t)blockIdx.x + g.pf_dist) * W::WPB * EPW;
-    prefetch_elements<DIM, NQ>(c, g, eb, eb + W::WPB * EPW);
-  }
   const int64_t e0 = g.e_begin + ((int64_t)blockIdx.x * W::WPB + w) * EPW;
   if (e0 >= g.e_end) return;  // warp-uniform
   double* st_w = s_st[w];
@@ -967,183 +672,6 @@ __global__ void __launch_bounds__(Pair3Cfg<NP, NQ>::THREADS, EPFEM_WARP3_MINB)
       }
     }
   }
-}
-
-// k_newton_ws (2D): the warp kernel split by role inside a persistent CTA.
-// P producer warps run phase 1 (one group of EPW elements at a time, like
-// k_newton_warp) into a private double-buffered slot of staged records and
-// hand it over through an mbarrier; CW consumer warps run phase 2 from the
-// slots and bulk-store the element records.  The producers never wait on
-// phase-2 arithmetic, so their loads keep streaming while the consumers'
-// FP64 work proceeds on the other warps.
-#ifndef EPFEM_WS_P
-#define EPFEM_WS_P 6
-#endif
-#ifndef EPFEM_WS_C
-#define EPFEM_WS_C 2
-#endif
-#ifndef EPFEM_WS_MINB
-#define EPFEM_WS_MINB 3
-#endif
-#ifndef EPFEM_WS_SUB
-#define EPFEM_WS_SUB 3
-#endif
-template <int NP, int NQ>
-struct WsCfg {
-  using W = WarpCfg<2, NP, NQ>;
-  static constexpr int P = EPFEM_WS_P, CW = EPFEM_WS_C, THREADS = 32 * (P + CW);
-  static constexpr int SLOT = W::EPW * NQ * W::REC;  // doubles per staged slot
-  static constexpr int RECB = W::NB * W::D2;
-  static constexpr size_t SMEM = sizeof(double) * ((size_t)P * 2 * SLOT + (size_t)CW * W::EPW * RECB);
-};
-template <int MODEL, int NP, int NQ>
-__global__ void __launch_bounds__(WsCfg<NP, NQ>::THREADS, EPFEM_WS_MINB)
-    k_newton_ws(ConstArgs c, GatherArgs g) {
-  pdl_trigger();
-  constexpr int DIM = 2;
-  using W = WarpCfg<DIM, NP, NQ>;
-  using S = WsCfg<NP, NQ>;
-  constexpr int P = S::P, CW = S::CW, EPW = W::EPW, REC = W::REC, SLOT = S::SLOT, RECB = S::RECB;
-  constexpr unsigned QMASK = NQ >= 32 ? 0xffffffffu : (1u << NQ) - 1u;
-  extern __shared__ __align__(128) double ws_smem[];
-  double* slots = ws_smem;                 // [P][2][SLOT]
-  double* outb = ws_smem + P * 2 * SLOT;   // [CW][EPW * RECB]
-  __shared__ uint64_t full[P][2], empty[P][2];
-  __shared__ unsigned s_bal[P][2];
-  __shared__ long long s_e0[P][2];
-  c.DS = nullptr;  // hot path: S, flags, packed D only
-  c.Ep_out = c.Hard_out = nullptr;
-  c.pm = c.sm = c.am = nullptr;
-  c.crit = nullptr;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    for (int p = 0; p < P; ++p)
-      for (int b = 0; b < 2; ++b) {
-        mbar_init(&full[p][b], 1);
-        mbar_init(&empty[p][b], 1);
-      }
-    mbar_init_fence();
-  }
-  __syncthreads();
-  const int64_t n_groups = (g.e_end - g.e_begin + EPW - 1) / EPW;
-  if (w < P) {
-    // ---- producer: phase 1
-    const int64_t stride = (int64_t)gridDim.x * P;
-    int it = 0;
-    for (int64_t grp = (int64_t)blockIdx.x * P + w;; grp += stride, ++it) {
-      const int b = it & 1;
-      if (it >= 2) mbar_wait(&empty[w][b], ((it >> 1) & 1) ^ 1);
-      if (grp >= n_groups) {
-        if (lane == 0) {
-          s_e0[w][b] = -1;
-          mbar_arrive(&full[w][b]);
-        }
-        break;
-      }
-      double* st_w = slots + (w * 2 + b) * SLOT;
-      const int64_t e0 = g.e_begin + grp * EPW;
-      bool plastic = false;
-      if (lane < EPW * NQ) {
-        const int le = lane / NQ, q = lane - le * NQ;
-        const int64_t e = e0 + le;
-        if (e < g.e_end) {
-          const int64_t m = e * NQ + q;
-          double* st = st_w + lane * REC;
-          auto stage = [&](auto&& f) {
-            stage_geometry<DIM, NP>(st, g.inv + m * W::D2, g.gradhat, q);
-            stage_dw<DIM>(st + NP * DIM, __ldg(g.weight + m), g, m, f);
-          };
-          plastic = eval_point<MODEL>(c, m, GlobalIn{c.E, c.Ep, c.Hard}, stage);
-        }
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, plastic);
-      if (lane < EPW && e0 + lane < g.e_end) g.emask[e0 + lane] = (bal >> (lane * NQ)) & QMASK;
-      if (lane == 0) {
-        s_bal[w][b] = bal;
-        s_e0[w][b] = e0;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&full[w][b]);
-    }
-  } else {
-    // ---- consumer: phase 2 for producers cw, cw + CW, ...
-    const int cw = w - P;
-    double* out_w = outb + cw * EPW * RECB;
-    constexpr int NMY = (P + CW - 1) / CW;
-    int its[NMY];
-    unsigned done = 0;
-    const int nmy = (P - cw + CW - 1) / CW;
-#pragma unroll
-    for (int k = 0; k < NMY; ++k) its[k] = 0;
-    bool pending = false;  // bulk stores in flight from out_w
-    while (done != (1u << nmy) - 1u) {
-#pragma unroll
-      for (int k = 0; k < NMY; ++k) {
-        if (k >= nmy || ((done >> k) & 1u)) continue;
-        const int p = cw + k * CW, b = its[k] & 1;
-        mbar_wait(&full[p][b], (its[k] >> 1) & 1);
-        const long long e0 = s_e0[p][b];
-        if (e0 < 0) {
-          done |= 1u << k;
-          continue;
-        }
-        const unsigned bal = s_bal[p][b];
-        if (pending) {  // out_w must have been read by the previous bulk stores
-          if (lane == 0) tma_store_wait_read_only();
-          __syncwarp();
-          pending = false;
-        }
-        const double* st_w = slots + (p * 2 + b) * SLOT;
-        if (lane < EPW * W::NT) {
-          const int le = lane / W::NT;
-          const unsigned mask = (bal >> (le * NQ)) & QMASK;
-          if (e0 + le < g.e_end && mask) {
-            int a, c0;
-            chunk_of<NP, W::CS>(lane - le * W::NT, a, c0);
-            delta_chunk_uniform<DIM, NP, W::CS, REC, EPFEM_WS_SUB>(st_w + le * NQ * REC, mask, a, c0,
-                                                                     out_w + le * RECB);
-          }
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&empty[p][b]);  // staged records consumed
-          for (int le = 0; le < EPW; ++le)
-            if (e0 + le < g.e_end && ((bal >> (le * NQ)) & QMASK)) {
-              tma_store_1d(g.scratch + (size_t)(e0 + le) * RECB, out_w + le * RECB,
-                           (unsigned)(RECB * sizeof(double)));
-              pending = true;
-            }
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        pending = __shfl_sync(0xffffffffu, pending, 0);
-        ++its[k];
-      }
-    }
-    if (lane == 0) tma_store_wait_read_only();
-  }
-}
-
-template <int MODEL, int NP, int NQ>
-static int launch_ws(const ConstArgs& c, const GatherArgs& g, cudaStream_t st) {
-  using S = WsCfg<NP, NQ>;
-  auto kern = k_newton_ws<MODEL, NP, NQ>;
-  static int per_sm = -1, num_sms = 0;
-  if (per_sm < 0) {
-    EPFEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
-    EPFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, S::THREADS, S::SMEM));
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (per_sm < 1) per_sm = 1;
-  }
-  using W = WarpCfg<2, NP, NQ>;
-  const int64_t n_groups = (g.e_end - g.e_begin + W::EPW - 1) / W::EPW;
-  const int64_t need = (n_groups + S::P - 1) / S::P;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)per_sm * num_sms));
-  kern<<<(unsigned)grid, S::THREADS, S::SMEM, st>>>(c, g);
-  EPFEM_CUDA_TRY(cudaGetLastError());
-  return 0;
 }
 
 // k_newton_mma: k_newton_warp's phase 1 (EPW = 32 / NQ elements per warp)
@@ -1189,105 +717,55 @@ __global__ void __launch_bounds__(MmaCfg<DIM, NP, NQ>::THREADS, DIM == 2 ? EPFEM
   delta_mma_warp<DIM, NP, NQ>(st_w, s_out[w], bal, e0, g.e_end, g.scratch, lane);
 }
 
-// Per-buffer shared-memory tile of the pipelined kernel (doubles): the
-// group's E, Ep, Hard (6 per point), J^-1 (dim^2 per point, one extra point
-// for the 16-byte alignment shift) and w (two extra).
-template <int DIM, int NP, int NQ>
-struct PipeTile {
-  static constexpr int PPG = DeltaCfg<DIM, NP, NQ>::EPB * NQ;  // points per group
-  static constexpr int D2 = DIM * DIM;
-  static constexpr int r2(int n) { return (n + 1) & ~1; }
-  static constexpr int OE = 0, OEP = OE + 6 * PPG, OH = OEP + 6 * PPG, OI = OH + 6 * PPG;
-  static constexpr int OW = OI + r2((PPG + 1) * D2);
-  static constexpr int SIZE = OW + r2(PPG + 2);
-  static constexpr size_t BYTES = 2 * SIZE * sizeof(double);
-};
-
-// k_newton_pipe: the fused kernel made persistent and software-pipelined.
-// Each CTA walks groups of EPB elements (grid-stride); one elected thread
-// issues TMA bulk copies of the NEXT group's E / Ep / Hard / J^-1 / w into
-// the other half of a double-buffered tile (mbarrier completion) while the
-// CTA computes the current group from shared memory, so the point update
-// never waits on a global load.  Outputs and arithmetic are identical to
-// k_newton_fused.
-template <int MODEL, int DIM, int NP, int NQ>
-__global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS)
-    k_newton_pipe(ConstArgs c, GatherArgs g, int64_t n_groups) {
-  pdl_trigger();
-  using Cfg = DeltaCfg<DIM, NP, NQ>;
-  using Tile = PipeTile<DIM, NP, NQ>;
-  constexpr int EPB = Cfg::EPB, PPG = Tile::PPG, D2 = Tile::D2;
-  extern __shared__ __align__(128) double tiles[];
-  __shared__ double s_st[EPB][NQ][Cfg::REC];
-  __shared__ unsigned s_mask[EPB];
-  __shared__ uint64_t s_bar[2];
-  c.DS = nullptr;  // hot path: S, flags, packed D only
-  c.Ep_out = c.Hard_out = nullptr;
-  c.pm = c.sm = c.am = nullptr;
-  c.crit = nullptr;
-  const int tid = threadIdx.x;
-  const int64_t n_int = g.e_end * NQ;
-  const int64_t pbase = g.e_begin * NQ;
-
-  if (tid == 0) {
-    mbar_init(&s_bar[0], 1);
-    mbar_init(&s_bar[1], 1);
-    mbar_init_fence();
+// One fused launch over [g.e_begin, g.e_end): the kernel per element shape
+// (2D: k_newton_warp; tetrahedra: k_newton_warp3; hexahedra: k_newton_fused;
+// MMA: k_newton_mma, the FP64 tensor-pipe phase 2), instantiated per model.
+template <class L>
+void by_model(int model, L&& launch) {
+  switch (model) {
+    case EPFEM_MODEL_VON_MISES: launch(std::integral_constant<int, EPFEM_MODEL_VON_MISES>{}); break;
+    case EPFEM_MODEL_DRUCKER_PRAGER: launch(std::integral_constant<int, EPFEM_MODEL_DRUCKER_PRAGER>{}); break;
+    default: launch(std::integral_constant<int, EPFEM_MODEL_ELASTIC>{}); break;
   }
-  __syncthreads();
-  auto issue = [&](int64_t grp, int b) {  // one thread
-    double* t = tiles + b * Tile::SIZE;
-    const int64_t p0 = pbase + grp * PPG;
-    const int np = (int)min((int64_t)PPG, n_int - p0);
-    const int sh = (int)(p0 & 1);  // J^-1 / w source shifted down to a 16-byte boundary
-    const unsigned be = (unsigned)np * 48u;
-    const unsigned bi = (unsigned)(((np + sh) * D2 * 8 + 15) & ~15);
-    const unsigned bw = (unsigned)(((np + sh) * 8 + 15) & ~15);
-    unsigned total = be + bi + bw;
-    if (c.Ep) total += be;
-    if (c.Hard) total += be;
-    mbar_expect_tx(&s_bar[b], total);
-    tma_load_1d(t + Tile::OE, c.E + 6 * p0, be, &s_bar[b]);
-    if (c.Ep) tma_load_1d(t + Tile::OEP, c.Ep + 6 * p0, be, &s_bar[b]);
-    if (c.Hard) tma_load_1d(t + Tile::OH, c.Hard + 6 * p0, be, &s_bar[b]);
-    tma_load_1d(t + Tile::OI, g.inv + (p0 - sh) * D2, bi, &s_bar[b]);
-    tma_load_1d(t + Tile::OW, g.weight + (p0 - sh), bw, &s_bar[b]);
-  };
-  int64_t grp = blockIdx.x;
-  if (tid == 0 && grp < n_groups) issue(grp, 0);
-  for (int it = 0; grp < n_groups; grp += gridDim.x, ++it) {
-    const int b = it & 1;
-    const int64_t nxt = grp + gridDim.x;
-    // buffer b^1 was released by the barrier that closed the previous iteration;
-    // order those generic-proxy reads before the async-proxy (TMA) writes
-    if (tid == 0 && nxt < n_groups) {
-      fence_proxy_async_smem();
-      issue(nxt, b ^ 1);
+}
+
+template <bool FROM_U>
+int launch_fused_impl(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g, bool mma,
+                      cudaStream_t st) {
+  if (g.e_end <= g.e_begin) return 0;
+  const int64_t n_e = g.e_end - g.e_begin;
+  auto grid = [&](int64_t per) { return (unsigned)((n_e + per - 1) / per); };
+  bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
+    constexpr int DIM = decltype(D)::value;
+    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
+    if (!FROM_U && mma) {
+      using M = MmaCfg<DIM, NP, NQ>;
+      by_model(model, [&](auto md) {
+        k_newton_mma<decltype(md)::value, DIM, NP, NQ><<<grid(M::EPW * M::WPB), M::THREADS, 0, st>>>(c, g);
+      });
+    } else if constexpr (DIM == 2) {
+      using W = WarpCfg<DIM, NP, NQ>;
+      by_model(model, [&](auto md) {
+        k_newton_warp<decltype(md)::value, NP, NQ, FROM_U><<<grid(W::EPW * W::WPB), W::THREADS, 0, st>>>(c, g);
+      });
+    } else if constexpr (NP != 8 && NP != 20) {
+      // tetrahedra: warp-owned elements (measured on cfg3: 3.61 vs 4.08 ms
+      // for the CTA kernel; for Q1 hexahedra the CTA kernel is faster, 4.17
+      // vs 4.73 ms)
+      using W = Pair3Cfg<NP, NQ>;
+      by_model(model, [&](auto md) {
+        k_newton_warp3<decltype(md)::value, NP, NQ, FROM_U><<<grid(W::EPW * W::WPB), W::THREADS, 0, st>>>(c, g);
+      });
+    } else {
+      using FC = FusedCfg<DIM, NP, NQ>;
+      by_model(model, [&](auto md) {
+        k_newton_fused<decltype(md)::value, DIM, NP, NQ, FROM_U><<<grid(FC::EPB), FC::THREADS, 0, st>>>(c, g);
+      });
     }
-    if (tid < EPB) s_mask[tid] = 0u;
-    mbar_wait(&s_bar[b], (unsigned)(it >> 1) & 1u);
-    __syncthreads();
-    const double* t = tiles + b * Tile::SIZE;
-    const int64_t e0 = g.e_begin + grp * EPB;
-    const int sh = (int)((pbase + grp * PPG) & 1);
-    for (int k = tid; k < PPG; k += blockDim.x) {
-      const int le = k / NQ, q = k - le * NQ;
-      const int64_t e = e0 + le;
-      if (e >= g.e_end) continue;
-      const int64_t m = e * NQ + q;
-      double* st = s_st[le][q];
-      auto stage = [&](auto&& f) {
-        atomicOr(&s_mask[le], 1u << q);
-        stage_geometry<DIM, NP, true>(st, t + Tile::OI + (k + sh) * D2, g.gradhat, q);
-        stage_dw<DIM>(st + NP * DIM, t[Tile::OW + k + sh], g, m, f);
-      };
-      eval_point<MODEL>(c, m, SmemIn{t + Tile::OE, t + Tile::OEP, t + Tile::OH, k}, stage);
-    }
-    __syncthreads();
-    if (tid < EPB && e0 + tid < g.e_end) g.emask[e0 + tid] = s_mask[tid];
-    delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, g.e_end, g.scratch);
-    __syncthreads();
-  }
+  });
+  if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
+  EPFEM_CUDA_TRY(cudaGetLastError());
+  return 0;
 }
 
 }  // namespace
@@ -1318,587 +796,22 @@ int launch_constitutive(int model, const ConstArgs& a, cudaStream_t st, int num_
   return 0;
 }
 
-template <int MODEL, int DIM, int NP, int NQ>
-static int launch_pipe(const ConstArgs& c, const GatherArgs& g, cudaStream_t st) {
-  using Cfg = DeltaCfg<DIM, NP, NQ>;
-  using Tile = PipeTile<DIM, NP, NQ>;
-  auto kern = k_newton_pipe<MODEL, DIM, NP, NQ>;
-  static int per_sm = -1, num_sms = 0;
-  if (per_sm < 0) {
-    EPFEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)Tile::BYTES));
-    EPFEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::THREADS,
-                                                                 Tile::BYTES));
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (per_sm < 1) per_sm = 1;
-  }
-  const int64_t n_groups = (g.e_end - g.e_begin + Cfg::EPB - 1) / Cfg::EPB;
-  const int64_t grid = std::min<int64_t>(n_groups, (int64_t)per_sm * num_sms);
-  kern<<<(unsigned)grid, Cfg::THREADS, Tile::BYTES, st>>>(c, g, n_groups);
-  EPFEM_CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
 int launch_newton_fused_u(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
                           cudaStream_t st) {
-  if (g.e_end <= g.e_begin) return 0;
-  bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
-    constexpr int DIM = decltype(D)::value;
-    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
-    if constexpr (DIM == 3 && NP < 20 && NP != 8) {  // tetrahedra: warp kernel (as launch_newton_fused)
-      using W = Pair3Cfg<NP, NQ>;
-      const int64_t per = (int64_t)W::EPW * W::WPB;
-      const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
-      switch (model) {
-        case EPFEM_MODEL_VON_MISES:
-          k_newton_warp3<EPFEM_MODEL_VON_MISES, NP, NQ, true><<<blocks, W::THREADS, 0, st>>>(c, g);
-          break;
-        case EPFEM_MODEL_DRUCKER_PRAGER:
-          k_newton_warp3<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ, true><<<blocks, W::THREADS, 0, st>>>(c, g);
-          break;
-        default:
-          k_newton_warp3<EPFEM_MODEL_ELASTIC, NP, NQ, true><<<blocks, W::THREADS, 0, st>>>(c, g);
-          break;
-      }
-    } else if constexpr (DIM == 3) {  // hexahedra: CTA kernel
-      using Cfg = FusedCfg<DIM, NP, NQ>;
-      const unsigned blocks = (unsigned)((g.e_end - g.e_begin + Cfg::EPB - 1) / Cfg::EPB);
-      switch (model) {
-        case EPFEM_MODEL_VON_MISES:
-          k_newton_fused<EPFEM_MODEL_VON_MISES, DIM, NP, NQ, true><<<blocks, Cfg::THREADS, 0, st>>>(c, g);
-          break;
-        case EPFEM_MODEL_DRUCKER_PRAGER:
-          k_newton_fused<EPFEM_MODEL_DRUCKER_PRAGER, DIM, NP, NQ, true><<<blocks, Cfg::THREADS, 0, st>>>(c, g);
-          break;
-        default:
-          k_newton_fused<EPFEM_MODEL_ELASTIC, DIM, NP, NQ, true><<<blocks, Cfg::THREADS, 0, st>>>(c, g);
-          break;
-      }
-    }
-    if constexpr (DIM == 2) {
-      using W = WarpCfg<DIM, NP, NQ>;
-      const int64_t per = (int64_t)W::EPW * W::WPB;
-      const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
-      switch (model) {
-        case EPFEM_MODEL_VON_MISES:
-          k_newton_warp<EPFEM_MODEL_VON_MISES, NP, NQ, true><<<blocks, W::THREADS, 0, st>>>(c, g);
-          break;
-        case EPFEM_MODEL_DRUCKER_PRAGER:
-          k_newton_warp<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ, true><<<blocks, W::THREADS, 0, st>>>(c, g);
-          break;
-        default:
-          k_newton_warp<EPFEM_MODEL_ELASTIC, NP, NQ, true><<<blocks, W::THREADS, 0, st>>>(c, g);
-          break;
-      }
-    }
-  });
-  if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
-  EPFEM_CUDA_TRY(cudaGetLastError());
-  return 0;
+  return launch_fused_impl<true>(model, family, dim, c, g, false, st);
 }
 
-// ---------------------------------------------------------------------------
-// k_newton_mega (2D): the whole Newton step in ONE launch.  Every warp of a
-// cooperative (all CTAs co-resident) persistent grid is an independent
-// worker walking an ordered item list round-robin (worker w takes items w,
-// w + W, w + 2W, ...): producer items are k_newton_warp's element groups
-// (fused update + element deltas), consumer items are node ranges of the
-// row stream (rows.cuh, one warp per range).  The list puts every range
-// after all the groups it reads (plus a slack), so the smallest unfinished
-// item can always progress (its worker's earlier items are finished and the
-// groups it waits on have smaller positions): no deadlock.  The roles share
-// the SMs, so the latency-bound update and the bandwidth-bound row stream
-// overlap instead of running back to back, and the element records are
-// still L2-resident when read.  A group is published with a release store
-// of the launch generation (deferred to the worker's next item, so the
-// fence finds its stores drained); a range waits with acquire loads.  The
-// last CTA to finish bumps the generation: the launch is replayable (CUDA
-// graphs) without a memset.  Same per-entry arithmetic and add order as the
-// two-launch step, hence the same bits.
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_gpu(int* p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-template <int NP, int NQ>
-struct MegaCfg {
-  using W = WarpCfg<2, NP, NQ>;
-  static constexpr int ST = ((W::EPW * NQ * W::REC + 1) / 2) * 2;  // doubles (even: 16-B aligned)
-  static constexpr int OUT = W::EPW * W::NB * W::D2;
-  static constexpr int PRODUCER = ST + OUT;                        // doubles per warp
-};
-
-template <int MODEL, int NP, int NQ>
-__global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
-    k_newton_mega(ConstArgs c, GatherArgs g, MegaArgs m, int slice) {
-  using W = WarpCfg<2, NP, NQ>;
-  using MC = MegaCfg<NP, NQ>;
-  extern __shared__ __align__(128) double dyn[];
-  __shared__ uint64_t s_bar[W::WPB];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t workers = (int64_t)gridDim.x * W::WPB;
-  double* my = dyn + (size_t)w * slice;
-  const int gen = *((volatile int*)&m.sync->gen);  // bumped only after every CTA has finished
-  if (lane == 0) {
-    mbar_init(&s_bar[w], 1);
-    mbar_init_fence();
-  }
-  __syncwarp();
-  unsigned parity = 0;
-  int pending = -1;  // produced group not yet published
-  auto publish = [&] {
-    if (pending >= 0 && lane == 0) {
-      __threadfence();
-      st_release_gpu(m.flag + pending, gen + 1);
-    }
-    pending = -1;
-  };
-  for (int64_t t = (int64_t)blockIdx.x * W::WPB + w; t < m.n_items; t += workers) {
-    const int item = __ldg(m.sched + t);
-    if (item >= 0) {
-      if (m.exp != 2) {
-        newton_warp_group<MODEL, NP, NQ, false, true>(c, g, (int64_t)item * W::EPW, my, my + MC::ST, lane);
-        __syncwarp();
-      }
-      publish();
-      pending = item;
-    } else {
-      publish();
-      if (m.exp == 1) continue;
-      const int r = ~item;
-      if (row_range<2, NP, NQ, 32, true>(
-              g, g.npc, r, my, &s_bar[w], parity,
-              [&] {
-                if (m.exp == 0) {
-                  const int lo = __ldg(m.rlo + r), hi = __ldg(m.rhi + r);
-                  for (int k = lo + lane; k <= hi; k += 32)
-                    while (ld_acquire_gpu(m.flag + k) != gen + 1) __nanosleep(32);
-                }
-                __syncwarp();
-              },
-              lane))
-        parity ^= 1u;
-    }
-    // this worker's generic smem writes are next overwritten by TMA
-    fence_proxy_async_smem();
-    __syncwarp();
-  }
-  publish();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&m.sync->finished, 1) == (int)gridDim.x - 1) {
-      m.sync->finished = 0;
-      atomicAdd(&m.sync->gen, 1);
-      __threadfence();
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// k_newton_warp_ovl (2D): k_newton_warp made persistent for the overlapped
-// step.  The grid is sized below full occupancy (EPFEM_OVL_CTAS per SM) so
-// that the row stream's CTAs, launched with programmatic dependent launch,
-// share the SMs with it; each warp walks the element groups (warp-strided,
-// so groups complete roughly in order) and publishes every group with a
-// release store of the step generation (deferred to its next group, so the
-// fence finds the stores drained).  The trigger at entry lets the row
-// stream launch as soon as every producer CTA is resident, which is what
-// makes the row stream's flag waits deadlock-free.
-template <int MODEL, int NP, int NQ>
-__global__ void __launch_bounds__(WarpCfg<2, NP, NQ>::THREADS, EPFEM_WARP_MINB)
-    k_newton_warp_ovl(ConstArgs c, GatherArgs g, OvlArgs o) {
-  pdl_trigger();
-  using W = WarpCfg<2, NP, NQ>;
-  __shared__ double s_st[W::WPB][W::EPW * NQ * W::REC];
-  __shared__ __align__(16) double s_out[W::WPB][W::EPW * W::NB * W::D2];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int gen = *((volatile int*)&o.sync->gen);
-  int pending = -1;
-  for (int64_t grp = (int64_t)blockIdx.x * W::WPB + w; grp < o.n_groups; grp += (int64_t)gridDim.x * W::WPB) {
-    newton_warp_group<MODEL, NP, NQ, false, true>(c, g, grp * W::EPW, s_st[w], s_out[w], lane);
-    __syncwarp();
-    if (pending >= 0 && lane == 0) {
-      __threadfence();
-      st_release_gpu(o.flag + pending, gen + 1);
-    }
-    pending = (int)grp;
-  }
-  if (pending >= 0 && lane == 0) {
-    __threadfence();
-    st_release_gpu(o.flag + pending, gen + 1);
-  }
-}
-
-bool ovl_supported(int family, int dim, int* group_elems) {
-  bool ok = false;
-  dispatch_element(family, dim, [&](auto F, auto D) {
-    constexpr int DIM = decltype(D)::value;
-    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
-    if constexpr (DIM == 2) {
-      *group_elems = WarpCfg<2, NP, NQ>::EPW;
-      ok = true;
-    }
-  });
-  return ok;
-}
-
-int launch_newton_ovl(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g, const OvlArgs& o,
-                      int ctas_per_sm, cudaStream_t st) {
-  if (o.n_groups <= 0) return 0;
-  int rc = 0;
-  bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
-    constexpr int DIM = decltype(D)::value;
-    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
-    if constexpr (DIM == 2) {
-      using W = WarpCfg<2, NP, NQ>;
-      int dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      const int64_t want = (o.n_groups + W::WPB - 1) / W::WPB;
-      const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)std::max(ctas_per_sm, 1) * sms);
-      switch (model) {
-        case EPFEM_MODEL_VON_MISES:
-          k_newton_warp_ovl<EPFEM_MODEL_VON_MISES, NP, NQ><<<grid, W::THREADS, 0, st>>>(c, g, o);
-          break;
-        case EPFEM_MODEL_DRUCKER_PRAGER:
-          k_newton_warp_ovl<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ><<<grid, W::THREADS, 0, st>>>(c, g, o);
-          break;
-        default: k_newton_warp_ovl<EPFEM_MODEL_ELASTIC, NP, NQ><<<grid, W::THREADS, 0, st>>>(c, g, o); break;
-      }
-    } else {
-      rc = fail(EPFEM_ERR_INVALID, "overlapped step: 2D meshes only");
-    }
-  });
-  if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
-  if (rc) return rc;
-  EPFEM_CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
-// per node range: the first and last producer group whose elements touch it
-__global__ void k_range_groups(int64_t n_nodes, int npc, int np, int group_elems,
-                               const int64_t* __restrict__ n2e_ptr, const int32_t* __restrict__ n2e,
-                               int32_t* rlo, int32_t* rhi) {
-  const int64_t n_ranges = (n_nodes + npc - 1) / npc;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_ranges;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t n0 = r * npc, n1 = min(n0 + (int64_t)npc, n_nodes);
-    int lo = INT32_MAX, hi = -1;
-    for (int64_t a = n0; a < n1; ++a) {
-      const int64_t b = n2e_ptr[a], e = n2e_ptr[a + 1];
-      if (e > b) {  // a node's items are sorted by element
-        lo = min(lo, (int)(n2e[b] / np / group_elems));
-        hi = max(hi, (int)(n2e[e - 1] / np / group_elems));
-      }
-    }
-    rlo[r] = lo;
-    rhi[r] = hi;
-  }
-}
-
-// group_elems: elements per producer item (one warp group); slice_bytes:
-// the per-warp shared-memory slice (at least the producer's, sized so that
-// EPFEM_WARP_MINB CTAs fit an SM); workers: warps of the co-resident grid.
-bool mega_supported(int family, int dim, int* group_elems, int* slice_bytes, int* workers) {
-  bool ok = false;
-  dispatch_element(family, dim, [&](auto F, auto D) {
-    constexpr int DIM = decltype(D)::value;
-    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
-    if constexpr (DIM == 2) {
-      using W = WarpCfg<2, NP, NQ>;
-      *group_elems = W::EPW;
-      const int per_warp = ((200 * 1024 / EPFEM_WARP_MINB) / W::WPB) & ~127;
-      const int prod = (int)(MegaCfg<NP, NQ>::PRODUCER * sizeof(double));
-      *slice_bytes = per_warp > prod ? per_warp : prod;
-      if (const char* v = getenv("EPFEM_MEGA_SLICE")) *slice_bytes = atoi(v);  // tuning / debugging
-      int per_sm = 0, dev = 0, sms = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      auto kern = k_newton_mega<EPFEM_MODEL_VON_MISES, NP, NQ>;
-      const size_t smem = (size_t)*slice_bytes * W::WPB;
-      if (smem > 48 * 1024 &&
-          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W::THREADS, smem) != cudaSuccess ||
-          per_sm <= 0)
-        return;
-      *workers = per_sm * sms * W::WPB;
-      ok = true;
-    }
-  });
-  cudaGetLastError();
-  return ok;
-}
-
-int launch_range_groups(int64_t n_nodes, int npc, int np, int group_elems, const int64_t* n2e_ptr,
-                        const int32_t* n2e, int32_t* rlo, int32_t* rhi, cudaStream_t st) {
-  k_range_groups<<<256, 128, 0, st>>>(n_nodes, npc, np, group_elems, n2e_ptr, n2e, rlo, rhi);
-  EPFEM_CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
-int launch_newton_mega(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g, const MegaArgs& m,
-                       int slice_bytes, int workers, cudaStream_t st) {
-  if (m.n_items <= 0) return 0;
-  int rc = 0;
-  bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
-    constexpr int DIM = decltype(D)::value;
-    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
-    if constexpr (DIM == 2) {
-      using W = WarpCfg<2, NP, NQ>;
-      const size_t smem = (size_t)slice_bytes * W::WPB;
-      const int slice = slice_bytes / (int)sizeof(double);
-      auto run = [&](auto kern) {
-        if (smem > 48 * 1024) {
-          cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-          if (e != cudaSuccess) { rc = cuda_fail(e, "cudaFuncSetAttribute"); return; }
-        }
-        // cooperative: every CTA co-resident (the item walk relies on it)
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)(workers / W::WPB));
-        cfg.blockDim = dim3(W::THREADS);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, c, g, m, slice);
-        if (e != cudaSuccess) rc = cuda_fail(e, "one-launch Newton step");
-      };
-      switch (model) {
-        case EPFEM_MODEL_VON_MISES: run(k_newton_mega<EPFEM_MODEL_VON_MISES, NP, NQ>); break;
-        case EPFEM_MODEL_DRUCKER_PRAGER: run(k_newton_mega<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ>); break;
-        default: run(k_newton_mega<EPFEM_MODEL_ELASTIC, NP, NQ>); break;
-      }
-    } else {
-      rc = fail(EPFEM_ERR_INVALID, "one-launch Newton step: 2D meshes only");
-    }
-  });
-  if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
-  if (rc) return rc;
-  EPFEM_CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
-// Fused internal-forces step (2D warp kernel with FORCES).
-bool forces_fused_supported(int family, int dim) { return dim == 2 && family >= 0; }
-
-int launch_newton_forces(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g, cudaStream_t st) {
-  if (g.e_end <= g.e_begin) return 0;
-  bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
-    constexpr int DIM = decltype(D)::value;
-    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
-    if constexpr (DIM == 2) {
-      using W = WarpCfg<DIM, NP, NQ>;
-      const int64_t per = (int64_t)W::EPW * W::WPB;
-      const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
-      switch (model) {
-        case EPFEM_MODEL_VON_MISES:
-          k_newton_warp<EPFEM_MODEL_VON_MISES, NP, NQ, false, true><<<blocks, W::THREADS, 0, st>>>(c, g);
-          break;
-        case EPFEM_MODEL_DRUCKER_PRAGER:
-          k_newton_warp<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ, false, true><<<blocks, W::THREADS, 0, st>>>(c, g);
-          break;
-        default: k_newton_warp<EPFEM_MODEL_ELASTIC, NP, NQ, false, true><<<blocks, W::THREADS, 0, st>>>(c, g); break;
-      }
-    }
-  });
-  if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
-  EPFEM_CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
-// Prefetch distance of the fused kernels, in CTAs: EPFEM_PF occupancy waves
-// times the CTAs resident on the device.  Opt-in (default 0): measured on
-// B200 neutral in 2D (cfg2 0.210 vs 0.213 ms at half a wave) and slower in 3D
-// (cfg3 4.34 vs 3.70 ms at one wave): the first-phase load stalls are
-// queueing under load, not DRAM latency an L2 hit would remove.
-static int prefetch_distance(const void* kern, int threads) {
-  static const double waves = getenv("EPFEM_PF") ? atof(getenv("EPFEM_PF")) : 0.0;
-  if (waves <= 0) return 0;
-  static std::mutex mu;
-  static std::map<const void*, int> resident;
-  std::lock_guard<std::mutex> lock(mu);
-  auto it = resident.find(kern);
-  if (it == resident.end()) {
-    int per_sm = 0, dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0) != cudaSuccess) per_sm = 0;
-    cudaGetLastError();
-    it = resident.emplace(kern, per_sm * sms).first;
-  }
-  return (int)(waves * it->second);
-}
-
+// The DMMA phase 2 (k_newton_mma, mma.sync.m8n8k4.f64) is opt-in,
+// EPFEM_FUSED=mma: parity-tested, and measured slower than the DFMA row
+// pairs / chunks on B200 (cfg2 0.253 vs 0.211 ms, cfg4 14.7 vs 4.2 ms): the
+// per-lane fragment gathers cost more issue slots than the DMMA saves.
 int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
                         cudaStream_t st) {
-  if (g.e_end <= g.e_begin) return 0;
-  // The TMA-pipelined variant measured slower than the plain one on B200
-  // (cfg2: 0.255 vs 0.224 ms; the kernel is bound by FP64 dependency chains,
-  // not load latency), so it is opt-in: EPFEM_FUSED=pipe.
-  // EPFEM_FUSED=cta forces the CTA kernel in 2D (default there: k_newton_warp).
-  static const bool pipe = [] {
+  static const bool mma = [] {
     const char* v = getenv("EPFEM_FUSED");
-    return v && v[0] == 'p' && v[1] == 'i';
+    return v && v[0] == 'm';
   }();
-  static const bool cta = [] {
-    const char* v = getenv("EPFEM_FUSED");
-    return v && v[0] == 'c' && v[1] == 't';
-  }();
-  // phase 2 on the tensor pipe (k_newton_mma): opt-in, EPFEM_FUSED=mma.
-  // Correct (same parity tests) but measured slower on B200 for cfg2
-  // (0.253 vs 0.211 ms): the per-lane fragment gathers cost more issue
-  // slots than the DMMA saves.
-  static const int mma = [] {
-    const char* v = getenv("EPFEM_FUSED");
-    return (v && v[0] == 'm') ? 2 : 0;
-  }();
-  // 3D tetrahedra: warp kernel with row-pair phase 2 by default (hexahedra
-  // keep the CTA kernel); EPFEM_FUSED=cta forces the CTA kernel
-  static const bool warp3 = [] {
-    const char* v = getenv("EPFEM_FUSED");
-    return !(v && v[0] == 'c' && v[1] == 't') && !getenv("EPFEM_NO_WARP3");
-  }();
-  // two groups per warp with TMA prefetch of the second (2D): EPFEM_FUSED=pf
-  static const bool pf = [] {
-    const char* v = getenv("EPFEM_FUSED");
-    return v && v[0] == 'p' && v[1] == 'f';
-  }();
-  // warp-specialized producer / consumer kernel (2D): EPFEM_FUSED=ws
-  static const bool ws = [] {
-    const char* v = getenv("EPFEM_FUSED");
-    return v && v[0] == 'w' && v[1] == 's';
-  }();
-  int rc = 0;
-  bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
-    constexpr int DIM = decltype(D)::value;
-    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
-    using Cfg = DeltaCfg<DIM, NP, NQ>;
-    if (pipe) {
-      switch (model) {
-        case EPFEM_MODEL_VON_MISES: rc = launch_pipe<EPFEM_MODEL_VON_MISES, DIM, NP, NQ>(c, g, st); break;
-        case EPFEM_MODEL_DRUCKER_PRAGER:
-          rc = launch_pipe<EPFEM_MODEL_DRUCKER_PRAGER, DIM, NP, NQ>(c, g, st);
-          break;
-        default: rc = launch_pipe<EPFEM_MODEL_ELASTIC, DIM, NP, NQ>(c, g, st); break;
-      }
-      return;
-    }
-    if (mma == 2) {
-      using M = MmaCfg<DIM, NP, NQ>;
-      const int64_t per = (int64_t)M::EPW * M::WPB;
-      const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
-      switch (model) {
-        case EPFEM_MODEL_VON_MISES:
-          k_newton_mma<EPFEM_MODEL_VON_MISES, DIM, NP, NQ><<<blocks, M::THREADS, 0, st>>>(c, g);
-          break;
-        case EPFEM_MODEL_DRUCKER_PRAGER:
-          k_newton_mma<EPFEM_MODEL_DRUCKER_PRAGER, DIM, NP, NQ><<<blocks, M::THREADS, 0, st>>>(c, g);
-          break;
-        default:
-          k_newton_mma<EPFEM_MODEL_ELASTIC, DIM, NP, NQ><<<blocks, M::THREADS, 0, st>>>(c, g);
-          break;
-      }
-      return;
-    }
-    // (measured: P2 tet cfg3 3.61 vs 4.08 ms; Q1 hex cfg4 4.73 vs 4.17 ms -> CTA kernel for Q1)
-    if constexpr (DIM == 3 && NP < 20 && NP != 8) {
-      if (warp3) {
-        using W = Pair3Cfg<NP, NQ>;
-        const int64_t per = (int64_t)W::EPW * W::WPB;
-        const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
-        GatherArgs gp = g;
-        gp.pf_dist = prefetch_distance((const void*)k_newton_warp3<EPFEM_MODEL_VON_MISES, NP, NQ>, W::THREADS);
-        switch (model) {
-          case EPFEM_MODEL_VON_MISES:
-            k_newton_warp3<EPFEM_MODEL_VON_MISES, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, gp);
-            break;
-          case EPFEM_MODEL_DRUCKER_PRAGER:
-            k_newton_warp3<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, gp);
-            break;
-          default:
-            k_newton_warp3<EPFEM_MODEL_ELASTIC, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, gp);
-            break;
-        }
-        return;
-      }
-    }
-    if constexpr (DIM == 2) {
-      if (pf) {
-        using W = WarpCfg<DIM, NP, NQ>;
-        const int64_t per = 2 * (int64_t)W::EPW * PFW;
-        const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
-        switch (model) {
-          case EPFEM_MODEL_VON_MISES:
-            k_newton_warp_pf<EPFEM_MODEL_VON_MISES, NP, NQ><<<blocks, 32 * PFW, 0, st>>>(c, g);
-            break;
-          case EPFEM_MODEL_DRUCKER_PRAGER:
-            k_newton_warp_pf<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ><<<blocks, 32 * PFW, 0, st>>>(c, g);
-            break;
-          default:
-            k_newton_warp_pf<EPFEM_MODEL_ELASTIC, NP, NQ><<<blocks, 32 * PFW, 0, st>>>(c, g);
-            break;
-        }
-        return;
-      }
-      if (ws) {
-        switch (model) {
-          case EPFEM_MODEL_VON_MISES: rc = launch_ws<EPFEM_MODEL_VON_MISES, NP, NQ>(c, g, st); break;
-          case EPFEM_MODEL_DRUCKER_PRAGER: rc = launch_ws<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ>(c, g, st); break;
-          default: rc = launch_ws<EPFEM_MODEL_ELASTIC, NP, NQ>(c, g, st); break;
-        }
-        return;
-      }
-      if (!cta) {
-        using W = WarpCfg<DIM, NP, NQ>;
-        const int64_t per = (int64_t)W::EPW * W::WPB;
-        const unsigned blocks = (unsigned)((g.e_end - g.e_begin + per - 1) / per);
-        GatherArgs gp = g;
-        gp.pf_dist = prefetch_distance((const void*)k_newton_warp<EPFEM_MODEL_VON_MISES, NP, NQ>, W::THREADS);
-        switch (model) {
-          case EPFEM_MODEL_VON_MISES:
-            k_newton_warp<EPFEM_MODEL_VON_MISES, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, gp);
-            break;
-          case EPFEM_MODEL_DRUCKER_PRAGER:
-            k_newton_warp<EPFEM_MODEL_DRUCKER_PRAGER, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, gp);
-            break;
-          default:
-            k_newton_warp<EPFEM_MODEL_ELASTIC, NP, NQ><<<blocks, W::THREADS, 0, st>>>(c, gp);
-            break;
-        }
-        return;
-      }
-    }
-    using FC = FusedCfg<DIM, NP, NQ>;
-    const unsigned blocks = (unsigned)((g.e_end - g.e_begin + FC::EPB - 1) / FC::EPB);
-    GatherArgs gp = g;
-      gp.pf_dist = prefetch_distance((const void*)k_newton_fused<EPFEM_MODEL_VON_MISES, DIM, NP, NQ>, FC::THREADS);
-      switch (model) {
-      case EPFEM_MODEL_VON_MISES:
-        k_newton_fused<EPFEM_MODEL_VON_MISES, DIM, NP, NQ><<<blocks, FC::THREADS, 0, st>>>(c, gp);
-        break;
-      case EPFEM_MODEL_DRUCKER_PRAGER:
-        k_newton_fused<EPFEM_MODEL_DRUCKER_PRAGER, DIM, NP, NQ><<<blocks, FC::THREADS, 0, st>>>(c, gp);
-        break;
-      default:
-        k_newton_fused<EPFEM_MODEL_ELASTIC, DIM, NP, NQ><<<blocks, FC::THREADS, 0, st>>>(c, gp);
-        break;
-    }
-  });
-  if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
-  if (rc) return rc;
-  EPFEM_CUDA_TRY(cudaGetLastError());
-  return 0;
+  return launch_fused_impl<false>(model, family, dim, c, g, mma, st);
 }
 
 }  // namespace epfem_gpu

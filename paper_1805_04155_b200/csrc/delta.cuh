@@ -81,7 +81,7 @@ struct DeltaCfg {
   static constexpr int MINB = DIM == 2 ? 1024 / THREADS : (NP < 20 ? EPFEM_MINB3 : EPFEM_MINB20);
 };
 
-// assembly row r -> Voigt row (2D plane strain uses {0,1,3}, assembly.cpp:92)
+// assembly row r -> Voigt row (2D plane strain uses {0,1,3}, assembly.cpp:16)
 template <int DIM>
 __device__ __forceinline__ constexpr int arow(int r) {
   return (DIM == 2 && r == 2) ? 3 : r;
@@ -239,13 +239,13 @@ __device__ __forceinline__ void delta_phase2(
 #pragma unroll
     for (int c = 0; c < NS; ++c) {
       if constexpr (DIM == 3) {
-        // B rows e11,e22,e33,2e12,2e23,2e31 (assembly.cpp:162-171)
+        // B rows e11,e22,e33,2e12,2e23,2e31 (assembly.cpp:86-95)
         T[0][c] = __fma_rn(ga[2], Dw(5, c), __fma_rn(ga[1], Dw(3, c), __dmul_rn(ga[0], Dw(0, c))));
         T[1][c] = __fma_rn(ga[2], Dw(4, c), __fma_rn(ga[0], Dw(3, c), __dmul_rn(ga[1], Dw(1, c))));
         T[DIM - 1][c] =
             __fma_rn(ga[0], Dw(5, c), __fma_rn(ga[1], Dw(4, c), __dmul_rn(ga[2], Dw(2, c))));
       } else {
-        // rows e11, e22, 2e12 (assembly.cpp:173-176)
+        // rows e11, e22, 2e12 (assembly.cpp:96-100)
         T[0][c] = __fma_rn(ga[1], Dw(2, c), __dmul_rn(ga[0], Dw(0, c)));
         T[1][c] = __fma_rn(ga[0], Dw(2, c), __dmul_rn(ga[1], Dw(1, c)));
       }
@@ -274,111 +274,6 @@ __device__ __forceinline__ void delta_phase2(
 #pragma unroll
   for (int bb = 0; bb < CS; ++bb) {
     if (bb < nb) {
-      double* o = rec + blk_index<NP>(a, c0 + bb) * D2;
-#pragma unroll
-      for (int i = 0; i < DIM; ++i)
-#pragma unroll
-        for (int j = 0; j < DIM; ++j) o[i * DIM + j] = blk[bb][i][j];
-    }
-  }
-}
-
-// Phase 2 with T shared through shared memory (CTA kernel): the CTA walks
-// the union of its elements' plastic points; per point, step A forms every
-// T_a = B_a^T Dw once (thread per (element, node)) into s_T, a barrier, then
-// step B has each phase-2 thread (element, row a, CS-block chunk, uniform
-// length) add T_a B_b to its accumulators, and a second barrier.  Each T_a is
-// computed once instead of once per chunk of its row; the FMA sequence per
-// block entry is the one of delta_phase2, so the bits are identical.
-template <int DIM, int NP, int NQ>
-__device__ __forceinline__ void delta_phase2_tshared(
-    const double (*s_st)[NQ][DeltaCfg<DIM, NP, NQ>::REC], const unsigned* s_mask,
-    double (*s_T)[NP][DIM * DeltaCfg<DIM, NP, NQ>::NS], int tid, int nthreads, int64_t e0, int64_t e_end,
-    double* __restrict__ scratch) {
-  using Cfg = DeltaCfg<DIM, NP, NQ>;
-  constexpr int NS = Cfg::NS, D2 = Cfg::D2, NB = Cfg::NB, CS = Cfg::CS, NT = Cfg::NT, EPB = Cfg::EPB;
-  int le = 0, a = 0, c0 = 0;
-  unsigned mask = 0u;
-  if (tid < EPB * NT) {
-    le = tid / NT;
-    chunk_of<NP, CS>(tid - le * NT, a, c0);
-    if (e0 + le < e_end) mask = s_mask[le];
-  }
-  unsigned umask = 0u;
-#pragma unroll 1
-  for (int l = 0; l < EPB; ++l) umask |= s_mask[l];
-  double blk[CS][DIM][DIM];
-#pragma unroll
-  for (int b = 0; b < CS; ++b)
-#pragma unroll
-    for (int i = 0; i < DIM; ++i)
-#pragma unroll
-      for (int j = 0; j < DIM; ++j) blk[b][i][j] = 0.0;
-#pragma unroll 1
-  while (umask) {
-    const int q = __ffs(umask) - 1;
-    umask &= umask - 1u;
-    // step A: T_a for every (element with q plastic, node a)
-    for (int t = tid; t < EPB * NP; t += nthreads) {
-      const int l2 = t / NP, a2 = t - l2 * NP;
-      if (!((s_mask[l2] >> q) & 1u)) continue;
-      const double* st = s_st[l2][q];
-      const double* dw = st + NP * DIM;
-      auto Dw = [&](int r, int c) {
-        const int lo = r < c ? r : c, hi = r < c ? c : r;
-        return dw[lo * NS - lo * (lo - 1) / 2 + (hi - lo)];
-      };
-      double ga[DIM];
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) ga[i] = st[a2 * DIM + i];
-      double* T = s_T[l2][a2];
-#pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        if constexpr (DIM == 3) {
-          T[0 * NS + c] = __fma_rn(ga[2], Dw(5, c), __fma_rn(ga[1], Dw(3, c), __dmul_rn(ga[0], Dw(0, c))));
-          T[1 * NS + c] = __fma_rn(ga[2], Dw(4, c), __fma_rn(ga[0], Dw(3, c), __dmul_rn(ga[1], Dw(1, c))));
-          T[(DIM - 1) * NS + c] =
-              __fma_rn(ga[0], Dw(5, c), __fma_rn(ga[1], Dw(4, c), __dmul_rn(ga[2], Dw(2, c))));
-        } else {
-          T[0 * NS + c] = __fma_rn(ga[1], Dw(2, c), __dmul_rn(ga[0], Dw(0, c)));
-          T[1 * NS + c] = __fma_rn(ga[0], Dw(2, c), __dmul_rn(ga[1], Dw(1, c)));
-        }
-      }
-    }
-    __syncthreads();
-    // step B: the thread's chunk of block row a
-    if ((mask >> q) & 1u) {
-      const double* st = s_st[le][q];
-      const double* T = s_T[le][a];
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) {
-        double Ti[NS];
-#pragma unroll
-        for (int c = 0; c < NS; ++c) Ti[c] = T[i * NS + c];
-#pragma unroll
-        for (int bb = 0; bb < CS; ++bb) {
-          const int b = c0 + bb < NP ? c0 + bb : NP - 1;  // clamped: result dropped below
-          const double* h = st + b * DIM;
-          const double h0 = h[0], h1 = h[1], h2 = DIM == 3 ? h[DIM - 1] : 0.0;
-          if constexpr (DIM == 3) {
-            blk[bb][i][0] = __fma_rn(Ti[5], h2, __fma_rn(Ti[3], h1, __fma_rn(Ti[0], h0, blk[bb][i][0])));
-            blk[bb][i][1] = __fma_rn(Ti[4], h2, __fma_rn(Ti[3], h0, __fma_rn(Ti[1], h1, blk[bb][i][1])));
-            blk[bb][i][DIM - 1] =
-                __fma_rn(Ti[5], h0, __fma_rn(Ti[4], h1, __fma_rn(Ti[2], h2, blk[bb][i][DIM - 1])));
-          } else {
-            blk[bb][i][0] = __fma_rn(Ti[2], h1, __fma_rn(Ti[0], h0, blk[bb][i][0]));
-            blk[bb][i][1] = __fma_rn(Ti[2], h0, __fma_rn(Ti[1], h1, blk[bb][i][1]));
-          }
-        }
-      }
-    }
-    __syncthreads();
-  }
-  if (!mask) return;
-  double* rec = scratch + (size_t)(e0 + le) * NB * D2;
-#pragma unroll
-  for (int bb = 0; bb < CS; ++bb) {
-    if (c0 + bb < NP) {
       double* o = rec + blk_index<NP>(a, c0 + bb) * D2;
 #pragma unroll
       for (int i = 0; i < DIM; ++i)
@@ -603,77 +498,6 @@ __device__ __forceinline__ void delta_pairs3(const double* st_e, unsigned mask, 
   }
 }
 
-// Q2-20 (cfg5): the row pair of delta_pairs3 split in two halves, lane (pair
-// p, component i, half h): half 0 owns the first ceil((NP+1)/2) blocks of the
-// pair (all in row a0 = p, so only T_a0 row i is formed), half 1 the rest
-// (the tail of row a0 and row a1).  33 instead of 63 accumulators per lane,
-// 7,290 FMA per plastic point against 9,720 for padded chunks of 4 (6,750
-// optimal).  Per-entry FMA sequences are those of delta_phase2: same bits.
-template <int NP, int NQ>
-__device__ __forceinline__ void delta_pairs3_half(const double* st_e, unsigned mask, int p, int i, int half,
-                                                  double* __restrict__ rec) {
-  using C = Pair3Cfg<NP, NQ>;
-  constexpr int NS = C::NS, REC = C::REC, D2 = C::D2, NBLK = C::NBLK;
-  constexpr int KH = (NBLK + 1) / 2;
-  static_assert(NP - (NP / 2 - 1) >= KH, "half 0 stays in row a0 for every pair");
-  const int a0 = p, a1 = NP - 1 - p;
-  const bool twin = a1 != a0;
-  const int k0 = half * KH;
-  const int d0 = i, d1 = i == 2 ? 4 : 3, d2 = i == 0 ? 5 : (i == 1 ? 4 : 5);
-  const int e1 = i == 0 ? 1 : (i == 1 ? 0 : 1), e2 = i == 0 ? 2 : (i == 1 ? 2 : 0);
-  auto pk = [](int r, int c) {
-    const int lo = r < c ? r : c, hi = r < c ? c : r;
-    return lo * NS - lo * (lo - 1) / 2 + (hi - lo);
-  };
-  double acc[KH][3];
-#pragma unroll
-  for (int k = 0; k < KH; ++k) acc[k][0] = acc[k][1] = acc[k][2] = 0.0;
-  while (mask) {
-    const int q = __ffs(mask) - 1;
-    mask &= mask - 1u;
-    const double* st = st_e + q * REC;
-    const double* dw = st + NP * 3;
-    double T0[NS], T1[NS];
-    {
-      const double* g0 = st + a0 * 3;
-      const double* g1 = st + a1 * 3;
-      const double gA0 = g0[d0], gA1 = g0[e1], gA2 = g0[e2];
-      const double gB0 = g1[d0], gB1 = g1[e1], gB2 = g1[e2];
-#pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        const double w0 = dw[pk(d0, c)], w1 = dw[pk(d1, c)], w2 = dw[pk(d2, c)];
-        T0[c] = __fma_rn(gA2, w2, __fma_rn(gA1, w1, __dmul_rn(gA0, w0)));
-        T1[c] = half ? __fma_rn(gB2, w2, __fma_rn(gB1, w1, __dmul_rn(gB0, w0))) : 0.0;
-      }
-    }
-#pragma unroll
-    for (int kk = 0; kk < KH; ++kk) {
-      const int k = k0 + kk;
-      const bool first = k < NP - a0;
-      const int b = first ? a0 + k : a1 + (k - (NP - a0));
-      const bool ok = k < NBLK && (first || (twin && k - (NP - a0) < NP - a1));
-      const double* T = first ? T0 : T1;
-      const double* h = st + (ok ? b : NP - 1) * 3;
-      const double h0 = h[0], h1 = h[1], h2 = h[2];
-      acc[kk][0] = __fma_rn(T[5], h2, __fma_rn(T[3], h1, __fma_rn(T[0], h0, acc[kk][0])));
-      acc[kk][1] = __fma_rn(T[4], h2, __fma_rn(T[3], h0, __fma_rn(T[1], h1, acc[kk][1])));
-      acc[kk][2] = __fma_rn(T[5], h0, __fma_rn(T[4], h1, __fma_rn(T[2], h2, acc[kk][2])));
-    }
-  }
-#pragma unroll
-  for (int kk = 0; kk < KH; ++kk) {
-    const int k = k0 + kk;
-    const bool first = k < NP - a0;
-    const int b = first ? a0 + k : a1 + (k - (NP - a0));
-    const bool ok = k < NBLK && (first || (twin && k - (NP - a0) < NP - a1));
-    if (!ok) continue;
-    double* o = rec + blk_index<NP>(first ? a0 : a1, b) * D2 + i * 3;
-    o[0] = acc[kk][0];
-    o[1] = acc[kk][1];
-    o[2] = acc[kk][2];
-  }
-}
-
 // 2D row pairs (delta_pairs3's scheme with dim 2): lane (element, pair p,
 // component i) owns row i of block rows p and NP - 1 - p; 2 * ceil(NP / 2)
 // lanes per element (8 for Q2-8), NP + 1 blocks per lane, optimal FMA count.
@@ -791,7 +615,7 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 }
 
 // B[k][(node, comp)] of the strain-displacement operator from the node's
-// physical gradient g (assembly.cpp:162-176 row order)
+// physical gradient g (assembly.cpp:86-100 row order)
 template <int DIM>
 __device__ __forceinline__ double b_entry(int k, int comp, const double* g) {
   // 2 bits per (k, comp): index into g, 3 = structural zero

@@ -50,56 +50,16 @@ struct GatherArgs {
   double* scratch;   // tangent workspace: symmetric dK_e per element
   unsigned* emask;   // per-element plastic-point bitmask
   int npc;           // nodes per CTA of the row stream
-  const int32_t* range_order;  // row stream: CTA b assembles range range_order[b] (whole-mesh launches)
   int max_span;      // widest value range of any row-stream CTA (doubles)
   int max_items;     // most (element, node) items of any row-stream CTA
   double Cu[21];     // packed elastic operator when the material is uniform
-  // sub-range processed by one launch (chunked, overlapped schedule)
+  // sub-range processed by one launch (element / node ranges of a slab)
   int64_t e_begin, e_end;  // elements of the delta / fused kernels
   int64_t n_begin, n_end;  // nodes of the row stream
   // strain-fused Newton step (epfem_newton_step_u): nodal displacements in,
   // optional strain output
   const double* u;
   double* E_out;
-  int pf_dist;  // fused kernels: CTA b prefetches (L2) the inputs of CTA b + pf_dist (0: off)
-  // internal forces fused into the step (epfem_newton_step_f): per-element
-  // force records (n_elements x n_p x dim) and the assembled F (n_dofs)
-  double* fws;
-  double* F_out;
-};
-// One-launch Newton step (k_newton_mega): an ordered item list of producer
-// groups (>= 0: one warp group of EPW elements through the fused update) and
-// node ranges (< 0: ~range through the row stream), walked round-robin by
-// the warps of a cooperative grid; a range sits after every group it reads;
-// per-group ready flags carry the launch generation.
-struct MegaSync {
-  int ticket;    // unused (static round-robin walk)
-  int finished;  // CTAs done in this launch
-  int gen;       // launch generation (flags of this launch read gen + 1)
-  int pad;
-};
-struct MegaArgs {
-  const int32_t* sched;  // item list
-  const int32_t* rlo;    // per node range: first / last producer group it reads
-  const int32_t* rhi;
-  int* flag;             // per producer group: generation that completed it
-  MegaSync* sync;
-  int64_t n_items;
-  int group_elems;       // elements per producer group
-  int exp;               // timing experiments (EPFEM_MEGA_EXP): 1 = ranges skipped, 2 = groups skipped, no waits
-};
-// Overlapped two-kernel Newton step (2D): a persistent fused update publishes
-// each warp group with a release flag; the row stream, launched with
-// programmatic dependent launch (so every producer CTA is already resident
-// when any of its CTAs starts), waits on the flags of the groups it reads
-// instead of on the whole producer grid.
-struct OvlArgs {
-  const int32_t* rlo;  // per node range: first / last producer group it reads
-  const int32_t* rhi;
-  int* flag;           // per producer group: generation that completed it
-  MegaSync* sync;      // finished counter + generation (bumped by the last row-stream CTA)
-  int64_t n_groups;
-  int group_elems;
 };
 struct PatternOut {
   int64_t* n2e_ptr = nullptr;
@@ -126,22 +86,11 @@ int launch_gather(int family, int dim, int mode, const GatherArgs& a, cudaStream
 int launch_elastic_p1(int family, int dim, const GatherArgs& a, cudaStream_t st);  // K5, P1 meshes
 int launch_tangent(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);
 int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st);
-bool forces_fused_supported(int family, int dim);
-int launch_newton_forces(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g, cudaStream_t st);
 int launch_delta(int family, int dim, int mode, const GatherArgs& a, cudaStream_t st);  // pass 1 over [e_begin, e_end)
 int launch_newton_fused_u(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
                           cudaStream_t st);  // E = B u inside (GatherArgs::u)
 int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
                         cudaStream_t st);
-bool mega_supported(int family, int dim, int* group_elems, int* slice_bytes, int* workers);
-int launch_newton_mega(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
-                       const MegaArgs& m, int slice_bytes, int workers, cudaStream_t st);
-int launch_range_groups(int64_t n_nodes, int npc, int np, int group_elems, const int64_t* n2e_ptr,
-                        const int32_t* n2e, int32_t* rlo, int32_t* rhi, cudaStream_t st);
-bool ovl_supported(int family, int dim, int* group_elems);
-int launch_newton_ovl(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g, const OvlArgs& o,
-                      int ctas_per_sm, cudaStream_t st);
-int launch_row_stream_ovl(int family, int dim, const GatherArgs& a, const OvlArgs& o, cudaStream_t st);
 int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, const uint8_t* mask,
              const double* b, double* x_out, double rel_tol, int64_t max_iters, cudaStream_t st,
              int64_t* iters_out, double* residual_out, int block = 1);
@@ -150,11 +99,6 @@ int energy_norm(int64_t n, const int64_t* rp, const int32_t* ci, const double* v
 size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements);
 int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
                     cudaStream_t st, int* npc_out, int* span_out, int* items_out, int budget_bytes = 0);
-int plan_range_order(int64_t n_nodes, int dim, int npc, const double* coord, cudaStream_t st,
-                     int32_t** order_out);
-int plan_chunks(int64_t n_nodes, int64_t n_elements, int np, const int64_t* n2e_ptr,
-                const int32_t* n2e, int npc, int n_chunks, int64_t* nchunk, int64_t* echunk,
-                cudaStream_t st);
 int launch_strains(int family, int dim, int64_t n_e, const int32_t* elem, const double* inv,
                    const double* gradhat, const double* u, double* E, cudaStream_t st,
                    int num_sms);

@@ -1,8 +1,8 @@
 // Newton-loop linear algebra on the device:
-// restricted_solve (linalg.cpp:37-121) as Jacobi-preconditioned conjugate
+// restricted_solve (linalg.cpp:69-115) as Jacobi-preconditioned conjugate
 // gradients on K[free, free] — the reference's LinearSolver::conjugate_gradient
 // (Eigen ConjugateGradient, DiagonalPreconditioner, tolerance rel_tol on
-// |r| / |b|, at most 10 m iterations) — and energy_norm (linalg.cpp:123-127).
+// |r| / |b|, at most 10 m iterations) — and energy_norm (linalg.cpp:117-121).
 //
 // The restriction is never formed: the masked SpMV y = M (K (M x)), M =
 // diag(free), acts on the free block and leaves fixed dofs at zero, which is
@@ -339,7 +339,7 @@ int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, c
   // CG on the recurrence residual, then the true residual |M (b - K x)|; on
   // recurrence drift (true residual above the tolerance although the
   // recurrence met it) restart from the true residual, at most 3 times (the
-  // reference's direct solve refines likewise, linalg.cpp:97-103)
+  // reference's direct solve refines likewise, linalg.cpp:92-96)
   for (int restart = 0;; ++restart) {
     if (bnorm > 0.0) {
       while (it < max_iters) {
@@ -370,7 +370,7 @@ int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, c
         if (!(rn > rel_tol * bnorm)) break;  // also stops on NaN
       }
     }
-    // true residual |M (b - K x)| / |M b| (linalg.cpp:109-113)
+    // true residual |M (b - K x)| / |M b| (linalg.cpp:105-109)
     k_spmv_masked<<<grid_rows(n), kThreads, 0, st>>>(n, rp, ci, v, mask, w.x, w.Ap);
     k_resid<<<gb, kThreads, 0, st>>>(n, mask, b, w.Ap, w.z);
     k_dot2<<<gb, kThreads, 0, st>>>(n, w.z, w.z, nullptr, nullptr, w.partial);
@@ -413,7 +413,7 @@ int energy_norm(int64_t n, const int64_t* rp, const int32_t* ci, const double* v
   cudaFree(partial);
   cudaFree(sc);
   EPFEM_CUDA_TRY(cudaGetLastError());
-  *out = std::sqrt(std::max(h[S_PAP], 0.0));  // linalg.cpp:123-127
+  *out = std::sqrt(std::max(h[S_PAP], 0.0));  // linalg.cpp:117-121
   return 0;
 }
 

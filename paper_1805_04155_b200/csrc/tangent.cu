@@ -1,5 +1,5 @@
 // K2 + K6: the per-iteration tangent  K = K_elast + sum_{plastic q} B_q^T w_q (D_q - C_q) B_q
-// (assembly.cpp:262-289), as two deterministic passes without atomics.
+// (assembly.cpp:186-213), as two deterministic passes without atomics.
 //
 // Pass 1 (element delta, k_elem_delta_staged here; fused into the
 // constitutive kernel by epfem_newton_step, see constitutive.cu).  Phase 1:
@@ -24,7 +24,12 @@
 #include <climits>
 #include <vector>
 
-#include "rows.cuh"
+#include "delta.cuh"
+
+#ifndef EPFEM_K_EVICT_FIRST
+#define EPFEM_K_EVICT_FIRST 1  // 3D Q1 / P2: K_elast and K streamed through L2 with evict_first (measured
+                               // cfg3 row stream 3.08 -> 2.97 ms, cfg4 3.76 -> 3.66; neutral or worse in 2D / Q2-20)
+#endif
 
 namespace epfem_gpu {
 
@@ -220,36 +225,16 @@ constexpr int kStreamThreads = 256;
 // 16-byte-aligned range into the shared image (the K_elast allocation is
 // padded by two doubles), overlapped with the item staging; the image goes
 // back to K with one TMA bulk store of the aligned interior plus at most two
-// edge doubles.  (rows.cuh holds the same range pass as a device function
-// for the warp-owned ranges of the one-launch step; this stand-alone kernel
-// keeps its own code: written as the shared function it compiled to 17 %
-// slower 3D instances.)
-// FLAGS: the overlapped step (OvlArgs): wait on the ready flags of the
-// producer groups this range reads instead of griddepcontrol.wait, read the
-// element records with plain (coherent) loads, and let the last CTA bump the
-// generation.
-__device__ __forceinline__ int ld_acquire_gpu_i(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// FORCES: also fold the element internal-force records (GatherArgs::fws,
-// written by the fused kernel) into F for the range's nodes, every item in
-// item order from zero (k_internal_forces' association, hence its bits).
-#ifndef EPFEM_ROW_DYN
-#define EPFEM_ROW_DYN 0
-#endif
-template <int DIM, int NP, int NQ, bool FLAGS = false, bool FORCES = false>
+// edge doubles.
+template <int DIM, int NP, int NQ>
 __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM_ROW_MINB20 : 0)
-    k_row_stream(GatherArgs a, int npc, OvlArgs o) {
+    k_row_stream(GatherArgs a, int npc) {
   extern __shared__ __align__(128) double img_raw[];
   __shared__ uint64_t s_bar;
-  __shared__ int s_next;  // EPFEM_ROW_DYN: next unclaimed node of the range
   constexpr int NB = NP * (NP + 1) / 2;
   constexpr int D2 = DIM * DIM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t range = a.range_order ? (int64_t)__ldg(a.range_order + blockIdx.x) : (int64_t)blockIdx.x;
+  const int64_t range = blockIdx.x;
   const int64_t n0 = a.n_begin + range * npc;
   const int64_t n1 = min(n0 + (int64_t)npc, a.n_end);
   const int nloc = (int)(n1 - n0);
@@ -266,7 +251,6 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
   if (tid == 0) {
     mbar_init(&s_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    s_next = kStreamThreads / 32;
   }
   __syncthreads();
   const bool zero_base = a.base == nullptr;  // elastic assembly: K = sum of element blocks
@@ -286,30 +270,11 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
     s_vptr[k] = (int)(__ldg(a.nbr_ptr + n0 + k) * D2 - v0);
   }
   // everything below reads the producer's emask / workspace
-  int gen = 0;
-  if constexpr (FLAGS) {
-    gen = *((volatile int*)&o.sync->gen);
-    if (warp == 0) {
-      const int lo = __ldg(o.rlo + range), hi = __ldg(o.rhi + range);
-      for (int k = lo + lane; k <= hi; k += 32)
-        while (ld_acquire_gpu_i(o.flag + k) != gen + 1) __nanosleep(64);
-    }
-    __syncthreads();
-  } else {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // stage the range's items (plastic ones kept, others -1)
   for (int k = tid; k < nitems; k += blockDim.x) {
     const int32_t it = __ldg(a.n2e + i_begin + k);
     s_item[k] = __ldcg(a.emask + it / NP) ? it : -1;
-  }
-  if constexpr (FORCES) {  // the range's force records, folded after the K adds
-    double* s_fv = reinterpret_cast<double*>(
-        (reinterpret_cast<uintptr_t>(s_vptr + npc + 1) + 15) & ~uintptr_t(15));
-    for (int k = tid; k < nitems * DIM; k += blockDim.x) {
-      const int it = __ldg(a.n2e + i_begin + k / DIM);
-      s_fv[k] = a.fws[(size_t)it * DIM + k % DIM];
-    }
   }
   __syncthreads();
   if (a1 > a0 && !zero_base) mbar_wait(&s_bar, 0);
@@ -345,7 +310,7 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
             const int lo = up ? pa : pb, hi = up ? pb : pa;
             const int src = blk_index<NP>(lo, hi) * D2 + (up ? ij : j * DIM + i);
             sl[u][kk] = __ldg(a.slot + (int64_t)it * NP + pb);
-            v[u][kk] = FLAGS ? rec[src] : __ldg(rec + src);  // FLAGS: written in this step's overlap
+            v[u][kk] = __ldg(rec + src);
           }
         }
       }
@@ -365,28 +330,9 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
         __syncwarp();
       }
     }
-#if EPFEM_ROW_DYN
-    // dynamic node claim: warps that drew light nodes take the next ones
-    // (one warp per node and item order as before, so the same bits)
-    int nx = 0;
-    if (lane == 0) nx = atomicAdd(&s_next, 1);
-    ln = __shfl_sync(0xffffffffu, nx, 0);
-#else
+    // (claiming nodes dynamically from a shared counter gave the same bits
+    // and measured no faster: warp imbalance inside a range is not the limit)
     ln += kStreamThreads / 32;
-#endif
-  }
-  if constexpr (FORCES) {
-    // the range's force records (item = (element, local node) = record
-    // index) staged by all threads, then one thread per (node, component)
-    // sums them in item order from zero
-    const double* s_fv = reinterpret_cast<const double*>(
-        (reinterpret_cast<uintptr_t>(s_vptr + npc + 1) + 15) & ~uintptr_t(15));
-    for (int t = tid; t < nloc * DIM; t += blockDim.x) {
-      const int ln = t / DIM, i = t - (t / DIM) * DIM;
-      double f = 0.0;
-      for (int k = s_iptr[ln]; k < s_iptr[ln + 1]; ++k) f = __dadd_rn(f, s_fv[k * DIM + i]);
-      a.F_out[(n0 + ln) * DIM + i] = f;
-    }
   }
   fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
   __syncthreads();
@@ -399,14 +345,6 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
         tma_store_1d_sync_hint(a.out + s0, img + (s0 - v0), (unsigned)((s1 - s0) * 8), l2_evict_first());
       else
         tma_store_1d_sync(a.out + s0, img + (s0 - v0), (unsigned)((s1 - s0) * 8));
-    }
-  }
-  if constexpr (FLAGS) {
-    // every CTA of this grid has read gen once the counter completes
-    if (tid == 0 && atomicAdd(&o.sync->finished, 1) == (int)gridDim.x - 1) {
-      o.sync->finished = 0;
-      atomicAdd(&o.sync->gen, 1);
-      __threadfence();
     }
   }
 }
@@ -425,53 +363,7 @@ __global__ void k_range_span(int64_t n_nodes, int npc, int d2, const int64_t* __
   atomicMax(out + 1, mi);
 }
 
-// largest element touching each node chunk (items are sorted, so a node's
-// last item holds its largest element)
-__global__ void k_chunk_emax(int64_t n_nodes, int np, int64_t nodes_per_chunk,
-                             const int64_t* __restrict__ n2e_ptr, const int32_t* __restrict__ n2e,
-                             unsigned long long* emax) {
-  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < n_nodes;
-       a += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t hi = n2e_ptr[a + 1];
-    if (hi > n2e_ptr[a]) atomicMax(emax + a / nodes_per_chunk, (unsigned long long)(n2e[hi - 1] / np));
-  }
-}
-
 }  // namespace
-
-// Split the nodes into n_chunks ranges aligned to the row-stream CTA size and
-// the elements so that element chunk k holds exactly the elements the rows of
-// node chunk k need beyond chunks < k (monotone by construction).
-int plan_chunks(int64_t n_nodes, int64_t n_elements, int np, const int64_t* n2e_ptr,
-                const int32_t* n2e, int npc, int n_chunks, int64_t* nchunk, int64_t* echunk,
-                cudaStream_t st) {
-  int64_t per = ((n_nodes + n_chunks - 1) / n_chunks + npc - 1) / npc * npc;
-  if (per < npc) per = npc;
-  n_chunks = (int)((n_nodes + per - 1) / per);
-  unsigned long long* d = nullptr;
-  unsigned long long h[64];
-  // returns -1 (message set) on failure: the chunk count is the success value
-  if (cudaMalloc(&d, sizeof(unsigned long long) * n_chunks) != cudaSuccess ||
-      cudaMemsetAsync(d, 0, sizeof(unsigned long long) * n_chunks, st) != cudaSuccess)
-    return cuda_fail(cudaGetLastError(), "plan_chunks"), -1;
-  k_chunk_emax<<<256, 256, 0, st>>>(n_nodes, np, per, n2e_ptr, n2e, d);
-  if (cudaMemcpyAsync(h, d, sizeof(unsigned long long) * n_chunks, cudaMemcpyDeviceToHost, st) !=
-          cudaSuccess ||
-      cudaStreamSynchronize(st) != cudaSuccess) {
-    cudaFree(d);
-    return cuda_fail(cudaGetLastError(), "plan_chunks"), -1;
-  }
-  cudaFree(d);
-  nchunk[0] = 0;
-  echunk[0] = 0;
-  int64_t run = 0;
-  for (int k = 0; k < n_chunks; ++k) {
-    nchunk[k + 1] = std::min<int64_t>(n_nodes, (int64_t)(k + 1) * per);
-    run = std::max<int64_t>(run, (int64_t)h[k] + 1);
-    echunk[k + 1] = k + 1 == n_chunks ? n_elements : std::min<int64_t>(run, n_elements);
-  }
-  return n_chunks;
-}
 
 size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements) {
   size_t nb = 0;
@@ -480,112 +372,6 @@ size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements) {
     nb = (size_t)NP * (NP + 1) / 2 * decltype(D)::value * decltype(D)::value;
   });
   return nb * (size_t)n_elements;
-}
-
-// Row-stream CTA order along a space-filling curve.  A node range's K
-// values are contiguous whatever order the ranges run in, but the element
-// records it reads are shared with the ranges of the neighbouring node rows
-// and planes: in node order those sit a whole plane of K apart, too far for
-// the records to stay in L2 (cfg5: 15 KB per Q2-20 record, 8 GB of records
-// re-read).  Ordering the ranges by the Morton code of their first node's
-// coordinates (normalised to the mesh box) runs geometric neighbours
-// together, so a record's readers meet while it is L2-resident.  Generic: it
-// uses only the coordinates, not the structured numbering.
-__global__ void k_coord_box(int64_t n, int dim, const double* __restrict__ coord, double* box) {
-  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-  for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < n; a += (int64_t)gridDim.x * blockDim.x)
-    for (int d = 0; d < dim; ++d) {
-      const double x = coord[a * dim + d];
-      lo[d] = fmin(lo[d], x);
-      hi[d] = fmax(hi[d], x);
-    }
-  for (int d = 0; d < dim; ++d)
-    for (int o = 16; o > 0; o >>= 1) {
-      lo[d] = fmin(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
-      hi[d] = fmax(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
-    }
-  if ((threadIdx.x & 31) == 0) {
-    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    for (int d = 0; d < dim; ++d) {
-      box[w * 6 + d] = lo[d];
-      box[w * 6 + 3 + d] = hi[d];
-    }
-  }
-}
-
-__device__ __forceinline__ uint64_t spread3(uint64_t v) {  // 21 bits -> every third bit
-  v &= 0x1fffff;
-  v = (v | v << 32) & 0x1f00000000ffffull;
-  v = (v | v << 16) & 0x1f0000ff0000ffull;
-  v = (v | v << 8) & 0x100f00f00f00f00full;
-  v = (v | v << 4) & 0x10c30c30c30c30c3ull;
-  v = (v | v << 2) & 0x1249249249249249ull;
-  return v;
-}
-__device__ __forceinline__ uint64_t spread2(uint64_t v) {  // 32 bits -> every second bit
-  v &= 0xffffffffull;
-  v = (v | v << 16) & 0x0000ffff0000ffffull;
-  v = (v | v << 8) & 0x00ff00ff00ff00ffull;
-  v = (v | v << 4) & 0x0f0f0f0f0f0f0f0full;
-  v = (v | v << 2) & 0x3333333333333333ull;
-  v = (v | v << 1) & 0x5555555555555555ull;
-  return v;
-}
-
-__global__ void k_range_keys(int64_t n_nodes, int npc, int dim, const double* __restrict__ coord,
-                             const double* __restrict__ box, uint64_t* keys) {
-  const int64_t n_ranges = (n_nodes + npc - 1) / npc;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_ranges;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t a = r * npc;
-    uint64_t q[3] = {0, 0, 0};
-    const double scale = dim == 3 ? 2097151.0 : 4294967295.0;
-    for (int d = 0; d < dim; ++d) {
-      const double ext = box[3 + d] - box[d];
-      const double t = ext > 0 ? (coord[a * dim + d] - box[d]) / ext : 0.0;
-      q[d] = (uint64_t)fmin(fmax(t * scale, 0.0), scale);
-    }
-    keys[r] = dim == 3 ? (spread3(q[0]) | spread3(q[1]) << 1 | spread3(q[2]) << 2)
-                       : (spread2(q[0]) | spread2(q[1]) << 1);
-  }
-}
-
-int plan_range_order(int64_t n_nodes, int dim, int npc, const double* coord, cudaStream_t st,
-                     int32_t** order_out) {
-  *order_out = nullptr;
-  const int64_t n_ranges = (n_nodes + npc - 1) / npc;
-  if (n_ranges <= 1 || n_ranges >= INT32_MAX || !coord) return 0;
-  constexpr int B = 256, T = 256, WARPS = B * T / 32;
-  double* box = nullptr;
-  uint64_t* keys = nullptr;
-  EPFEM_CUDA_TRY(cudaMalloc(&box, sizeof(double) * 6 * WARPS));
-  EPFEM_CUDA_TRY(cudaMalloc(&keys, sizeof(uint64_t) * n_ranges));
-  k_coord_box<<<B, T, 0, st>>>(n_nodes, dim, coord, box);
-  std::vector<double> hb(6 * WARPS);
-  EPFEM_CUDA_TRY(cudaMemcpyAsync(hb.data(), box, sizeof(double) * hb.size(), cudaMemcpyDeviceToHost, st));
-  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
-  double g[6] = {1e300, 1e300, 1e300, -1e300, -1e300, -1e300};
-  for (int w = 0; w < WARPS; ++w)
-    for (int d = 0; d < dim; ++d) {
-      g[d] = std::min(g[d], hb[w * 6 + d]);
-      g[3 + d] = std::max(g[3 + d], hb[w * 6 + 3 + d]);
-    }
-  EPFEM_CUDA_TRY(cudaMemcpyAsync(box, g, sizeof(g), cudaMemcpyHostToDevice, st));
-  k_range_keys<<<256, 256, 0, st>>>(n_nodes, npc, dim, coord, box, keys);
-  std::vector<uint64_t> hk(n_ranges);
-  EPFEM_CUDA_TRY(cudaMemcpyAsync(hk.data(), keys, sizeof(uint64_t) * n_ranges, cudaMemcpyDeviceToHost, st));
-  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
-  cudaFree(box);
-  cudaFree(keys);
-  std::vector<int32_t> order(n_ranges);
-  for (int64_t r = 0; r < n_ranges; ++r) order[r] = (int32_t)r;
-  std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return hk[x] < hk[y]; });
-  int32_t* d = nullptr;
-  EPFEM_CUDA_TRY(cudaMalloc(&d, sizeof(int32_t) * n_ranges));
-  EPFEM_CUDA_TRY(cudaMemcpyAsync(d, order.data(), sizeof(int32_t) * n_ranges, cudaMemcpyHostToDevice, st));
-  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
-  *order_out = d;
-  return 0;
 }
 
 // Nodes per CTA for the row stream: the largest power of two <= 64 whose
@@ -619,6 +405,11 @@ int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int6
   return 0;
 }
 
+// dynamic shared memory of one node range: image + items + node offsets
+static size_t row_range_smem(const GatherArgs& a) {
+  return sizeof(double) * ((size_t)a.max_span + 2) + sizeof(int) * ((size_t)a.max_items + 2 * ((size_t)a.npc + 1));
+}
+
 int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st) {
   if (a.n_nodes == 0) return 0;
   int rc = 0;
@@ -627,8 +418,8 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
     constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
     const int64_t rblocks = (a.n_end - a.n_begin + a.npc - 1) / a.npc;
     if (rblocks <= 0) return;
-    const size_t smem = row_range_smem(a) + (a.F_out ? 16 + sizeof(double) * DIM * (size_t)a.max_items : 0);
-    auto kern = a.F_out ? k_row_stream<DIM, NP, NQ, false, true> : k_row_stream<DIM, NP, NQ>;
+    const size_t smem = row_range_smem(a);
+    auto kern = k_row_stream<DIM, NP, NQ>;
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) { rc = cuda_fail(e, "cudaFuncSetAttribute"); return; }
@@ -652,51 +443,8 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    GatherArgs b = a;
-    if (a.n_begin != 0 || a.n_end != a.n_nodes) b.range_order = nullptr;  // the order covers whole-mesh launches
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, b, a.npc, OvlArgs{});
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, a.npc);
     if (e != cudaSuccess) rc = cuda_fail(e, "row stream launch");
-  });
-  if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
-  if (rc) return rc;
-  EPFEM_CUDA_TRY(cudaGetLastError());
-  return 0;
-}
-
-// Row stream of the overlapped step: PDL launch (its CTAs start once every
-// producer CTA has started) waiting on per-group flags (k_row_stream<FLAGS>).
-int launch_row_stream_ovl(int family, int dim, const GatherArgs& a, const OvlArgs& o, cudaStream_t st) {
-  if (a.n_nodes == 0) return 0;
-  int rc = 0;
-  bool ok = dispatch_element(family, dim, [&](auto F, auto D) {
-    constexpr int DIM = decltype(D)::value;
-    constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
-    if constexpr (DIM == 2) {
-      const int64_t rblocks = (a.n_nodes + a.npc - 1) / a.npc;
-      const size_t smem = sizeof(double) * ((size_t)a.max_span + 2) +
-                          sizeof(int) * ((size_t)a.max_items + 2 * ((size_t)a.npc + 1));
-      auto kern = k_row_stream<DIM, NP, NQ, true>;
-      if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) { rc = cuda_fail(e, "cudaFuncSetAttribute"); return; }
-      }
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)rblocks);
-      cfg.blockDim = dim3(kStreamThreads);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = st;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[0].val.programmaticStreamSerializationAllowed = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      GatherArgs b = a;
-      b.range_order = nullptr;  // flags are ordered by node range
-      cudaError_t e = cudaLaunchKernelEx(&cfg, kern, b, a.npc, o);
-      if (e != cudaSuccess) rc = cuda_fail(e, "overlapped row stream launch");
-    } else {
-      rc = fail(EPFEM_ERR_INVALID, "overlapped step: 2D meshes only");
-    }
   });
   if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
   if (rc) return rc;

@@ -178,8 +178,9 @@ class DistributedTangent:
         self.mat_ext = mat_factory(n_ext)
         self.cache = api.build_assembly_cache(api.Mesh.from_structured(plan.mesh, device), self.mat_ext)
         p0, p1 = plan.own_points
-        self.mat_own = mat_factory(p1 - p0)
-        self._mat_factory = mat_factory
+        # own points' material = the extended field's [p0, p1) slice (per-point
+        # arrays sliced, not rebuilt)
+        self.mat_own = self.mat_ext.slice(p0, p1)
         self.ctx = api.Context(device.index or 0, synchronous=False)
         self.S = torch.empty((n_ext, 6), dtype=torch.float64, device=device)
         self.flags = torch.zeros((n_ext,), dtype=torch.uint8, device=device)
@@ -223,7 +224,7 @@ class DistributedTangent:
         out = api.L.ConstitutiveOut()
         out.S, out.flags, out.D = (api._ptr(self.S[q0:q1]), api._ptr(self.flags[q0:q1]),
                                    api._ptr(self.D[q0:q1]))
-        mat = self.mat_own if (o0, o1) == (0, self.mat_own.n_int) else self._mat_part(o1 - o0)
+        mat = self.mat_own if (o0, o1) == (0, self.mat_own.n_int) else self._mat_part(o0, o1)
         mv = mat.view()
         sl = (lambda x: None if x is None else x[o0:o1])
         self.ctx.use_current_stream()
@@ -231,11 +232,12 @@ class DistributedTangent:
             self.ctx.handle, self.cache.handle, C.byref(mv), api._ptr(sl(E_own)), api._ptr(sl(Ep_own)),
             api._ptr(sl(Hard_own)), C.byref(out), e0, e1))
 
-    def _mat_part(self, n):
+    def _mat_part(self, o0, o1):
+        """The own material of own points [o0, o1) (per-point arrays sliced)."""
         cache = self.__dict__.setdefault("_mat_parts", {})
-        if n not in cache:
-            cache[n] = self._mat_factory(n)
-        return cache[n]
+        if (o0, o1) not in cache:
+            cache[(o0, o1)] = self.mat_own.slice(o0, o1)
+        return cache[(o0, o1)]
 
     def assemble(self):
         from . import api

@@ -3,7 +3,7 @@ driver, like the reference): ``external_forces`` (proj/src/assembly.cpp:231-296)
 with a volume force at the volume quadrature points (weights |det J| w_q from
 the device cache) and a traction on the mesh's Neumann faces with the face
 rule and the face restriction of the basis (reference_elements.cpp:87-115,
-117-135,196-244,392-412,466-498); ``boundary_faces`` (mesh.cpp:294-310).
+117-135,196-244,392-412,466-498); ``boundary_faces`` (mesh.cpp:293-310).
 
 2D faces are segments (Gauss rules, segment basis); 3D faces use the 2D
 volume rule and basis of the same family (triangles for tetrahedra,
@@ -21,7 +21,7 @@ from .mesh import StructuredMesh
 
 ForceField = Callable[[np.ndarray], np.ndarray]  # x (n, dim) -> value (n, dim)
 
-# face_nodes (reference_elements.cpp:466-498), 2D
+# face_nodes (reference_elements.cpp:466-494), 2D
 FACE_NODES_2D = {
     "P1": [[0, 1], [1, 2], [2, 0]],
     "P2": [[0, 1, 3], [1, 2, 4], [2, 0, 5]],
@@ -38,7 +38,7 @@ FACE_NODES_3D = {
 
 
 def face_nodes(family: str, dim: int) -> list:
-    """face_nodes (reference_elements.cpp:466-498)."""
+    """face_nodes (reference_elements.cpp:466-494)."""
     return (FACE_NODES_2D if dim == 2 else FACE_NODES_3D)[family]
 
 
@@ -78,7 +78,7 @@ def _segment_basis(order: int, x: np.ndarray):
 
 
 def volume_rule_2d(family: str):
-    """quadrature_volume (reference_elements.cpp:345-372) in 2D: points (2, n_q), weights."""
+    """quadrature_volume (reference_elements.cpp:345-374) in 2D: points (2, n_q), weights."""
     if family == "P1":
         return np.full((2, 1), 1.0 / 3.0), np.array([0.5])
     if family == "P2":
@@ -195,7 +195,7 @@ def volume_basis_values_3d(family: str, pts: np.ndarray) -> np.ndarray:
 
 
 def boundary_faces(mesh: StructuredMesh) -> list:
-    """boundary_faces (mesh.cpp:294-310): the (element, face) pairs whose node
+    """boundary_faces (mesh.cpp:293-310): the (element, face) pairs whose node
     set occurs once, sorted."""
     faces = face_nodes(mesh.elem_type.family, mesh.dim)
     table = {}

@@ -1,6 +1,6 @@
 """The semismooth-Newton time step on the GPU:
 ``newton_solve`` mirrors proj/src/solver.cpp:7-62 and proj/include/epfem/solver.hpp,
-``restricted_solve`` / ``energy_norm`` mirror proj/src/linalg.cpp:37-127.
+``restricted_solve`` / ``energy_norm`` mirror proj/src/linalg.cpp:69-121.
 
 Every iteration stays on the device: strains E = B u (K8), the step with its
 internal forces (constitutive update, tangent K, F = B^T (w S);
@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import warnings
 from dataclasses import dataclass, field
 from typing import List, Optional
 
@@ -43,8 +44,13 @@ class LinearSolver(enum.Enum):
 
 @dataclass
 class SolveSettings:
-    """linalg.hpp:19-22.  ``direct`` is served by the same device CG (no
-    device sparse factorisation here); the tolerance contract is the same."""
+    """linalg.hpp:19-22.  ``direct`` (the reference's SimplicialLDLT +
+    refinement sweeps, linalg.cpp:84-96) has no device counterpart here: the
+    same Jacobi CG runs under the same tolerance contract, with a warning
+    (once per process) and ``SolveInfo.substituted`` / the time-step record's
+    ``direct_substituted`` saying so.  Near a limit load CG may then need many
+    more iterations than the direct solve, or fail the tolerance where
+    LDLT + refinement would pass."""
     method: LinearSolver = LinearSolver.direct
     rel_tol: float = 1e-10
 
@@ -77,6 +83,7 @@ class TimeStepRecord:
     iterations: List[IterationSample] = field(default_factory=list)
     linear_iters: List[int] = field(default_factory=list)
     ratios: List[float] = field(default_factory=list)  # |du|_e / (|u_prev|_e + |u|_e) per iteration
+    direct_substituted: bool = False  # LinearSolver.direct requested: Jacobi CG stood in
 
 
 @dataclass
@@ -99,20 +106,30 @@ class SolveInfo:
     """What a restricted_solve did: CG iterations and the true relative residual."""
     iterations: int = 0
     residual: float = 0.0
+    substituted: bool = False  # LinearSolver.direct requested, CG ran
+
+
+_warned_direct = False
 
 
 def restricted_solve(K: CsrMatrix, rhs: torch.Tensor, free_mask: Optional[torch.Tensor] = None,
                      settings: SolveSettings = SolveSettings(), ctx=None,
                      info: Optional[SolveInfo] = None, block: int = 1) -> torch.Tensor:
-    """Solve K[free, free] x = rhs[free]; x is zero on fixed dofs (linalg.cpp:83-121).
+    """Solve K[free, free] x = rhs[free]; x is zero on fixed dofs (linalg.cpp:69-115).
     Raises SolverError with the reference's message above tolerance; `info`
     (optional) receives the iteration count and the residual.  ``block`` > 1
     (the mesh dimension) uses the node-block Jacobi preconditioner
     (epfem_restricted_solve_blocked) instead of the scalar one."""
+    global _warned_direct
     from .api import default_context
     n = K.n
     if rhs.numel() != n:
         raise Error("restricted_solve: dimension mismatch")
+    substituted = settings.method == LinearSolver.direct
+    if substituted and not _warned_direct:
+        _warned_direct = True
+        warnings.warn("restricted_solve: LinearSolver.direct (SimplicialLDLT) has no device implementation; "
+                      "Jacobi-preconditioned CG runs under the same tolerance", RuntimeWarning, stacklevel=2)
     dev = K.values.device
     ctx = ctx or default_context(dev)
     ctx.use_current_stream()
@@ -123,7 +140,7 @@ def restricted_solve(K: CsrMatrix, rhs: torch.Tensor, free_mask: Optional[torch.
                                                 _ptr(_mask_u8(free_mask, n, dev)), settings.rel_tol, 0, int(block),
                                                 _ptr(x), C.byref(it), C.byref(res))
     if info is not None:
-        info.iterations, info.residual = it.value, res.value
+        info.iterations, info.residual, info.substituted = it.value, res.value, substituted
     if rc == 7:  # EPFEM_ERR_SOLVER
         raise SolverError(L.last_error(), res.value)
     if rc != 0:
@@ -132,7 +149,7 @@ def restricted_solve(K: CsrMatrix, rhs: torch.Tensor, free_mask: Optional[torch.
 
 
 def energy_norm(K: CsrMatrix, v: torch.Tensor, ctx=None) -> float:
-    """sqrt(max(v . K v, 0)) (linalg.cpp:123-127)."""
+    """sqrt(max(v . K v, 0)) (linalg.cpp:117-121)."""
     from .api import default_context
     if v.numel() != K.n:
         raise Error("energy_norm: dimension mismatch")
@@ -187,6 +204,7 @@ def newton_solve(cache: AssemblyCache, mat: MaterialField, state_prev: Integrati
         n_pl = int((flags & 1).sum().item())
         rec.iterations.append(IterationSample(n_pl, t0.elapsed_time(t1) * 1e-3))
         rec.linear_iters.append(lin.iterations)
+        rec.direct_substituted = rec.direct_substituted or lin.substituted
         rec.tangent_seconds += rec.iterations[-1].tangent_seconds
         rec.newton_iters = it
         norm_prev = energy_norm(Ke, u, ctx=eng.ctx)

@@ -77,7 +77,7 @@ T3 hooke(double K, double G, const T3& eps) {
   return lin(1.0, eye(K * tr(eps)), 2.0 * G, devi(eps));
 }
 
-// Voigt deviatoric operator times a vector (voigt.hpp:62-69) used only to
+// Voigt deviatoric operator times a vector (voigt.hpp:24-31) used only to
 // build the deviatoric back-stress inputs the reference test draws.
 void dev_mul(const double* v, double* out) {
   for (int i = 0; i < 6; ++i) {

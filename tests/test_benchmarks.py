@@ -1,6 +1,6 @@
 """The strip-footing benchmark: the mesh and its
 Dirichlet data against the reference's per-node constraint loop
-(mesh.cpp:262-293) restated over the oracle's mesh numbering (CPU), and the
+(mesh.cpp:260-291) restated over the oracle's mesh numbering (CPU), and the
 load driver run_dp_footing (benchmarks.cpp:120-205) on the GPU against the
 same driver restated on the oracle with the reference's direct solves."""
 import math
@@ -12,7 +12,7 @@ torch = pytest.importorskip("torch")
 
 
 def _footing_ref(O, level, family, dim, layers=-1):
-    """mesh.cpp:262-293 restated per node, in the reference's call order
+    """mesh.cpp:260-291 restated per node, in the reference's call order
     (a later constrain on the same dof overrides an earlier one)."""
     cells = (5 if family in ("P2", "Q2") else 10) << level
     h = 10.0 / cells
@@ -397,7 +397,7 @@ def test_mesh_text_format_and_errors(tmp_path):
 
 @pytest.mark.parametrize("family,dim", [("P1", 2), ("Q2", 2), ("P2", 3), ("Q2", 3)])
 def test_boundary_nodes_of_a_box(family, dim):
-    """boundary_faces / boundary_nodes (mesh.cpp:294-321) on a structured box:
+    """boundary_faces / boundary_nodes (mesh.cpp:293-321) on a structured box:
     the boundary nodes are exactly those on the box's faces, and every
     boundary face lies in one of them."""
     import paper_1805_04155_b200 as P

@@ -320,36 +320,6 @@ def test_config_pipeline_vs_oracle(cuda, oracle, name):
     assert np.array_equal(_np(K2).view(np.uint64), _np(eng.K).view(np.uint64))
 
 
-@pytest.mark.parametrize("name,chunks", [("cfg2", 5), ("cfg3", 3), ("cfg4", 4), ("cfg5", 2)])
-def test_overlapped_chunked_step_is_bitwise_identical(cuda, name, chunks, monkeypatch):
-    """The two-stream chunked schedule (fused chunk k || row chunk k-1) gives
-    the same bits as the single-launch step."""
-    import paper_1805_04155_b200 as P
-    from paper_1805_04155_b200.synthetic import CONFIGS, calibrate, displacement
-    cfg = CONFIGS[name]
-    mesh = cfg.mesh(REDUCED[name] * 2 if cfg.dim == 2 else REDUCED[name])
-    mat = cfg.material(mesh.n_int)
-    monkeypatch.setenv("EPFEM_CHUNKS", "1")
-    c1 = P.build_assembly_cache(P.Mesh.from_structured(mesh, cuda), mat)
-    monkeypatch.setenv("EPFEM_CHUNKS", str(chunks))
-    ck = P.build_assembly_cache(P.Mesh.from_structured(mesh, cuda), mat)
-    E1 = c1.strains(torch.from_numpy(displacement(mesh.coord, cfg.seed)).to(cuda))
-    s, frac = calibrate(E1, mat, 0.4)
-    E = (s * E1).contiguous()
-    e1, ek = P.TangentEngine(c1, mat), P.TangentEngine(ck, mat)
-    S1, f1, D1, K1 = e1.step(E)
-    Sk, fk, Dk, Kk = ek.step(E)
-    torch.cuda.synchronize()
-    assert 0.2 < frac < 0.6
-    assert np.array_equal(_np(f1), _np(fk)) and np.array_equal(_np(S1), _np(Sk))
-    assert np.array_equal(_np(K1).view(np.uint64), _np(Kk).view(np.uint64))
-    # and the graph-captured overlapped step replays to the same bits
-    ek.capture(E)
-    ek.replay()
-    torch.cuda.synchronize()
-    assert np.array_equal(_np(ek.K).view(np.uint64), _np(K1).view(np.uint64))
-
-
 @pytest.mark.parametrize("name", ["cfg2", "cfg4"])
 def test_slab_data_path_on_one_rank(cuda, name):
     """dist.DistributedTangent (K1 on own points, exchange, tangent on the
@@ -474,26 +444,14 @@ def test_full_size_pattern_and_properties(cuda, name):
 
 
 # ---------------------------------------------------------------------------
-# opt-in kernel variants (EPFEM_FUSED, read once per process): each in a
-# fresh interpreter, same bar as the default path
-@pytest.mark.parametrize("variant,name", [("mma", "cfg2"), ("mma", "cfg3"), ("mma", "cfg4"), ("ws", "cfg2"), ("cta", "cfg3"), ("pf", "cfg2"),
-                                          ("cta", "cfg2"), ("pipe", "cfg2"), ("pipe", "cfg4"),
-                                          ("MEGA=1", "cfg2"), ("MEGA=1,MEGA_SLACK=0", "cfg2"),
-                                          ("MEGA=1,MEGA_SLACK=4", "cfg2"), ("OVL=1", "cfg2"),
-                                          ("OVL=1,OVL_CTAS=1", "cfg2")])
-def test_kernel_variants(cuda, oracle, variant, name):
-    """EPFEM_FUSED variants; the one-launch step (MEGA=1), also with a small
-    MEGA_SLACK (node ranges right behind their producer groups in the walk,
-    so they wait on the ready flags); the overlapped two-kernel step (OVL=1),
-    also with one producer CTA per SM (row-stream CTAs far ahead of the
-    producers: flag waits)."""
+# the opt-in FP64 tensor-pipe phase 2 (EPFEM_FUSED=mma, read once per
+# process): in a fresh interpreter, same bar as the default path
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4", "cfg5"])
+def test_mma_phase2(cuda, oracle, name):
     import subprocess
     import sys
-    if "=" in variant:
-        env = dict(os.environ, **{"EPFEM_" + kv.split("=")[0]: kv.split("=")[1] for kv in variant.split(",")})
-    else:
-        env = dict(os.environ, EPFEM_FUSED=variant)
-    n = {"cfg2": 24, "cfg3": 4, "cfg4": 6}[name]
+    env = dict(os.environ, EPFEM_FUSED="mma")
+    n = {"cfg2": 24, "cfg3": 4, "cfg4": 6, "cfg5": 3}[name]
     r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "variant_check.py"), name,
                         str(n)], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
@@ -544,16 +502,13 @@ def test_elastic_assembly_both_paths(cuda, oracle, k5):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("fused", ["0", "1"])
 @pytest.mark.parametrize("name", ["cfg2", "cfg1", "cfg3", "cfg4", "cfg5"])
-def test_newton_step_with_internal_forces(cuda, oracle, name, fused, monkeypatch):
+def test_newton_step_with_internal_forces(cuda, oracle, name):
     """epfem_newton_step_f (fused in 2D): S, flags, D
     and K are the bits of epfem_newton_step, F the bits of K9
     (epfem_internal_forces on the step's S), and F matches the oracle's
-    internal_forces (assembly.cpp:215-225) within 1e-12 of max |F|; for the
-    default (step + two-pass K9) and the fused 2D form (EPFEM_FORCES_FUSED)."""
+    internal_forces (assembly.cpp:215-225) within 1e-12 of max |F|."""
     import paper_1805_04155_b200 as P
-    monkeypatch.setenv("EPFEM_FORCES_FUSED", fused)
     from paper_1805_04155_b200.synthetic import CONFIGS, calibrate, displacement
     cfg = CONFIGS[name]
     mesh = cfg.mesh(REDUCED[name])
