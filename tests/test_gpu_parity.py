@@ -399,51 +399,6 @@ def test_slab_ranks_emulated_in_one_process(cuda, name, world):
 
 
 # ---------------------------------------------------------------------------
-# full-size configurations: size-independent properties
-
-FULL_NNZ = {"cfg1": 1_841_156, "cfg2": 49_315_844, "cfg3": 547_739_145,
-            "cfg4": 1_001_561_769, "cfg5": 2_118_711_609}
-
-
-@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
-def test_full_size_pattern_and_properties(cuda, name):
-    import paper_1805_04155_b200 as P
-    from paper_1805_04155_b200.synthetic import CONFIGS, make_workload
-    cfg = CONFIGS[name]
-    target = {"cfg4": 0.25, "cfg5": 0.5}.get(name)
-    wl = make_workload(cfg, target=target, device=cuda)
-    gc = wl.cache
-    assert gc.nnz == FULL_NNZ[name]
-    rp = gc.row_ptr
-    assert int(rp[0]) == 0 and int(rp[-1]) == gc.nnz and bool((rp[1:] >= rp[:-1]).all())
-    # columns sorted ascending within each row
-    ci = gc.col_idx.long()
-    starts = torch.zeros(gc.nnz, dtype=torch.bool, device=cuda)
-    starts[rp[:-1].clamp(max=gc.nnz - 1)] = True
-    assert bool(((ci[1:] > ci[:-1]) | starts[1:]).all())
-    # rigid translation in the nullspace of K_elast; K_elast symmetric
-    Kel = gc.K_elast
-    scale = float(Kel.values.abs().max())
-    ones = torch.ones(gc.info.n_dofs, dtype=torch.float64, device=cuda)
-    assert float(Kel.matvec(ones).abs().max()) <= 1e-9 * scale
-    x = torch.randn(gc.info.n_dofs, dtype=torch.float64, device=cuda)
-    y = torch.randn(gc.info.n_dofs, dtype=torch.float64, device=cuda)
-    lhs, rhs = float(y @ Kel.matvec(x)), float(x @ Kel.matvec(y))
-    assert abs(lhs - rhs) <= 1e-9 * max(abs(lhs), 1.0)
-    if cfg.model == "elastic":
-        return
-    eng = P.TangentEngine(gc, wl.mat)
-    S, flags, D, Kv = eng.step(wl.E)
-    eng.sync()
-    frac = float((flags & 1).double().mean())
-    assert abs(frac - wl.fraction) < 1e-12
-    # tangent symmetric too, and rows without plastic neighbours equal K_elast bitwise
-    Kt = P.CsrMatrix(gc.row_ptr, gc.col_idx, Kv)
-    lhs, rhs = float(y @ Kt.matvec(x)), float(x @ Kt.matvec(y))
-    assert abs(lhs - rhs) <= 1e-9 * max(abs(lhs), 1.0)
-
-
-# ---------------------------------------------------------------------------
 # the opt-in FP64 tensor-pipe phase 2 (EPFEM_FUSED=mma, read once per
 # process): in a fresh interpreter, same bar as the default path
 @pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4", "cfg5"])
