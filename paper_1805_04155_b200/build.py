@@ -55,7 +55,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     os.makedirs(LIBDIR, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "epfem_gpu.h")]
-    objs = []
+    objs, jobs = [], []
     for src, extra in SOURCES.items():
         path = os.path.join(CSRC, src)
         obj = os.path.join(OBJ, src + ".o")
@@ -69,7 +69,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 cmd = [nvcc()] + NVCC_COMMON + extra + ["-c", path, "-o", obj]
             if verbose:
                 print(" ".join(cmd), flush=True)
-            subprocess.check_call(cmd)
+            jobs.append((cmd, subprocess.Popen(cmd)))
+    # the translation units compile in parallel
+    failed = [cmd for cmd, p in jobs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, failed[0])
     if force or _stale(LIB, objs):
         cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart_static"]
         if verbose:

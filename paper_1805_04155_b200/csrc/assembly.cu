@@ -48,56 +48,13 @@ __global__ void k_jacobians(int64_t n_e, const int32_t* __restrict__ elem,
        m += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = m / NQ;
     const int q = (int)(m - e * NQ);
-    double J[DIM][DIM];
-#pragma unroll
-    for (int i = 0; i < DIM; ++i)
-#pragma unroll
-      for (int j = 0; j < DIM; ++j) J[i][j] = 0.0;
-#pragma unroll 4
-    for (int p = 0; p < NP; ++p) {
-      const int32_t node = __ldg(elem + e * NP + p);
-      double x[DIM];
-#pragma unroll
-      for (int j = 0; j < DIM; ++j) x[j] = __ldg(coord + (int64_t)DIM * node + j);
-#pragma unroll
-      for (int i = 0; i < DIM; ++i) {
-        const double g = __ldg(gradhat + (q * NP + p) * DIM + i);
-#pragma unroll
-        for (int j = 0; j < DIM; ++j) J[i][j] += g * x[j];
-      }
-    }
+    const int32_t* en = elem + e * NP;
     double* inv = inv_out + m * DIM * DIM;
-    double det;
-    if constexpr (DIM == 3) {
-      det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) -
-            J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
-            J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
-      // cofactor inverse (Eigen's compute_inverse_size3)
-      double cof[3][3];
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const int i1 = (i + 1) % 3, i2 = (i + 2) % 3, j1 = (j + 1) % 3, j2 = (j + 2) % 3;
-          cof[i][j] = J[i1][j1] * J[i2][j2] - J[i1][j2] * J[i2][j1];
-        }
-      const double d2 = cof[0][0] * J[0][0] + cof[1][0] * J[1][0] + cof[2][0] * J[2][0];
-      const double invdet = 1.0 / d2;
-#pragma unroll
-      for (int i = 0; i < 3; ++i)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) inv[j * 3 + i] = cof[j][i] * invdet;
-    } else {
-      det = J[0][0] * J[1][1] - J[1][0] * J[0][1];
-      const double invdet = 1.0 / det;
-      inv[0] = J[1][1] * invdet;
-      inv[1] = -J[1][0] * invdet;
-      inv[2] = -J[0][1] * invdet;
-      inv[3] = J[0][0] * invdet;
-    }
+    const double det = point_geometry<DIM, NP>(
+        [&](int p, int j) { return __ldg(coord + (int64_t)DIM * __ldg(en + p) + j); }, gradhat, q, inv);
     if (!(det > 0.0)) raise_dev(err, EPFEM_ERR_DEGENERATE, (unsigned long long)e);
     det_out[m] = det;
-    weight[m] = fabs(det) * __ldg(wq + q);
+    weight[m] = __dmul_rn(fabs(det), __ldg(wq + q));
   }
 }
 

@@ -87,6 +87,66 @@ __device__ __forceinline__ constexpr int arow(int r) {
   return (DIM == 2 && r == 2) ? 3 : r;
 }
 
+// Geometry at one integration point from the element's nodal coordinates
+// (jacobians, assembly.cpp:20-61): J(i, j) = sum_p ghat_i(p, q) x_p(j) in
+// node order, det J by the first-row cofactor expansion and J^-1 by Eigen's
+// cofactor inverse (compute_inverse_size3), each product and sum rounded
+// separately in the reference's evaluation order (the reference's Release
+// x86-64 build has no FMA).  Used by the one-time geometry kernel and, with
+// the same bits, by kernels that form J^-1 on the fly.  `inv` is column-major
+// dim x dim like JacobianData::inv; returns det J.  `xs(p, j)` gives
+// coordinate j of local node p.
+template <int DIM, int NP, class X>
+__device__ __forceinline__ double point_geometry(X&& xs, const double* __restrict__ gradhat, int q, double* inv) {
+  double J[DIM][DIM];
+#pragma unroll
+  for (int i = 0; i < DIM; ++i)
+#pragma unroll
+    for (int j = 0; j < DIM; ++j) J[i][j] = 0.0;
+#pragma unroll 4
+  for (int p = 0; p < NP; ++p) {
+    double x[DIM], g[DIM];
+#pragma unroll
+    for (int j = 0; j < DIM; ++j) x[j] = xs(p, j);
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) g[i] = __ldg(gradhat + (q * NP + p) * DIM + i);
+#pragma unroll
+    for (int i = 0; i < DIM; ++i)
+#pragma unroll
+      for (int j = 0; j < DIM; ++j) J[i][j] = __dadd_rn(J[i][j], __dmul_rn(g[i], x[j]));
+  }
+  auto mul = [](double a, double b) { return __dmul_rn(a, b); };
+  auto sub = [](double a, double b) { return __dsub_rn(a, b); };
+  double det;
+  if constexpr (DIM == 3) {
+    det = __dadd_rn(sub(mul(J[0][0], sub(mul(J[1][1], J[2][2]), mul(J[1][2], J[2][1]))),
+                        mul(J[0][1], sub(mul(J[1][0], J[2][2]), mul(J[1][2], J[2][0])))),
+                    mul(J[0][2], sub(mul(J[1][0], J[2][1]), mul(J[1][1], J[2][0]))));
+    double cof[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int i1 = (i + 1) % 3, i2 = (i + 2) % 3, j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+        cof[i][j] = sub(mul(J[i1][j1], J[i2][j2]), mul(J[i1][j2], J[i2][j1]));
+      }
+    const double d2 = __dadd_rn(__dadd_rn(mul(cof[0][0], J[0][0]), mul(cof[1][0], J[1][0])), mul(cof[2][0], J[2][0]));
+    const double invdet = __drcp_rn(d2);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) inv[j * 3 + i] = mul(cof[j][i], invdet);
+  } else {
+    det = sub(mul(J[0][0], J[1][1]), mul(J[1][0], J[0][1]));
+    const double invdet = __drcp_rn(det);
+    inv[0] = mul(J[1][1], invdet);
+    inv[1] = mul(-J[1][0], invdet);
+    inv[2] = mul(-J[0][1], invdet);
+    inv[3] = mul(J[0][0], invdet);
+  }
+  return det;
+}
+
 // dphi_p = J^-1 ghat_p for every node of the element at point q.
 template <int DIM, int NP, bool INV_IN_SMEM = false>
 __device__ __forceinline__ void stage_geometry(double* st, const double* inv_m,
