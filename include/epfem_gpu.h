@@ -67,7 +67,8 @@ enum epfem_status {
   EPFEM_ERR_CUDA = 4,           /* CUDA runtime / launch failure */
   EPFEM_ERR_NOMEM = 5,
   EPFEM_ERR_UNSUPPORTED = 6,    /* e.g. node valence > 255 */
-  EPFEM_ERR_SOLVER = 7          /* restricted_solve above tolerance (reference: epfem::SolverError) */
+  EPFEM_ERR_SOLVER = 7,         /* restricted_solve above tolerance (reference: epfem::SolverError) */
+  EPFEM_ERR_NCCL = 8            /* NCCL missing or failed (multi-GPU interface exchange) */
 };
 
 /* epfem::ElementFamily order (reference_elements.hpp:10) */
@@ -242,6 +243,27 @@ int epfem_newton_range(epfem_ctx* ctx, const epfem_cache* cache, const epfem_mat
                        const epfem_constitutive_out* out, int64_t e_begin, int64_t e_end);
 int epfem_delta_range(epfem_ctx* ctx, const epfem_cache* cache, int64_t n_int, const double* D,
                       const uint8_t* flags, int64_t e_begin, int64_t e_end);
+
+/* Multi-GPU: the interface exchange between z-neighbour slabs over NCCL
+ * (the ncclComm_t of §8(b)(1)), for a C / C++ caller with no
+ * torch.  NCCL is loaded at run time (libnccl.so.2); EPFEM_ERR_NCCL when it
+ * is missing or fails.
+ * epfem_nccl_unique_id: 128 bytes (ncclUniqueId) to share from rank 0.
+ * epfem_ctx_attach_nccl: a communicator of `world` ranks on the context's
+ *   device, owned by the context (destroyed with it).
+ * epfem_ctx_set_nccl_comm: use an existing ncclComm_t (not owned).
+ * epfem_exchange_interface: one grouped send/recv on the context's stream:
+ *   points [send_begin, send_end) of `flags` (1 byte per point) and `D`
+ *   (EPFEM_D_STRIDE doubles per point) to rank + 1, points [recv_begin,
+ *   recv_end) from rank - 1 (rank 0 receives nothing, the last rank sends
+ *   nothing).  The sequence per Newton iteration is epfem_newton_range (top
+ *   layer first), epfem_exchange_interface, epfem_newton_range (interior),
+ *   epfem_delta_range (halo), epfem_assemble_rows. */
+int epfem_nccl_unique_id(void* id_out);
+int epfem_ctx_attach_nccl(epfem_ctx* ctx, const void* id, int world, int rank);
+int epfem_ctx_set_nccl_comm(epfem_ctx* ctx, void* nccl_comm, int world, int rank);
+int epfem_exchange_interface(epfem_ctx* ctx, uint8_t* flags, double* D, int64_t send_begin, int64_t send_end,
+                             int64_t recv_begin, int64_t recv_end);
 
 /* K8: E = B u, 2D embedded in Voigt rows {0,1,3} (assembly.cpp:135-146). */
 int epfem_strains(epfem_ctx* ctx, const epfem_cache* cache, const double* u, double* E);

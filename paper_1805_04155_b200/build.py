@@ -32,6 +32,7 @@ SOURCES = {
     "tangent.cu": [],
     "capi.cu": [],
     "solve.cu": [],
+    "exchange.cu": [],
     "tables.cpp": [],
 }
 HEADERS = ["common.cuh", "kernels.cuh", "delta.cuh", "tma.cuh"]
@@ -75,7 +76,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if failed:
         raise subprocess.CalledProcessError(1, failed[0])
     if force or _stale(LIB, objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart_static"]
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart_static", "-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.check_call(cmd)

@@ -36,6 +36,9 @@ struct epfem_ctx {
   cudaStream_t stream = nullptr;
   bool sync = false;
   DevErr* err = nullptr;  // device
+  void* comm = nullptr;   // ncclComm_t of the multi-GPU exchange
+  bool own_comm = false;
+  int world = 1, rank = 0;
 };
 
 struct epfem_cache {
@@ -192,6 +195,7 @@ int epfem_ctx_sync(epfem_ctx* ctx) {
 int epfem_ctx_destroy(epfem_ctx* ctx) {
   if (!ctx) return 0;
   DeviceGuard guard(ctx);
+  if (ctx->own_comm) nccl_comm_destroy(ctx->comm);
   if (ctx->err) cudaFree(ctx->err);
   delete ctx;
   return 0;
@@ -676,6 +680,52 @@ int epfem_delta_range(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int, const
   g.e_begin = e_begin;
   g.e_end = e_end;
   if (int rc = launch_delta(c->info.family, c->info.dim, G_TANGENT_PACKED, g, ctx->stream)) return rc;
+  return finish(ctx);
+}
+
+int epfem_nccl_unique_id(void* id_out) {
+  if (!id_out) return fail(EPFEM_ERR_INVALID, "nccl_unique_id: null argument");
+  return nccl_unique_id(id_out);
+}
+
+int epfem_ctx_attach_nccl(epfem_ctx* ctx, const void* id, int world, int rank) {
+  DeviceGuard guard(ctx);
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!id || world < 1 || rank < 0 || rank >= world) return fail(EPFEM_ERR_INVALID, "attach_nccl: invalid rank / world");
+  void* comm = nullptr;
+  if (int rc = nccl_comm_init(id, world, rank, &comm)) return rc;
+  if (ctx->own_comm) nccl_comm_destroy(ctx->comm);
+  ctx->comm = comm;
+  ctx->own_comm = true;
+  ctx->world = world;
+  ctx->rank = rank;
+  return 0;
+}
+
+int epfem_ctx_set_nccl_comm(epfem_ctx* ctx, void* nccl_comm, int world, int rank) {
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!nccl_comm || world < 1 || rank < 0 || rank >= world)
+    return fail(EPFEM_ERR_INVALID, "set_nccl_comm: invalid communicator / rank / world");
+  if (ctx->own_comm) nccl_comm_destroy(ctx->comm);
+  ctx->comm = nccl_comm;
+  ctx->own_comm = false;
+  ctx->world = world;
+  ctx->rank = rank;
+  return 0;
+}
+
+int epfem_exchange_interface(epfem_ctx* ctx, uint8_t* flags, double* D, int64_t send_begin, int64_t send_end,
+                             int64_t recv_begin, int64_t recv_end) {
+  DeviceGuard guard(ctx);
+  if (int rc = check_ctx(ctx)) return rc;
+  if (!ctx->comm) return fail(EPFEM_ERR_INVALID, "exchange_interface: no NCCL communicator attached");
+  if (send_end < send_begin || recv_end < recv_begin || send_begin < 0 || recv_begin < 0)
+    return fail(EPFEM_ERR_INVALID, "exchange_interface: invalid point range");
+  if ((send_end > send_begin || recv_end > recv_begin) && (!flags || !D))
+    return fail(EPFEM_ERR_INVALID, "exchange_interface: null argument");
+  if (int rc = nccl_exchange(ctx->comm, ctx->world, ctx->rank, ctx->stream, flags, D, send_begin, send_end, recv_begin,
+                             recv_end))
+    return rc;
   return finish(ctx);
 }
 

@@ -91,6 +91,11 @@ int launch_newton_fused_u(int model, int family, int dim, const ConstArgs& c, co
                           cudaStream_t st);  // E = B u inside (GatherArgs::u)
 int launch_newton_fused(int model, int family, int dim, const ConstArgs& c, const GatherArgs& g,
                         cudaStream_t st);
+int nccl_unique_id(void* out);
+int nccl_comm_init(const void* id_bytes, int world, int rank, void** comm_out);
+void nccl_comm_destroy(void* comm);
+int nccl_exchange(void* comm, int world, int rank, cudaStream_t st, uint8_t* flags, double* D, int64_t send_begin,
+                  int64_t send_end, int64_t recv_begin, int64_t recv_end);
 int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, const uint8_t* mask,
              const double* b, double* x_out, double rel_tol, int64_t max_iters, cudaStream_t st,
              int64_t* iters_out, double* residual_out, int block = 1);

@@ -167,12 +167,18 @@ class DistributedTangent:
     """GPU data path of one rank: K1 on own points, interface exchange over
     the process group (NCCL), tangent assembly on the extended slab."""
 
-    def __init__(self, plan: SlabPlan, mat_factory, device, group=None):
+    def __init__(self, plan: SlabPlan, mat_factory, device, group=None, exchange: str = "torch"):
+        """exchange: "torch" = torch.distributed P2P (NCCL on its own stream,
+        overlapping the interior update; gloo on the CPU); "capi" = the
+        C-ABI's own NCCL communicator (epfem_ctx_attach_nccl /
+        epfem_exchange_interface, the path a C++ caller uses), ordered on
+        the context's stream."""
         import torch
 
         from . import api
         self.plan = plan
         self.group = group
+        self.exchange = exchange
         self.device = device
         n_ext = plan.mesh.n_int
         self.mat_ext = mat_factory(n_ext)
@@ -189,6 +195,37 @@ class DistributedTangent:
         r0, r1 = plan.own_rows
         rp = self.cache.row_ptr
         self.own_values = (int(rp[r0]), int(rp[r1]))
+        if exchange == "capi":
+            self._attach_nccl()
+
+    def _attach_nccl(self):
+        """One NCCL communicator for the C-ABI exchange: rank 0's unique id
+        broadcast over the process group, then epfem_ctx_attach_nccl."""
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from . import api
+        uid = C.create_string_buffer(128)
+        if self.plan.rank == 0:
+            api._check(api.L.lib().epfem_nccl_unique_id(uid))
+        obj = [bytes(uid.raw)]
+        if self.plan.world > 1:
+            dist.broadcast_object_list(obj, src=0, group=self.group)
+        uid = C.create_string_buffer(obj[0], 128)
+        api._check(api.L.lib().epfem_ctx_attach_nccl(self.ctx.handle, uid, self.plan.world, self.plan.rank))
+
+    def _exchange_capi(self):
+        from . import api
+        s0, s1 = self.plan.send_points
+        h0, h1 = self.plan.halo_points
+        if self.plan.rank + 1 >= self.plan.world:
+            s0 = s1 = 0
+        if self.plan.rank == 0:
+            h0 = h1 = 0
+        self.ctx.use_current_stream()
+        api._check(api.L.lib().epfem_exchange_interface(self.ctx.handle, api._ptr(self.flags), api._ptr(self.D),
+                                                        s0, s1, h0, h1))
 
     def step(self, E_own, Ep_own=None, Hard_own=None):
         """One Newton iteration of this rank: fused constitutive update +
@@ -201,6 +238,15 @@ class DistributedTangent:
         Returns this rank's S, flag bytes and owned K values."""
         n_e = self.plan.mesh.n_elements
         top = max(self.plan.halo_elems, n_e - self.plan.layer_elems)
+        if self.exchange == "capi":
+            if self.plan.rank + 1 < self.plan.world and top > self.plan.halo_elems:
+                self.update_own(E_own, Ep_own, Hard_own, (top, n_e))
+                self._exchange_capi()
+                self.update_own(E_own, Ep_own, Hard_own, (self.plan.halo_elems, top))
+            else:
+                self.update_own(E_own, Ep_own, Hard_own)
+                self._exchange_capi()
+            return self.assemble()
         if self.plan.rank + 1 < self.plan.world and top > self.plan.halo_elems:
             self.update_own(E_own, Ep_own, Hard_own, (top, n_e))
             reqs = exchange_interface(self.plan, self.flags, self.D, self.group, wait=False)

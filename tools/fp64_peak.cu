@@ -42,6 +42,31 @@ __global__ void k_dmma(double* out, int iters) {
   if (s == 12345.0) out[threadIdx.x] = s;
 }
 
+// both pipes at once: does DMMA run beside DFMA (separate datapaths)?
+__global__ void k_mixed(double* out, int iters) {
+  double d[4][2];
+  double a2[8], b2 = 1.0000001, c2 = 0.9999999;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) d[k][0] = d[k][1] = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a2[k] = threadIdx.x + k;
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dmma(d[k][0], d[k][1], a, b);
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a2[k] = fma(a2[k], b2, c2);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) s += d[k][0] + d[k][1];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a2[k];
+  if (s == 12345.0) out[threadIdx.x] = s;
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -70,6 +95,20 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     const double fm = 2.0 * 256 * 8 * (double)iters * blocks * wpb;
     printf("DMMA  warps/CTA %2d x %d CTAs: %.1f TFLOP/s\n", wpb, blocks, fm / (ms * 1e-3) / 1e12);
+  }
+  for (int wpb : {8, 16}) {
+    const int blocks = sms * 4, threads = 32 * wpb;
+    k_mixed<<<blocks, threads>>>(out, 100);
+    cudaEventRecord(e0);
+    k_mixed<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    // per iteration per warp: 4 DMMA (4 x 256 FMA) + 32 DFMA instructions (32 x 32 FMA)
+    const double fl = 2.0 * (4.0 * 256 + 32.0 * 32) * (double)iters * blocks * wpb;
+    printf("MIXED warps/CTA %2d x %d CTAs: %.1f TFLOP/s (half DMMA, half DFMA flops)\n", wpb, blocks,
+           fl / (ms * 1e-3) / 1e12);
   }
   return 0;
 }

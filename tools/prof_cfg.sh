@@ -5,7 +5,7 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 C=${CFG:-cfg2}
-CMD="python bench.py --config $C --steps 2 --warmup 3 --no-cpu --no-e2e"
+CMD="python bench.py --config $C --steps 2 --warmup 3 --no-cpu --no-e2e --no-side --extra none"
 $CMD > gpurun_out/prof_${C}_bench.json 2> gpurun_out/prof_${C}_bench.err || exit 1
 NCU=/usr/local/cuda/bin/ncu
 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum,sm__warps_active.avg.pct_of_peak_sustained_active \

@@ -3,7 +3,7 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 C=${CFG:-cfg2}; KR=${K:-k_newton_warp}
-CMD="python bench.py --config $C --steps 2 --warmup 3 --no-cpu --no-e2e"
+CMD="python bench.py --config $C --steps 2 --warmup 3 --no-cpu --no-e2e --no-side --extra none"
 $CMD > /dev/null 2>&1 || exit 1
 NCU=/usr/local/cuda/bin/ncu
 $NCU --set full --import-source on --clock-control none -k regex:"$KR" -s 1 -c 1 -o /tmp/src_prof -f $CMD > gpurun_out/src_ncu.log 2>&1
