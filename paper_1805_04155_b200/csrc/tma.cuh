@@ -65,15 +65,17 @@ __device__ __forceinline__ void tma_store_1d_sync_hint(void* dst, const void* sr
                "r"(smem_u32(src)), "r"(bytes), "l"(policy)
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
-// shared -> global bulk store, then wait for its completion
+// shared -> global bulk store, then wait until its source has been read
+// (the CTA may retire while the writes drain; the grid's completion orders
+// them before any later kernel)
 __device__ __forceinline__ void tma_store_1d_sync(void* dst, const void* src, unsigned bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
                "r"(smem_u32(src)), "r"(bytes)
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 // shared -> global bulk store (bulk group; commit + wait with the helpers below)
 __device__ __forceinline__ void tma_store_1d(void* dst, const void* src, unsigned bytes) {

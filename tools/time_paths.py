@@ -20,7 +20,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 
-def main(names):
+def main(names, target=None):
     import paper_1805_04155_b200 as P
     from paper_1805_04155_b200.synthetic import CONFIGS, make_workload
     dev = torch.device("cuda", 0)
@@ -28,7 +28,7 @@ def main(names):
     C = P.api.C
     for name in names:
         cfg = CONFIGS[name]
-        wl = make_workload(cfg, device=dev)
+        wl = make_workload(cfg, device=dev, target=target)
         cache, mat = wl.cache, wl.mat
         E = wl.E.contiguous()
         Ep = torch.zeros_like(E)
@@ -83,4 +83,9 @@ def main(names):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["cfg4"])
+    args = sys.argv[1:] or ["cfg4"]
+    tgt = None
+    if args and args[0].startswith("--target="):
+        tgt = float(args[0].split("=")[1])
+        args = args[1:]
+    main(args, tgt)

@@ -16,7 +16,7 @@ while [ $# -gt 0 ]; do
     -Xcompiler -ffp-contract=off --expt-relaxed-constexpr -I include $FMAD $flags \
     -c $P/csrc/$SRC -o $out/$SRC.o
   objs=$(ls $P/_obj/*.o | grep -v "/$SRC.o")
-  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libepfem_gpu.so $out/$SRC.o $objs -lcudart_static
+  nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libepfem_gpu.so $out/$SRC.o $objs -lcudart_static -ldl
   rm $out/$SRC.o
   echo $out/libepfem_gpu.so
 done
