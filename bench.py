@@ -39,6 +39,20 @@ sys.path.insert(0, ROOT)
 METRIC = "tangent-stiffness assembly: integration points/s and achieved HBM GB/s vs peak"
 
 
+# optimal FMA per plastic point of the element delta:
+# n_p n_s g + n_p (n_p + 1) / 2 g dim, g = 9 (3D) / 4 (2D)
+FMA_PER_PLASTIC_POINT = {("P1", 2): 84, ("Q2", 2): 384, ("P2", 3): 2025, ("Q1", 3): 1404, ("Q2", 3): 6750}
+
+
+def load_fp64_peak():
+    p = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    try:
+        d = json.load(open(p))
+        return float(d["fp64_tflops"]), d["source"]
+    except (OSError, ValueError, KeyError):
+        return 36.6, "fallback (tools/fp64_peak.cu measurement, DESIGN.md)"
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -533,6 +547,16 @@ def measure_step(name, args, dev, local, world, target=None):
         dom_bytes, dom_ms, dom = asm_b, ms_per_step, "k_elastic_p1 (K5, P1 meshes)"
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     step_gbs = step_bytes / (ms_per_step * 1e-3) / 1e9
+    fp64 = None
+    fma_pt = FMA_PER_PLASTIC_POINT.get((cfg.family, cfg.dim))
+    if not elastic and fma_pt and k_ms:
+        fp_peak, fp_src = load_fp64_peak()
+        flops = 2.0 * fma_pt * n_plastic
+        tf = flops / (k_ms[KF] * 1e-3) / 1e12
+        fp64 = {"bound": "fp64", "kernel": KF, "achieved": tf, "peak": fp_peak, "unit": "TFLOP/s",
+                "frac": tf / fp_peak, "algorithmic_flops": flops,
+                "how": f"2 x {fma_pt} FMA (optimal element-delta contraction, SURVEY 8(d)) per plastic point / "
+                       f"the fused kernel's CUDA-event time", "peak_source": fp_src}
     working_set = step_bytes + (8 * nnz if not elastic else 0)
     l2 = (f"inputs larger than L2 (working set {working_set / 1e9:.2f} GB > 126 MB)" if working_set > 126e6 else
           f"L2-RESIDENT: the working set ({working_set / 1e6:.0f} MB) fits the 126 MB L2, so this is an L2 "
@@ -552,6 +576,7 @@ def measure_step(name, args, dev, local, world, target=None):
                      "traffic_source": "profiles/traffic.json (ncu --set full, bytes per launch)",
                      "algorithmic_bytes": dom_bytes, "kernel_ms": dom_ms, "peak_source": peak_src},
         "roofline_step": {"algorithmic_bytes": step_bytes, "achieved": step_gbs, "frac": step_gbs / hbm_peak},
+        "roofline_fp64": fp64,
         "kernels_ms": k_ms,
         "kernels_algorithmic_gbs": k_gbs,
         "clocks": clk.summary(),
@@ -812,7 +837,8 @@ def main():
         gc.collect()
         torch.cuda.empty_cache()
         extras[name] = {k: xl[k] for k in ("value", "ms_per_step", "config", "roofline", "roofline_step",
-                                           "kernels_ms", "kernels_algorithmic_gbs", "clocks", "gpu_launches")}
+                                           "roofline_fp64", "kernels_ms", "kernels_algorithmic_gbs", "clocks",
+                                           "gpu_launches")}
         line["gpu_launches"] += xl["gpu_launches"]
 
     cpu = None

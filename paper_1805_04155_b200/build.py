@@ -52,9 +52,16 @@ def _stale(out: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+LIB_DEBUG = os.path.join(LIBDIR, "debug", "libepfem_gpu.so")
+
+
+def build(force: bool = False, verbose: bool = False, debug_checks: bool = False) -> str:
+    """debug_checks: the test build with device-side bounds / single-writer
+    assertions (EPFEM_DEBUG_CHECKS=1) into lib/debug/ (own object dir)."""
+    OBJ = os.path.join(PKG, "_obj_debug") if debug_checks else globals()["OBJ"]
+    LIB = LIB_DEBUG if debug_checks else globals()["LIB"]
     os.makedirs(OBJ, exist_ok=True)
-    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "epfem_gpu.h")]
     objs, jobs = [], []
     for src, extra in SOURCES.items():
@@ -67,7 +74,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
                        "-I", "/usr/local/cuda/include", "-I", os.path.join(ROOT, "include"),
                        "-c", path, "-o", obj]
             else:
-                cmd = [nvcc()] + NVCC_COMMON + extra + ["-c", path, "-o", obj]
+                cmd = [nvcc()] + NVCC_COMMON + extra + (["-DEPFEM_DEBUG_CHECKS=1"] if debug_checks else []) + \
+                    ["-c", path, "-o", obj]
             if verbose:
                 print(" ".join(cmd), flush=True)
             jobs.append((cmd, subprocess.Popen(cmd)))
@@ -87,8 +95,9 @@ def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--debug-checks", action="store_true")
     args = ap.parse_args(argv)
-    print(build(force=args.force, verbose=args.verbose))
+    print(build(force=args.force, verbose=args.verbose, debug_checks=args.debug_checks))
 
 
 if __name__ == "__main__":

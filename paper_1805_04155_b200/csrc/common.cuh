@@ -3,6 +3,19 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cassert>
+
+// EPFEM_DEBUG_CHECKS=1 (a test build, tools/variants.sh): device-side bounds
+// and single-writer assertions on the scatter paths (compute-sanitizer is not
+// available on this pool); off in the shipped library.
+#ifndef EPFEM_DEBUG_CHECKS
+#define EPFEM_DEBUG_CHECKS 0
+#endif
+#if EPFEM_DEBUG_CHECKS
+#define EPFEM_CHECK(c) assert(c)
+#else
+#define EPFEM_CHECK(c) ((void)0)
+#endif
 
 #include <string>
 

@@ -462,6 +462,7 @@ __device__ __forceinline__ void delta_chunk_uniform1(const double* st_e, unsigne
 #pragma unroll
   for (int bb = 0; bb < CS; ++bb) {
     if (c0 + bb < NP) {
+      EPFEM_CHECK(a <= c0 + bb && blk_index<NP>(a, c0 + bb) < NP * (NP + 1) / 2);
       double* o = rec + blk_index<NP>(a, c0 + bb) * D2;
 #pragma unroll
       for (int i = 0; i < DIM; ++i)
@@ -551,6 +552,7 @@ __device__ __forceinline__ void delta_pairs3(const double* st_e, unsigned mask, 
     const int b = first ? a0 + k : a1 + (k - (NP - a0));
     const bool ok = first || (twin && k - (NP - a0) < NP - a1);
     if (!ok) continue;
+    EPFEM_CHECK(blk_index<NP>(first ? a0 : a1, b) < C::NB && b < NP);
     double* o = rec + blk_index<NP>(first ? a0 : a1, b) * D2 + i * 3;
     o[0] = acc[k][0];
     o[1] = acc[k][1];
