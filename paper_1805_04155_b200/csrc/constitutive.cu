@@ -403,13 +403,21 @@ __global__ void __launch_bounds__(256) k_constitutive(ConstArgs a) {
 // minBlocks: 1024 threads/SM in 2D (caps at 64 registers, measured faster); 0 in 3D
 // leaves ptxas its own heuristic (126 registers; an explicit 1 gives 144 and
 // is ~15% slower on cfg4).
-// One CTA group of EPB elements starting at e0 (phase 1, barrier, phase 2).
-template <int MODEL, int DIM, int NP, int NQ, bool FROM_U>
-__device__ __forceinline__ void fused_group(const ConstArgs& c, const GatherArgs& g, int64_t e0,
-                                            double (*s_st)[NQ][FusedCfg<DIM, NP, NQ>::REC], unsigned* s_mask) {
+template <int MODEL, int DIM, int NP, int NQ, bool FROM_U = false>
+__global__ void __launch_bounds__(FusedCfg<DIM, NP, NQ>::THREADS, FusedCfg<DIM, NP, NQ>::MINB)
+    k_newton_fused(ConstArgs c, GatherArgs g) {
+  pdl_trigger();
   using Cfg = FusedCfg<DIM, NP, NQ>;
   constexpr int EPB = Cfg::EPB;
+  __shared__ double s_st[EPB][NQ][Cfg::REC];
+  __shared__ unsigned s_mask[EPB];
+  c.DS = nullptr;  // hot path: S, flags, packed D only
+  c.Ep_out = c.Hard_out = nullptr;
+  c.pm = c.sm = c.am = nullptr;
+  c.crit = nullptr;
+
   const int tid = threadIdx.x;
+  const int64_t e0 = g.e_begin + (int64_t)blockIdx.x * EPB;
   if (tid < EPB) s_mask[tid] = 0u;
   __syncthreads();
   for (int k = tid; k < EPB * NQ; k += blockDim.x) {
@@ -475,27 +483,6 @@ __device__ __forceinline__ void fused_group(const ConstArgs& c, const GatherArgs
       delta_chunk_uniform<DIM, NP, Cfg::CS, Cfg::REC, Cfg::SUB>(&s_st[le][0][0], mask, a, c0,
                                                                 g.scratch + (size_t)e * Cfg::NB * Cfg::D2);
     }
-  }
-}
-
-// k_newton_fused: one group per CTA, or (EPFEM_PERSIST_FUSED = CTAs per SM,
-// a timing experiment) a persistent grid walking the groups.
-template <int MODEL, int DIM, int NP, int NQ, bool FROM_U = false>
-__global__ void __launch_bounds__(FusedCfg<DIM, NP, NQ>::THREADS, FusedCfg<DIM, NP, NQ>::MINB)
-    k_newton_fused(ConstArgs c, GatherArgs g) {
-  pdl_trigger();
-  using Cfg = FusedCfg<DIM, NP, NQ>;
-  constexpr int EPB = Cfg::EPB;
-  __shared__ double s_st[EPB][NQ][Cfg::REC];
-  __shared__ unsigned s_mask[EPB];
-  c.DS = nullptr;  // hot path: S, flags, packed D only
-  c.Ep_out = c.Hard_out = nullptr;
-  c.pm = c.sm = c.am = nullptr;
-  c.crit = nullptr;
-  const int64_t n_groups = (g.e_end - g.e_begin + EPB - 1) / EPB;
-  for (int64_t grp = blockIdx.x; grp < n_groups; grp += gridDim.x) {
-    fused_group<MODEL, DIM, NP, NQ, FROM_U>(c, g, g.e_begin + grp * EPB, s_st, s_mask);
-    if (grp + gridDim.x < n_groups) __syncthreads();
   }
 }
 
@@ -772,16 +759,8 @@ int launch_fused_impl(int model, int family, int dim, const ConstArgs& c, const 
       });
     } else {
       using FC = FusedCfg<DIM, NP, NQ>;
-      static const int persist = getenv("EPFEM_PERSIST_FUSED") ? atoi(getenv("EPFEM_PERSIST_FUSED")) : 0;
-      unsigned blocks = grid(FC::EPB);
-      if (persist > 0) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        blocks = std::min<unsigned>(blocks, (unsigned)(persist * sms));
-      }
       by_model(model, [&](auto md) {
-        k_newton_fused<decltype(md)::value, DIM, NP, NQ, FROM_U><<<blocks, FC::THREADS, 0, st>>>(c, g);
+        k_newton_fused<decltype(md)::value, DIM, NP, NQ, FROM_U><<<grid(FC::EPB), FC::THREADS, 0, st>>>(c, g);
       });
     }
   });

@@ -234,16 +234,7 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
   constexpr int NB = NP * (NP + 1) / 2;
   constexpr int D2 = DIM * DIM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    mbar_init(&s_bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  // one range per CTA, or (EPFEM_PERSIST_ROWS, a timing experiment) a
-  // persistent grid walking the ranges; the mbarrier phase flips per load
-  const int64_t n_ranges = (a.n_end - a.n_begin + npc - 1) / npc;
-  unsigned phase = 0;
-  for (int64_t range = blockIdx.x; range < n_ranges; range += gridDim.x) {
+  const int64_t range = blockIdx.x;
   const int64_t n0 = a.n_begin + range * npc;
   const int64_t n1 = min(n0 + (int64_t)npc, a.n_end);
   const int nloc = (int)(n1 - n0);
@@ -258,6 +249,11 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
   int* s_item = reinterpret_cast<int*>(img_raw + a.max_span + 2);
   int* s_iptr = s_item + a.max_items;
   int* s_vptr = s_iptr + npc + 1;
+  if (tid == 0) {
+    mbar_init(&s_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   const bool zero_base = a.base == nullptr;  // elastic assembly: K = sum of element blocks
   if (zero_base)
     for (int64_t k = tid; k < a1 - a0; k += blockDim.x) img_raw[k] = 0.0;
@@ -282,10 +278,7 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
     s_item[k] = __ldcg(a.emask + it / NP) ? it : -1;
   }
   __syncthreads();
-  if (a1 > a0 && !zero_base) {
-    mbar_wait(&s_bar, phase);
-    phase ^= 1u;
-  }
+  if (a1 > a0 && !zero_base) mbar_wait(&s_bar, 0);
   // Items are taken UB at a time: every lane first issues the loads of all
   // UB items (slot byte + workspace value), then applies the adds in item
   // order, so a node costs one memory round trip per UB items instead of
@@ -357,8 +350,6 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
       else
         tma_store_1d_sync(a.out + s0, img + (s0 - v0), (unsigned)((s1 - s0) * 8));
     }
-  }
-  if (range + gridDim.x < n_ranges) __syncthreads();  // the image is reused by the next range
   }
 }
 
@@ -446,16 +437,8 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
     // 24.76 ms); on the other meshes PDL is neutral to slightly positive.
     static const bool pdl_env = getenv("EPFEM_NO_PDL") == nullptr;
     const bool pdl = pdl_env && !(DIM == 3 && NP >= 20);
-    static const int persist = getenv("EPFEM_PERSIST_ROWS") ? atoi(getenv("EPFEM_PERSIST_ROWS")) : 0;
-    int64_t gblocks = rblocks;
-    if (persist > 0) {
-      int dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      gblocks = std::min<int64_t>(rblocks, (int64_t)persist * sms);
-    }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)gblocks);
+    cfg.gridDim = dim3((unsigned)rblocks);
     cfg.blockDim = dim3(kStreamThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
