@@ -671,7 +671,7 @@ class TangentEngine:
                Hard: Optional[torch.Tensor] = None, F: Optional[torch.Tensor] = None):
         """step() plus the internal forces F = B^T (w S) of its stresses
         (internal_forces, assembly.cpp:215-225; the reference forms them every
-        Newton iteration, solver.cpp:25): fused in 2D (epfem_newton_step_f),
+        Newton iteration, solver.cpp:25) in one call (epfem_newton_step_f),
         bitwise cache.internal_forces(S).  Returns (S, flags, D, K, F)."""
         if F is None:
             F = torch.empty((self.cache.info.n_dofs,), dtype=torch.float64, device=self.device)

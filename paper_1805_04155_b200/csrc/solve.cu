@@ -254,12 +254,18 @@ unsigned grid_rows(int64_t n) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kThreads / 32 - 1) / (kThreads / 32), 1 << 22));
 }
 
-struct Work {  // device scratch of one solve
+// Device scratch of one solve / norm: stream-ordered allocations
+// (cudaMallocAsync / cudaFreeAsync on the solve's stream: no device-wide
+// synchronisation per call, and freed on every return path).
+struct Work {
+  cudaStream_t st = nullptr;
   double *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *Ap = nullptr, *d = nullptr;
-  double *partial = nullptr, *sc = nullptr, *binv = nullptr;
+  double *partial = nullptr, *sc = nullptr, *binv = nullptr, *y = nullptr;
+  explicit Work(cudaStream_t s) : st(s) {}
+  cudaError_t alloc(double** q, size_t n) { return cudaMallocAsync(reinterpret_cast<void**>(q), sizeof(double) * n, st); }
   ~Work() {
-    for (double* q : {x, r, z, p, Ap, d, partial, sc, binv})
-      if (q) cudaFree(q);
+    for (double* q : {x, r, z, p, Ap, d, partial, sc, binv, y})
+      if (q) cudaFreeAsync(q, st);
   }
 };
 
@@ -290,11 +296,10 @@ int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, c
   EPFEM_CUDA_TRY(cudaEventRecord(ps.e, caller));
   EPFEM_CUDA_TRY(cudaStreamWaitEvent(ps.s, ps.e, 0));
   cudaStream_t st = ps.s;
-  Work w;
-  for (double** q : {&w.x, &w.r, &w.z, &w.p, &w.Ap, &w.d})
-    EPFEM_CUDA_TRY(cudaMalloc(q, sizeof(double) * n));
-  EPFEM_CUDA_TRY(cudaMalloc(&w.partial, sizeof(double) * 2 * kBlocks));
-  EPFEM_CUDA_TRY(cudaMalloc(&w.sc, sizeof(double) * 8));
+  Work w(st);
+  for (double** q : {&w.x, &w.r, &w.z, &w.p, &w.Ap, &w.d}) EPFEM_CUDA_TRY(w.alloc(q, n));
+  EPFEM_CUDA_TRY(w.alloc(&w.partial, 2 * kBlocks));
+  EPFEM_CUDA_TRY(w.alloc(&w.sc, 8));
   const unsigned gb = (unsigned)std::min<int64_t>(kBlocks, (n + kThreads - 1) / kThreads);
   const unsigned gbb = (unsigned)std::min<int64_t>(kBlocks, (nb + kThreads - 1) / kThreads);
   // block > 1: z = M Binv r replaces the scalar z = M r / d after every
@@ -307,7 +312,7 @@ int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, c
     return 0;
   };
   if (block > 1) {
-    EPFEM_CUDA_TRY(cudaMalloc(&w.binv, sizeof(double) * nb * block * block));
+    EPFEM_CUDA_TRY(w.alloc(&w.binv, nb * block * block));
     if (block == 2) k_bj_setup<2><<<gbb, kThreads, 0, st>>>(nb, rp, ci, v, mask, w.binv);
     else k_bj_setup<3><<<gbb, kThreads, 0, st>>>(nb, rp, ci, v, mask, w.binv);
   }
@@ -396,10 +401,11 @@ int energy_norm(int64_t n, const int64_t* rp, const int32_t* ci, const double* v
                 cudaStream_t st, double* out) {
   *out = 0.0;
   if (n == 0) return 0;
-  double *y = nullptr, *partial = nullptr, *sc = nullptr;
-  EPFEM_CUDA_TRY(cudaMalloc(&y, sizeof(double) * n));
-  EPFEM_CUDA_TRY(cudaMalloc(&partial, sizeof(double) * 2 * kBlocks));
-  EPFEM_CUDA_TRY(cudaMalloc(&sc, sizeof(double) * 8));
+  Work w(st);
+  EPFEM_CUDA_TRY(w.alloc(&w.y, n));
+  EPFEM_CUDA_TRY(w.alloc(&w.partial, 2 * kBlocks));
+  EPFEM_CUDA_TRY(w.alloc(&w.sc, 8));
+  double *y = w.y, *partial = w.partial, *sc = w.sc;
   const unsigned gb = (unsigned)std::min<int64_t>(kBlocks, (n + kThreads - 1) / kThreads);
   k_spmv_masked<<<grid_rows(n), kThreads, 0, st>>>(n, rp, ci, v, nullptr, x, y);
   k_dot2<<<gb, kThreads, 0, st>>>(n, x, y, nullptr, nullptr, partial);
@@ -409,9 +415,6 @@ int energy_norm(int64_t n, const int64_t* rp, const int32_t* ci, const double* v
   double h[8];
   EPFEM_CUDA_TRY(cudaMemcpyAsync(h, sc, sizeof(h), cudaMemcpyDeviceToHost, st));
   EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
-  cudaFree(y);
-  cudaFree(partial);
-  cudaFree(sc);
   EPFEM_CUDA_TRY(cudaGetLastError());
   *out = std::sqrt(std::max(h[S_PAP], 0.0));  // linalg.cpp:117-121
   return 0;

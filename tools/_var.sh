@@ -1,5 +1,2 @@
 cd $GRAFT_REPO_ROOT
-for pr in "0 0" "2 3" "3 2" "2 2" "1 4" "3 3"; do
-  set -- $pr
-  EPFEM_PERSIST_FUSED=$1 EPFEM_PERSIST_ROWS=$2 python tools/exp_concurrent.py --config cfg4 --reps 10 --prio 2>&1 | grep prio | sed "s/^/F=$1 R=$2 /" >> gpurun_out/corun.txt
-done
+for v in p20m16 p20m12 p20m10 p20m8; do EPFEM_GPU_LIB=paper_1805_04155_b200/lib/variants/$v/libepfem_gpu.so python tools/time_paths.py cfg5 | sed "s/^{/{\"v\": \"$v\", /" >> gpurun_out/p20.jsonl 2>&1; done
