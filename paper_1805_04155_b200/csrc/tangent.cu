@@ -220,6 +220,13 @@ constexpr int kStreamThreads = 256;
 #ifndef EPFEM_ROW_MINB20
 #define EPFEM_ROW_MINB20 4
 #endif
+// Q1 hexahedra: the items' block rows are copied into a per-warp double buffer in
+// shared memory with cp.async one plastic item ahead of its adds (the slot
+// bytes one item ahead in registers), so a node's record reads overlap the
+// adds of its previous item instead of costing one memory round trip each
+#ifndef EPFEM_ROW_ASYNC
+#define EPFEM_ROW_ASYNC 1
+#endif
 
 // The K_elast range [v0, v1) is read with ONE TMA bulk copy of the enclosing
 // 16-byte-aligned range into the shared image (the K_elast allocation is
@@ -285,7 +292,80 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
   // one per item (the add order, hence the bits, is unchanged).
   constexpr int KP = (NP * D2 + 31) / 32;
   constexpr int UB = KP == 1 ? 4 : 1;  // 3D: wider rows already give ILP; registers matter more
-  for (int ln = warp; ln < nloc;) {
+  constexpr bool ASYNC = EPFEM_ROW_ASYNC && KP > 1 && NP == 8;
+  if constexpr (ASYNC) {
+    // per-warp double buffer after the node offsets (16-byte aligned)
+    double* wbuf = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_vptr + npc + 1) + 15) & ~uintptr_t(15)) +
+                   warp * 2 * (32 * KP);
+    // lane-invariant parts of the entry index: lane <-> entry (pb, i, j) of block row pa
+    int pbk[KP], ijk[KP], ijt[KP];
+#pragma unroll
+    for (int kk = 0; kk < KP; ++kk) {
+      const int k = lane + 32 * kk;
+      pbk[kk] = k / D2;
+      ijk[kk] = k - pbk[kk] * D2;
+      const int i = ijk[kk] / DIM, j = ijk[kk] - i * DIM;
+      ijt[kk] = j * DIM + i;
+    }
+    auto issue = [&](int it, double* buf, int* sl) {
+      const int64_t el = it / NP;
+      const int pa = it - (int)el * NP;
+      const double* rec = a.scratch + (size_t)el * NB * D2;
+#pragma unroll
+      for (int kk = 0; kk < KP; ++kk) {
+        const int k = lane + 32 * kk;
+        sl[kk] = -1;
+        if (k < NP * D2) {
+          const int pb = pbk[kk];
+          const bool up = pa <= pb;
+          const int lo = up ? pa : pb, hi = up ? pb : pa;
+          cp_async8(buf + k, rec + blk_index<NP>(lo, hi) * D2 + (up ? ijk[kk] : ijt[kk]));
+          sl[kk] = __ldg(a.slot + (int64_t)it * NP + pb);
+        }
+      }
+      cp_async_commit();
+    };
+    for (int ln = warp; ln < nloc; ln += kStreamThreads / 32) {
+      const int ib = s_iptr[ln], ie = s_iptr[ln + 1];
+      const int row_len = (s_vptr[ln + 1] - s_vptr[ln]) / DIM;
+      double* seg = img + s_vptr[ln];
+      int kb = ib;
+      while (kb < ie && s_item[kb] < 0) ++kb;  // warp-uniform: the node's first plastic item
+      if (kb >= ie) continue;
+      int sl[KP], sln[KP];
+      int b = 0;
+      issue(s_item[kb], wbuf, sl);
+      while (kb < ie) {
+        int kn = kb + 1;
+        while (kn < ie && s_item[kn] < 0) ++kn;
+        if (kn < ie) {
+          issue(s_item[kn], wbuf + (b ^ 1) * (32 * KP), sln);
+          cp_async_wait_prev();  // item kb's copies have landed
+        } else {
+          cp_async_wait_all();
+        }
+        __syncwarp();
+        const double* cur = wbuf + b * (32 * KP);
+#pragma unroll
+        for (int kk = 0; kk < KP; ++kk)
+          if (sl[kk] >= 0) {
+            const int k = lane + 32 * kk;
+            const int i = ijk[kk] / DIM, j = ijk[kk] - i * DIM;
+            EPFEM_CHECK(sl[kk] < row_len / DIM && s_vptr[ln] + i * row_len + sl[kk] * DIM + j < s_vptr[ln + 1]);
+            seg[i * row_len + sl[kk] * DIM + j] += cur[k];
+          }
+        // every lane's adds of this item are done (add order = item order)
+        // and the buffer is free before the next copy into it
+        __syncwarp();
+#pragma unroll
+        for (int kk = 0; kk < KP; ++kk) sl[kk] = sln[kk];
+        b ^= 1;
+        kb = kn;
+      }
+    }
+  }
+  for (int ln = ASYNC ? nloc : warp; ln < nloc;) {
+
     const int ib = s_iptr[ln], ie = s_iptr[ln + 1];
     const int row_len = (s_vptr[ln + 1] - s_vptr[ln]) / DIM;
     double* seg = img + s_vptr[ln];
@@ -410,8 +490,9 @@ int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int6
 }
 
 // dynamic shared memory of one node range: image + items + node offsets
-static size_t row_range_smem(const GatherArgs& a) {
-  return sizeof(double) * ((size_t)a.max_span + 2) + sizeof(int) * ((size_t)a.max_items + 2 * ((size_t)a.npc + 1));
+static size_t row_range_smem(const GatherArgs& a, int kp_async) {
+  return sizeof(double) * ((size_t)a.max_span + 2) + sizeof(int) * ((size_t)a.max_items + 2 * ((size_t)a.npc + 1)) +
+         (kp_async ? 16 + sizeof(double) * (kStreamThreads / 32) * 2 * 32 * (size_t)kp_async : 0);
 }
 
 int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st) {
@@ -422,7 +503,8 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
     constexpr int NP = ET<decltype(F)::value, DIM>::NP, NQ = ET<decltype(F)::value, DIM>::NQ;
     const int64_t rblocks = (a.n_end - a.n_begin + a.npc - 1) / a.npc;
     if (rblocks <= 0) return;
-    const size_t smem = row_range_smem(a);
+    constexpr int KP = (NP * DIM * DIM + 31) / 32;
+    const size_t smem = row_range_smem(a, (EPFEM_ROW_ASYNC && KP > 1 && NP == 8) ? KP : 0);
     auto kern = k_row_stream<DIM, NP, NQ>;
     if (smem > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
