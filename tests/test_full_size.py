@@ -104,19 +104,24 @@ def _log(rec):
 
 
 @pytest.mark.parametrize("name,variant", [("cfg1", ""), ("cfg2", ""), ("cfg3", ""), ("cfg4", ""), ("cfg5", ""),
-                                          ("cfg3", "apex")])
+                                          ("cfg3", "apex"), ("cfg4", "0.0"), ("cfg4", "0.5"), ("cfg4", "1.0"),
+                                          ("cfg5", "0.0"), ("cfg5", "1.0")])
 def test_full_size_parity(cuda, oracle, name, variant):
     """variant "apex" (Drucker-Prager): the workload's strains plus the
     hydrostatic tension c / (3 K eta) on every point, the apex threshold of
     a zero deviator, so the apex branch (constitutive.cpp:188-193) is taken
     at a large fraction of the points, as the reference's forced-apex test
-    does at its scale (tests/test_constitutive.cpp:432-435)."""
+    does at its scale (tests/test_constitutive.cpp:432-435).  A numeric
+    variant is the plastic fraction of BASELINE's sweeps (configs 4 and 5:
+    0 / 25 / 50 / 100 % and 0 / 50 / 100 %; 100 % through a simple shear
+    above first yield plus the perturbation, synthetic.make_workload)."""
     import paper_1805_04155_b200 as P
     from paper_1805_04155_b200.synthetic import CONFIGS, make_workload
     cfg = CONFIGS[name]
     n = cfg.n
     nz = n if cfg.dim == 3 else 0
-    wl = make_workload(cfg, device=cuda)
+    target = float(variant) if variant not in ("", "apex") else None
+    wl = make_workload(cfg, device=cuda, target=target)
     coord, elem, _ = oracle.structured_mesh(cfg.family, cfg.dim, n, n, nz)
     assert np.array_equal(wl.mesh.coord.view(np.uint64), coord.view(np.uint64))
     assert np.array_equal(wl.mesh.elem, elem)
@@ -167,7 +172,14 @@ def test_full_size_parity(cuda, oracle, name, variant):
     pl_index = np.flatnonzero(fl_h & 1)
     Dp = D[torch.from_numpy(pl_index).to(cuda)].cpu().numpy()
     npl, nsm, nap = _check_points(oracle, cfg, E_h, S.cpu().numpy(), fl_h, Dp, pl_index)
-    assert npl == pl_index.size and 0 < npl < fl_h.size
+    assert npl == pl_index.size
+    if target == 0.0:
+        # an all-elastic iteration returns K bitwise equal to K_elast (assembly.cpp:190)
+        assert npl == 0 and torch.equal(Kv, gcache.K_elast.values)
+    elif target == 1.0:
+        assert npl == fl_h.size
+    else:
+        assert 0 < npl < fl_h.size
     if variant == "apex":
         assert nap > 0.1 * fl_h.size and nsm > 0.1 * fl_h.size, (nsm, nap)
     rec = {"config": name + (f"+{variant}" if variant else ""), "n_int": int(fl_h.size), "plastic": npl,
