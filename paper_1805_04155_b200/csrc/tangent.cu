@@ -227,6 +227,9 @@ constexpr int kStreamThreads = 256;
 #ifndef EPFEM_ROW_ASYNC
 #define EPFEM_ROW_ASYNC 1
 #endif
+#ifndef EPFEM_ROW_STAGES
+#define EPFEM_ROW_STAGES 2  // items in flight + 1
+#endif
 
 // The K_elast range [v0, v1) is read with ONE TMA bulk copy of the enclosing
 // 16-byte-aligned range into the shared image (the K_elast allocation is
@@ -294,9 +297,12 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
   constexpr int UB = KP == 1 ? 4 : 1;  // 3D: wider rows already give ILP; registers matter more
   constexpr bool ASYNC = EPFEM_ROW_ASYNC && KP > 1 && NP == 8;
   if constexpr (ASYNC) {
-    // per-warp double buffer after the node offsets (16-byte aligned)
+    // per-warp ring of STAGES buffers after the node offsets (16-byte
+    // aligned): an item's block row (NP * D2 doubles) and its NP slot bytes
+    constexpr int STAGES = EPFEM_ROW_STAGES;
+    constexpr int BUF = ((NP * D2 + 1) / 2) * 2 + 2;  // doubles; the last two hold the slot bytes
     double* wbuf = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_vptr + npc + 1) + 15) & ~uintptr_t(15)) +
-                   warp * 2 * (32 * KP);
+                   warp * STAGES * BUF;
     // lane-invariant parts of the entry index: lane <-> entry (pb, i, j) of block row pa
     int pbk[KP], ijk[KP], ijt[KP];
 #pragma unroll
@@ -307,60 +313,73 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
       const int i = ijk[kk] / DIM, j = ijk[kk] - i * DIM;
       ijt[kk] = j * DIM + i;
     }
-    auto issue = [&](int it, double* buf, int* sl) {
+    // copy item `it`'s block row and slots into buffer `buf` (one commit group)
+    auto issue = [&](int it, double* buf) {
       const int64_t el = it / NP;
       const int pa = it - (int)el * NP;
       const double* rec = a.scratch + (size_t)el * NB * D2;
 #pragma unroll
       for (int kk = 0; kk < KP; ++kk) {
         const int k = lane + 32 * kk;
-        sl[kk] = -1;
         if (k < NP * D2) {
           const int pb = pbk[kk];
           const bool up = pa <= pb;
           const int lo = up ? pa : pb, hi = up ? pb : pa;
           cp_async8(buf + k, rec + blk_index<NP>(lo, hi) * D2 + (up ? ijk[kk] : ijt[kk]));
-          sl[kk] = __ldg(a.slot + (int64_t)it * NP + pb);
         }
       }
+      if (lane == 0) cp_async8(buf + BUF - 2, a.slot + (int64_t)it * NP);  // NP = 8 slot bytes, 8-byte aligned
       cp_async_commit();
     };
     for (int ln = warp; ln < nloc; ln += kStreamThreads / 32) {
-      const int ib = s_iptr[ln], ie = s_iptr[ln + 1];
+      const int ie = s_iptr[ln + 1];
       const int row_len = (s_vptr[ln + 1] - s_vptr[ln]) / DIM;
       double* seg = img + s_vptr[ln];
-      int kb = ib;
-      while (kb < ie && s_item[kb] < 0) ++kb;  // warp-uniform: the node's first plastic item
+      auto next = [&](int k) {  // the node's next plastic item at or after k (warp-uniform)
+        while (k < ie && s_item[k] < 0) ++k;
+        return k;
+      };
+      int kb = next(s_iptr[ln]);
       if (kb >= ie) continue;
-      int sl[KP], sln[KP];
-      int b = 0;
-      issue(s_item[kb], wbuf, sl);
-      while (kb < ie) {
-        int kn = kb + 1;
-        while (kn < ie && s_item[kn] < 0) ++kn;
-        if (kn < ie) {
-          issue(s_item[kn], wbuf + (b ^ 1) * (32 * KP), sln);
-          cp_async_wait_prev();  // item kb's copies have landed
-        } else {
-          cp_async_wait_all();
-        }
-        __syncwarp();
-        const double* cur = wbuf + b * (32 * KP);
+      // prologue: STAGES - 1 items in flight (empty groups past the node's end)
+      int kiss = kb;
 #pragma unroll
-        for (int kk = 0; kk < KP; ++kk)
-          if (sl[kk] >= 0) {
-            const int k = lane + 32 * kk;
+      for (int s = 0; s < STAGES - 1; ++s) {
+        if (kiss < ie) {
+          issue(s_item[kiss], wbuf + s * BUF);
+          kiss = next(kiss + 1);
+        } else {
+          cp_async_commit();
+        }
+      }
+      int r = 0;
+      while (kb < ie) {
+        const int w = (r + STAGES - 1) % STAGES;
+        if (kiss < ie) {
+          issue(s_item[kiss], wbuf + w * BUF);
+          kiss = next(kiss + 1);
+        } else {
+          cp_async_commit();
+        }
+        cp_async_wait_n<STAGES - 1>();  // item kb's group is complete
+        __syncwarp();
+        const double* cur = wbuf + r * BUF;
+        const uint8_t* sls = reinterpret_cast<const uint8_t*>(cur + BUF - 2);
+#pragma unroll
+        for (int kk = 0; kk < KP; ++kk) {
+          const int k = lane + 32 * kk;
+          if (k < NP * D2) {
+            const int sl = sls[pbk[kk]];
             const int i = ijk[kk] / DIM, j = ijk[kk] - i * DIM;
-            EPFEM_CHECK(sl[kk] < row_len / DIM && s_vptr[ln] + i * row_len + sl[kk] * DIM + j < s_vptr[ln + 1]);
-            seg[i * row_len + sl[kk] * DIM + j] += cur[k];
+            EPFEM_CHECK(sl < row_len / DIM && s_vptr[ln] + i * row_len + sl * DIM + j < s_vptr[ln + 1]);
+            seg[i * row_len + sl * DIM + j] += cur[k];
           }
+        }
         // every lane's adds of this item are done (add order = item order)
         // and the buffer is free before the next copy into it
         __syncwarp();
-#pragma unroll
-        for (int kk = 0; kk < KP; ++kk) sl[kk] = sln[kk];
-        b ^= 1;
-        kb = kn;
+        r = (r + 1) % STAGES;
+        kb = next(kb + 1);
       }
     }
   }
@@ -490,9 +509,9 @@ int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int6
 }
 
 // dynamic shared memory of one node range: image + items + node offsets
-static size_t row_range_smem(const GatherArgs& a, int kp_async) {
+static size_t row_range_smem(const GatherArgs& a, int async_buf) {
   return sizeof(double) * ((size_t)a.max_span + 2) + sizeof(int) * ((size_t)a.max_items + 2 * ((size_t)a.npc + 1)) +
-         (kp_async ? 16 + sizeof(double) * (kStreamThreads / 32) * 2 * 32 * (size_t)kp_async : 0);
+         (async_buf ? 16 + sizeof(double) * (kStreamThreads / 32) * EPFEM_ROW_STAGES * (size_t)async_buf : 0);
 }
 
 int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st) {
@@ -504,9 +523,9 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
     const int64_t rblocks = (a.n_end - a.n_begin + a.npc - 1) / a.npc;
     if (rblocks <= 0) return;
     constexpr int KP = (NP * DIM * DIM + 31) / 32;
-    const size_t smem = row_range_smem(a, (EPFEM_ROW_ASYNC && KP > 1 && NP == 8) ? KP : 0);
+    const size_t smem = row_range_smem(a, (EPFEM_ROW_ASYNC && KP > 1 && NP == 8) ? ((NP * DIM * DIM + 1) / 2) * 2 + 2 : 0);
     auto kern = k_row_stream<DIM, NP, NQ>;
-    if (smem > 48 * 1024) {
+    if (smem + 1024 > 48 * 1024) {  // the static mbarrier and the reserved 1 KB count against the 48 KB default
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) { rc = cuda_fail(e, "cudaFuncSetAttribute"); return; }
     }
@@ -530,7 +549,9 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, a.npc);
-    if (e != cudaSuccess) rc = cuda_fail(e, "row stream launch");
+    if (e != cudaSuccess)
+      rc = cuda_fail(e, ("row stream launch: " + std::to_string(rblocks) + " CTAs, " + std::to_string(smem) +
+                         " B shared memory").c_str());
   });
   if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
   if (rc) return rc;

@@ -1,2 +1,4 @@
 cd $GRAFT_REPO_ROOT
-for v in p20m16 p20m12 p20m10 p20m8; do EPFEM_GPU_LIB=paper_1805_04155_b200/lib/variants/$v/libepfem_gpu.so python tools/time_paths.py cfg5 | sed "s/^{/{\"v\": \"$v\", /" >> gpurun_out/p20.jsonl 2>&1; done
+python tools/time_paths.py cfg4 | sed 's/^{/{"v": "st2", /' >> gpurun_out/st.jsonl 2>&1
+for v in st3 st4; do EPFEM_GPU_LIB=paper_1805_04155_b200/lib/variants/$v/libepfem_gpu.so python tools/time_paths.py cfg4 | sed "s/^{/{\"v\": \"$v\", /" >> gpurun_out/st.jsonl 2>&1; done
+python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "cfg4 or Q1" > gpurun_out/st_pytest.log 2>&1
