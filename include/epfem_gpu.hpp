@@ -9,13 +9,14 @@
 //
 //   reference (C++ / Eigen)                          here
 //   -----------------------------------------------  ---------------------------------------
-//   build_assembly_cache (assembly.hpp:53)            epfem_gpu::AssemblyCache::build
+//   build_assembly_cache (assembly.hpp:53)            epfem_gpu::AssemblyCache (constructor)
 //   evaluate_constitutive (constitutive.hpp:96-98)    epfem_gpu::evaluate_constitutive
 //   assemble_tangent_stiffness (assembly.hpp:59-60)   epfem_gpu::assemble_tangent_stiffness
 //   evaluate_constitutive + assemble_tangent_...      epfem_gpu::NewtonStep::run (fused)
 //     (solver.cpp:24,28-29)
 //   AssemblyCache::strains (assembly.hpp:50)          epfem_gpu::AssemblyCache::strains
 //   internal_forces (assembly.hpp:63)                 epfem_gpu::AssemblyCache::internal_forces
+//   newton_solve (solver.cpp:7-62)                    epfem_gpu::newton_solve
 //
 // Host vectors use the reference's column-major byte layout (a 6 x n_int Mat
 // is n_int * 6 doubles, point-major); K comes back as CSR arrays (== the
@@ -251,6 +252,97 @@ inline void evaluate_constitutive(Context& ctx, const Material& mat, const doubl
                                   const double* Hard_prev, const epfem_constitutive_out& out) {
   const epfem_material mv = mat.view();
   check(epfem_constitutive(ctx.get(), &mv, E, Ep_prev, Hard_prev, &out));
+}
+
+// newton_solve (solver.cpp:7-62): one time step of the semismooth Newton
+// iteration from the Dirichlet lift (free dofs from u_start when given).
+// Every iteration: strains E = B u (K8), the step with its internal forces
+// (epfem_newton_step_f: constitutive update, tangent K, F = B^T (w S)), du =
+// restricted_solve(K, f_ext - F, free) (the device CG, the reference's
+// conjugate-gradient method), and the stopping test |du|_e <= eps (|u_prev|_e
+// + |u|_e) in the K_elast energy norm.  u and the vector updates live on the
+// host (n_dofs doubles), everything per integration point on the device.
+// Zero plastic history (Ep_prev = Hard_prev = 0), as the BASELINE steps.
+struct NewtonResult {
+  std::vector<double> u;
+  int newton_iters = 0;
+  int64_t n_plastic = 0;              // plastic points at the converged u (the committed state)
+  std::vector<int64_t> linear_iters;  // CG iterations per Newton iteration
+};
+
+inline NewtonResult newton_solve(Context& ctx, const AssemblyCache& cache, const Material& mat,
+                                 const std::vector<double>& dirichlet, const std::vector<uint8_t>& free_mask,
+                                 const std::vector<double>& f_ext, double eps_newton = 1e-10, int max_iters = 25,
+                                 double rel_tol = 1e-10, const std::vector<double>* u_start = nullptr) {
+  if (eps_newton <= 0.0 || max_iters < 1) throw Error("newton_solve: invalid settings", EPFEM_ERR_INVALID);
+  const epfem_cache_info& I = cache.info();
+  const int64_t n = I.n_dofs, n_int = I.n_int;
+  if ((int64_t)dirichlet.size() != n || (int64_t)free_mask.size() != n || (int64_t)f_ext.size() != n)
+    throw Error("restricted_solve: dimension mismatch", EPFEM_ERR_INVALID);
+  const int64_t* rp = nullptr;
+  const int32_t* ci = nullptr;
+  const double* kel = nullptr;
+  check(epfem_cache_pattern(cache.get(), &rp, &ci));
+  check(epfem_cache_K_elast(cache.get(), &kel));
+  std::vector<double> u(dirichlet);
+  if (u_start)
+    for (int64_t k = 0; k < n; ++k)
+      if (free_mask[k]) u[k] = (*u_start)[k];
+  DeviceBuffer<double> d_u(u), d_E((size_t)6 * n_int), d_F(n), d_rhs(n), d_du(n);
+  DeviceBuffer<double> d_zero((size_t)6 * n_int);
+  check_cuda(cudaMemset(d_zero.data(), 0, d_zero.size() * sizeof(double)), "cudaMemset");
+  DeviceBuffer<uint8_t> d_free(free_mask);
+  NewtonStep step(cache, mat);
+  const epfem_material mv = mat.view();
+  const double* hard = mat.model == EPFEM_MODEL_VON_MISES ? d_zero.data() : nullptr;
+  const double* ep = mat.model == EPFEM_MODEL_ELASTIC ? nullptr : d_zero.data();
+  auto energy = [&](const DeviceBuffer<double>& v) {
+    double e = 0.0;
+    check(epfem_energy_norm(ctx.get(), n, rp, ci, kel, v.data(), &e));
+    return e;
+  };
+  NewtonResult res;
+  bool converged = false;
+  std::vector<double> F, du, rhs(n);
+  for (int it = 1; it <= max_iters; ++it) {
+    check(epfem_strains(ctx.get(), cache.get(), d_u.data(), d_E.data()));
+    epfem_constitutive_out out{};
+    out.S = step.S.data();
+    out.flags = step.flags.data();
+    out.D = step.D.data();
+    check(epfem_newton_step_f(ctx.get(), cache.get(), &mv, d_E.data(), ep, hard, &out, step.K.data(), d_F.data()));
+    F = d_F.download();
+    for (int64_t k = 0; k < n; ++k) rhs[k] = f_ext[k] - F[k];
+    d_rhs.upload(rhs);
+    int64_t its = 0;
+    double r = 0.0;
+    check(epfem_restricted_solve(ctx.get(), n, rp, ci, step.K.data(), d_rhs.data(), d_free.data(), rel_tol, 0,
+                                 d_du.data(), &its, &r));
+    res.linear_iters.push_back(its);
+    res.newton_iters = it;
+    const double norm_prev = energy(d_u);
+    du = d_du.download();
+    for (int64_t k = 0; k < n; ++k) u[k] = u[k] + du[k];
+    d_u.upload(u);
+    const double norm_curr = energy(d_u);
+    const double denom = norm_prev + norm_curr;
+    if (denom == 0.0 || energy(d_du) <= eps_newton * denom) {
+      converged = true;
+      break;
+    }
+  }
+  if (!converged)
+    throw Error("newton_solve: no convergence within " + std::to_string(max_iters) + " iterations",
+                EPFEM_ERR_SOLVER);
+  // commit: the constitutive state at the converged displacement
+  check(epfem_strains(ctx.get(), cache.get(), d_u.data(), d_E.data()));
+  DeviceBuffer<uint8_t> pm(n_int);
+  epfem_constitutive_out out{};
+  out.plastic_mask = pm.data();
+  check(epfem_constitutive(ctx.get(), &mv, d_E.data(), ep, hard, &out));
+  for (uint8_t b : pm.download()) res.n_plastic += b;
+  res.u = std::move(u);
+  return res;
 }
 
 }  // namespace epfem_gpu
