@@ -227,6 +227,13 @@ constexpr int kStreamThreads = 256;
 #ifndef EPFEM_ROW_ASYNC
 #define EPFEM_ROW_ASYNC 1
 #endif
+#ifndef EPFEM_ROW_ASYNC20
+#define EPFEM_ROW_ASYNC20 1
+#endif
+// element types whose row stream takes the async item ring (measured: Q1
+// cfg4 rows 3.70 -> 3.55 ms, Q2-20 cfg5 9.44 -> 9.21 ms; P2 tetrahedra
+// slower, 3.00 -> 3.05 ms: the ring's shared memory costs a CTA per SM)
+__host__ __device__ constexpr bool async_row_stream(int np) { return np == 8 || (EPFEM_ROW_ASYNC20 && np == 20); }
 #ifndef EPFEM_ROW_STAGES
 #define EPFEM_ROW_STAGES 2  // items in flight + 1
 #endif
@@ -295,12 +302,13 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
   // one per item (the add order, hence the bits, is unchanged).
   constexpr int KP = (NP * D2 + 31) / 32;
   constexpr int UB = KP == 1 ? 4 : 1;  // 3D: wider rows already give ILP; registers matter more
-  constexpr bool ASYNC = EPFEM_ROW_ASYNC && KP > 1 && NP == 8;
+  constexpr bool ASYNC = EPFEM_ROW_ASYNC && KP > 1 && async_row_stream(NP);
   if constexpr (ASYNC) {
     // per-warp ring of STAGES buffers after the node offsets (16-byte
     // aligned): an item's block row (NP * D2 doubles) and its NP slot bytes
     constexpr int STAGES = EPFEM_ROW_STAGES;
-    constexpr int BUF = ((NP * D2 + 1) / 2) * 2 + 2;  // doubles; the last two hold the slot bytes
+    constexpr int SLW = (NP + 7) / 8;                   // doubles holding the NP slot bytes
+    constexpr int BUF = ((NP * D2 + 1) / 2) * 2 + ((SLW + 1) / 2) * 2;  // doubles (even: 16-byte steps)
     double* wbuf = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_vptr + npc + 1) + 15) & ~uintptr_t(15)) +
                    warp * STAGES * BUF;
     // lane-invariant parts of the entry index: lane <-> entry (pb, i, j) of block row pa
@@ -328,7 +336,9 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
           cp_async8(buf + k, rec + blk_index<NP>(lo, hi) * D2 + (up ? ijk[kk] : ijt[kk]));
         }
       }
-      if (lane == 0) cp_async8(buf + BUF - 2, a.slot + (int64_t)it * NP);  // NP = 8 slot bytes, 8-byte aligned
+      // the NP slot bytes in 4-byte words (NP % 4 == 0: 4-byte aligned source)
+      if (lane < NP / 4)
+        cp_async4(reinterpret_cast<uint8_t*>(buf + NP * D2 + (NP * D2) % 2) + 4 * lane, a.slot + (int64_t)it * NP + 4 * lane);
       cp_async_commit();
     };
     for (int ln = warp; ln < nloc; ln += kStreamThreads / 32) {
@@ -364,7 +374,7 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
         cp_async_wait_n<STAGES - 1>();  // item kb's group is complete
         __syncwarp();
         const double* cur = wbuf + r * BUF;
-        const uint8_t* sls = reinterpret_cast<const uint8_t*>(cur + BUF - 2);
+        const uint8_t* sls = reinterpret_cast<const uint8_t*>(cur + NP * D2 + (NP * D2) % 2);
 #pragma unroll
         for (int kk = 0; kk < KP; ++kk) {
           const int k = lane + 32 * kk;
@@ -523,7 +533,9 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
     const int64_t rblocks = (a.n_end - a.n_begin + a.npc - 1) / a.npc;
     if (rblocks <= 0) return;
     constexpr int KP = (NP * DIM * DIM + 31) / 32;
-    const size_t smem = row_range_smem(a, (EPFEM_ROW_ASYNC && KP > 1 && NP == 8) ? ((NP * DIM * DIM + 1) / 2) * 2 + 2 : 0);
+    constexpr int SLW = (NP + 7) / 8;
+    const size_t smem = row_range_smem(
+        a, (EPFEM_ROW_ASYNC && KP > 1 && async_row_stream(NP)) ? ((NP * DIM * DIM + 1) / 2) * 2 + ((SLW + 1) / 2) * 2 : 0);
     auto kern = k_row_stream<DIM, NP, NQ>;
     if (smem + 1024 > 48 * 1024) {  // the static mbarrier and the reserved 1 KB count against the 48 KB default
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
