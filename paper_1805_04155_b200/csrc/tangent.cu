@@ -493,7 +493,7 @@ int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int6
                     cudaStream_t st, int* npc_out, int* span_out, int* items_out, int budget_bytes) {
   // bytes of dynamic smem per CTA and the starting node count; EPFEM_ROW_KB /
   // EPFEM_ROW_NPC override them for tuning runs (budget_bytes > 0: the
-  // caller's budget, e.g. one warp's slice in the one-launch step)
+  // caller's budget)
   int budget = (dim == 2 ? 100 : 40) * 1024;  // measured optimum (2D: 32 nodes, Q1 hex: 16)
   int npc = 32;
   if (const char* v = getenv("EPFEM_ROW_KB")) budget = atoi(v) * 1024;
