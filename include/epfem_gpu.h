@@ -289,15 +289,24 @@ int epfem_restricted_solve(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, co
                            double* residual);
 /* epfem_restricted_solve_blocked: the same solve with a node-block Jacobi
  *   preconditioner (block = dim: the inverse of each dim x dim diagonal block of
- *   the restricted operator; block = 1 is epfem_restricted_solve).  There is
- *   no device sparse factorisation here: the reference's default
- *   LinearSolver::direct (SimplicialLDLT + refinement, linalg.cpp:84-96) is
- *   NOT reproduced; a host caller asking for it gets this CG under the same
- *   tolerance contract (the Python solver warns and records the substitution). */
+ *   the restricted operator; block = 1 is epfem_restricted_solve).  The
+ *   reference's default LinearSolver::direct is epfem_restricted_solve_direct
+ *   below. */
 int epfem_restricted_solve_blocked(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                                    const double* values, const double* rhs, const uint8_t* free_mask,
                                    double rel_tol, int64_t max_iters, int block, double* x, int64_t* iters,
                                    double* residual);
+/* epfem_restricted_solve_direct: the reference's default LinearSolver::direct
+ *   (SimplicialLDLT + up to three refinement sweeps, linalg.cpp:84-96) on the
+ *   device: K[free, free] formed on the device, factorised by cuSOLVER's sparse
+ *   Cholesky (QR when not positive definite; cuSOLVER loaded at run time),
+ *   then up to three refinement sweeps on the true residual.  Same contract:
+ *   EPFEM_ERR_SOLVER "restricted_solve: factorization failed" or "... residual
+ *   <r> above tolerance"; EPFEM_ERR_UNSUPPORTED without cuSOLVER or past int32
+ *   sizes.  sweeps / residual (may be NULL) report the solve. */
+int epfem_restricted_solve_direct(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                                  const double* values, const double* rhs, const uint8_t* free_mask, double rel_tol,
+                                  double* x, int* sweeps, double* residual);
 int epfem_energy_norm(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                       const double* values, const double* v, double* out);
 

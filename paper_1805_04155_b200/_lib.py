@@ -57,7 +57,7 @@ EXPORTS = [
     "epfem_newton_step", "epfem_newton_step_u", "epfem_newton_step_f", "epfem_constitutive_delta", "epfem_assemble_rows", "epfem_newton_range",
     "epfem_delta_range", "epfem_strains", "epfem_internal_forces", "epfem_restricted_solve",
     "epfem_restricted_solve_blocked", "epfem_energy_norm",
-    "epfem_nccl_unique_id", "epfem_ctx_attach_nccl", "epfem_ctx_set_nccl_comm", "epfem_exchange_interface",
+    "epfem_restricted_solve_direct", "epfem_nccl_unique_id", "epfem_ctx_attach_nccl", "epfem_ctx_set_nccl_comm", "epfem_exchange_interface",
 ]
 
 _lib = None
@@ -113,6 +113,8 @@ def lib() -> C.CDLL:
     L.epfem_restricted_solve_blocked.argtypes = [_P, _I64, _P, _P, _P, _P, _P, _D, _I64, C.c_int, _P,
                                                  C.POINTER(_I64), C.POINTER(_D)]
     L.epfem_energy_norm.argtypes = [_P, _I64, _P, _P, _P, _P, C.POINTER(_D)]
+    L.epfem_restricted_solve_direct.argtypes = [_P, _I64, _P, _P, _P, _P, _P, _D, _P, C.POINTER(C.c_int),
+                                                C.POINTER(_D)]
     L.epfem_nccl_unique_id.argtypes = [_P]
     L.epfem_ctx_attach_nccl.argtypes = [_P, _P, C.c_int, C.c_int]
     L.epfem_ctx_set_nccl_comm.argtypes = [_P, _P, C.c_int, C.c_int]

@@ -783,6 +783,24 @@ int epfem_restricted_solve_blocked(epfem_ctx* ctx, int64_t n, const int64_t* row
   return 0;
 }
 
+int epfem_restricted_solve_direct(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
+                                  const double* values, const double* rhs, const uint8_t* free_mask, double rel_tol,
+                                  double* x, int* sweeps, double* residual) {
+  DeviceGuard guard(ctx);
+  if (int rc = check_ctx(ctx)) return rc;
+  if (n < 0 || (n > 0 && (!row_ptr || !col_idx || !values || !rhs || !x)))
+    return fail(EPFEM_ERR_INVALID, "restricted_solve: dimension mismatch");
+  int sw = 0;
+  double res = 0.0;
+  if (int rc = direct_solve(n, row_ptr, col_idx, values, free_mask, rhs, x, rel_tol, ctx->stream, &sw, &res))
+    return rc;
+  if (sweeps) *sweeps = sw;
+  if (residual) *residual = res;
+  if (!std::isfinite(res) || res > rel_tol)
+    return fail(EPFEM_ERR_SOLVER, "restricted_solve: residual " + std::to_string(res) + " above tolerance");
+  return 0;
+}
+
 int epfem_energy_norm(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                       const double* values, const double* v, double* out) {
   DeviceGuard guard(ctx);

@@ -11,8 +11,13 @@
 // in order), so a solve is bitwise reproducible run to run.  The scalars
 // (alpha, beta, r.z) stay on the device; the host reads the residual every
 // kCheck iterations.
+#include <dlfcn.h>
+
 #include <cmath>
+#include <cub/cub.cuh>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "kernels.cuh"
 
@@ -417,6 +422,236 @@ int energy_norm(int64_t n, const int64_t* rp, const int32_t* ci, const double* v
   EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
   EPFEM_CUDA_TRY(cudaGetLastError());
   *out = std::sqrt(std::max(h[S_PAP], 0.0));  // linalg.cpp:117-121
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// LinearSolver::direct (linalg.cpp:84-96): the reference factorises
+// K[free, free] (SimplicialLDLT) and applies up to three refinement sweeps.
+// Here: the restricted matrix is formed on the device (free-index map by a
+// prefix sum, per-row counts, fill), factorised and solved by cuSOLVER's
+// sparse Cholesky (cusolverSpDcsrlsvchol, symamd reordering) -- QR
+// (cusolverSpDcsrlsvqr) when the Cholesky finds the matrix not positive
+// definite -- then up to three refinement sweeps on the true residual
+// |M (b - K x)| / |M b| with the deterministic masked SpMV above.  cuSOLVER /
+// cuSPARSE are loaded at run time (dlopen), so the library has no link
+// dependency on them.
+namespace {
+
+struct SpApi {
+  using Create = int (*)(void**);
+  using Destroy = int (*)(void*);
+  using SetStream = int (*)(void*, cudaStream_t);
+  using Solve = int (*)(void*, int, int, const void*, const double*, const int*, const int*, const double*, double,
+                        int, double*, int*);
+  using DescrCreate = int (*)(void**);
+  using DescrDestroy = int (*)(void*);
+  using DescrSet = int (*)(void*, int);
+  Create create = nullptr;
+  Destroy destroy = nullptr;
+  SetStream set_stream = nullptr;
+  Solve chol = nullptr, qr = nullptr;
+  DescrCreate descr_create = nullptr;
+  DescrDestroy descr_destroy = nullptr;
+  DescrSet set_type = nullptr, set_base = nullptr;
+  bool ok = false;
+};
+
+const SpApi& sp_api() {
+  static SpApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto open = [](const char* soname, const char* path) {
+      void* h = dlopen(soname, RTLD_NOW | RTLD_GLOBAL);
+      return h ? h : dlopen(path, RTLD_NOW | RTLD_GLOBAL);
+    };
+    void* hs = open("libcusparse.so.12", "/usr/local/cuda/lib64/libcusparse.so.12");
+    void* hv = open("libcusolver.so.11", "/usr/local/cuda/lib64/libcusolver.so.11");
+    if (!hs || !hv) return;
+    api.create = reinterpret_cast<SpApi::Create>(dlsym(hv, "cusolverSpCreate"));
+    api.destroy = reinterpret_cast<SpApi::Destroy>(dlsym(hv, "cusolverSpDestroy"));
+    api.set_stream = reinterpret_cast<SpApi::SetStream>(dlsym(hv, "cusolverSpSetStream"));
+    api.chol = reinterpret_cast<SpApi::Solve>(dlsym(hv, "cusolverSpDcsrlsvchol"));
+    api.qr = reinterpret_cast<SpApi::Solve>(dlsym(hv, "cusolverSpDcsrlsvqr"));
+    api.descr_create = reinterpret_cast<SpApi::DescrCreate>(dlsym(hs, "cusparseCreateMatDescr"));
+    api.descr_destroy = reinterpret_cast<SpApi::DescrDestroy>(dlsym(hs, "cusparseDestroyMatDescr"));
+    api.set_type = reinterpret_cast<SpApi::DescrSet>(dlsym(hs, "cusparseSetMatType"));
+    api.set_base = reinterpret_cast<SpApi::DescrSet>(dlsym(hs, "cusparseSetMatIndexBase"));
+    api.ok = api.create && api.destroy && api.set_stream && api.chol && api.qr && api.descr_create &&
+             api.descr_destroy && api.set_type && api.set_base;
+  });
+  return api;
+}
+
+// free[i] -> 1 / 0 (int) for the prefix sum of the free-index map
+__global__ void k_free_flags(int64_t n, const uint8_t* __restrict__ mask, int* flag) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads)
+    flag[i] = (!mask || mask[i]) ? 1 : 0;
+}
+// per free row: its free entries (counts indexed by the row's free index)
+__global__ void k_free_row_count(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                 const uint8_t* __restrict__ mask, const int* __restrict__ fidx, int* cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
+    if (mask && !mask[i]) continue;
+    int c = 0;
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) c += (!mask || mask[ci[k]]) ? 1 : 0;
+    cnt[fidx[i]] = c;
+  }
+}
+// fill K[free, free] (columns stay sorted: the free-index map is monotone)
+__global__ void k_free_fill(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const double* __restrict__ v, const uint8_t* __restrict__ mask,
+                            const int* __restrict__ fidx, const int* __restrict__ frp, int* fci, double* fv) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
+    if (mask && !mask[i]) continue;
+    int o = frp[fidx[i]];
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+      const int32_t c = ci[k];
+      if (!mask || mask[c]) {
+        fci[o] = fidx[c];
+        fv[o] = v[k];
+        ++o;
+      }
+    }
+  }
+}
+__global__ void k_gather_free(int64_t n, const uint8_t* __restrict__ mask, const int* __restrict__ fidx,
+                              const double* __restrict__ r, double* rf) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads)
+    if (!mask || mask[i]) rf[fidx[i]] = r[i];
+}
+// x += scatter(xf) on free dofs (fixed dofs stay zero)
+__global__ void k_scatter_add_free(int64_t n, const uint8_t* __restrict__ mask, const int* __restrict__ fidx,
+                                   const double* __restrict__ xf, double* x) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads)
+    if (!mask || mask[i]) x[i] = __dadd_rn(x[i], xf[fidx[i]]);
+}
+
+}  // namespace
+
+int direct_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, const uint8_t* mask,
+                 const double* b, double* x_out, double rel_tol, cudaStream_t caller, int* sweeps_out,
+                 double* residual_out) {
+  *sweeps_out = 0;
+  *residual_out = 0.0;
+  EPFEM_CUDA_TRY(cudaMemsetAsync(x_out, 0, sizeof(double) * std::max<int64_t>(n, 1), caller));
+  if (n == 0) return 0;
+  const SpApi& api = sp_api();
+  if (!api.ok) return fail(EPFEM_ERR_UNSUPPORTED, "restricted_solve: cuSOLVER sparse is not available");
+  if (n >= INT32_MAX) return fail(EPFEM_ERR_UNSUPPORTED, "restricted_solve: direct solve needs int32 sizes");
+  cudaStream_t st = caller;
+  Work w(st);
+  int *fidx = nullptr, *cnt = nullptr, *frp = nullptr, *fci = nullptr;
+  auto ialloc = [&](int** p, size_t k) { return cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(int) * k, st); };
+  struct IntBufs {
+    cudaStream_t s;
+    std::vector<int*> p;
+    ~IntBufs() {
+      for (int* q : p)
+        if (q) cudaFreeAsync(q, s);
+    }
+  } ib{st, {}};
+  const unsigned gb = (unsigned)std::min<int64_t>(kBlocks * 4, (n + kThreads - 1) / kThreads);
+  EPFEM_CUDA_TRY(ialloc(&fidx, n + 1));
+  ib.p.push_back(fidx);
+  // free-index map: exclusive prefix sum of the free flags
+  EPFEM_CUDA_TRY(ialloc(&cnt, n + 1));
+  ib.p.push_back(cnt);
+  k_free_flags<<<gb, kThreads, 0, st>>>(n, mask, cnt);
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, fidx, (int)n + 1, st);
+  void* tmp = nullptr;
+  EPFEM_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, st));
+  EPFEM_CUDA_TRY(cudaMemsetAsync(cnt + n, 0, sizeof(int), st));
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, fidx, (int)n + 1, st);
+  int m = 0;
+  EPFEM_CUDA_TRY(cudaMemcpyAsync(&m, fidx + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+  if (m == 0) {
+    cudaFreeAsync(tmp, st);
+    return 0;
+  }
+  // restricted CSR (int32, cuSOLVER's index type)
+  EPFEM_CUDA_TRY(ialloc(&frp, (size_t)m + 1));
+  ib.p.push_back(frp);
+  EPFEM_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * ((size_t)m + 1), st));
+  k_free_row_count<<<gb, kThreads, 0, st>>>(n, rp, ci, mask, fidx, cnt);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, frp, m + 1, st);
+  int nnz = 0;
+  EPFEM_CUDA_TRY(cudaMemcpyAsync(&nnz, frp + m, sizeof(int), cudaMemcpyDeviceToHost, st));
+  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+  cudaFreeAsync(tmp, st);
+  EPFEM_CUDA_TRY(ialloc(&fci, (size_t)std::max(nnz, 1)));
+  ib.p.push_back(fci);
+  double *fv = nullptr, *bf = nullptr, *xf = nullptr, *r = nullptr, *Ax = nullptr;
+  EPFEM_CUDA_TRY(w.alloc(&w.binv, (size_t)std::max(nnz, 1)));  // restricted values
+  fv = w.binv;
+  EPFEM_CUDA_TRY(w.alloc(&w.r, n));
+  EPFEM_CUDA_TRY(w.alloc(&w.Ap, n));
+  EPFEM_CUDA_TRY(w.alloc(&w.z, (size_t)m));  // restricted rhs
+  EPFEM_CUDA_TRY(w.alloc(&w.p, (size_t)m));  // restricted solution
+  EPFEM_CUDA_TRY(w.alloc(&w.partial, 2 * kBlocks));
+  EPFEM_CUDA_TRY(w.alloc(&w.sc, 8));
+  r = w.r;
+  Ax = w.Ap;
+  bf = w.z;
+  xf = w.p;
+  k_free_fill<<<gb, kThreads, 0, st>>>(n, rp, ci, v, mask, fidx, frp, fci, fv);
+  EPFEM_CUDA_TRY(cudaGetLastError());
+  void* handle = nullptr;
+  void* descr = nullptr;
+  struct Handles {
+    const SpApi& a;
+    void** h;
+    void** d;
+    ~Handles() {
+      if (*d) a.descr_destroy(*d);
+      if (*h) a.destroy(*h);
+    }
+  } hs{api, &handle, &descr};
+  if (api.create(&handle) != 0 || api.descr_create(&descr) != 0)
+    return fail(EPFEM_ERR_SOLVER, "restricted_solve: cuSOLVER initialisation failed");
+  api.set_stream(handle, st);
+  api.set_type(descr, 0);  // CUSPARSE_MATRIX_TYPE_GENERAL (both triangles stored)
+  api.set_base(descr, 0);  // CUSPARSE_INDEX_BASE_ZERO
+  auto residual = [&](double* rr) -> int {  // r = M (b - K x); rr = |r| / |M b|
+    k_spmv_masked<<<grid_rows(n), kThreads, 0, st>>>(n, rp, ci, v, mask, x_out, Ax);
+    k_resid<<<gb, kThreads, 0, st>>>(n, mask, b, Ax, r);
+    const unsigned gd = (unsigned)std::min<int64_t>(kBlocks, (n + kThreads - 1) / kThreads);
+    k_dot2<<<gd, kThreads, 0, st>>>(n, r, r, b, b, w.partial);
+    k_finish<<<1, kFinish, 0, st>>>(w.partial, gd, w.sc, 2);
+    double h[8];
+    EPFEM_CUDA_TRY(cudaMemcpyAsync(h, w.sc, sizeof(h), cudaMemcpyDeviceToHost, st));
+    EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+    // masked b.b (k_dot2's second dot is unmasked): |M b| from the first residual
+    *rr = h[S_RZ];
+    return 0;
+  };
+  // the first solve has x = 0, so its residual norm is |M b|
+  double rr = 0.0;
+  if (int rc = residual(&rr)) return rc;
+  const double bnorm = std::sqrt(rr);
+  if (bnorm == 0.0) return 0;
+  bool qr = false;
+  for (int sweep = 0; sweep < 4; ++sweep) {
+    k_gather_free<<<gb, kThreads, 0, st>>>(n, mask, fidx, r, bf);
+    int sing = -1;
+    int rc = qr ? api.qr(handle, m, nnz, descr, fv, frp, fci, bf, 1e-14, 2, xf, &sing)
+                : api.chol(handle, m, nnz, descr, fv, frp, fci, bf, 1e-14, 2, xf, &sing);
+    if (rc != 0) return fail(EPFEM_ERR_SOLVER, "restricted_solve: factorization failed");
+    if (sing >= 0 && !qr) {  // not positive definite: QR on the same system
+      qr = true;
+      --sweep;
+      continue;
+    }
+    if (sing >= 0) return fail(EPFEM_ERR_SOLVER, "restricted_solve: factorization failed");
+    k_scatter_add_free<<<gb, kThreads, 0, st>>>(n, mask, fidx, xf, x_out);
+    EPFEM_CUDA_TRY(cudaGetLastError());
+    *sweeps_out = sweep + 1;
+    if (int rc2 = residual(&rr)) return rc2;
+    *residual_out = std::sqrt(rr) / bnorm;
+    if (!(*residual_out > rel_tol)) break;  // refinement sweeps keep the residual contract
+  }
   return 0;
 }
 

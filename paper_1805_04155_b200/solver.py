@@ -5,9 +5,10 @@
 Every iteration stays on the device: strains E = B u (K8), the step with its
 internal forces (constitutive update, tangent K, F = B^T (w S);
 epfem_newton_step_f), the restricted solve of K[free, free] du = (f_ext -
-F)[free] (Jacobi-preconditioned CG, epfem_restricted_solve: the reference's
-LinearSolver::conjugate_gradient; there is no direct sparse factorisation on
-the device), and the energy-norm stopping test with K_elast.  The host reads
+F)[free] (the reference's default LinearSolver::direct: device sparse
+Cholesky + refinement, epfem_restricted_solve_direct; or its
+LinearSolver::conjugate_gradient: Jacobi-preconditioned device CG,
+epfem_restricted_solve), and the energy-norm stopping test with K_elast.  The host reads
 back only the scalars of the stopping test.
 """
 from __future__ import annotations
@@ -44,13 +45,13 @@ class LinearSolver(enum.Enum):
 
 @dataclass
 class SolveSettings:
-    """linalg.hpp:19-22.  ``direct`` (the reference's SimplicialLDLT +
-    refinement sweeps, linalg.cpp:84-96) has no device counterpart here: the
-    same Jacobi CG runs under the same tolerance contract, with a warning
-    (once per process) and ``SolveInfo.substituted`` / the time-step record's
-    ``direct_substituted`` saying so.  Near a limit load CG may then need many
-    more iterations than the direct solve, or fail the tolerance where
-    LDLT + refinement would pass."""
+    """linalg.hpp:19-22.  ``direct`` (the default, the reference's
+    SimplicialLDLT + up to three refinement sweeps, linalg.cpp:84-96) runs
+    epfem_restricted_solve_direct: K[free, free] formed on the device, sparse
+    Cholesky (QR when not positive definite) from cuSOLVER, refinement on the
+    true residual.  Only when cuSOLVER cannot be loaded does the Jacobi CG
+    stand in, with a warning (once per process) and ``SolveInfo.substituted``
+    / the time-step record's ``direct_substituted`` saying so."""
     method: LinearSolver = LinearSolver.direct
     rel_tol: float = 1e-10
 
@@ -125,15 +126,31 @@ def restricted_solve(K: CsrMatrix, rhs: torch.Tensor, free_mask: Optional[torch.
     n = K.n
     if rhs.numel() != n:
         raise Error("restricted_solve: dimension mismatch")
-    substituted = settings.method == LinearSolver.direct
-    if substituted and not _warned_direct:
-        _warned_direct = True
-        warnings.warn("restricted_solve: LinearSolver.direct (SimplicialLDLT) has no device implementation; "
-                      "Jacobi-preconditioned CG runs under the same tolerance", RuntimeWarning, stacklevel=2)
     dev = K.values.device
     ctx = ctx or default_context(dev)
     ctx.use_current_stream()
     x = torch.empty((n,), dtype=torch.float64, device=dev)
+    substituted = False
+    if settings.method == LinearSolver.direct and block == 1:
+        sweeps, res = C.c_int(), C.c_double()
+        rc = L.lib().epfem_restricted_solve_direct(ctx.handle, n, _ptr(K.row_ptr), _ptr(K.col_idx),
+                                                   _ptr(K.values), _ptr(rhs.contiguous()),
+                                                   _ptr(_mask_u8(free_mask, n, dev)), settings.rel_tol, _ptr(x),
+                                                   C.byref(sweeps), C.byref(res))
+        if rc != 6:  # EPFEM_ERR_UNSUPPORTED: no cuSOLVER (or past int32 sizes) -> CG below
+            if info is not None:
+                info.iterations, info.residual, info.substituted = sweeps.value, res.value, False
+            if rc == 7:  # EPFEM_ERR_SOLVER
+                raise SolverError(L.last_error(), res.value)
+            if rc != 0:
+                raise Error(L.last_error())
+            return x
+        substituted = True
+        if not _warned_direct:
+            _warned_direct = True
+            warnings.warn("restricted_solve: LinearSolver.direct is unavailable on this device ("
+                          + L.last_error() + "); Jacobi-preconditioned CG runs under the same tolerance",
+                          RuntimeWarning, stacklevel=2)
     it, res = C.c_int64(), C.c_double()
     rc = L.lib().epfem_restricted_solve_blocked(ctx.handle, n, _ptr(K.row_ptr), _ptr(K.col_idx),
                                                 _ptr(K.values), _ptr(rhs.contiguous()),

@@ -54,10 +54,16 @@ def test_restricted_solve_random_spd(cuda):
 
 
 def test_restricted_solve_reports_singular_systems(cuda):
-    """test_linalg.cpp:153-162: rank-deficient K, incompatible rhs -> SolverError."""
-    from paper_1805_04155_b200.solver import SolverError, restricted_solve
+    """test_linalg.cpp:153-162: rank-deficient K, incompatible rhs -> SolverError:
+    with the default direct method the factorisation fails (the reference's
+    SimplicialLDLT meets a zero pivot: "factorization failed", linalg.cpp:86-88);
+    with conjugate gradients the residual stays above the tolerance."""
+    from paper_1805_04155_b200.solver import LinearSolver, SolveSettings, SolverError, restricted_solve
+    rhs = torch.tensor([1.0, -1.0], dtype=torch.float64, device=cuda)
+    with pytest.raises(SolverError, match="restricted_solve: factorization failed"):
+        restricted_solve(_csr(np.ones((2, 2)), cuda), rhs)
     with pytest.raises(SolverError, match="restricted_solve: residual .* above tolerance"):
-        restricted_solve(_csr(np.ones((2, 2)), cuda), torch.tensor([1.0, -1.0], dtype=torch.float64, device=cuda))
+        restricted_solve(_csr(np.ones((2, 2)), cuda), rhs, None, SolveSettings(LinearSolver.conjugate_gradient))
 
 
 def test_energy_norm(cuda):
@@ -188,7 +194,7 @@ def test_restricted_solve_block_jacobi(cuda, block):
     same restricted SPD system as the scalar one, to the same tolerance, with
     fixed dofs zero; a dimension not divisible by the block is rejected."""
     import paper_1805_04155_b200 as P
-    from paper_1805_04155_b200.solver import SolveInfo, SolveSettings, restricted_solve
+    from paper_1805_04155_b200.solver import LinearSolver, SolveInfo, SolveSettings, restricted_solve
     rng = np.random.default_rng(7 + block)
     n = 60 * block
     A = rng.standard_normal((n, n))
@@ -198,7 +204,7 @@ def test_restricted_solve_block_jacobi(cuda, block):
     b = rng.standard_normal(n)
     free = rng.random(n) > 0.2
     K = _csr(A, cuda)
-    s = SolveSettings(rel_tol=1e-12)
+    s = SolveSettings(LinearSolver.conjugate_gradient, rel_tol=1e-12)
     i1, ib = SolveInfo(), SolveInfo()
     x1 = restricted_solve(K, torch.from_numpy(b).to(cuda), torch.from_numpy(free).to(cuda), s, info=i1).cpu().numpy()
     xb = restricted_solve(K, torch.from_numpy(b).to(cuda), torch.from_numpy(free).to(cuda), s, info=ib,
@@ -212,3 +218,33 @@ def test_restricted_solve_block_jacobi(cuda, block):
     assert ib.residual <= 1e-12
     with pytest.raises(P.Error, match="dimension mismatch"):
         restricted_solve(_csr(A[:n - 1, :n - 1], cuda), torch.from_numpy(b[:n - 1]).to(cuda), None, s, block=block)
+
+
+def test_restricted_solve_direct(cuda):
+    """LinearSolver::direct (linalg.cpp:84-96) on the device: a random SPD
+    system with a random free set vs a dense solve, zero on fixed dofs,
+    deterministic; an indefinite (not positive definite) restricted system
+    through the QR fallback; the reference's singular case raises SolverError
+    (tests/test_linalg.cpp:153-162)."""
+    from paper_1805_04155_b200.solver import SolveInfo, SolveSettings, SolverError, restricted_solve
+    rng = np.random.default_rng(31)
+    n = 80
+    A = rng.uniform(-1, 1, (n, n))
+    Kd = A.T @ A + 0.5 * np.eye(n)
+    rhs = rng.uniform(-1, 1, n)
+    mask = rng.uniform(size=n) < 0.7
+    info = SolveInfo()
+    x = restricted_solve(_csr(Kd, cuda), torch.from_numpy(rhs).to(cuda), torch.from_numpy(mask).to(cuda),
+                         SolveSettings(rel_tol=1e-12), info=info).cpu().numpy()
+    f = np.nonzero(mask)[0]
+    xf = np.linalg.solve(Kd[np.ix_(f, f)], rhs[f])
+    assert np.abs(x[f] - xf).max() <= 1e-10 * np.abs(xf).max()
+    assert np.all(x[~mask] == 0.0) and not info.substituted and info.residual <= 1e-12 and info.iterations >= 1
+    x2 = restricted_solve(_csr(Kd, cuda), torch.from_numpy(rhs).to(cuda), torch.from_numpy(mask).to(cuda),
+                          SolveSettings(rel_tol=1e-12)).cpu().numpy()
+    assert np.array_equal(x.view(np.uint64), x2.view(np.uint64))
+    # symmetric indefinite: Cholesky declines, QR solves
+    S = rng.uniform(-1, 1, (n, n))
+    S = 0.5 * (S + S.T) + np.diag(np.where(np.arange(n) % 2 == 0, 3.0, -3.0))
+    xs = restricted_solve(_csr(S, cuda), torch.from_numpy(rhs).to(cuda), None, SolveSettings(rel_tol=1e-10)).cpu().numpy()
+    assert np.abs(xs - np.linalg.solve(S, rhs)).max() <= 1e-8 * np.abs(np.linalg.solve(S, rhs)).max()
