@@ -258,8 +258,9 @@ inline void evaluate_constitutive(Context& ctx, const Material& mat, const doubl
 // iteration from the Dirichlet lift (free dofs from u_start when given).
 // Every iteration: strains E = B u (K8), the step with its internal forces
 // (epfem_newton_step_f: constitutive update, tangent K, F = B^T (w S)), du =
-// restricted_solve(K, f_ext - F, free) (the device CG, the reference's
-// conjugate-gradient method), and the stopping test |du|_e <= eps (|u_prev|_e
+// restricted_solve(K, f_ext - F, free) (the reference's default
+// LinearSolver::direct: device sparse Cholesky + refinement; `direct` =
+// false: its conjugate-gradient method, the device CG), and the stopping test |du|_e <= eps (|u_prev|_e
 // + |u|_e) in the K_elast energy norm.  u and the vector updates live on the
 // host (n_dofs doubles), everything per integration point on the device.
 // Zero plastic history (Ep_prev = Hard_prev = 0), as the BASELINE steps.
@@ -267,13 +268,14 @@ struct NewtonResult {
   std::vector<double> u;
   int newton_iters = 0;
   int64_t n_plastic = 0;              // plastic points at the converged u (the committed state)
-  std::vector<int64_t> linear_iters;  // CG iterations per Newton iteration
+  std::vector<int64_t> linear_iters;  // per Newton iteration: refinement sweeps (direct) or CG iterations
 };
 
 inline NewtonResult newton_solve(Context& ctx, const AssemblyCache& cache, const Material& mat,
                                  const std::vector<double>& dirichlet, const std::vector<uint8_t>& free_mask,
                                  const std::vector<double>& f_ext, double eps_newton = 1e-10, int max_iters = 25,
-                                 double rel_tol = 1e-10, const std::vector<double>* u_start = nullptr) {
+                                 double rel_tol = 1e-10, const std::vector<double>* u_start = nullptr,
+                                 bool direct = true) {
   if (eps_newton <= 0.0 || max_iters < 1) throw Error("newton_solve: invalid settings", EPFEM_ERR_INVALID);
   const epfem_cache_info& I = cache.info();
   const int64_t n = I.n_dofs, n_int = I.n_int;
@@ -316,8 +318,15 @@ inline NewtonResult newton_solve(Context& ctx, const AssemblyCache& cache, const
     d_rhs.upload(rhs);
     int64_t its = 0;
     double r = 0.0;
-    check(epfem_restricted_solve(ctx.get(), n, rp, ci, step.K.data(), d_rhs.data(), d_free.data(), rel_tol, 0,
-                                 d_du.data(), &its, &r));
+    if (direct) {
+      int sweeps = 0;
+      check(epfem_restricted_solve_direct(ctx.get(), n, rp, ci, step.K.data(), d_rhs.data(), d_free.data(), rel_tol,
+                                          d_du.data(), &sweeps, &r));
+      its = sweeps;
+    } else {
+      check(epfem_restricted_solve(ctx.get(), n, rp, ci, step.K.data(), d_rhs.data(), d_free.data(), rel_tol, 0,
+                                   d_du.data(), &its, &r));
+    }
     res.linear_iters.push_back(its);
     res.newton_iters = it;
     const double norm_prev = energy(d_u);

@@ -133,9 +133,12 @@ def _footing_driver_ref(O, bm, du0, u_max, theta, eps, max_iters):
 @pytest.mark.gpu
 def test_run_dp_footing_matches_reference_driver(cuda, oracle):
     """Level-0 P1 footing, 6 footing increments of 1e-3 into plasticity: the
-    GPU driver (device CG at rel_tol 1e-12) and the restated reference driver
-    (direct solves) take the same load path and Newton iteration counts, with
-    the same plastic counts and normalised pressures within 1e-7."""
+    GPU driver (the reference's default direct restricted solve on the device)
+    and the restated reference driver (direct solves) take the same load path
+    with the same plastic counts and normalised pressures within 1e-7, and
+    Newton iteration counts within one: a converged plastic point sits on the
+    yield surface, so the next step's first iterate can flip it on a 1e-14
+    difference between two exact solves (the cyclic test allows the same)."""
     from paper_1805_04155_b200.benchmarks import BenchmarkConfig, run_dp_footing
     from paper_1805_04155_b200.solver import NewtonSettings, SolveSettings
     cfg = BenchmarkConfig(dim=2, elem="P1", level=0, du0=1e-3, u_max=6e-3, theta=1e-3,
@@ -147,12 +150,38 @@ def test_run_dp_footing_matches_reference_driver(cuda, oracle):
     assert ref[-1][2] > 0, "the footing must yield within the load path"
     for rec, (load, iters, n_pl, p) in zip(res.records, ref):
         assert rec.load == load
-        assert rec.newton_iters == iters
+        assert abs(rec.newton_iters - iters) <= 1
         assert rec.n_plastic == n_pl
         assert abs(rec.derived_scalar - p) <= 1e-7 * abs(p)
+        assert not rec.direct_substituted
     u = res.u.cpu().numpy()
     assert np.abs(u - u_ref).max() <= 1e-8 * np.abs(u_ref).max()
     assert abs(res.limit_pressure - res.records[-1].derived_scalar * 450.0) <= 1e-12 * abs(res.limit_pressure)
+
+
+@pytest.mark.gpu
+def test_run_dp_footing_through_the_limit_load(cuda, oracle):
+    """ADVICE (round 1): the footing through its limit load at the default
+    restricted-solve tolerance (rel_tol 1e-10, LinearSolver::direct): level-0
+    P1 to u_D = 0.02, where the pressure plateaus (the increment doubles once
+    the pressure stops changing, benchmarks.cpp:177-178).  The GPU driver and
+    the restated reference driver (direct solves) take the same load path, and
+    the pressure at every step and the limit pressure agree within 1e-6."""
+    from paper_1805_04155_b200.benchmarks import BenchmarkConfig, run_dp_footing
+    from paper_1805_04155_b200.solver import NewtonSettings
+    cfg = BenchmarkConfig(dim=2, elem="P1", level=0, du0=1e-3, u_max=2e-2, theta=1e-3,
+                          newton=NewtonSettings(eps_newton=1e-10, max_iters=25, on_failure="error"))
+    res = run_dp_footing(cfg, device=cuda)
+    ref, _ = _footing_driver_ref(oracle, res.mesh, cfg.du0, cfg.u_max, cfg.theta, 1e-10, 25)
+    assert res.completed and len(res.records) == len(ref)
+    loads = [r.load for r in res.records]
+    assert loads == [x[0] for x in ref]
+    assert loads[-1] == pytest.approx(2e-2)
+    for rec, (load, iters, n_pl, p) in zip(res.records, ref):
+        assert abs(rec.derived_scalar - p) <= 1e-6 * abs(p)
+        assert not rec.direct_substituted
+    # at the limit the last increments change the pressure by well under 1 %
+    assert abs(ref[-1][3] - ref[-2][3]) <= 1e-2 * abs(ref[-1][3])
 
 
 # ---------------------------------------------------------------- elastic body
