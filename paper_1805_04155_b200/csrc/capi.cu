@@ -39,6 +39,7 @@ struct epfem_ctx {
   void* comm = nullptr;   // ncclComm_t of the multi-GPU exchange
   bool own_comm = false;
   int world = 1, rank = 0;
+  void* direct = nullptr;  // cached restricted pattern + symbolic factorisation (solve.cu)
 };
 
 struct epfem_cache {
@@ -196,6 +197,7 @@ int epfem_ctx_destroy(epfem_ctx* ctx) {
   if (!ctx) return 0;
   DeviceGuard guard(ctx);
   if (ctx->own_comm) nccl_comm_destroy(ctx->comm);
+  if (ctx->direct) direct_cache_free(ctx->direct);
   if (ctx->err) cudaFree(ctx->err);
   delete ctx;
   return 0;
@@ -792,7 +794,8 @@ int epfem_restricted_solve_direct(epfem_ctx* ctx, int64_t n, const int64_t* row_
     return fail(EPFEM_ERR_INVALID, "restricted_solve: dimension mismatch");
   int sw = 0;
   double res = 0.0;
-  if (int rc = direct_solve(n, row_ptr, col_idx, values, free_mask, rhs, x, rel_tol, ctx->stream, &sw, &res))
+  if (int rc = direct_solve(n, row_ptr, col_idx, values, free_mask, rhs, x, rel_tol, ctx->stream, &ctx->direct, &sw,
+                            &res))
     return rc;
   if (sweeps) *sweeps = sw;
   if (residual) *residual = res;

@@ -97,8 +97,9 @@ void nccl_comm_destroy(void* comm);
 int nccl_exchange(void* comm, int world, int rank, cudaStream_t st, uint8_t* flags, double* D, int64_t send_begin,
                   int64_t send_end, int64_t recv_begin, int64_t recv_end);
 int direct_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, const uint8_t* mask,
-                 const double* b, double* x_out, double rel_tol, cudaStream_t st, int* sweeps_out,
+                 const double* b, double* x_out, double rel_tol, cudaStream_t st, void** cache_slot, int* sweeps_out,
                  double* residual_out);
+void direct_cache_free(void* cache);
 int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, const uint8_t* mask,
              const double* b, double* x_out, double rel_tol, int64_t max_iters, cudaStream_t st,
              int64_t* iters_out, double* residual_out, int block = 1);

@@ -429,31 +429,56 @@ int energy_norm(int64_t n, const int64_t* rp, const int32_t* ci, const double* v
 // LinearSolver::direct (linalg.cpp:84-96): the reference factorises
 // K[free, free] (SimplicialLDLT) and applies up to three refinement sweeps.
 // Here: the restricted matrix is formed on the device (free-index map by a
-// prefix sum, per-row counts, fill), factorised and solved by cuSOLVER's
-// sparse Cholesky (cusolverSpDcsrlsvchol, symamd reordering) -- QR
-// (cusolverSpDcsrlsvqr) when the Cholesky finds the matrix not positive
-// definite -- then up to three refinement sweeps on the true residual
-// |M (b - K x)| / |M b| with the deterministic masked SpMV above.  cuSOLVER /
-// cuSPARSE are loaded at run time (dlopen), so the library has no link
-// dependency on them.
+// prefix sum, per-row counts, fill); cuSOLVER's sparse Cholesky factorises it
+// on the device (cusolverSpXcsrcholAnalysis once per pattern and free mask,
+// cached in the context, then cusolverSpDcsrcholFactor / Solve per call);
+// when the factor meets a zero pivot (not positive definite) that call falls
+// back to QR (cusolverSpDcsrlsvqr).  Then up to three refinement sweeps on the
+// true residual |M (b - K x)| / |M b| with the deterministic masked SpMV
+// above.  cuSOLVER / cuSPARSE are loaded at run time (dlopen), so the library
+// has no link dependency on them.
 namespace {
 
 struct SpApi {
   using Create = int (*)(void**);
   using Destroy = int (*)(void*);
   using SetStream = int (*)(void*, cudaStream_t);
-  using Solve = int (*)(void*, int, int, const void*, const double*, const int*, const int*, const double*, double,
-                        int, double*, int*);
-  using DescrCreate = int (*)(void**);
-  using DescrDestroy = int (*)(void*);
-  using DescrSet = int (*)(void*, int);
-  Create create = nullptr;
-  Destroy destroy = nullptr;
+  using Lsv = int (*)(void*, int, int, const void*, const double*, const int*, const int*, const double*, double,
+                      int, double*, int*);
+  using Analysis = int (*)(void*, int, int, const void*, const int*, const int*, void*);
+  using BufInfo = int (*)(void*, int, int, const void*, const double*, const int*, const int*, void*, size_t*,
+                          size_t*);
+  using Factor = int (*)(void*, int, int, const void*, const double*, const int*, const int*, void*, void*);
+  using ZeroPivot = int (*)(void*, void*, double, int*);
+  using CholSolve = int (*)(void*, int, const double*, double*, void*, void*);
+  Create create = nullptr, info_create = nullptr, descr_create = nullptr;
+  Destroy destroy = nullptr, info_destroy = nullptr, descr_destroy = nullptr;
   SetStream set_stream = nullptr;
-  Solve chol = nullptr, qr = nullptr;
-  DescrCreate descr_create = nullptr;
-  DescrDestroy descr_destroy = nullptr;
+  Lsv qr = nullptr;
+  Analysis analysis = nullptr;
+  BufInfo buf_info = nullptr;
+  Factor factor = nullptr;
+  ZeroPivot zero_pivot = nullptr;
+  CholSolve solve = nullptr;
+  using DescrSet = int (*)(void*, int);
   DescrSet set_type = nullptr, set_base = nullptr;
+  // dense cuSOLVER (the restricted systems of the drivers are small)
+  using DnBuf = int (*)(void*, int, int, double*, int, int*);      // potrf_bufferSize(h, uplo, n, A, lda, lwork)
+  using DnPotrf = int (*)(void*, int, int, double*, int, double*, int, int*);
+  using DnPotrs = int (*)(void*, int, int, int, const double*, int, double*, int, int*);
+  using DnGetrfBuf = int (*)(void*, int, int, double*, int, int*);
+  using DnGetrf = int (*)(void*, int, int, double*, int, double*, int*, int*);
+  using DnGetrs = int (*)(void*, int, int, int, const double*, int, const int*, double*, int, int*);
+  Create dn_create = nullptr;
+  Destroy dn_destroy = nullptr;
+  SetStream dn_set_stream = nullptr;
+  DnBuf potrf_buf = nullptr;
+  DnPotrf potrf = nullptr;
+  DnPotrs potrs = nullptr;
+  DnGetrfBuf getrf_buf = nullptr;
+  DnGetrf getrf = nullptr;
+  DnGetrs getrs = nullptr;
+  bool dense_ok = false;
   bool ok = false;
 };
 
@@ -468,16 +493,35 @@ const SpApi& sp_api() {
     void* hs = open("libcusparse.so.12", "/usr/local/cuda/lib64/libcusparse.so.12");
     void* hv = open("libcusolver.so.11", "/usr/local/cuda/lib64/libcusolver.so.11");
     if (!hs || !hv) return;
-    api.create = reinterpret_cast<SpApi::Create>(dlsym(hv, "cusolverSpCreate"));
-    api.destroy = reinterpret_cast<SpApi::Destroy>(dlsym(hv, "cusolverSpDestroy"));
-    api.set_stream = reinterpret_cast<SpApi::SetStream>(dlsym(hv, "cusolverSpSetStream"));
-    api.chol = reinterpret_cast<SpApi::Solve>(dlsym(hv, "cusolverSpDcsrlsvchol"));
-    api.qr = reinterpret_cast<SpApi::Solve>(dlsym(hv, "cusolverSpDcsrlsvqr"));
-    api.descr_create = reinterpret_cast<SpApi::DescrCreate>(dlsym(hs, "cusparseCreateMatDescr"));
-    api.descr_destroy = reinterpret_cast<SpApi::DescrDestroy>(dlsym(hs, "cusparseDestroyMatDescr"));
-    api.set_type = reinterpret_cast<SpApi::DescrSet>(dlsym(hs, "cusparseSetMatType"));
-    api.set_base = reinterpret_cast<SpApi::DescrSet>(dlsym(hs, "cusparseSetMatIndexBase"));
-    api.ok = api.create && api.destroy && api.set_stream && api.chol && api.qr && api.descr_create &&
+    auto sym = [](void* h, const char* n) { return dlsym(h, n); };
+    api.create = reinterpret_cast<SpApi::Create>(sym(hv, "cusolverSpCreate"));
+    api.destroy = reinterpret_cast<SpApi::Destroy>(sym(hv, "cusolverSpDestroy"));
+    api.set_stream = reinterpret_cast<SpApi::SetStream>(sym(hv, "cusolverSpSetStream"));
+    api.qr = reinterpret_cast<SpApi::Lsv>(sym(hv, "cusolverSpDcsrlsvqr"));
+    api.info_create = reinterpret_cast<SpApi::Create>(sym(hv, "cusolverSpCreateCsrcholInfo"));
+    api.info_destroy = reinterpret_cast<SpApi::Destroy>(sym(hv, "cusolverSpDestroyCsrcholInfo"));
+    api.analysis = reinterpret_cast<SpApi::Analysis>(sym(hv, "cusolverSpXcsrcholAnalysis"));
+    api.buf_info = reinterpret_cast<SpApi::BufInfo>(sym(hv, "cusolverSpDcsrcholBufferInfo"));
+    api.factor = reinterpret_cast<SpApi::Factor>(sym(hv, "cusolverSpDcsrcholFactor"));
+    api.zero_pivot = reinterpret_cast<SpApi::ZeroPivot>(sym(hv, "cusolverSpDcsrcholZeroPivot"));
+    api.solve = reinterpret_cast<SpApi::CholSolve>(sym(hv, "cusolverSpDcsrcholSolve"));
+    api.descr_create = reinterpret_cast<SpApi::Create>(sym(hs, "cusparseCreateMatDescr"));
+    api.descr_destroy = reinterpret_cast<SpApi::Destroy>(sym(hs, "cusparseDestroyMatDescr"));
+    api.set_type = reinterpret_cast<SpApi::DescrSet>(sym(hs, "cusparseSetMatType"));
+    api.set_base = reinterpret_cast<SpApi::DescrSet>(sym(hs, "cusparseSetMatIndexBase"));
+    api.dn_create = reinterpret_cast<SpApi::Create>(sym(hv, "cusolverDnCreate"));
+    api.dn_destroy = reinterpret_cast<SpApi::Destroy>(sym(hv, "cusolverDnDestroy"));
+    api.dn_set_stream = reinterpret_cast<SpApi::SetStream>(sym(hv, "cusolverDnSetStream"));
+    api.potrf_buf = reinterpret_cast<SpApi::DnBuf>(sym(hv, "cusolverDnDpotrf_bufferSize"));
+    api.potrf = reinterpret_cast<SpApi::DnPotrf>(sym(hv, "cusolverDnDpotrf"));
+    api.potrs = reinterpret_cast<SpApi::DnPotrs>(sym(hv, "cusolverDnDpotrs"));
+    api.getrf_buf = reinterpret_cast<SpApi::DnGetrfBuf>(sym(hv, "cusolverDnDgetrf_bufferSize"));
+    api.getrf = reinterpret_cast<SpApi::DnGetrf>(sym(hv, "cusolverDnDgetrf"));
+    api.getrs = reinterpret_cast<SpApi::DnGetrs>(sym(hv, "cusolverDnDgetrs"));
+    api.dense_ok = api.dn_create && api.dn_destroy && api.dn_set_stream && api.potrf_buf && api.potrf && api.potrs &&
+                   api.getrf_buf && api.getrf && api.getrs;
+    api.ok = api.create && api.destroy && api.set_stream && api.qr && api.info_create && api.info_destroy &&
+             api.analysis && api.buf_info && api.factor && api.zero_pivot && api.solve && api.descr_create &&
              api.descr_destroy && api.set_type && api.set_base;
   });
   return api;
@@ -487,6 +531,17 @@ const SpApi& sp_api() {
 __global__ void k_free_flags(int64_t n, const uint8_t* __restrict__ mask, int* flag) {
   for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads)
     flag[i] = (!mask || mask[i]) ? 1 : 0;
+}
+// number of positions where two masks differ (null = all free)
+__global__ void k_mask_diff(int64_t n, const uint8_t* __restrict__ a, const uint8_t* __restrict__ b, int* out) {
+  int c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads)
+    c += ((!a || a[i]) ? 1 : 0) != ((!b || b[i]) ? 1 : 0);
+  if (c) atomicAdd(out, c);
+}
+__global__ void k_copy_mask(int64_t n, const uint8_t* __restrict__ mask, uint8_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads)
+    out[i] = (!mask || mask[i]) ? 1 : 0;
 }
 // per free row: its free entries (counts indexed by the row's free index)
 __global__ void k_free_row_count(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
@@ -498,7 +553,8 @@ __global__ void k_free_row_count(int64_t n, const int64_t* __restrict__ rp, cons
     cnt[fidx[i]] = c;
   }
 }
-// fill K[free, free] (columns stay sorted: the free-index map is monotone)
+// fill K[free, free] (columns stay sorted: the free-index map is monotone);
+// fci == nullptr: values only (the pattern is cached)
 __global__ void k_free_fill(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                             const double* __restrict__ v, const uint8_t* __restrict__ mask,
                             const int* __restrict__ fidx, const int* __restrict__ frp, int* fci, double* fv) {
@@ -508,12 +564,18 @@ __global__ void k_free_fill(int64_t n, const int64_t* __restrict__ rp, const int
     for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
       const int32_t c = ci[k];
       if (!mask || mask[c]) {
-        fci[o] = fidx[c];
+        if (fci) fci[o] = fidx[c];
         fv[o] = v[k];
         ++o;
       }
     }
   }
+}
+// the restricted CSR into a dense column-major m x m matrix (zeroed before)
+__global__ void k_dense_scatter(int m, const int* __restrict__ frp, const int* __restrict__ fci,
+                                const double* __restrict__ fv, double* A) {
+  for (int r = blockIdx.x * kThreads + threadIdx.x; r < m; r += gridDim.x * kThreads)
+    for (int o = frp[r]; o < frp[r + 1]; ++o) A[(size_t)fci[o] * m + r] = fv[o];
 }
 __global__ void k_gather_free(int64_t n, const uint8_t* __restrict__ mask, const int* __restrict__ fidx,
                               const double* __restrict__ r, double* rf) {
@@ -529,123 +591,223 @@ __global__ void k_scatter_add_free(int64_t n, const uint8_t* __restrict__ mask, 
 
 }  // namespace
 
+// The restricted pattern and its symbolic Cholesky analysis, cached per
+// context for the last (matrix pattern, free mask) seen: a Newton loop
+// factorises the same pattern every iteration.
+struct DirectCache {
+  const int64_t* rp = nullptr;
+  const int32_t* ci = nullptr;
+  int64_t n = -1;
+  int m = 0, nnz = 0;
+  uint8_t* mask = nullptr;  // the cached free mask (1 byte per row)
+  int *fidx = nullptr, *frp = nullptr, *fci = nullptr, *cnt = nullptr;
+  double* fv = nullptr;
+  void *handle = nullptr, *descr = nullptr, *info = nullptr, *buf = nullptr;
+  bool analysed = false;
+  // dense path (m <= kDenseMax): factor, workspace, pivots, status word
+  void* dn = nullptr;
+  double *A = nullptr, *work = nullptr;
+  int *ipiv = nullptr, *dinfo = nullptr;
+  int lwork = 0;
+  void release() {
+    const SpApi& api = sp_api();
+    if (info) api.info_destroy(info);
+    info = nullptr;
+    for (void* p : {(void*)mask, (void*)fidx, (void*)frp, (void*)fci, (void*)cnt, (void*)fv, buf, (void*)A,
+                    (void*)work, (void*)ipiv, (void*)dinfo})
+      if (p) cudaFree(p);
+    A = work = nullptr;
+    ipiv = dinfo = nullptr;
+    lwork = 0;
+    mask = nullptr;
+    fidx = frp = fci = cnt = nullptr;
+    fv = nullptr;
+    buf = nullptr;
+    analysed = false;
+    n = -1;
+  }
+  ~DirectCache() {
+    release();
+    const SpApi& api = sp_api();
+    if (descr) api.descr_destroy(descr);
+    if (handle) api.destroy(handle);
+    if (dn) api.dn_destroy(dn);
+  }
+};
+
+// restricted systems up to this size are factorised dense (cusolverDn potrf,
+// getrf when not positive definite): the drivers' systems are small, and the
+// dense factorisation on the device is far faster than the sparse one there
+constexpr int kDenseMax = 16384;
+
+void direct_cache_free(void* c) { delete static_cast<DirectCache*>(c); }
+
 int direct_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, const uint8_t* mask,
-                 const double* b, double* x_out, double rel_tol, cudaStream_t caller, int* sweeps_out,
+                 const double* b, double* x_out, double rel_tol, cudaStream_t st, void** cache_slot, int* sweeps_out,
                  double* residual_out) {
   *sweeps_out = 0;
   *residual_out = 0.0;
-  EPFEM_CUDA_TRY(cudaMemsetAsync(x_out, 0, sizeof(double) * std::max<int64_t>(n, 1), caller));
+  EPFEM_CUDA_TRY(cudaMemsetAsync(x_out, 0, sizeof(double) * std::max<int64_t>(n, 1), st));
   if (n == 0) return 0;
   const SpApi& api = sp_api();
   if (!api.ok) return fail(EPFEM_ERR_UNSUPPORTED, "restricted_solve: cuSOLVER sparse is not available");
   if (n >= INT32_MAX) return fail(EPFEM_ERR_UNSUPPORTED, "restricted_solve: direct solve needs int32 sizes");
-  cudaStream_t st = caller;
-  Work w(st);
-  int *fidx = nullptr, *cnt = nullptr, *frp = nullptr, *fci = nullptr;
-  auto ialloc = [&](int** p, size_t k) { return cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(int) * k, st); };
-  struct IntBufs {
-    cudaStream_t s;
-    std::vector<int*> p;
-    ~IntBufs() {
-      for (int* q : p)
-        if (q) cudaFreeAsync(q, s);
-    }
-  } ib{st, {}};
-  const unsigned gb = (unsigned)std::min<int64_t>(kBlocks * 4, (n + kThreads - 1) / kThreads);
-  EPFEM_CUDA_TRY(ialloc(&fidx, n + 1));
-  ib.p.push_back(fidx);
-  // free-index map: exclusive prefix sum of the free flags
-  EPFEM_CUDA_TRY(ialloc(&cnt, n + 1));
-  ib.p.push_back(cnt);
-  k_free_flags<<<gb, kThreads, 0, st>>>(n, mask, cnt);
-  size_t tmp_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, fidx, (int)n + 1, st);
-  void* tmp = nullptr;
-  EPFEM_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, st));
-  EPFEM_CUDA_TRY(cudaMemsetAsync(cnt + n, 0, sizeof(int), st));
-  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, fidx, (int)n + 1, st);
-  int m = 0;
-  EPFEM_CUDA_TRY(cudaMemcpyAsync(&m, fidx + n, sizeof(int), cudaMemcpyDeviceToHost, st));
-  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
-  if (m == 0) {
-    cudaFreeAsync(tmp, st);
-    return 0;
+  if (!*cache_slot) *cache_slot = new DirectCache;
+  DirectCache& dc = *static_cast<DirectCache*>(*cache_slot);
+  if (!dc.handle) {
+    if (api.create(&dc.handle) != 0 || api.descr_create(&dc.descr) != 0)
+      return fail(EPFEM_ERR_SOLVER, "restricted_solve: cuSOLVER initialisation failed");
+    api.set_type(dc.descr, 0);  // CUSPARSE_MATRIX_TYPE_GENERAL (both triangles stored)
+    api.set_base(dc.descr, 0);  // CUSPARSE_INDEX_BASE_ZERO
   }
-  // restricted CSR (int32, cuSOLVER's index type)
-  EPFEM_CUDA_TRY(ialloc(&frp, (size_t)m + 1));
-  ib.p.push_back(frp);
-  EPFEM_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * ((size_t)m + 1), st));
-  k_free_row_count<<<gb, kThreads, 0, st>>>(n, rp, ci, mask, fidx, cnt);
-  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, frp, m + 1, st);
-  int nnz = 0;
-  EPFEM_CUDA_TRY(cudaMemcpyAsync(&nnz, frp + m, sizeof(int), cudaMemcpyDeviceToHost, st));
-  EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
-  cudaFreeAsync(tmp, st);
-  EPFEM_CUDA_TRY(ialloc(&fci, (size_t)std::max(nnz, 1)));
-  ib.p.push_back(fci);
-  double *fv = nullptr, *bf = nullptr, *xf = nullptr, *r = nullptr, *Ax = nullptr;
-  EPFEM_CUDA_TRY(w.alloc(&w.binv, (size_t)std::max(nnz, 1)));  // restricted values
-  fv = w.binv;
+  api.set_stream(dc.handle, st);
+  const unsigned gb = (unsigned)std::min<int64_t>(kBlocks * 4, (n + kThreads - 1) / kThreads);
+  // same pattern and free mask as the cached analysis?
+  bool same = dc.analysed && dc.rp == rp && dc.ci == ci && dc.n == n;
+  if (same) {
+    int* diff = nullptr;
+    EPFEM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&diff), sizeof(int), st));
+    EPFEM_CUDA_TRY(cudaMemsetAsync(diff, 0, sizeof(int), st));
+    k_mask_diff<<<gb, kThreads, 0, st>>>(n, mask, dc.mask, diff);
+    int h = 0;
+    EPFEM_CUDA_TRY(cudaMemcpyAsync(&h, diff, sizeof(int), cudaMemcpyDeviceToHost, st));
+    EPFEM_CUDA_TRY(cudaFreeAsync(diff, st));
+    EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+    same = h == 0;
+  }
+  if (!same) {
+    EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+    dc.release();
+    EPFEM_CUDA_TRY(cudaMalloc(&dc.mask, n));
+    EPFEM_CUDA_TRY(cudaMalloc(&dc.fidx, sizeof(int) * (n + 1)));
+    EPFEM_CUDA_TRY(cudaMalloc(&dc.cnt, sizeof(int) * (n + 1)));
+    k_copy_mask<<<gb, kThreads, 0, st>>>(n, mask, dc.mask);
+    k_free_flags<<<gb, kThreads, 0, st>>>(n, mask, dc.cnt);
+    EPFEM_CUDA_TRY(cudaMemsetAsync(dc.cnt + n, 0, sizeof(int), st));
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, dc.cnt, dc.fidx, (int)n + 1, st);
+    void* tmp = nullptr;
+    EPFEM_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, st));
+    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, dc.cnt, dc.fidx, (int)n + 1, st);
+    EPFEM_CUDA_TRY(cudaMemcpyAsync(&dc.m, dc.fidx + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+    EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+    if (dc.m > 0) {
+      EPFEM_CUDA_TRY(cudaMalloc(&dc.frp, sizeof(int) * ((size_t)dc.m + 1)));
+      EPFEM_CUDA_TRY(cudaMemsetAsync(dc.cnt, 0, sizeof(int) * ((size_t)dc.m + 1), st));
+      k_free_row_count<<<gb, kThreads, 0, st>>>(n, rp, ci, mask, dc.fidx, dc.cnt);
+      cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, dc.cnt, dc.frp, dc.m + 1, st);
+      EPFEM_CUDA_TRY(cudaMemcpyAsync(&dc.nnz, dc.frp + dc.m, sizeof(int), cudaMemcpyDeviceToHost, st));
+      EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+      EPFEM_CUDA_TRY(cudaMalloc(&dc.fci, sizeof(int) * std::max(dc.nnz, 1)));
+      EPFEM_CUDA_TRY(cudaMalloc(&dc.fv, sizeof(double) * std::max(dc.nnz, 1)));
+      k_free_fill<<<gb, kThreads, 0, st>>>(n, rp, ci, v, mask, dc.fidx, dc.frp, dc.fci, dc.fv);
+      if (dc.m <= kDenseMax && api.dense_ok) {
+        if (!dc.dn && api.dn_create(&dc.dn) != 0)
+          return fail(EPFEM_ERR_SOLVER, "restricted_solve: cuSOLVER initialisation failed");
+        api.dn_set_stream(dc.dn, st);
+        EPFEM_CUDA_TRY(cudaMalloc(&dc.A, sizeof(double) * (size_t)dc.m * dc.m));
+        EPFEM_CUDA_TRY(cudaMalloc(&dc.ipiv, sizeof(int) * dc.m));
+        EPFEM_CUDA_TRY(cudaMalloc(&dc.dinfo, sizeof(int)));
+        int l1 = 0, l2 = 0;
+        if (api.potrf_buf(dc.dn, 0, dc.m, dc.A, dc.m, &l1) != 0 || api.getrf_buf(dc.dn, dc.m, dc.m, dc.A, dc.m, &l2) != 0)
+          return fail(EPFEM_ERR_SOLVER, "restricted_solve: factorization failed");
+        dc.lwork = std::max(std::max(l1, l2), 1);
+        EPFEM_CUDA_TRY(cudaMalloc(&dc.work, sizeof(double) * dc.lwork));
+      } else {
+      // symbolic analysis once per pattern and mask (natural order: the mesh
+      // numbering is lexicographic, hence banded)
+      if (api.info_create(&dc.info) != 0 ||
+          api.analysis(dc.handle, dc.m, dc.nnz, dc.descr, dc.frp, dc.fci, dc.info) != 0)
+        return fail(EPFEM_ERR_SOLVER, "restricted_solve: factorization failed");
+      size_t internal = 0, work = 0;
+      if (api.buf_info(dc.handle, dc.m, dc.nnz, dc.descr, dc.fv, dc.frp, dc.fci, dc.info, &internal, &work) != 0)
+        return fail(EPFEM_ERR_SOLVER, "restricted_solve: factorization failed");
+      EPFEM_CUDA_TRY(cudaMalloc(&dc.buf, std::max<size_t>(work, 16)));
+      }
+    }
+    EPFEM_CUDA_TRY(cudaFreeAsync(tmp, st));
+    dc.rp = rp;
+    dc.ci = ci;
+    dc.n = n;
+    dc.analysed = true;
+  } else if (dc.m > 0) {
+    k_free_fill<<<gb, kThreads, 0, st>>>(n, rp, ci, v, mask, dc.fidx, dc.frp, nullptr, dc.fv);
+  }
+  if (dc.m == 0) return 0;
+  const int m = dc.m;
+  Work w(st);
   EPFEM_CUDA_TRY(w.alloc(&w.r, n));
   EPFEM_CUDA_TRY(w.alloc(&w.Ap, n));
   EPFEM_CUDA_TRY(w.alloc(&w.z, (size_t)m));  // restricted rhs
   EPFEM_CUDA_TRY(w.alloc(&w.p, (size_t)m));  // restricted solution
   EPFEM_CUDA_TRY(w.alloc(&w.partial, 2 * kBlocks));
   EPFEM_CUDA_TRY(w.alloc(&w.sc, 8));
-  r = w.r;
-  Ax = w.Ap;
-  bf = w.z;
-  xf = w.p;
-  k_free_fill<<<gb, kThreads, 0, st>>>(n, rp, ci, v, mask, fidx, frp, fci, fv);
-  EPFEM_CUDA_TRY(cudaGetLastError());
-  void* handle = nullptr;
-  void* descr = nullptr;
-  struct Handles {
-    const SpApi& a;
-    void** h;
-    void** d;
-    ~Handles() {
-      if (*d) a.descr_destroy(*d);
-      if (*h) a.destroy(*h);
-    }
-  } hs{api, &handle, &descr};
-  if (api.create(&handle) != 0 || api.descr_create(&descr) != 0)
-    return fail(EPFEM_ERR_SOLVER, "restricted_solve: cuSOLVER initialisation failed");
-  api.set_stream(handle, st);
-  api.set_type(descr, 0);  // CUSPARSE_MATRIX_TYPE_GENERAL (both triangles stored)
-  api.set_base(descr, 0);  // CUSPARSE_INDEX_BASE_ZERO
-  auto residual = [&](double* rr) -> int {  // r = M (b - K x); rr = |r| / |M b|
+  double *r = w.r, *Ax = w.Ap, *bf = w.z, *xf = w.p;
+  auto residual = [&](double* rr) -> int {  // r = M (b - K x); rr = |r|^2
     k_spmv_masked<<<grid_rows(n), kThreads, 0, st>>>(n, rp, ci, v, mask, x_out, Ax);
     k_resid<<<gb, kThreads, 0, st>>>(n, mask, b, Ax, r);
     const unsigned gd = (unsigned)std::min<int64_t>(kBlocks, (n + kThreads - 1) / kThreads);
-    k_dot2<<<gd, kThreads, 0, st>>>(n, r, r, b, b, w.partial);
+    k_dot2<<<gd, kThreads, 0, st>>>(n, r, r, nullptr, nullptr, w.partial);
     k_finish<<<1, kFinish, 0, st>>>(w.partial, gd, w.sc, 2);
     double h[8];
     EPFEM_CUDA_TRY(cudaMemcpyAsync(h, w.sc, sizeof(h), cudaMemcpyDeviceToHost, st));
     EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
-    // masked b.b (k_dot2's second dot is unmasked): |M b| from the first residual
     *rr = h[S_RZ];
     return 0;
   };
+  // numeric factorisation; not positive definite -> LU (dense) / QR (sparse)
+  const bool dense = dc.A != nullptr;
+  bool qr = false, lu = false;
+  auto dense_matrix = [&]() -> int {
+    EPFEM_CUDA_TRY(cudaMemsetAsync(dc.A, 0, sizeof(double) * (size_t)m * m, st));
+    k_dense_scatter<<<std::max(1, std::min(kBlocks * 4, (m + kThreads - 1) / kThreads)), kThreads, 0, st>>>(
+        m, dc.frp, dc.fci, dc.fv, dc.A);
+    return 0;
+  };
+  auto dense_info = [&]() -> int {
+    int h = 0;
+    EPFEM_CUDA_TRY(cudaMemcpyAsync(&h, dc.dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
+    EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+    return h;
+  };
+  if (dense) {
+    api.dn_set_stream(dc.dn, st);
+    if (int rc = dense_matrix()) return rc;
+    if (api.potrf(dc.dn, 0, m, dc.A, m, dc.work, dc.lwork, dc.dinfo) != 0)
+      return fail(EPFEM_ERR_SOLVER, "restricted_solve: factorization failed");
+    if (dense_info() != 0) {  // not positive definite: partial-pivoting LU on a fresh copy
+      lu = true;
+      if (int rc = dense_matrix()) return rc;
+      if (api.getrf(dc.dn, m, m, dc.A, m, dc.work, dc.ipiv, dc.dinfo) != 0 || dense_info() != 0)
+        return fail(EPFEM_ERR_SOLVER, "restricted_solve: factorization failed");
+    }
+  } else {
+    if (api.factor(dc.handle, m, dc.nnz, dc.descr, dc.fv, dc.frp, dc.fci, dc.info, dc.buf) != 0)
+      return fail(EPFEM_ERR_SOLVER, "restricted_solve: factorization failed");
+    int pos = -1;
+    if (api.zero_pivot(dc.handle, dc.info, 1e-14, &pos) != 0) pos = 0;
+    if (pos >= 0) qr = true;
+  }
   // the first solve has x = 0, so its residual norm is |M b|
   double rr = 0.0;
   if (int rc = residual(&rr)) return rc;
   const double bnorm = std::sqrt(rr);
   if (bnorm == 0.0) return 0;
-  bool qr = false;
   for (int sweep = 0; sweep < 4; ++sweep) {
-    k_gather_free<<<gb, kThreads, 0, st>>>(n, mask, fidx, r, bf);
-    int sing = -1;
-    int rc = qr ? api.qr(handle, m, nnz, descr, fv, frp, fci, bf, 1e-14, 2, xf, &sing)
-                : api.chol(handle, m, nnz, descr, fv, frp, fci, bf, 1e-14, 2, xf, &sing);
-    if (rc != 0) return fail(EPFEM_ERR_SOLVER, "restricted_solve: factorization failed");
-    if (sing >= 0 && !qr) {  // not positive definite: QR on the same system
-      qr = true;
-      --sweep;
-      continue;
+    k_gather_free<<<gb, kThreads, 0, st>>>(n, mask, dc.fidx, r, bf);
+    if (dense) {
+      EPFEM_CUDA_TRY(cudaMemcpyAsync(xf, bf, sizeof(double) * m, cudaMemcpyDeviceToDevice, st));
+      const int rc = lu ? api.getrs(dc.dn, 0, m, 1, dc.A, m, dc.ipiv, xf, m, dc.dinfo)
+                        : api.potrs(dc.dn, 0, m, 1, dc.A, m, xf, m, dc.dinfo);
+      if (rc != 0) return fail(EPFEM_ERR_SOLVER, "restricted_solve: factorization failed");
+    } else if (qr) {
+      int sing = -1;
+      if (api.qr(dc.handle, m, dc.nnz, dc.descr, dc.fv, dc.frp, dc.fci, bf, 1e-14, 2, xf, &sing) != 0 || sing >= 0)
+        return fail(EPFEM_ERR_SOLVER, "restricted_solve: factorization failed");
+    } else if (api.solve(dc.handle, m, bf, xf, dc.info, dc.buf) != 0) {
+      return fail(EPFEM_ERR_SOLVER, "restricted_solve: factorization failed");
     }
-    if (sing >= 0) return fail(EPFEM_ERR_SOLVER, "restricted_solve: factorization failed");
-    k_scatter_add_free<<<gb, kThreads, 0, st>>>(n, mask, fidx, xf, x_out);
+    k_scatter_add_free<<<gb, kThreads, 0, st>>>(n, mask, dc.fidx, xf, x_out);
     EPFEM_CUDA_TRY(cudaGetLastError());
     *sweeps_out = sweep + 1;
     if (int rc2 = residual(&rr)) return rc2;
