@@ -539,6 +539,21 @@ __global__ void k_mask_diff(int64_t n, const uint8_t* __restrict__ a, const uint
     c += ((!a || a[i]) ? 1 : 0) != ((!b || b[i]) ? 1 : 0);
   if (c) atomicAdd(out, c);
 }
+// the cached pattern differs from (rp, ci)?  rp first, then (only when the
+// row pointers agree, so ci has the cached length) the column indices
+__global__ void k_rp_diff(int64_t n, const int64_t* __restrict__ rp, const int64_t* __restrict__ crp, int* out) {
+  int c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i <= n; i += (int64_t)gridDim.x * kThreads)
+    c += rp[i] != crp[i];
+  if (c) atomicAdd(out, c);
+}
+__global__ void k_ci_diff(int64_t nnz, const int32_t* __restrict__ ci, const int32_t* __restrict__ cci, int* out) {
+  if (*(volatile int*)out) return;
+  int c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * kThreads)
+    c += ci[i] != cci[i];
+  if (c) atomicAdd(out, c);
+}
 __global__ void k_copy_mask(int64_t n, const uint8_t* __restrict__ mask, uint8_t* out) {
   for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads)
     out[i] = (!mask || mask[i]) ? 1 : 0;
@@ -595,11 +610,12 @@ __global__ void k_scatter_add_free(int64_t n, const uint8_t* __restrict__ mask, 
 // context for the last (matrix pattern, free mask) seen: a Newton loop
 // factorises the same pattern every iteration.
 struct DirectCache {
-  const int64_t* rp = nullptr;
-  const int32_t* ci = nullptr;
   int64_t n = -1;
   int m = 0, nnz = 0;
   uint8_t* mask = nullptr;  // the cached free mask (1 byte per row)
+  int64_t* crp = nullptr;   // copies of the analysed pattern: a caller may free (rp, ci) and reuse the
+  int32_t* cci = nullptr;   // addresses for another pattern, so the key is the content, not the pointers
+  int64_t full_nnz = 0;
   int *fidx = nullptr, *frp = nullptr, *fci = nullptr, *cnt = nullptr;
   double* fv = nullptr;
   void *handle = nullptr, *descr = nullptr, *info = nullptr, *buf = nullptr;
@@ -613,13 +629,16 @@ struct DirectCache {
     const SpApi& api = sp_api();
     if (info) api.info_destroy(info);
     info = nullptr;
-    for (void* p : {(void*)mask, (void*)fidx, (void*)frp, (void*)fci, (void*)cnt, (void*)fv, buf, (void*)A,
+    for (void* p : {(void*)mask, (void*)crp, (void*)cci, (void*)fidx, (void*)frp, (void*)fci, (void*)cnt, (void*)fv, buf, (void*)A,
                     (void*)work, (void*)ipiv, (void*)dinfo})
       if (p) cudaFree(p);
     A = work = nullptr;
     ipiv = dinfo = nullptr;
     lwork = 0;
     mask = nullptr;
+    crp = nullptr;
+    cci = nullptr;
+    full_nnz = 0;
     fidx = frp = fci = cnt = nullptr;
     fv = nullptr;
     buf = nullptr;
@@ -637,8 +656,13 @@ struct DirectCache {
 
 // restricted systems up to this size are factorised dense (cusolverDn potrf,
 // getrf when not positive definite): the drivers' systems are small, and the
-// dense factorisation on the device is far faster than the sparse one there
+// dense factorisation on the device is far faster than the sparse one there.
+// EPFEM_DIRECT_DENSE_MAX overrides it (tests: 0 forces the sparse path).
 constexpr int kDenseMax = 16384;
+static int dense_max() {
+  const char* v = getenv("EPFEM_DIRECT_DENSE_MAX");
+  return v ? atoi(v) : kDenseMax;
+}
 
 void direct_cache_free(void* c) { delete static_cast<DirectCache*>(c); }
 
@@ -663,12 +687,14 @@ int direct_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* 
   api.set_stream(dc.handle, st);
   const unsigned gb = (unsigned)std::min<int64_t>(kBlocks * 4, (n + kThreads - 1) / kThreads);
   // same pattern and free mask as the cached analysis?
-  bool same = dc.analysed && dc.rp == rp && dc.ci == ci && dc.n == n;
+  bool same = dc.analysed && dc.n == n;
   if (same) {
     int* diff = nullptr;
     EPFEM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&diff), sizeof(int), st));
     EPFEM_CUDA_TRY(cudaMemsetAsync(diff, 0, sizeof(int), st));
     k_mask_diff<<<gb, kThreads, 0, st>>>(n, mask, dc.mask, diff);
+    k_rp_diff<<<gb, kThreads, 0, st>>>(n, rp, dc.crp, diff);
+    k_ci_diff<<<gb, kThreads, 0, st>>>(dc.full_nnz, ci, dc.cci, diff);
     int h = 0;
     EPFEM_CUDA_TRY(cudaMemcpyAsync(&h, diff, sizeof(int), cudaMemcpyDeviceToHost, st));
     EPFEM_CUDA_TRY(cudaFreeAsync(diff, st));
@@ -679,6 +705,12 @@ int direct_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* 
     EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
     dc.release();
     EPFEM_CUDA_TRY(cudaMalloc(&dc.mask, n));
+    EPFEM_CUDA_TRY(cudaMemcpyAsync(&dc.full_nnz, rp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    EPFEM_CUDA_TRY(cudaStreamSynchronize(st));
+    EPFEM_CUDA_TRY(cudaMalloc(&dc.crp, sizeof(int64_t) * (n + 1)));
+    EPFEM_CUDA_TRY(cudaMalloc(&dc.cci, sizeof(int32_t) * std::max<int64_t>(dc.full_nnz, 1)));
+    EPFEM_CUDA_TRY(cudaMemcpyAsync(dc.crp, rp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToDevice, st));
+    EPFEM_CUDA_TRY(cudaMemcpyAsync(dc.cci, ci, sizeof(int32_t) * dc.full_nnz, cudaMemcpyDeviceToDevice, st));
     EPFEM_CUDA_TRY(cudaMalloc(&dc.fidx, sizeof(int) * (n + 1)));
     EPFEM_CUDA_TRY(cudaMalloc(&dc.cnt, sizeof(int) * (n + 1)));
     k_copy_mask<<<gb, kThreads, 0, st>>>(n, mask, dc.mask);
@@ -701,7 +733,7 @@ int direct_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* 
       EPFEM_CUDA_TRY(cudaMalloc(&dc.fci, sizeof(int) * std::max(dc.nnz, 1)));
       EPFEM_CUDA_TRY(cudaMalloc(&dc.fv, sizeof(double) * std::max(dc.nnz, 1)));
       k_free_fill<<<gb, kThreads, 0, st>>>(n, rp, ci, v, mask, dc.fidx, dc.frp, dc.fci, dc.fv);
-      if (dc.m <= kDenseMax && api.dense_ok) {
+      if (dc.m <= dense_max() && api.dense_ok) {
         if (!dc.dn && api.dn_create(&dc.dn) != 0)
           return fail(EPFEM_ERR_SOLVER, "restricted_solve: cuSOLVER initialisation failed");
         api.dn_set_stream(dc.dn, st);
@@ -726,8 +758,6 @@ int direct_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* 
       }
     }
     EPFEM_CUDA_TRY(cudaFreeAsync(tmp, st));
-    dc.rp = rp;
-    dc.ci = ci;
     dc.n = n;
     dc.analysed = true;
   } else if (dc.m > 0) {

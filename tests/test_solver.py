@@ -248,3 +248,82 @@ def test_restricted_solve_direct(cuda):
     S = 0.5 * (S + S.T) + np.diag(np.where(np.arange(n) % 2 == 0, 3.0, -3.0))
     xs = restricted_solve(_csr(S, cuda), torch.from_numpy(rhs).to(cuda), None, SolveSettings(rel_tol=1e-10)).cpu().numpy()
     assert np.abs(xs - np.linalg.solve(S, rhs)).max() <= 1e-8 * np.abs(np.linalg.solve(S, rhs)).max()
+
+
+def test_restricted_solve_direct_sparse_path(cuda, monkeypatch):
+    """The sparse cuSOLVER path (restricted systems above the dense limit;
+    forced here with EPFEM_DIRECT_DENSE_MAX=0): Cholesky with the cached
+    symbolic analysis on an SPD system, repeated with new values on the same
+    pattern, and the QR fallback on an indefinite one."""
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.solver import SolveInfo, SolveSettings, restricted_solve
+    monkeypatch.setenv("EPFEM_DIRECT_DENSE_MAX", "0")
+    ctx = P.Context(cuda)
+    rng = np.random.default_rng(37)
+    n = 120
+    # banded SPD (a 1D chain with a few couplings), like a mesh numbering
+    A = np.zeros((n, n))
+    for i in range(n):
+        for j in range(max(0, i - 4), min(n, i + 5)):
+            A[i, j] = rng.uniform(-1, 1)
+    Kd = A @ A.T + n * np.eye(n)
+    mask = rng.uniform(size=n) < 0.8
+    f = np.nonzero(mask)[0]
+    M = _csr(Kd, cuda)
+    for scale in (1.0, 3.0):  # second call: same pattern and mask, new values (numeric factorisation only)
+        M.values.mul_(scale)
+        Ks = Kd * (3.0 if scale == 3.0 else 1.0)
+        rhs = rng.uniform(-1, 1, n)
+        info = SolveInfo()
+        x = restricted_solve(M, torch.from_numpy(rhs).to(cuda), torch.from_numpy(mask).to(cuda),
+                             SolveSettings(rel_tol=1e-12), ctx=ctx, info=info).cpu().numpy()
+        xf = np.linalg.solve(Ks[np.ix_(f, f)], rhs[f])
+        assert np.abs(x[f] - xf).max() <= 1e-10 * np.abs(xf).max()
+        assert np.all(x[~mask] == 0.0) and not info.substituted and info.residual <= 1e-12
+    S = rng.uniform(-1, 1, (n, n))
+    S = 0.5 * (S + S.T) + np.diag(np.where(np.arange(n) % 2 == 0, 3.0, -3.0))
+    rhs = rng.uniform(-1, 1, n)
+    xs = restricted_solve(_csr(S, cuda), torch.from_numpy(rhs).to(cuda), None, SolveSettings(rel_tol=1e-10),
+                          ctx=ctx).cpu().numpy()
+    ref = np.linalg.solve(S, rhs)
+    assert np.abs(xs - ref).max() <= 1e-8 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("dense_max", ["16384", "0"])
+def test_restricted_solve_direct_pattern_rewritten_in_place(cuda, monkeypatch, dense_max):
+    """The direct solve caches the restricted pattern and its analysis; the
+    key is the pattern's content, so a caller that rewrites row_ptr / col_idx
+    in place (same addresses, same n, same free mask, same nnz) gets a solve
+    of the new matrix, not of the cached pattern."""
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.solver import SolveSettings, restricted_solve
+    monkeypatch.setenv("EPFEM_DIRECT_DENSE_MAX", dense_max)
+    ctx = P.Context(cuda)
+    rng = np.random.default_rng(41)
+    n = 60
+
+    def spd(offsets):
+        A = np.eye(n) * 8.0
+        for d in offsets:
+            for i in range(n - d):
+                A[i, i + d] = A[i + d, i] = rng.uniform(-1, 1)
+        return A
+
+    # offsets (1, 4) and (2, 3): the same nnz (2 (59 + 56) = 2 (58 + 57)), different columns
+    import scipy.sparse as sp
+    c1, c2 = sp.csr_matrix(spd((1, 4))), sp.csr_matrix(spd((2, 3)))
+    c1.sort_indices()
+    c2.sort_indices()
+    assert c1.nnz == c2.nnz and not np.array_equal(c1.indices, c2.indices)
+    M = P.CsrMatrix(torch.from_numpy(c1.indptr.astype(np.int64)).to(cuda),
+                    torch.from_numpy(c1.indices.astype(np.int32)).to(cuda),
+                    torch.from_numpy(c1.data.astype(np.float64)).to(cuda))
+    rhs = rng.uniform(-1, 1, n)
+    b = torch.from_numpy(rhs).to(cuda)
+    x1 = restricted_solve(M, b, None, SolveSettings(rel_tol=1e-12), ctx=ctx).cpu().numpy()
+    assert np.abs(x1 - np.linalg.solve(c1.toarray(), rhs)).max() <= 1e-10
+    M.row_ptr.copy_(torch.from_numpy(c2.indptr.astype(np.int64)))
+    M.col_idx.copy_(torch.from_numpy(c2.indices.astype(np.int32)))
+    M.values.copy_(torch.from_numpy(c2.data.astype(np.float64)))
+    x2 = restricted_solve(M, b, None, SolveSettings(rel_tol=1e-12), ctx=ctx).cpu().numpy()
+    assert np.abs(x2 - np.linalg.solve(c2.toarray(), rhs)).max() <= 1e-10
