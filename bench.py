@@ -375,33 +375,62 @@ def run_slabs(args, rank, world, dev, cfg):
     n_total = float(n_own)
 
     # e2e: every step uploads this rank's E / Ep / Hard from pinned host memory
-    # and downloads its S, flag bytes and owned K rows (max over ranks)
+    # and downloads its S, flag bytes and owned K rows (max over ranks).  As in
+    # e2e_section, steps are pipelined: the upload of step i+1 (h2d stream) and
+    # the download of step i (d2h stream, from a device staging copy, since the
+    # engine's outputs are rewritten by the next step) overlap the compute.
     e2e = None
     if not args.no_e2e:
         host_in = [x for x in (E, Ep0, Hard0) if x is not None]
         h_in = [torch.empty_like(x, device="cpu").pin_memory() for x in host_in]
         for h, x in zip(h_in, host_in):
             h.copy_(x)
-        d_in = [torch.empty_like(x) for x in host_in]
+        d_in = [[torch.empty_like(x) for x in host_in] for _ in range(2)]
         S_, f_, K_ = eng.step(E, Ep0, Hard0)
-        h_out = [torch.empty_like(y, device="cpu").pin_memory() for y in (S_, f_, K_)]
+        stage = [[torch.empty_like(y) for y in (S_, f_, K_)] for _ in range(2)]
+        h_out = [[torch.empty_like(y, device="cpu").pin_memory() for y in (S_, f_, K_)] for _ in range(2)]
         bi = sum(x.numel() * x.element_size() for x in host_in)
-        bo = sum(y.numel() * y.element_size() for y in h_out)
+        bo = sum(y.numel() * y.element_size() for y in h_out[0])
+        h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_used = [torch.cuda.Event() for _ in range(2)]
+        ev_st = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        used = [False, False]
 
-        def e2e_step():
-            for d, h in zip(d_in, h_in):
-                d.copy_(h, non_blocking=True)
-            outs = eng.step(*(d_in + [None] * (3 - len(d_in))))
-            for h, y in zip(h_out, outs):
-                h.copy_(y, non_blocking=True)
-        for _ in range(max(1, args.warmup)):
-            e2e_step()
+        def e2e_step(i):
+            b = i % 2
+            if used[b]:
+                h2d_s.wait_event(ev_used[b])   # step i-2 has consumed d_in[b]
+                stream.wait_event(ev_out[b])   # stage[b] has been downloaded
+            with torch.cuda.stream(h2d_s):
+                for d, h in zip(d_in[b], h_in):
+                    d.copy_(h, non_blocking=True)
+                ev_in[b].record(h2d_s)
+            stream.wait_event(ev_in[b])
+            outs = eng.step(*(d_in[b] + [None] * (3 - len(d_in[b]))))
+            ev_used[b].record(stream)
+            for d, y in zip(stage[b], outs):
+                d.copy_(y, non_blocking=True)
+            ev_st[b].record(stream)
+            d2h_s.wait_event(ev_st[b])
+            with torch.cuda.stream(d2h_s):
+                for h, y in zip(h_out[b], stage[b]):
+                    h.copy_(y, non_blocking=True)
+                ev_out[b].record(d2h_s)
+            used[b] = True
+        for i in range(max(2, args.warmup)):
+            e2e_step(i)
         torch.cuda.synchronize(dev)
         dist.barrier()
-        k2 = max(3, min(args.steps, 10))
+        k2 = max(4, min(args.steps, 10))
         ev0.record(stream)
-        for _ in range(k2):
-            e2e_step()
+        h2d_s.wait_event(ev0)
+        d2h_s.wait_event(ev0)
+        for i in range(k2):
+            e2e_step(i)
+        stream.wait_stream(d2h_s)
+        stream.wait_stream(h2d_s)
         ev1.record(stream)
         torch.cuda.synchronize(dev)
         t2 = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
@@ -411,7 +440,14 @@ def run_slabs(args, rank, world, dev, cfg):
         ms2 = float(t2) / k2
         e2e = {"value": n_total / (ms2 * 1e-3), "unit": "ip/s", "h2d_bytes_per_step": int(tb[0]),
                "d2h_bytes_per_step": int(tb[1]), "ms_per_step": ms2,
-               "how": "per rank: H2D of own E/Ep/Hard, step, D2H of own S/flags/K rows; all ranks summed"}
+               "how": "per rank: H2D of own E/Ep/Hard, step, D2H of own S/flags/K rows (pipelined across steps "
+                      "over two buffer sets and three streams); all ranks summed"}
+    # our kernel launches per step on this rank (dist.py DistributedTangent.step): the fused update (two launches
+    # when the top layer goes first), the halo deltas (ranks with a halo), the row stream; summed over ranks
+    top = max(plan.halo_elems, plan.mesh.n_elements - plan.layer_elems)
+    n_launch = (2 if (rank + 1 < world and top > plan.halo_elems) else 1) + (1 if plan.halo_elems else 0) + 1
+    launches = torch.tensor([float(n_launch * args.steps)], dtype=torch.float64, device=dev)
+    dist.all_reduce(launches)
     npl = torch.tensor([float((eng.flags[p0:p1] & 1).sum())], dtype=torch.float64, device=dev)
     dist.all_reduce(npl)
     # whole-job algorithmic bytes from the owned shares, against
@@ -436,7 +472,7 @@ def run_slabs(args, rank, world, dev, cfg):
                        "plastic_fraction": float(npl) / n_total,
                        "parallelism": f"slab x{world} (one halo cell layer, NCCL interface exchange)",
                        "l2": "inputs larger than L2"},
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": "whole step (fused update + halo deltas + row stream)",
                          "achieved": step_gbs, "peak": hbm_peak * world, "unit": "GB/s",
                          "frac": step_gbs / (hbm_peak * world), "traffic": None,
@@ -790,6 +826,9 @@ def main():
     ap.add_argument("--no-side", action="store_true", help="skip the from-displacements / with-forces timings")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    # stdout carries exactly one JSON line: keep NCCL's version banner (NCCL_DEBUG=VERSION) off it
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
