@@ -181,7 +181,16 @@ def _cpu_worker(name, slabs, core, scale, reps, warmup, conn):
             cl = np.ascontiguousarray(coord[nodes])
             cache = O.Cache(cfg.family, cfg.dim, cl, el, G, K)
             if cfg.model == "elastic":
-                out.append((cache.n_int, [cache.elastic_assembly_seconds], 0))
+                # the timed region is assemble_elastic_stiffness inside the cache build: one build per
+                # iteration (the first `warmup` builds untimed)
+                times = []
+                for it in range(warmup + reps):
+                    if it:
+                        del cache
+                        cache = O.Cache(cfg.family, cfg.dim, cl, el, G, K)
+                    if it >= warmup:
+                        times.append(cache.elastic_assembly_seconds)
+                out.append((cache.n_int, times, 0))
                 del cache
                 continue
             E1 = cache.strains(displacement(cl, cfg.seed))
@@ -280,9 +289,17 @@ def run_reference(args, rank, world):
     slabs = [(k, min(cfg.n, k + L)) for k in range(0, cfg.n, L)]
     W = max(1, min(cores, len(slabs)))
     assign = [slabs[w * len(slabs) // W:(w + 1) * len(slabs) // W] for w in range(W)]
-    reps = max(1, min(args.steps, args.ref_reps))
-    warm = 1 if args.warmup > 0 else 0
     t0 = time.perf_counter()
+    if args.ref_reps is not None:
+        reps = max(1, min(args.steps, args.ref_reps))
+    else:
+        # --steps K timed whole-configuration steps, bounded so the arm ends within a few minutes:
+        # one iteration of the first slab on core 0 estimates a step (the busiest worker's slabs)
+        budget = float(os.environ.get("EPFEM_REF_BUDGET_S", "180"))
+        (cal,) = cpu_run(args.config, [[slabs[0]]], None, 1, 0)
+        est = cal[0][1][0] * max(len(a) for a in assign)
+        reps = max(1, min(args.steps, int(budget / max(est, 1e-9))))
+    warm = 1 if args.warmup > 0 else 0
     res = cpu_run(args.config, assign, None, reps, warm)
     wall = time.perf_counter() - t0
     n_int = sum(r[0] for wr in res for r in wr)
@@ -298,6 +315,8 @@ def run_reference(args, rank, world):
     line = {
         "metric": METRIC, "value": value, "unit": "ip/s", "impl": "reference",
         "n_gpus": world, "steps": reps, "warmup": warm,
+        "warmup_note": "one untimed iteration per slab (one whole-configuration step) before the timed steps; "
+                       "steps = --steps unless the estimated run exceeds EPFEM_REF_BUDGET_S (180 s)",
         "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "n_int": n_int, "plastic_fraction": npl / n_int if n_int else 0.0,
@@ -820,7 +839,8 @@ def main():
                          "default cfg5,cfg3 for the cfg4 headline at N=1, 'none' to skip)")
     ap.add_argument("--target", type=float, default=None, help="plastic fraction override")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-reps", type=int, default=3, help="--impl reference: timed iterations per slab")
+    ap.add_argument("--ref-reps", type=int, default=None,
+                    help="--impl reference: timed iterations per slab (default: --steps, within a time budget)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-side", action="store_true", help="skip the from-displacements / with-forces timings")
