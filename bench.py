@@ -846,9 +846,11 @@ def main():
     ap.add_argument("--no-side", action="store_true", help="skip the from-displacements / with-forces timings")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    # stdout carries exactly one JSON line: keep NCCL's version banner (NCCL_DEBUG=VERSION) off it
-    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-        os.environ["NCCL_DEBUG"] = "WARN"
+    # stdout carries exactly one JSON line: Python's prints keep the original stdout, while anything native
+    # libraries printf to fd 1 (NCCL's version banner at NCCL_DEBUG=VERSION / WARN) goes to stderr
+    sys.stdout.flush()
+    sys.stdout = os.fdopen(os.dup(1), "w", buffering=1)
+    os.dup2(2, 1)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
