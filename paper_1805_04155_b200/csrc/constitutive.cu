@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(FusedCfg<DIM, NP, NQ>::THREADS, FusedCfg<DIM, 
       const unsigned mask = s_mask[le];
       EPFEM_CHECK(!(e < g.e_end) || e < g.n_elements);
       if (e < g.e_end && mask)
-        delta_pairs3<NP, NQ>(&s_st[le][0][0], mask, k / 3, k % 3, g.scratch + (size_t)e * Cfg::NB * Cfg::D2);
+        delta_rowpair3<NP, NQ>(&s_st[le][0][0], mask, k, g.scratch + (size_t)e * Cfg::NB * Cfg::D2);
     }
     return;
   }
@@ -668,8 +668,7 @@ __global__ void __launch_bounds__(Pair3Cfg<NP, NQ>::THREADS, EPFEM_WARP3_MINB)
       if (le < EPW && e0 + le < g.e_end) {
         const unsigned mask = (bal >> (le * NQ)) & QMASK;
         if (mask)
-          delta_pairs3<NP, NQ>(st_w + le * NQ * REC, mask, k / 3, k % 3,
-                               g.scratch + (size_t)(e0 + le) * W::NB * W::D2);
+          delta_rowpair3<NP, NQ>(st_w + le * NQ * REC, mask, k, g.scratch + (size_t)(e0 + le) * W::NB * W::D2);
       }
     }
   }

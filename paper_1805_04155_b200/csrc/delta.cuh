@@ -560,6 +560,103 @@ __device__ __forceinline__ void delta_pairs3(const double* st_e, unsigned mask, 
   }
 }
 
+// Cyclic row pairs (even NP: Q1 hexahedra, P2 tetrahedra).  delta_pairs3's
+// lane (pair p, component i) needs T_a for its first NP - p blocks and T_a'
+// after that; with p a per-lane value every block selects its T row (12 FSEL
+// per block).  Here a symmetric block {a, b} is owned by the row from which b
+// lies 0 .. H = NP / 2 steps ahead cyclically (b - a mod NP in [0, H), or
+// = H with a < H), and lane r in [0, H) owns rows r and r + H: blocks
+// (r, r + k mod NP) for k = 0 .. H with T_r, then (r + H, r + H + k mod NP)
+// for k = 0 .. H - 1 with T_{r+H}.  The T row of every block is a constant,
+// the same NP + 1 blocks per lane and the same (optimal) FMA count.  A block
+// whose column node precedes its row node is the transpose of a stored
+// (a <= b) block: the lane writes its row i as that block's column i.  The
+// standalone element-delta kernel (k_elem_delta_staged) uses the same
+// function, so fused and separate paths give the same bits.
+#ifndef EPFEM_CYC3
+#define EPFEM_CYC3 1
+#endif
+template <int NP>
+struct UseCyc3 {
+  static constexpr bool value = EPFEM_CYC3 && NP % 2 == 0 && NP < 20;  // Q2-20 keeps its chunks
+};
+template <int NP, int NQ>
+__device__ __forceinline__ void delta_cyc3(const double* st_e, unsigned mask, int r, int i,
+                                           double* __restrict__ rec) {
+  static_assert(NP % 2 == 0, "cyclic row pairs need an even node count");
+  using C = Pair3Cfg<NP, NQ>;
+  constexpr int NS = C::NS, REC = C::REC, D2 = C::D2, NBLK = C::NBLK, H = NP / 2;
+  const int R0 = r, R1 = r + H;
+  const int d0 = i, d1 = i == 2 ? 4 : 3, d2 = i == 0 ? 5 : (i == 1 ? 4 : 5);
+  const int e1 = i == 0 ? 1 : (i == 1 ? 0 : 1), e2 = i == 0 ? 2 : (i == 1 ? 2 : 0);
+  auto pk = [](int a, int b) {
+    const int lo = a < b ? a : b, hi = a < b ? b : a;
+    return lo * NS - lo * (lo - 1) / 2 + (hi - lo);
+  };
+  // column node of block k (k <= H: row R0, else row R1)
+  auto col = [&](int k) {
+    const int c = k <= H ? R0 + k : R1 + (k - H - 1);
+    return c >= NP ? c - NP : c;
+  };
+  double acc[NBLK][3];
+#pragma unroll
+  for (int k = 0; k < NBLK; ++k) acc[k][0] = acc[k][1] = acc[k][2] = 0.0;
+  while (mask) {
+    const int q = __ffs(mask) - 1;
+    mask &= mask - 1u;
+    const double* st = st_e + q * REC;
+    const double* dw = st + NP * 3;
+    double T0[NS], T1[NS];
+    {
+      const double* g0 = st + R0 * 3;
+      const double* g1 = st + R1 * 3;
+      const double gA0 = g0[d0], gA1 = g0[e1], gA2 = g0[e2];
+      const double gB0 = g1[d0], gB1 = g1[e1], gB2 = g1[e2];
+#pragma unroll
+      for (int c = 0; c < NS; ++c) {
+        const double w0 = dw[pk(d0, c)], w1 = dw[pk(d1, c)], w2 = dw[pk(d2, c)];
+        T0[c] = __fma_rn(gA2, w2, __fma_rn(gA1, w1, __dmul_rn(gA0, w0)));
+        T1[c] = __fma_rn(gB2, w2, __fma_rn(gB1, w1, __dmul_rn(gB0, w0)));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NBLK; ++k) {
+      const double* T = k <= H ? T0 : T1;
+      const double* h = st + col(k) * 3;
+      const double h0 = h[0], h1 = h[1], h2 = h[2];
+      acc[k][0] = __fma_rn(T[5], h2, __fma_rn(T[3], h1, __fma_rn(T[0], h0, acc[k][0])));
+      acc[k][1] = __fma_rn(T[4], h2, __fma_rn(T[3], h0, __fma_rn(T[1], h1, acc[k][1])));
+      acc[k][2] = __fma_rn(T[5], h0, __fma_rn(T[4], h1, __fma_rn(T[2], h2, acc[k][2])));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NBLK; ++k) {
+    const int a = k <= H ? R0 : R1, b = col(k);
+    if (b >= a) {
+      EPFEM_CHECK(blk_index<NP>(a, b) < C::NB);
+      double* o = rec + blk_index<NP>(a, b) * D2 + i * 3;
+      o[0] = acc[k][0];
+      o[1] = acc[k][1];
+      o[2] = acc[k][2];
+    } else {  // block (b, a) = this block transposed: row i here is its column i
+      EPFEM_CHECK(blk_index<NP>(b, a) < C::NB);
+      double* o = rec + blk_index<NP>(b, a) * D2 + i;
+      o[0] = acc[k][0];
+      o[3] = acc[k][1];
+      o[6] = acc[k][2];
+    }
+  }
+}
+// The 3D row-pair phase 2 of one (element, lane k < PL) task.
+template <int NP, int NQ>
+__device__ __forceinline__ void delta_rowpair3(const double* st_e, unsigned mask, int k,
+                                               double* __restrict__ rec) {
+  if constexpr (UseCyc3<NP>::value)
+    delta_cyc3<NP, NQ>(st_e, mask, k / 3, k % 3, rec);
+  else
+    delta_pairs3<NP, NQ>(st_e, mask, k / 3, k % 3, rec);
+}
+
 // 2D row pairs (delta_pairs3's scheme with dim 2): lane (element, pair p,
 // component i) owns row i of block rows p and NP - 1 - p; 2 * ceil(NP / 2)
 // lanes per element (8 for Q2-8), NP + 1 blocks per lane, optimal FMA count.

@@ -82,7 +82,19 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS) k_elem_delta_s
   }
   __syncthreads();
   if (tid < EPB && e0 + tid < a.e_end) a.emask[e0 + tid] = s_mask[tid];
-  delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, a.e_end, a.scratch);
+  if constexpr (DIM == 3 && UseCyc3<NP>::value && MODE != G_ELASTIC) {
+    // the fused kernels' phase 2 (cyclic row pairs), so the records match
+    // theirs bit for bit
+    using PC = Pair3Cfg<NP, NQ>;
+    for (int t = tid; t < EPB * PC::PL; t += blockDim.x) {
+      const int le = t / PC::PL;
+      const int64_t e = e0 + le;
+      if (e < a.e_end && s_mask[le])
+        delta_rowpair3<NP, NQ>(&s_st[le][0][0], s_mask[le], t - le * PC::PL, a.scratch + (size_t)e * Cfg::NB * Cfg::D2);
+    }
+  } else {
+    delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, a.e_end, a.scratch);
+  }
 }
 
 // k_delta_warp (2D): pass 1 from a finished constitutive update (flags +
