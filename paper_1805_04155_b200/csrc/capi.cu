@@ -415,7 +415,7 @@ int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_materi
   CT(cudaMalloc(&c->emask, sizeof(unsigned) * std::max<int64_t>(I.n_elements, 1)));
   CT(cudaMalloc(&c->fws, sizeof(double) * std::max<size_t>((size_t)I.n_elements * I.n_p * I.dim, 1)));
   if (I.n_nodes > 0)
-    if (int rc = plan_row_stream(I.n_nodes, I.dim, c->pat.nbr_ptr, c->pat.n2e_ptr, st, &c->npc,
+    if (int rc = plan_row_stream(I.n_nodes, I.dim, I.n_p, c->pat.nbr_ptr, c->pat.n2e_ptr, st, &c->npc,
                                  &c->max_span, &c->max_items))
       return bail(rc);
   GatherArgs g = gather_args(c);

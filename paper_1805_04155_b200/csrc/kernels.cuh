@@ -106,7 +106,7 @@ int cg_solve(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, c
 int energy_norm(int64_t n, const int64_t* rp, const int32_t* ci, const double* v, const double* x,
                 cudaStream_t st, double* out);
 size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements);
-int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
+int plan_row_stream(int64_t n_nodes, int dim, int np, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
                     cudaStream_t st, int* npc_out, int* span_out, int* items_out, int budget_bytes = 0);
 int launch_strains(int family, int dim, int64_t n_e, const int32_t* elem, const double* inv,
                    const double* gradhat, const double* u, double* E, cudaStream_t st,

@@ -226,7 +226,20 @@ __global__ void __launch_bounds__(MmaCfg<DIM, NP, NQ>::THREADS) k_delta_mma(Gath
   delta_mma_warp<DIM, NP, NQ>(st_w, s_out[w], bal, e0, a.e_end, a.scratch, lane);
 }
 
-constexpr int kStreamThreads = 256;
+constexpr int kStreamThreads = 256;  // the most threads of a row-stream CTA
+// Threads per row-stream CTA (a warp per node at a time).  Measured on B200
+// with the row-task add loop (32 registers): Q1 hexahedra 8 nodes on 128 threads
+// 3.34 ms against 3.48 ms for 16 nodes on 256 (cfg4); P2 tetrahedra 4 nodes on
+// 128 threads 2.79 against 2.84 ms (cfg3); Q2-20 and 2D stay at 256 threads
+// (cfg5 9.06 against 9.54 ms at 128).  EPFEM_ROW_THREADS overrides (tuning).
+static int row_stream_threads(int dim, int np) {
+  static const int env = [] {
+    const char* v = getenv("EPFEM_ROW_THREADS");
+    return v ? atoi(v) : 0;
+  }();
+  if (env >= 32 && env <= kStreamThreads && env % 32 == 0) return env;
+  return (dim == 3 && np < 20) ? 128 : kStreamThreads;
+}
 // Q2-20: 4 CTAs per SM (64 registers) measured 9.6 vs 11.2 ms on cfg5; the
 // same bound on Q1 / P2 tetrahedra is slower (ptxas then uses 56 registers)
 #ifndef EPFEM_ROW_MINB20
@@ -262,7 +275,7 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
   __shared__ uint64_t s_bar;
   constexpr int NB = NP * (NP + 1) / 2;
   constexpr int D2 = DIM * DIM;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int64_t range = blockIdx.x;
   const int64_t n0 = a.n_begin + range * npc;
   const int64_t n1 = min(n0 + (int64_t)npc, a.n_end);
@@ -323,37 +336,40 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
     constexpr int BUF = ((NP * D2 + 1) / 2) * 2 + ((SLW + 1) / 2) * 2;  // doubles (even: 16-byte steps)
     double* wbuf = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_vptr + npc + 1) + 15) & ~uintptr_t(15)) +
                    warp * STAGES * BUF;
-    // lane-invariant parts of the entry index: lane <-> entry (pb, i, j) of block row pa
-    int pbk[KP], ijk[KP], ijt[KP];
-#pragma unroll
-    for (int kk = 0; kk < KP; ++kk) {
-      const int k = lane + 32 * kk;
-      pbk[kk] = k / D2;
-      ijk[kk] = k - pbk[kk] * D2;
-      const int i = ijk[kk] / DIM, j = ijk[kk] - i * DIM;
-      ijt[kk] = j * DIM + i;
-    }
+    // lane <-> row task t = (pb, i): the three entries (i, 0..2) of block
+    // (pa, pb), contiguous in the buffer and in the K row (one slot lookup and
+    // one address per task instead of per entry)
+    constexpr int NTASK = NP * DIM, TR = (NTASK + 31) / 32;
+    static_assert(DIM == 3, "row tasks are written for dim 3");
     // copy item `it`'s block row and slots into buffer `buf` (one commit group)
     auto issue = [&](int it, double* buf) {
       const int64_t el = it / NP;
       const int pa = it - (int)el * NP;
       const double* rec = a.scratch + (size_t)el * NB * D2;
 #pragma unroll
-      for (int kk = 0; kk < KP; ++kk) {
-        const int k = lane + 32 * kk;
-        if (k < NP * D2) {
-          const int pb = pbk[kk];
+      for (int rr = 0; rr < TR; ++rr) {
+        const int t = lane + 32 * rr;
+        if (t < NTASK) {
+          const int pb = t / DIM, i = t - pb * DIM;
           const bool up = pa <= pb;
           const int lo = up ? pa : pb, hi = up ? pb : pa;
-          cp_async8(buf + k, rec + blk_index<NP>(lo, hi) * D2 + (up ? ijk[kk] : ijt[kk]));
+          // block (pb, pa) is read transposed when pb < pa
+          const double* src = rec + blk_index<NP>(lo, hi) * D2 + (up ? DIM * i : i);
+          const int step = up ? 1 : DIM;
+          double* dst = buf + DIM * t;
+          cp_async8(dst, src);
+          cp_async8(dst + 1, src + step);
+          cp_async8(dst + 2, src + 2 * step);
         }
       }
-      // the NP slot bytes in 4-byte words (NP % 4 == 0: 4-byte aligned source)
-      if (lane < NP / 4)
-        cp_async4(reinterpret_cast<uint8_t*>(buf + NP * D2 + (NP * D2) % 2) + 4 * lane, a.slot + (int64_t)it * NP + 4 * lane);
+      // the NP slot bytes in 4-byte words (NP % 4 == 0: 4-byte aligned source), on the last lanes
+      if (lane >= 32 - NP / 4) {
+        const int w = lane - (32 - NP / 4);
+        cp_async4(reinterpret_cast<uint8_t*>(buf + NP * D2 + (NP * D2) % 2) + 4 * w, a.slot + (int64_t)it * NP + 4 * w);
+      }
       cp_async_commit();
     };
-    for (int ln = warp; ln < nloc; ln += kStreamThreads / 32) {
+    for (int ln = warp; ln < nloc; ln += nwarps) {
       const int ie = s_iptr[ln + 1];
       const int row_len = (s_vptr[ln + 1] - s_vptr[ln]) / DIM;
       double* seg = img + s_vptr[ln];
@@ -388,13 +404,17 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
         const double* cur = wbuf + r * BUF;
         const uint8_t* sls = reinterpret_cast<const uint8_t*>(cur + NP * D2 + (NP * D2) % 2);
 #pragma unroll
-        for (int kk = 0; kk < KP; ++kk) {
-          const int k = lane + 32 * kk;
-          if (k < NP * D2) {
-            const int sl = sls[pbk[kk]];
-            const int i = ijk[kk] / DIM, j = ijk[kk] - i * DIM;
-            EPFEM_CHECK(sl < row_len / DIM && s_vptr[ln] + i * row_len + sl * DIM + j < s_vptr[ln + 1]);
-            seg[i * row_len + sl * DIM + j] += cur[k];
+        for (int rr = 0; rr < TR; ++rr) {
+          const int t = lane + 32 * rr;
+          if (t < NTASK) {
+            const int pb = t / DIM, i = t - pb * DIM;
+            const int sl = sls[pb];
+            EPFEM_CHECK(sl < row_len / DIM && s_vptr[ln] + i * row_len + sl * DIM + DIM - 1 < s_vptr[ln + 1]);
+            double* p = seg + i * row_len + sl * DIM;
+            const double* c3 = cur + DIM * t;
+            p[0] += c3[0];
+            p[1] += c3[1];
+            p[2] += c3[2];
           }
         }
         // every lane's adds of this item are done (add order = item order)
@@ -405,7 +425,52 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
       }
     }
   }
-  for (int ln = ASYNC ? nloc : warp; ln < nloc;) {
+  if constexpr (!ASYNC && DIM == 3) {
+    // tetrahedra: the same row tasks with the loads into registers (the ring's
+    // shared memory would cost a resident CTA)
+    constexpr int NTASK = NP * DIM, TR = (NTASK + 31) / 32;
+    for (int ln = warp; ln < nloc; ln += nwarps) {
+      const int ib = s_iptr[ln], ie = s_iptr[ln + 1];
+      const int row_len = (s_vptr[ln + 1] - s_vptr[ln]) / DIM;
+      double* seg = img + s_vptr[ln];
+      for (int kb = ib; kb < ie; ++kb) {
+        const int it = s_item[kb];  // warp-uniform
+        if (it < 0) continue;
+        const int64_t el = it / NP;
+        const int pa = it - (int)el * NP;
+        const double* rec = a.scratch + (size_t)el * NB * D2;
+        double v[TR][DIM];
+        int sl[TR];
+#pragma unroll
+        for (int rr = 0; rr < TR; ++rr) {
+          const int t = lane + 32 * rr;
+          if (t < NTASK) {
+            const int pb = t / DIM, i = t - pb * DIM;
+            const bool up = pa <= pb;
+            const int lo = up ? pa : pb, hi = up ? pb : pa;
+            const double* src = rec + blk_index<NP>(lo, hi) * D2 + (up ? DIM * i : i);
+            const int step = up ? 1 : DIM;
+            sl[rr] = __ldg(a.slot + (int64_t)it * NP + pb);
+#pragma unroll
+            for (int j = 0; j < DIM; ++j) v[rr][j] = __ldg(src + j * step);
+          }
+        }
+#pragma unroll
+        for (int rr = 0; rr < TR; ++rr) {
+          const int t = lane + 32 * rr;
+          if (t < NTASK) {
+            const int i = t % DIM;
+            EPFEM_CHECK(sl[rr] < row_len / DIM && s_vptr[ln] + i * row_len + sl[rr] * DIM + DIM - 1 < s_vptr[ln + 1]);
+            double* p = seg + i * row_len + sl[rr] * DIM;
+#pragma unroll
+            for (int j = 0; j < DIM; ++j) p[j] += v[rr][j];
+          }
+        }
+        __syncwarp();  // add order = item order (see below)
+      }
+    }
+  }
+  for (int ln = (ASYNC || DIM == 3) ? nloc : warp; ln < nloc;) {
 
     const int ib = s_iptr[ln], ie = s_iptr[ln + 1];
     const int row_len = (s_vptr[ln + 1] - s_vptr[ln]) / DIM;
@@ -457,7 +522,7 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
     }
     // (claiming nodes dynamically from a shared counter gave the same bits
     // and measured no faster: warp imbalance inside a range is not the limit)
-    ln += kStreamThreads / 32;
+    ln += nwarps;
   }
   fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
   __syncthreads();
@@ -501,13 +566,15 @@ size_t tangent_workspace_doubles(int family, int dim, int64_t n_elements) {
 
 // Nodes per CTA for the row stream: the largest power of two <= 64 whose
 // widest value range and item list fit the shared-memory budget.
-int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
+int plan_row_stream(int64_t n_nodes, int dim, int np, const int64_t* nbr_ptr, const int64_t* n2e_ptr,
                     cudaStream_t st, int* npc_out, int* span_out, int* items_out, int budget_bytes) {
   // bytes of dynamic smem per CTA and the starting node count; EPFEM_ROW_KB /
   // EPFEM_ROW_NPC override them for tuning runs (budget_bytes > 0: the
   // caller's budget)
-  int budget = (dim == 2 ? 100 : 40) * 1024;  // measured optimum (2D: 32 nodes, Q1 hex: 16)
+  int budget = (dim == 2 ? 100 : 40) * 1024;  // measured optimum (2D: 32 nodes; Q2-20: 8)
   int npc = 32;
+  if (dim == 3 && np == 8) npc = 8;        // Q1 hexahedra: 8 nodes on 128 threads (row_stream_threads)
+  else if (dim == 3 && np < 20) npc = 4;   // tetrahedra: 4 nodes on 128 threads
   if (const char* v = getenv("EPFEM_ROW_KB")) budget = atoi(v) * 1024;
   if (budget_bytes > 0) budget = budget_bytes;
   if (const char* v = getenv("EPFEM_ROW_NPC")) npc = atoi(v);
@@ -531,9 +598,9 @@ int plan_row_stream(int64_t n_nodes, int dim, const int64_t* nbr_ptr, const int6
 }
 
 // dynamic shared memory of one node range: image + items + node offsets
-static size_t row_range_smem(const GatherArgs& a, int async_buf) {
+static size_t row_range_smem(const GatherArgs& a, int async_buf, int threads) {
   return sizeof(double) * ((size_t)a.max_span + 2) + sizeof(int) * ((size_t)a.max_items + 2 * ((size_t)a.npc + 1)) +
-         (async_buf ? 16 + sizeof(double) * (kStreamThreads / 32) * EPFEM_ROW_STAGES * (size_t)async_buf : 0);
+         (async_buf ? 16 + sizeof(double) * (threads / 32) * EPFEM_ROW_STAGES * (size_t)async_buf : 0);
 }
 
 int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st) {
@@ -546,8 +613,10 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
     if (rblocks <= 0) return;
     constexpr int KP = (NP * DIM * DIM + 31) / 32;
     constexpr int SLW = (NP + 7) / 8;
+    const int threads = row_stream_threads(DIM, NP);
     const size_t smem = row_range_smem(
-        a, (EPFEM_ROW_ASYNC && KP > 1 && async_row_stream(NP)) ? ((NP * DIM * DIM + 1) / 2) * 2 + ((SLW + 1) / 2) * 2 : 0);
+        a, (EPFEM_ROW_ASYNC && KP > 1 && async_row_stream(NP)) ? ((NP * DIM * DIM + 1) / 2) * 2 + ((SLW + 1) / 2) * 2 : 0,
+        threads);
     auto kern = k_row_stream<DIM, NP, NQ>;
     if (smem + 1024 > 48 * 1024) {  // the static mbarrier and the reserved 1 KB count against the 48 KB default
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -564,7 +633,7 @@ int launch_row_stream(int family, int dim, const GatherArgs& a, cudaStream_t st)
     const bool pdl = pdl_env && !(DIM == 3 && NP >= 20);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)rblocks);
-    cfg.blockDim = dim3(kStreamThreads);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
