@@ -258,7 +258,12 @@ static int row_stream_threads(int dim, int np) {
 // element types whose row stream takes the async item ring (measured: Q1
 // cfg4 rows 3.70 -> 3.55 ms, Q2-20 cfg5 9.44 -> 9.21 ms; P2 tetrahedra
 // slower, 3.00 -> 3.05 ms: the ring's shared memory costs a CTA per SM)
-__host__ __device__ constexpr bool async_row_stream(int np) { return np == 8 || (EPFEM_ROW_ASYNC20 && np == 20); }
+#ifndef EPFEM_ROW_ASYNC10
+#define EPFEM_ROW_ASYNC10 1
+#endif
+__host__ __device__ constexpr bool async_row_stream(int np) {
+  return np == 8 || (EPFEM_ROW_ASYNC20 && np == 20) || (EPFEM_ROW_ASYNC10 && np == 10);
+}
 #ifndef EPFEM_ROW_STAGES
 #define EPFEM_ROW_STAGES 2  // items in flight + 1
 #endif
@@ -341,8 +346,16 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
     // one address per task instead of per entry)
     constexpr int NTASK = NP * DIM, TR = (NTASK + 31) / 32;
     static_assert(DIM == 3, "row tasks are written for dim 3");
+    // NP % 4 != 0 (P2 tetrahedra): an item's slot bytes are not 4-byte aligned,
+    // so each lane loads its task's slot byte into a register when the item's
+    // copies are issued, one item ahead of the adds (two stages)
+    constexpr bool SLOT_REG = NP % 4 != 0;
+    static_assert(!SLOT_REG || STAGES == 2, "register slots are written for one item in flight");
+    int sl_cur[TR], sl_nxt[TR];
+#pragma unroll
+    for (int rr = 0; rr < TR; ++rr) sl_cur[rr] = sl_nxt[rr] = 0;
     // copy item `it`'s block row and slots into buffer `buf` (one commit group)
-    auto issue = [&](int it, double* buf) {
+    auto issue = [&](int it, double* buf, int* sl_reg) {
       const int64_t el = it / NP;
       const int pa = it - (int)el * NP;
       const double* rec = a.scratch + (size_t)el * NB * D2;
@@ -360,10 +373,11 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
           cp_async8(dst, src);
           cp_async8(dst + 1, src + step);
           cp_async8(dst + 2, src + 2 * step);
+          if constexpr (SLOT_REG) sl_reg[rr] = __ldg(a.slot + (int64_t)it * NP + pb);
         }
       }
       // the NP slot bytes in 4-byte words (NP % 4 == 0: 4-byte aligned source), on the last lanes
-      if (lane >= 32 - NP / 4) {
+      if (!SLOT_REG && lane >= 32 - NP / 4) {
         const int w = lane - (32 - NP / 4);
         cp_async4(reinterpret_cast<uint8_t*>(buf + NP * D2 + (NP * D2) % 2) + 4 * w, a.slot + (int64_t)it * NP + 4 * w);
       }
@@ -384,7 +398,7 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
 #pragma unroll
       for (int s = 0; s < STAGES - 1; ++s) {
         if (kiss < ie) {
-          issue(s_item[kiss], wbuf + s * BUF);
+          issue(s_item[kiss], wbuf + s * BUF, sl_cur);
           kiss = next(kiss + 1);
         } else {
           cp_async_commit();
@@ -394,7 +408,7 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
       while (kb < ie) {
         const int w = (r + STAGES - 1) % STAGES;
         if (kiss < ie) {
-          issue(s_item[kiss], wbuf + w * BUF);
+          issue(s_item[kiss], wbuf + w * BUF, sl_nxt);
           kiss = next(kiss + 1);
         } else {
           cp_async_commit();
@@ -408,7 +422,7 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
           const int t = lane + 32 * rr;
           if (t < NTASK) {
             const int pb = t / DIM, i = t - pb * DIM;
-            const int sl = sls[pb];
+            const int sl = SLOT_REG ? sl_cur[rr] : sls[pb];
             EPFEM_CHECK(sl < row_len / DIM && s_vptr[ln] + i * row_len + sl * DIM + DIM - 1 < s_vptr[ln + 1]);
             double* p = seg + i * row_len + sl * DIM;
             const double* c3 = cur + DIM * t;
@@ -416,6 +430,10 @@ __global__ void __launch_bounds__(kStreamThreads, (DIM == 3 && NP >= 20) ? EPFEM
             p[1] += c3[1];
             p[2] += c3[2];
           }
+        }
+        if constexpr (SLOT_REG) {
+#pragma unroll
+          for (int rr = 0; rr < TR; ++rr) sl_cur[rr] = sl_nxt[rr];
         }
         // every lane's adds of this item are done (add order = item order)
         // and the buffer is free before the next copy into it
