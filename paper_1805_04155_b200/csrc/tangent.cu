@@ -35,10 +35,25 @@ namespace epfem_gpu {
 
 namespace {
 
+// CTA shape of the standalone element-delta kernel: DeltaCfg's, except for Q1
+// hexahedra, which take the fused kernel's 16 elements on 128 threads (one
+// thread per point in phase 1)
+#ifndef EPFEM_DELTA_EPB_Q1
+#define EPFEM_DELTA_EPB_Q1 16
+#endif
 template <int DIM, int NP, int NQ, int MODE>
-__global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS) k_elem_delta_staged(GatherArgs a) {
+struct StagedCfg : DeltaCfg<DIM, NP, NQ> {
+  using Base = DeltaCfg<DIM, NP, NQ>;
+  // (the elastic assembly keeps delta_phase2, written for DeltaCfg's shape)
+  static constexpr bool Q1 = DIM == 3 && NP == 8 && EPFEM_DELTA_EPB_Q1 > 0 && MODE != G_ELASTIC;
+  static constexpr int EPB = Q1 ? EPFEM_DELTA_EPB_Q1 : Base::EPB;
+  static constexpr int THREADS = Q1 ? ((EPB * NQ + 31) / 32) * 32 : Base::THREADS;
+};
+
+template <int DIM, int NP, int NQ, int MODE>
+__global__ void __launch_bounds__(StagedCfg<DIM, NP, NQ, MODE>::THREADS) k_elem_delta_staged(GatherArgs a) {
   pdl_trigger();
-  using Cfg = DeltaCfg<DIM, NP, NQ>;
+  using Cfg = StagedCfg<DIM, NP, NQ, MODE>;
   constexpr int EPB = Cfg::EPB;
   constexpr int NS = Cfg::NS, REC = Cfg::REC;
   __shared__ double s_st[EPB][NQ][REC];
@@ -93,6 +108,7 @@ __global__ void __launch_bounds__(DeltaCfg<DIM, NP, NQ>::THREADS) k_elem_delta_s
         delta_rowpair3<NP, NQ>(&s_st[le][0][0], s_mask[le], t - le * PC::PL, a.scratch + (size_t)e * Cfg::NB * Cfg::D2);
     }
   } else {
+    static_assert(EPB == DeltaCfg<DIM, NP, NQ>::EPB, "delta_phase2 uses DeltaCfg's shape");
     delta_phase2<DIM, NP, NQ>(s_st, s_mask, tid, e0, a.e_end, a.scratch);
   }
 }
@@ -708,13 +724,14 @@ int launch_delta(int family, int dim, int mode, const GatherArgs& a, cudaStream_
       return;
     }
     if (a.n_elements > 0) {
-      const int64_t blocks = (a.e_end - a.e_begin + Cfg::EPB - 1) / Cfg::EPB;
-      if (mode == G_TANGENT_PACKED)
-        k_elem_delta_staged<DIM, NP, NQ, G_TANGENT_PACKED><<<(unsigned)blocks, Cfg::THREADS, 0, st>>>(a);
-      else if (mode == G_ELASTIC)
-        k_elem_delta_staged<DIM, NP, NQ, G_ELASTIC><<<(unsigned)blocks, Cfg::THREADS, 0, st>>>(a);
-      else
-        k_elem_delta_staged<DIM, NP, NQ, G_TANGENT_DS36><<<(unsigned)blocks, Cfg::THREADS, 0, st>>>(a);
+      auto go = [&](auto m) {
+        using SC = StagedCfg<DIM, NP, NQ, decltype(m)::value>;
+        const int64_t blocks = (a.e_end - a.e_begin + SC::EPB - 1) / SC::EPB;
+        k_elem_delta_staged<DIM, NP, NQ, decltype(m)::value><<<(unsigned)blocks, SC::THREADS, 0, st>>>(a);
+      };
+      if (mode == G_TANGENT_PACKED) go(IC<G_TANGENT_PACKED>{});
+      else if (mode == G_ELASTIC) go(IC<G_ELASTIC>{});
+      else go(IC<G_TANGENT_DS36>{});
     }
   });
   if (!ok) return fail(EPFEM_ERR_INVALID, "invalid element type");
