@@ -2,6 +2,7 @@
 // assembly cache, argument validation with the reference's error texts, and
 // dispatch to the sm_100a kernels.  No CPU compute path exists: every entry
 // point fails with EPFEM_ERR_CUDA when no CUDA device is present.
+#include <nvtx3/nvToolsExt.h>
 #include <algorithm>
 #include <chrono>
 #include <climits>
@@ -96,6 +97,14 @@ bool aligned16(const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0
 // Every entry point taking a context runs on the context's device and
 // restores the caller's current device on return (torch or the host
 // application may have another device current).
+// NVTX range around an entry point (header-only NVTX 3: a no-op costing one
+// pointer test unless a profiler has injected itself), so a timeline shows
+// epfem_newton_step, epfem_cache_build, ... around the kernels they launch
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(const epfem_ctx* ctx) {
@@ -188,6 +197,7 @@ int epfem_ctx_set_sync(epfem_ctx* ctx, int synchronous) {
 
 int epfem_ctx_sync(epfem_ctx* ctx) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (int rc = check_ctx(ctx)) return rc;
   EPFEM_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
   return poll_device_error(ctx, nullptr);
@@ -196,6 +206,7 @@ int epfem_ctx_sync(epfem_ctx* ctx) {
 int epfem_ctx_destroy(epfem_ctx* ctx) {
   if (!ctx) return 0;
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (ctx->own_comm) nccl_comm_destroy(ctx->comm);
   if (ctx->direct) direct_cache_free(ctx->direct);
   if (ctx->err) cudaFree(ctx->err);
@@ -273,6 +284,7 @@ int epfem_constitutive(epfem_ctx* ctx, const epfem_material* mat, const double* 
                        const double* Ep_prev, const double* Hard_prev,
                        const epfem_constitutive_out* out) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   ConstArgs a;
   if (int rc = const_args(ctx, mat, E, Ep_prev, Hard_prev, out, &a)) return rc;
   if (int rc = launch_constitutive(mat->model, a, ctx->stream, ctx->num_sms)) return rc;
@@ -330,6 +342,7 @@ static GatherArgs gather_args(const epfem_cache* c) {
 int epfem_cache_build(epfem_ctx* ctx, const epfem_mesh* mesh, const epfem_material* mat,
                       epfem_cache** out) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (int rc = check_ctx(ctx)) return rc;
   if (!mesh || !mat || !out) return fail(EPFEM_ERR_INVALID, "build_assembly_cache: null argument");
   *out = nullptr;
@@ -479,6 +492,7 @@ int epfem_cache_geometry(const epfem_cache* c, const double** det, const double*
 
 int epfem_assemble_elastic(epfem_ctx* ctx, const epfem_cache* c, double* K_values) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (int rc = check_ctx(ctx)) return rc;
   if (!c || !K_values) return fail(EPFEM_ERR_INVALID, "assemble_elastic_stiffness: null argument");
   if (!aligned16(K_values))
@@ -510,12 +524,14 @@ static int tangent_common(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int, c
 int epfem_assemble_tangent(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int, const double* D,
                            const uint8_t* flags, double* K_values) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   return tangent_common(ctx, c, n_int, D, flags, K_values, 1);
 }
 
 int epfem_assemble_tangent_ds(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int,
                               const double* DS, const uint8_t* plastic_cols, double* K_values) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   return tangent_common(ctx, c, n_int, DS, plastic_cols, K_values, 2);
 }
 
@@ -561,6 +577,7 @@ int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* c, const epfem_material
                       const double* E, const double* Ep_prev, const double* Hard_prev,
                       const epfem_constitutive_out* out, double* K_values) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (!K_values || !aligned16(K_values))
     return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: K must be 16-byte aligned");
   if (int rc = delta_part(ctx, c, mat, E, Ep_prev, Hard_prev, out)) return rc;
@@ -572,6 +589,7 @@ int epfem_newton_step_f(epfem_ctx* ctx, const epfem_cache* c, const epfem_materi
                         const double* E, const double* Ep_prev, const double* Hard_prev,
                         const epfem_constitutive_out* out, double* K_values, double* F_out) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (!K_values || !aligned16(K_values))
     return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: K must be 16-byte aligned");
   if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
@@ -593,6 +611,7 @@ int epfem_newton_step_u(epfem_ctx* ctx, const epfem_cache* c, const epfem_materi
                         const double* u, const double* Ep_prev, const double* Hard_prev,
                         const epfem_constitutive_out* out, double* E_out, double* K_values) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (!K_values || !aligned16(K_values))
     return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: K must be 16-byte aligned");
   if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
@@ -614,12 +633,14 @@ int epfem_constitutive_delta(epfem_ctx* ctx, const epfem_cache* c, const epfem_m
                              const double* E, const double* Ep_prev, const double* Hard_prev,
                              const epfem_constitutive_out* out) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (int rc = delta_part(ctx, c, mat, E, Ep_prev, Hard_prev, out)) return rc;
   return finish(ctx);
 }
 
 int epfem_assemble_rows(epfem_ctx* ctx, const epfem_cache* c, double* K_values) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (int rc = rows_part(ctx, c, K_values)) return rc;
   return finish(ctx);
 }
@@ -632,6 +653,7 @@ int epfem_newton_range(epfem_ctx* ctx, const epfem_cache* c, const epfem_materia
                        const double* E, const double* Ep_prev, const double* Hard_prev,
                        const epfem_constitutive_out* out, int64_t e_begin, int64_t e_end) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
   if (e_begin < 0 || e_end < e_begin || e_end > c->info.n_elements)
     return fail(EPFEM_ERR_INVALID, "newton_range: element range out of bounds");
@@ -667,6 +689,7 @@ int epfem_newton_range(epfem_ctx* ctx, const epfem_cache* c, const epfem_materia
 int epfem_delta_range(epfem_ctx* ctx, const epfem_cache* c, int64_t n_int, const double* D,
                       const uint8_t* flags, int64_t e_begin, int64_t e_end) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (int rc = check_ctx(ctx)) return rc;
   if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
   if (n_int != c->info.n_int) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: size mismatch");
@@ -692,6 +715,7 @@ int epfem_nccl_unique_id(void* id_out) {
 
 int epfem_ctx_attach_nccl(epfem_ctx* ctx, const void* id, int world, int rank) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (int rc = check_ctx(ctx)) return rc;
   if (!id || world < 1 || rank < 0 || rank >= world) return fail(EPFEM_ERR_INVALID, "attach_nccl: invalid rank / world");
   void* comm = nullptr;
@@ -719,6 +743,7 @@ int epfem_ctx_set_nccl_comm(epfem_ctx* ctx, void* nccl_comm, int world, int rank
 int epfem_exchange_interface(epfem_ctx* ctx, uint8_t* flags, double* D, int64_t send_begin, int64_t send_end,
                              int64_t recv_begin, int64_t recv_end) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (int rc = check_ctx(ctx)) return rc;
   if (!ctx->comm) return fail(EPFEM_ERR_INVALID, "exchange_interface: no NCCL communicator attached");
   if (send_end < send_begin || recv_end < recv_begin || send_begin < 0 || recv_begin < 0)
@@ -733,6 +758,7 @@ int epfem_exchange_interface(epfem_ctx* ctx, uint8_t* flags, double* D, int64_t 
 
 int epfem_strains(epfem_ctx* ctx, const epfem_cache* c, const double* u, double* E) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (int rc = check_ctx(ctx)) return rc;
   if (!c || !u || !E) return fail(EPFEM_ERR_INVALID, "strains: null argument");
   if (!aligned16(E)) return fail(EPFEM_ERR_INVALID, "strains: E must be 16-byte aligned");
@@ -745,6 +771,7 @@ int epfem_strains(epfem_ctx* ctx, const epfem_cache* c, const double* u, double*
 
 int epfem_internal_forces(epfem_ctx* ctx, const epfem_cache* c, const double* S, double* F) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (int rc = check_ctx(ctx)) return rc;
   if (!c || !S || !F) return fail(EPFEM_ERR_INVALID, "internal_forces: null argument");
   if (c->info.n_nodes == 0) return 0;
@@ -760,6 +787,7 @@ int epfem_restricted_solve(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, co
                            double rel_tol, int64_t max_iters, double* x, int64_t* iters,
                            double* residual) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   return epfem_restricted_solve_blocked(ctx, n, row_ptr, col_idx, values, rhs, free_mask, rel_tol, max_iters,
                                         1, x, iters, residual);
 }
@@ -769,6 +797,7 @@ int epfem_restricted_solve_blocked(epfem_ctx* ctx, int64_t n, const int64_t* row
                                    double rel_tol, int64_t max_iters, int block, double* x, int64_t* iters,
                                    double* residual) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (int rc = check_ctx(ctx)) return rc;
   if (n < 0 || (n > 0 && (!row_ptr || !col_idx || !values || !rhs || !x)))
     return fail(EPFEM_ERR_INVALID, "restricted_solve: dimension mismatch");
@@ -789,6 +818,7 @@ int epfem_restricted_solve_direct(epfem_ctx* ctx, int64_t n, const int64_t* row_
                                   const double* values, const double* rhs, const uint8_t* free_mask, double rel_tol,
                                   double* x, int* sweeps, double* residual) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (int rc = check_ctx(ctx)) return rc;
   if (n < 0 || (n > 0 && (!row_ptr || !col_idx || !values || !rhs || !x)))
     return fail(EPFEM_ERR_INVALID, "restricted_solve: dimension mismatch");
@@ -807,6 +837,7 @@ int epfem_restricted_solve_direct(epfem_ctx* ctx, int64_t n, const int64_t* row_
 int epfem_energy_norm(epfem_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* col_idx,
                       const double* values, const double* v, double* out) {
   DeviceGuard guard(ctx);
+  NvtxRange nvtx_range(__func__);
   if (int rc = check_ctx(ctx)) return rc;
   if (!out || n < 0 || (n > 0 && (!row_ptr || !col_idx || !values || !v)))
     return fail(EPFEM_ERR_INVALID, "energy_norm: dimension mismatch");
