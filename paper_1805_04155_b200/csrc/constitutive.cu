@@ -59,6 +59,9 @@ namespace {
 #ifndef EPFEM_MINB_Q20
 #define EPFEM_MINB_Q20 16
 #endif
+#ifndef EPFEM_Q1_DWQUAD
+#define EPFEM_Q1_DWQUAD 1
+#endif
 template <int DIM, int NP, int NQ>
 struct FusedCfg : DeltaCfg<DIM, NP, NQ> {
   using Base = DeltaCfg<DIM, NP, NQ>;
@@ -455,8 +458,18 @@ __global__ void __launch_bounds__(FusedCfg<DIM, NP, NQ>::THREADS, FusedCfg<DIM, 
       const int64_t e = e0 + le;
       const unsigned mask = s_mask[le];
       EPFEM_CHECK(!(e < g.e_end) || e < g.n_elements);
-      if (e < g.e_end && mask)
-        delta_rowpair3<NP, NQ>(&s_st[le][0][0], mask, k, g.scratch + (size_t)e * Cfg::NB * Cfg::D2);
+      if (e < g.e_end && mask) {
+        if constexpr (Cfg::Q1 && EPFEM_Q1_DWQUAD && UseCyc3<NP>::value) {
+          // Lane order inside an element: quads (r, i), (r + 1, i), (r, i + 1), (r + 1, i + 1) for
+          // components {0, 1}, then the four row pairs of component 2.  The Dw loads (address by i)
+          // are then "aabb / aaaa" per quad: one shared-memory wavefront instead of two
+          // (profiles/r2_l1tex.md); the B-column loads stay at two.
+          const int r = k < 8 ? 2 * (k >> 2) + (k & 1) : k - 8, ci = k < 8 ? (k >> 1) & 1 : 2;
+          delta_cyc3<NP, NQ>(&s_st[le][0][0], mask, r, ci, g.scratch + (size_t)e * Cfg::NB * Cfg::D2);
+        } else {
+          delta_rowpair3<NP, NQ>(&s_st[le][0][0], mask, k, g.scratch + (size_t)e * Cfg::NB * Cfg::D2);
+        }
+      }
     }
     return;
   }
