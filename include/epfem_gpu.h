@@ -226,6 +226,10 @@ int epfem_constitutive_delta(epfem_ctx* ctx, const epfem_cache* cache, const epf
                              const double* E, const double* Ep_prev, const double* Hard_prev,
                              const epfem_constitutive_out* out);
 int epfem_assemble_rows(epfem_ctx* ctx, const epfem_cache* cache, double* K_values);
+/* The row stream for the rows of nodes [n_begin, n_end) only (K_values is the whole value array; the
+ * element records of every element touching those nodes must be final). */
+int epfem_assemble_rows_range(epfem_ctx* ctx, const epfem_cache* cache, double* K_values, int64_t n_begin,
+                              int64_t n_end);
 
 /* Element-range forms for a mesh partition (multi-GPU slabs, dist.py): the
  * reference has no partitioned entry point; these split

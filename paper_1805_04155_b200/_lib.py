@@ -54,7 +54,7 @@ EXPORTS = [
     "epfem_cache_get_info", "epfem_cache_pattern", "epfem_cache_K_elast", "epfem_cache_geometry",
     "epfem_cache_workspace",
     "epfem_assemble_elastic", "epfem_assemble_tangent", "epfem_assemble_tangent_ds",
-    "epfem_newton_step", "epfem_newton_step_u", "epfem_newton_step_f", "epfem_constitutive_delta", "epfem_assemble_rows", "epfem_newton_range",
+    "epfem_newton_step", "epfem_newton_step_u", "epfem_newton_step_f", "epfem_constitutive_delta", "epfem_assemble_rows", "epfem_assemble_rows_range", "epfem_newton_range",
     "epfem_delta_range", "epfem_strains", "epfem_internal_forces", "epfem_restricted_solve",
     "epfem_restricted_solve_blocked", "epfem_energy_norm",
     "epfem_restricted_solve_direct", "epfem_nccl_unique_id", "epfem_ctx_attach_nccl", "epfem_ctx_set_nccl_comm", "epfem_exchange_interface",
@@ -103,6 +103,7 @@ def lib() -> C.CDLL:
     L.epfem_constitutive_delta.argtypes = [_P, _P, C.POINTER(Material), _P, _P, _P,
                                            C.POINTER(ConstitutiveOut)]
     L.epfem_assemble_rows.argtypes = [_P, _P, _P]
+    L.epfem_assemble_rows_range.argtypes = [_P, _P, _P, C.c_int64, C.c_int64]
     L.epfem_newton_range.argtypes = [_P, _P, C.POINTER(Material), _P, _P, _P,
                                      C.POINTER(ConstitutiveOut), C.c_int64, C.c_int64]
     L.epfem_delta_range.argtypes = [_P, _P, C.c_int64, _P, _P, C.c_int64, C.c_int64]

@@ -562,7 +562,8 @@ static int delta_part(epfem_ctx* ctx, const epfem_cache* c, const epfem_material
   return launch_newton_fused(mat->model, c->info.family, c->info.dim, a, g, ctx->stream);
 }
 
-static int rows_part(epfem_ctx* ctx, const epfem_cache* c, double* K_values) {
+static int rows_part(epfem_ctx* ctx, const epfem_cache* c, double* K_values, int64_t n_begin = 0,
+                     int64_t n_end = -1) {
   if (int rc = check_ctx(ctx)) return rc;
   if (!c) return fail(EPFEM_ERR_INVALID, "assemble_tangent_stiffness: null cache");
   if (!K_values || !aligned16(K_values))
@@ -570,7 +571,20 @@ static int rows_part(epfem_ctx* ctx, const epfem_cache* c, double* K_values) {
   GatherArgs g = gather_args(c);
   g.base = c->K_elast;
   g.out = K_values;
+  if (n_end >= 0) {
+    if (n_begin < 0 || n_begin > n_end || n_end > c->info.n_nodes)
+      return fail(EPFEM_ERR_INVALID, "assemble_rows_range: node range out of bounds");
+    g.n_begin = n_begin;
+    g.n_end = n_end;
+  }
   return launch_row_stream(c->info.family, c->info.dim, g, ctx->stream);
+}
+
+int epfem_assemble_rows_range(epfem_ctx* ctx, const epfem_cache* c, double* K_values, int64_t n_begin,
+                              int64_t n_end) {
+  DeviceGuard guard(ctx);
+  if (int rc = rows_part(ctx, c, K_values, n_begin, n_end)) return rc;
+  return finish(ctx);
 }
 
 int epfem_newton_step(epfem_ctx* ctx, const epfem_cache* c, const epfem_material* mat,

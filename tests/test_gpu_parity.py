@@ -347,6 +347,42 @@ def test_slab_data_path_on_one_rank(cuda, name):
     assert np.array_equal(_np(K).view(np.uint64), _np(K2).view(np.uint64))
 
 
+@pytest.mark.parametrize("name", ["cfg2", "cfg4", "cfg3"])
+def test_assemble_rows_by_node_ranges(cuda, name):
+    """epfem_assemble_rows_range over three uneven node ranges writes the same K bits as the whole
+    row stream, and a range leaves the other rows untouched; a range outside the mesh is rejected."""
+    import ctypes as C
+
+    import paper_1805_04155_b200 as P
+    from paper_1805_04155_b200.dist import DistributedTangent, make_plan
+    from paper_1805_04155_b200.synthetic import CONFIGS, calibrate, displacement
+    api = P.api
+    cfg = CONFIGS[name]
+    plan = make_plan(cfg.family, cfg.dim, REDUCED[name], 1, 0)
+    dt = DistributedTangent(plan, cfg.material, cuda)
+    E1 = dt.cache.strains(torch.from_numpy(displacement(plan.mesh.coord, cfg.seed)).to(cuda))
+    s, _ = calibrate(E1, dt.mat_ext, 0.4)
+    eng = P.TangentEngine(dt.cache, dt.mat_ext)
+    S, f, D, K = eng.step((s * E1).contiguous())
+    eng.sync()
+    Kref = K.clone()
+    n_nodes = dt.cache.info.n_nodes
+    lib = api.L.lib()
+    eng.K.fill_(float("nan"))
+    eng.ctx.use_current_stream()
+    cuts = [0, n_nodes // 3 + 1, n_nodes // 3 + 2, n_nodes]
+    api._check(lib.epfem_assemble_rows_range(eng.ctx.handle, dt.cache.handle, api._ptr(eng.K), cuts[1], cuts[2]))
+    eng.sync()
+    written = int((~torch.isnan(eng.K)).sum())
+    assert 0 < written < eng.K.numel() // 2
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        api._check(lib.epfem_assemble_rows_range(eng.ctx.handle, dt.cache.handle, api._ptr(eng.K), a, b))
+    eng.sync()
+    assert np.array_equal(_np(eng.K).view(np.uint64), _np(Kref).view(np.uint64))
+    rc = lib.epfem_assemble_rows_range(eng.ctx.handle, dt.cache.handle, api._ptr(eng.K), 0, n_nodes + 1)
+    assert rc != 0 and b"node range" in lib.epfem_last_error()
+
+
 @pytest.mark.parametrize("name,world", [("cfg2", 2), ("cfg2", 3), ("cfg4", 2), ("cfg3", 3), ("cfg5", 2)])
 def test_slab_ranks_emulated_in_one_process(cuda, name, world):
     """The N-rank data path (dist.py) with the NCCL exchange replaced by the
