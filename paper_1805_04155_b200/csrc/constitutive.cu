@@ -47,7 +47,8 @@ namespace {
 // phase-2 chunks in two rounds over the warp) at up to 16 CTAs/SM (128
 // registers; shared memory admits 13).  Measured on B200, cfg5: fused 15.33 vs
 // 16.04 ms for DeltaCfg's 2 elements on 128 threads (54 of them busy in phase
-// 1); 2 elements on 64 threads: 15.69 ms.  The row stream after it is launched
+// 1); 2 elements on 64 threads: 15.69 ms; 1 element on 64 threads (its 60 chunks in
+// one round, 8 CTAs/SM): 16.03 ms.  The row stream after it is launched
 // without PDL (tangent.cu): its early CTAs slowed this many-CTA grid (step
 // 25.6 ms with PDL, 24.76 ms without).  EPFEM_EPB_Q20=0 restores DeltaCfg.
 #ifndef EPFEM_EPB_Q20
